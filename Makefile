@@ -1,0 +1,29 @@
+# Top-level build: the CUDA library (product) and the CPU oracle (test infrastructure).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG := paper_2511_13061_b200
+CSRC := $(PKG)/csrc
+SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu
+HDRS := $(wildcard $(CSRC)/*.cuh) include/macko_cuda.h
+OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+
+all: lib oracle
+
+lib: $(PKG)/libmacko_cuda.so
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+
+$(PKG)/libmacko_cuda.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(PKG)/libmacko_cuda.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle clean

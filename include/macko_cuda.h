@@ -1,0 +1,125 @@
+/*
+ * macko_cuda.h — the C-ABI drop-in boundary of the B200-native MACKO-SpMV library
+ * (libmacko_cuda.so, built from paper_2511_13061_b200/csrc/).
+ *
+ * The reference declares a shared library `macko` exposing "the extern-C surface declared in
+ * include/macko/macko.h" (proj/src/CMakeLists.txt:16-19) but ships neither capi.cpp nor the
+ * header.  The entry points below are what that surface has to bind for
+ * the hot path; each cites the reference C++ operation it replaces.  Plain pointers and sizes
+ * only.  `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ * device calls are stream-ordered and asynchronous unless stated.  Errors are returned as
+ * macko_status; no C++ exception crosses this boundary; macko_last_error() gives the
+ * thread-local message.  Status codes map onto the reference's exception taxonomy
+ * (errors.hpp:7-21, std::invalid_argument in bitpack.cpp:14-15,26-27,45-46).
+ *
+ * Matrix byte layout on the device is exactly the reference MackoMatrix (matrix.hpp:57-81):
+ * values = pad_nnz fp16 (+0 at padding entries) zero-padded to a 16-byte multiple;
+ * packed_deltas = codeword (delta-1) in b_delta bits, LSB-first, zero-padded to 16 bytes;
+ * row_pointers = rows+1 u32 element offsets.
+ */
+#ifndef MACKO_CUDA_H
+#define MACKO_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum macko_status {
+    MACKO_OK = 0,
+    MACKO_EINVAL = 1,      /* std::invalid_argument (bitpack.cpp:14-15; convert.hpp:25) */
+    MACKO_EFORMAT = 2,     /* macko::FormatError (errors.hpp:9-11) */
+    MACKO_EIO = 3,         /* macko::IoError (errors.hpp:14-16) */
+    MACKO_EINFEASIBLE = 4, /* macko::InfeasibleError (errors.hpp:19-21) */
+    MACKO_ECUDA = 5,       /* CUDA runtime failure (no reference counterpart) */
+    MACKO_ENCCL = 6,       /* reserved for collective failures */
+    MACKO_ENOMEM = 7       /* device allocation failure */
+} macko_status;
+
+/* Opaque device-resident MACKO matrix (owns its values / deltas / row_pointers buffers and
+ * the SpMV work plan).  Immutable after construction; usable from any stream on its device. */
+typedef struct macko_dev_matrix macko_dev_matrix;
+
+typedef struct macko_dev_info {
+    uint64_t rows, cols, pad_nnz;
+    uint64_t values_bytes;   /* macko_values_bytes(pad_nnz), matrix.hpp:77 */
+    uint64_t delta_bytes;    /* macko_delta_bytes(pad_nnz, b_delta), matrix.hpp:78-81 */
+    uint64_t row_ptr_bytes;  /* 4 * (rows + 1) */
+    uint64_t traffic_bytes;  /* spmv_traffic bytes_matrix + 2C + 2R */
+    uint32_t b_delta;
+    int32_t device;
+    /* device pointers (read-only views; owned by the handle) */
+    const uint16_t* d_values;
+    const uint8_t* d_deltas;
+    const uint32_t* d_row_ptrs;
+} macko_dev_info;
+
+const char* macko_last_error(void);
+const char* macko_version(void);
+
+/* Host MACKO arrays -> device handle (copies).  Replaces the host-resident MackoMatrix
+ * produced by macko_from_csr (convert.hpp:12-16) as the SpMV operand.  n_values /
+ * n_delta_bytes are the host array lengths (>= pad_nnz / ceil(pad_nnz*b_delta/8)).  The
+ * arrays are validated on the device (validate_macko, convert.hpp:25-27) before return. */
+macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t b_delta,
+                              const uint16_t* values, uint64_t n_values, const uint8_t* deltas,
+                              uint64_t n_delta_bytes, const uint32_t* row_ptrs, void* stream,
+                              macko_dev_matrix** out);
+
+/* GPU compressor: dense row-major fp16 (device pointer, leading dimension `ld` elements) ->
+ * MACKO on the device.  Replaces csr_from_dense + macko_from_csr (convert.hpp:8-16,
+ * SPEC.md:54-72); output bytes identical to the reference encoder.  Synchronises `stream`
+ * once (the output size is data dependent). */
+macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t rows, uint64_t cols,
+                                  uint64_t ld, uint32_t b_delta, void* stream, macko_dev_matrix** out);
+
+macko_status macko_dev_get_info(const macko_dev_matrix* m, macko_dev_info* out);
+
+/* Device -> host copy of the three arrays in reference layout (sizes from macko_dev_info;
+ * any pointer may be NULL to skip it).  Synchronous. */
+macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uint8_t* deltas,
+                                uint32_t* row_ptrs, void* stream);
+
+/* y = A*x on the device: fp16 in, fp32 accumulate, one RNE per row, fp16 out.
+ * Replaces reference_spmv / warp_spmv.  d_x: cols fp16, d_y: rows fp16. */
+macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y,
+                            void* stream);
+
+/* End-to-end call with HOST buffers (what a CPU caller of reference_spmv would bind): copies
+ * x host->device, runs macko_dev_spmv, copies y device->host, synchronises the stream.
+ * Pinned host buffers make the copies asynchronous DMA. */
+macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream);
+
+/* Device-side validate_macko (convert.hpp:25-27): every decoded column < cols.  Synchronous. */
+macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
+
+macko_status macko_dev_free(macko_dev_matrix* m);
+
+/* ---- synthetic inputs (counter-hash generator, bit-identical to oracle/macko_oracle.c) ---- */
+uint32_t macko_density_threshold(double density);
+/* Dense rows [row0, row0+rows) of a conceptual (row0+rows) x cols matrix; element (r, c) is
+ * drawn from hash(seed, (row0 + r) * cols + c). */
+macko_status macko_gen_dense(int device, uint16_t* d_out, uint64_t rows, uint64_t cols, uint64_t ld,
+                             uint64_t row0, uint32_t thr24, uint64_t seed, int int_mode, void* stream);
+macko_status macko_gen_vector(int device, uint16_t* d_out, uint64_t n, uint64_t seed, int int_mode,
+                              void* stream);
+
+/* ---- row sharding (contiguous equal-row slabs) ---- */
+macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, uint64_t* r0,
+                              uint64_t* r1);
+
+/* ---- introspection ---- */
+typedef struct macko_launch_info {
+    uint32_t grid, block, warps, ctas_per_sm, n_split_rows, x_in_smem;
+    uint64_t n_units, smem_bytes;
+} macko_launch_info;
+macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out);
+/* Number of kernels this library has launched in the process (for bench gpu_launches). */
+uint64_t macko_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MACKO_CUDA_H */

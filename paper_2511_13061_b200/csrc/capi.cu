@@ -1,0 +1,501 @@
+// capi.cu — host runtime and the extern "C" boundary of libmacko_cuda.so (include/macko_cuda.h).
+//
+// Owns device matrices (values / packed deltas / row pointers in the reference byte layout,
+// matrix.hpp:57-81), builds the static SpMV work plan once per matrix, drives the compressor
+// and maps every failure onto a status code + thread-local message (no exception crosses the
+// C boundary; the C++ wrapper include/macko/macko_cuda.hpp rethrows the reference types).
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/macko_cuda.h"
+#include "common.cuh"
+#include "compress.cuh"
+#include "spmv.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct Failure {
+    macko_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(macko_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    cudaGetLastError();  // clear sticky-less errors
+    fail(e == cudaErrorMemoryAllocation ? MACKO_ENOMEM : MACKO_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+macko_status guarded(F&& f) {
+    try {
+        f();
+        return MACKO_OK;
+    } catch (const Failure& x) {
+        g_err = x.msg;
+        return x.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return MACKO_ENOMEM;
+    } catch (...) {
+        g_err = "unknown failure";
+        return MACKO_ECUDA;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        ck(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+uint64_t align_up(uint64_t n, uint64_t a) { return (n + a - 1) / a * a; }
+uint64_t values_bytes(uint64_t pad_nnz) { return align_up(pad_nnz * 2, 16); }
+uint64_t delta_bytes(uint64_t pad_nnz, unsigned bits) { return align_up((pad_nnz * bits + 7) / 8, 16); }
+
+constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (element equivalents)
+constexpr size_t kMaxSmemX = 200 * 1024;    // x staged in shared memory up to 100k columns
+
+}  // namespace
+
+struct macko_dev_matrix {
+    int device = 0;
+    int sms = 0;
+    uint64_t rows = 0, cols = 0, pad_nnz = 0;
+    uint32_t b_delta = 4;
+    DevBuf<uint16_t> values;
+    DevBuf<uint8_t> deltas;
+    DevBuf<uint32_t> row_ptrs;
+    std::vector<uint32_t> h_row_ptrs;
+    // SpMV plan
+    bool x_in_smem = false;
+    size_t smem = 0;
+    int grid = 0, ctas_per_sm = 0;
+    uint32_t n_chunks = 0, n_split = 0;
+    uint64_t n_units = 0;
+    DevBuf<uint32_t> plan_u32;   // chunk_unit | chunk_row | chunk_j | split_slot | split_first | split_pieces | counters
+    DevBuf<int32_t> plan_i32;    // chunk_colbase | chunk_sid
+    DevBuf<float> partials;
+    mk::SpmvPlanDev plan{};
+    // scratch for macko_spmv_host
+    DevBuf<uint16_t> hx, hy;
+};
+
+namespace {
+
+int sm_count(int dev) {
+    int n = 0;
+    ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    return n;
+}
+
+void check_bits(uint32_t bits) {
+    if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
+        fail(MACKO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits; got " + std::to_string(bits));
+}
+
+// Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
+void build_plan(macko_dev_matrix* m, cudaStream_t st) {
+    using namespace mk;
+    m->x_in_smem = m->cols * 2 <= kMaxSmemX;
+    m->smem = m->x_in_smem ? align_up(m->cols * 2, 16) : 0;
+    ck(spmv_occupancy(m->x_in_smem, m->smem, &m->ctas_per_sm), "spmv occupancy");
+    if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
+    m->grid = m->sms * m->ctas_per_sm;
+    const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
+    m->n_chunks = W;
+    const uint64_t R = m->rows;
+    const std::vector<uint32_t>& rp = m->h_row_ptrs;
+
+    auto row_geom = [&](uint64_t r, uint64_t& T, uint64_t& n_r) {
+        const uint64_t s = rp[r], e = rp[r + 1], al = s & ~7ull;
+        T = e > s ? (e - al + kStepElts - 1) / kStepElts : 0;
+        n_r = T ? (T + kUnitSteps - 1) / kUnitSteps : 1;
+    };
+    auto unit_weight = [&](uint64_t T, uint64_t j) {
+        const uint64_t steps = T ? std::min<uint64_t>(kUnitSteps, T - j * kUnitSteps) : 0;
+        return steps * kStepElts + (j == 0 ? kRowOverhead : 0);
+    };
+    uint64_t total_w = 0, U = 0;
+    for (uint64_t r = 0; r < R; ++r) {
+        uint64_t T, n_r;
+        row_geom(r, T, n_r);
+        for (uint64_t j = 0; j < n_r; ++j) total_w += unit_weight(T, j);
+        U += n_r;
+    }
+    m->n_units = U;
+    if (U >= 0xFFFFFFFFull) fail(MACKO_EINVAL, "matrix too large for the u32 unit plan");
+    std::vector<uint32_t> chunk_unit(W + 1, (uint32_t)U), chunk_row(W, 0), chunk_j(W, 0);
+    std::vector<int32_t> chunk_sid(2 * (size_t)W, -1);
+    std::vector<uint32_t> split_slot, split_first, split_pieces;
+    uint64_t slots = 0;
+    int64_t prev_k = -1;
+    uint64_t cw = 0, u = 0;
+    for (uint64_t r = 0; r < R; ++r) {
+        uint64_t T, n_r;
+        row_geom(r, T, n_r);
+        int64_t kf = -1, kl = -1;
+        uint64_t first_units = 0, pieces = 0;
+        for (uint64_t j = 0; j < n_r; ++j, ++u) {
+            const uint64_t w = unit_weight(T, j);
+            const uint64_t mid2 = 2 * cw + w;  // twice the unit midpoint
+            int64_t k = (int64_t)((unsigned __int128)mid2 * W / (2 * (unsigned __int128)std::max<uint64_t>(total_w, 1)));
+            if (k >= (int64_t)W) k = W - 1;
+            if (k < prev_k) k = prev_k;
+            for (int64_t q = prev_k + 1; q <= k; ++q) {
+                chunk_unit[q] = (uint32_t)u;
+                chunk_row[q] = (uint32_t)r;
+                chunk_j[q] = (uint32_t)j;
+            }
+            prev_k = k;
+            if (j == 0) kf = k;
+            if (k == kf) ++first_units;
+            if (j == 0 || k != kl) ++pieces;  // distinct (non-empty) chunks touching the row
+            kl = k;
+            cw += w;
+        }
+        if (kf != kl) {
+            const int32_t sid = (int32_t)split_slot.size();
+            split_slot.push_back((uint32_t)slots);
+            split_first.push_back((uint32_t)first_units);
+            split_pieces.push_back((uint32_t)pieces);
+            slots += n_r;
+            chunk_sid[2 * kf + 1] = sid;
+            if (chunk_row[kf] == r && chunk_j[kf] == 0) chunk_sid[2 * kf] = sid;
+            for (int64_t k = kf + 1; k <= kl; ++k) {
+                chunk_sid[2 * k] = sid;
+                if (k < kl) chunk_sid[2 * k + 1] = sid;
+            }
+        }
+    }
+    const uint32_t S = (uint32_t)split_slot.size();
+    m->n_split = S;
+    // upload
+    const size_t n_u32 = (W + 1) + 2 * (size_t)W + 4 * (size_t)S + 1;
+    m->plan_u32.alloc(n_u32);
+    m->plan_i32.alloc(3 * (size_t)W);
+    m->partials.alloc(std::max<uint64_t>(slots, 1));
+    uint32_t* pu = m->plan_u32.p;
+    std::vector<uint32_t> hu;
+    hu.reserve(n_u32);
+    hu.insert(hu.end(), chunk_unit.begin(), chunk_unit.end());
+    hu.insert(hu.end(), chunk_row.begin(), chunk_row.end());
+    hu.insert(hu.end(), chunk_j.begin(), chunk_j.end());
+    hu.insert(hu.end(), split_slot.begin(), split_slot.end());
+    hu.insert(hu.end(), split_first.begin(), split_first.end());
+    hu.insert(hu.end(), split_pieces.begin(), split_pieces.end());
+    hu.resize(n_u32, 0);  // counters (S) zeroed + 1 spare
+    ck(cudaMemcpyAsync(pu, hu.data(), n_u32 * 4, cudaMemcpyHostToDevice, st), "plan upload");
+    int32_t* pi = m->plan_i32.p;
+    ck(cudaMemcpyAsync(pi + W, chunk_sid.data(), chunk_sid.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
+    mk::SpmvPlanDev& P = m->plan;
+    P.chunk_unit = pu;
+    P.chunk_row = pu + (W + 1);
+    P.chunk_j = pu + (W + 1) + W;
+    P.split_slot = pu + (W + 1) + 2 * (size_t)W;
+    P.split_first = P.split_slot + S;
+    P.split_pieces = P.split_first + S;
+    P.counters = pu + (W + 1) + 2 * (size_t)W + 3 * (size_t)S;
+    P.chunk_colbase = pi;
+    P.chunk_sid = pi + W;
+    P.partials = m->partials.p;
+    ck(launch_plan_colbase(m->deltas.p, m->row_ptrs.p, P.chunk_row, P.chunk_j, pi, W, st), "plan colbase");
+    g_launches.fetch_add(1);
+    ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
+}
+
+void device_validate(macko_dev_matrix* m, cudaStream_t st) {
+    DevBuf<uint32_t> err;
+    err.alloc(1);
+    ck(cudaMemsetAsync(err.p, 0, 4, st), "memset");
+    ck(mk::launch_validate(m->values.p, m->deltas.p, m->row_ptrs.p, (uint32_t)m->rows, (uint32_t)m->cols, m->b_delta,
+                           err.p, m->sms, st),
+       "validate");
+    g_launches.fetch_add(1);
+    uint32_t h = 0;
+    ck(cudaMemcpyAsync(&h, err.p, 4, cudaMemcpyDeviceToHost, st), "validate readback");
+    ck(cudaStreamSynchronize(st), "validate sync");
+    if (h & 4u) fail(MACKO_EFORMAT, "row_pointers not monotone");
+    if (h & 1u) fail(MACKO_EFORMAT, "decoded column index past the column bound");
+    if (h & 2u) fail(MACKO_EFORMAT, "padding value must be +0");
+}
+
+void check_shape(uint64_t rows, uint64_t cols) {
+    if (rows == 0 || cols == 0) fail(MACKO_EINVAL, "matrix dimensions must be >= 1");
+    if (rows >= 0x7FFFFFFFull || cols >= 0x7FFFFFFFull) fail(MACKO_EINVAL, "rows/cols must be < 2^31");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* macko_last_error(void) { return g_err.c_str(); }
+const char* macko_version(void) { return "macko-b200 0.1 (sm_100a, b_delta=4 SpMV, compressor b_delta in {1,2,4,8})"; }
+uint64_t macko_kernel_launches(void) { return g_launches.load(); }
+
+uint32_t macko_density_threshold(double d) {
+    if (!(d > 0)) return 0;
+    if (d >= 1) return 1u << 24;
+    return (uint32_t)__builtin_floor(d * 16777216.0 + 0.5);
+}
+
+macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t b_delta, const uint16_t* values,
+                              uint64_t n_values, const uint8_t* deltas, uint64_t n_delta_bytes, const uint32_t* row_ptrs,
+                              void* stream, macko_dev_matrix** out) {
+    return guarded([&] {
+        if (!out || !row_ptrs) fail(MACKO_EINVAL, "null argument");
+        *out = nullptr;
+        check_bits(b_delta);
+        check_shape(rows, cols);
+        if (row_ptrs[0] != 0) fail(MACKO_EFORMAT, "row_pointers[0] must be 0");
+        for (uint64_t r = 0; r < rows; ++r)
+            if (row_ptrs[r + 1] < row_ptrs[r]) fail(MACKO_EFORMAT, "row_pointers not monotone");
+        const uint64_t pad_nnz = row_ptrs[rows];
+        if (n_values < pad_nnz) fail(MACKO_EFORMAT, "values shorter than pad_nnz");
+        if (n_delta_bytes * 8 < pad_nnz * b_delta) fail(MACKO_EFORMAT, "packed_deltas shorter than pad_nnz");
+        if (pad_nnz && (!values || !deltas)) fail(MACKO_EINVAL, "null payload");
+        DeviceGuard g(device);
+        cudaStream_t st = (cudaStream_t)stream;
+        auto* m = new macko_dev_matrix;
+        std::unique_ptr<macko_dev_matrix> hold(m);
+        m->device = device;
+        m->sms = sm_count(device);
+        m->rows = rows;
+        m->cols = cols;
+        m->pad_nnz = pad_nnz;
+        m->b_delta = b_delta;
+        const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
+        m->values.alloc(std::max<uint64_t>(vb / 2, 8));
+        m->deltas.alloc(std::max<uint64_t>(db, 16));
+        m->row_ptrs.alloc(rows + 1);
+        ck(cudaMemsetAsync(m->values.p, 0, m->values.n * 2, st), "memset");
+        ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
+        if (pad_nnz) {
+            ck(cudaMemcpyAsync(m->values.p, values, std::min<uint64_t>(n_values * 2, vb), cudaMemcpyHostToDevice, st),
+               "upload values");
+            ck(cudaMemcpyAsync(m->deltas.p, deltas, std::min<uint64_t>(n_delta_bytes, db), cudaMemcpyHostToDevice, st),
+               "upload deltas");
+        }
+        ck(cudaMemcpyAsync(m->row_ptrs.p, row_ptrs, (rows + 1) * 4, cudaMemcpyHostToDevice, st), "upload row_ptrs");
+        m->h_row_ptrs.assign(row_ptrs, row_ptrs + rows + 1);
+        device_validate(m, st);
+        if (b_delta == 4) build_plan(m, st);
+        *out = hold.release();
+    });
+}
+
+macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t rows, uint64_t cols, uint64_t ld,
+                                  uint32_t b_delta, void* stream, macko_dev_matrix** out) {
+    return guarded([&] {
+        if (!out || !d_dense) fail(MACKO_EINVAL, "null argument");
+        *out = nullptr;
+        check_bits(b_delta);
+        check_shape(rows, cols);
+        if (ld < cols) fail(MACKO_EINVAL, "leading dimension < cols");
+        DeviceGuard g(device);
+        cudaStream_t st = (cudaStream_t)stream;
+        auto* m = new macko_dev_matrix;
+        std::unique_ptr<macko_dev_matrix> hold(m);
+        m->device = device;
+        m->sms = sm_count(device);
+        m->rows = rows;
+        m->cols = cols;
+        m->b_delta = b_delta;
+        DevBuf<uint32_t> counts;
+        DevBuf<int32_t> lastcol;
+        DevBuf<unsigned long long> total;
+        counts.alloc(rows);
+        lastcol.alloc(rows);
+        total.alloc(1);
+        m->row_ptrs.alloc(rows + 1);
+        ck(mk::launch_count_rows(d_dense, ld, (uint32_t)rows, (uint32_t)cols, b_delta, counts.p, lastcol.p, m->sms, st),
+           "count_rows");
+        ck(mk::launch_scan_counts(counts.p, (uint32_t)rows, m->row_ptrs.p, total.p, st), "scan_counts");
+        g_launches.fetch_add(2);
+        unsigned long long pad_nnz = 0;
+        ck(cudaMemcpyAsync(&pad_nnz, total.p, 8, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (pad_nnz > 0xFFFFFFFFull) fail(MACKO_EINVAL, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
+        m->pad_nnz = pad_nnz;
+        const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
+        m->values.alloc(std::max<uint64_t>(vb / 2, 8));
+        m->deltas.alloc(std::max<uint64_t>(align_up(db, 16), 16));
+        ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
+        if (m->values.n * 2 > pad_nnz * 2)
+            ck(cudaMemsetAsync(m->values.p + pad_nnz, 0, m->values.n * 2 - pad_nnz * 2, st), "memset");
+        if (pad_nnz)
+            ck(mk::launch_emit_rows(d_dense, ld, (uint32_t)rows, (uint32_t)cols, b_delta, m->row_ptrs.p, lastcol.p,
+                                    m->values.p, reinterpret_cast<uint32_t*>(m->deltas.p), m->sms, st),
+               "emit_rows");
+        g_launches.fetch_add(1);
+        m->h_row_ptrs.resize(rows + 1);
+        ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (b_delta == 4) build_plan(m, st);
+        *out = hold.release();
+    });
+}
+
+macko_status macko_dev_get_info(const macko_dev_matrix* m, macko_dev_info* out) {
+    return guarded([&] {
+        if (!m || !out) fail(MACKO_EINVAL, "null argument");
+        out->rows = m->rows;
+        out->cols = m->cols;
+        out->pad_nnz = m->pad_nnz;
+        out->values_bytes = values_bytes(m->pad_nnz);
+        out->delta_bytes = delta_bytes(m->pad_nnz, m->b_delta);
+        out->row_ptr_bytes = 4 * (m->rows + 1);
+        out->traffic_bytes = out->values_bytes + out->delta_bytes + out->row_ptr_bytes + 2 * m->cols + 2 * m->rows;
+        out->b_delta = m->b_delta;
+        out->device = m->device;
+        out->d_values = m->values.p;
+        out->d_deltas = m->deltas.p;
+        out->d_row_ptrs = m->row_ptrs.p;
+    });
+}
+
+macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uint8_t* deltas, uint32_t* row_ptrs,
+                                void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        if (values)
+            ck(cudaMemcpyAsync(values, m->values.p, values_bytes(m->pad_nnz), cudaMemcpyDeviceToHost, st), "download");
+        if (deltas)
+            ck(cudaMemcpyAsync(deltas, m->deltas.p, delta_bytes(m->pad_nnz, m->b_delta), cudaMemcpyDeviceToHost, st),
+               "download");
+        if (row_ptrs) ck(cudaMemcpyAsync(row_ptrs, m->row_ptrs.p, (m->rows + 1) * 4, cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
+    return guarded([&] {
+        if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
+        if (m->b_delta != 4)
+            fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only; got " + std::to_string(m->b_delta));
+        DeviceGuard g(m->device);
+        mk::SpmvArgs a;
+        a.values = m->values.p;
+        a.deltas = m->deltas.p;
+        a.row_ptrs = m->row_ptrs.p;
+        a.x = d_x;
+        a.y = d_y;
+        a.rows = (uint32_t)m->rows;
+        a.cols = (uint32_t)m->cols;
+        a.plan = m->plan;
+        ck(mk::launch_spmv(a, m->grid, m->x_in_smem, m->smem, (cudaStream_t)stream), "macko_spmv launch");
+        g_launches.fetch_add(1);
+    });
+}
+
+macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream) {
+    return guarded([&] {
+        if (!m || !h_x || !h_y) fail(MACKO_EINVAL, "null argument");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        if (!m->hx.p) m->hx.alloc(m->cols);
+        if (!m->hy.p) m->hy.alloc(m->rows);
+        ck(cudaMemcpyAsync(m->hx.p, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
+        const macko_status s = macko_dev_spmv(m, m->hx.p, m->hy.p, stream);
+        if (s != MACKO_OK) fail(s, g_err);
+        ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        DeviceGuard g(m->device);
+        device_validate(const_cast<macko_dev_matrix*>(m), (cudaStream_t)stream);
+    });
+}
+
+macko_status macko_dev_free(macko_dev_matrix* m) {
+    return guarded([&] {
+        if (!m) return;
+        DeviceGuard g(m->device);
+        delete m;
+    });
+}
+
+macko_status macko_gen_dense(int device, uint16_t* d_out, uint64_t rows, uint64_t cols, uint64_t ld, uint64_t row0,
+                             uint32_t thr24, uint64_t seed, int int_mode, void* stream) {
+    return guarded([&] {
+        if (!d_out) fail(MACKO_EINVAL, "null output");
+        if (ld < cols) fail(MACKO_EINVAL, "leading dimension < cols");
+        DeviceGuard g(device);
+        ck(mk::launch_gen_dense(d_out, rows, cols, ld, row0, thr24, seed, int_mode, sm_count(device), (cudaStream_t)stream),
+           "gen_dense");
+        g_launches.fetch_add(1);
+    });
+}
+
+macko_status macko_gen_vector(int device, uint16_t* d_out, uint64_t n, uint64_t seed, int int_mode, void* stream) {
+    return guarded([&] {
+        if (!d_out) fail(MACKO_EINVAL, "null output");
+        DeviceGuard g(device);
+        ck(mk::launch_gen_vector(d_out, n, seed, int_mode, (cudaStream_t)stream), "gen_vector");
+        g_launches.fetch_add(1);
+    });
+}
+
+macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, uint64_t* r0, uint64_t* r1) {
+    return guarded([&] {
+        if (!r0 || !r1 || n_shards == 0 || shard >= n_shards) fail(MACKO_EINVAL, "bad shard request");
+        *r0 = rows * shard / n_shards;
+        *r1 = rows * (shard + 1) / n_shards;
+    });
+}
+
+macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out) {
+    return guarded([&] {
+        if (!m || !out) fail(MACKO_EINVAL, "null argument");
+        out->grid = (uint32_t)m->grid;
+        out->block = mk::kSpmvWarpsPerCta * mk::kWarp;
+        out->warps = m->n_chunks;
+        out->ctas_per_sm = (uint32_t)m->ctas_per_sm;
+        out->n_split_rows = m->n_split;
+        out->x_in_smem = m->x_in_smem;
+        out->n_units = m->n_units;
+        out->smem_bytes = m->smem;
+    });
+}
+
+}  // extern "C"

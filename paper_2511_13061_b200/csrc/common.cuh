@@ -1,0 +1,90 @@
+// common.cuh — device helpers shared by the MACKO sm_100a kernels.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mk {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// One SpMV step = 32 lanes x 8 elements (512 B of values + 128 B of 4-bit
+// deltas per warp).  A "unit" is kUnitSteps steps; lane accumulators are tree-reduced once per
+// unit and unit sums are added sequentially into the row sum.
+constexpr int kEltsPerLane = 8;
+constexpr int kStepElts = kWarp * kEltsPerLane;  // 256
+constexpr int kUnitSteps = 4;
+constexpr int kUnitElts = kStepElts * kUnitSteps;  // 1024
+
+// ---- streaming loads (read-once data: no L1 allocation) ----
+__device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u32(const void* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// acc += a*b with a, b fp16 and acc fp32 (single rounding; the f16xf16 product is exact in
+// fp32, so this equals the reference's fp32 multiply-then-add).  SASS: FHFMA.
+__device__ __forceinline__ float fma_f16f16f32(uint16_t a, uint16_t b, float acc) {
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a), "h"(b));
+    return acc;
+}
+
+__device__ __forceinline__ uint16_t f32_to_f16_rn(float v) {
+    return __half_as_ushort(__float2half_rn(v));
+}
+
+// Inclusive warp scan (Algorithm 1 structure).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+    for (int off = 1; off < kWarp; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, v, off);
+        if (lane >= off) v += t;
+    }
+    return v;
+}
+
+// xor-butterfly sum; every lane ends with identical bits (oracle lane_tree()).
+__device__ __forceinline__ float warp_tree_sum(float v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+}
+
+// ---- counter-hash generator (oracle/macko_oracle.c mix64 / mo_gen_value) ----
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint16_t gen_value(uint64_t seed, uint64_t idx, uint32_t thr24, int int_mode) {
+    const uint64_t h = mix64(seed ^ (idx * 0xD1B54A32D192ED03ull));
+    if ((uint32_t)(h >> 40) >= thr24) return 0;
+    if (int_mode) {
+        int v = (int)(h & 15u) - 8;
+        if (v >= 0) v += 1;
+        return f32_to_f16_rn((float)v);
+    }
+    uint32_t u = (uint32_t)(h & 0xFFFFu);
+    if (u == 32768u) u = 32769u;
+    return f32_to_f16_rn((float)((int32_t)u - 32768) * (1.0f / 32768.0f));
+}
+
+__device__ __forceinline__ uint16_t gen_vector_value(uint64_t seed, uint64_t i, int int_mode) {
+    const uint64_t h = mix64(seed ^ (i * 0xD1B54A32D192ED03ull));
+    if (int_mode) return f32_to_f16_rn((float)((int)((h & 0xFFFFu) % 17u) - 8));
+    return f32_to_f16_rn((float)((int32_t)(h & 0xFFFFu) - 32768) * (1.0f / 32768.0f));
+}
+
+}  // namespace mk

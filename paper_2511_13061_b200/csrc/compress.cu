@@ -1,0 +1,259 @@
+// compress.cu — dense fp16 -> MACKO on the GPU (bit-exact with the reference encoder).
+//
+// Reference semantics: csr_from_dense + macko_from_csr (convert.hpp:8-16):
+// drop ±0, per row prev = -1, pad with (+0, 2^b) while c - prev > 2^b, no trailing pads,
+// codeword delta-1 LSB-first (bitpack.cpp:18-32), 16-byte zero tails (matrix.hpp:57-59).
+//
+// Parallel form (probe A.4): padding depends only on adjacent nonzeros.  For a
+// zero column c with previous nonzero p (or -1) it is a padding entry iff (c - p) % 2^b == 0
+// and a nonzero exists after c; a nonzero at c has delta ((c - p - 1) mod 2^b) + 1.  So every
+// column is classified independently once p (an exclusive max-scan over the row) and the last
+// nonzero column of the row are known:
+//   K2a count_rows : warp per row, 16-B loads, nonzero bitmask, max-scan -> entries per row
+//   K2b scan_counts: one CTA, exclusive u64 scan -> u32 row pointers + pad_nnz (overflow check)
+//   K2c emit_rows  : warp per row, same classification, lane-prefix of entry counts -> values
+//                    (2-B stores) and codewords staged per warp in shared memory and written as
+//                    whole 32-bit words; words shared with a neighbouring row use atomicOr.
+#include "common.cuh"
+#include "compress.cuh"
+
+#include <algorithm>
+
+namespace mk {
+
+namespace {
+
+constexpr int kCompressWarpsPerCta = 8;
+constexpr int kStageWords = 72;  // 256 entries x 8 bits = 64 words, + carry + spill
+
+// Loads the 8 columns [c, c+8) of a dense row (zeros past `cols`) and returns their nonzero
+// mask; `h` receives the raw fp16 bits.
+__device__ __forceinline__ uint32_t load8(const uint16_t* row, uint32_t c, uint32_t cols, bool vec_ok, uint16_t h[8]) {
+    if (vec_ok && c + 8 <= cols) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + c));
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            h[2 * m] = (uint16_t)(w[m] & 0xFFFFu);
+            h[2 * m + 1] = (uint16_t)(w[m] >> 16);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) h[k] = (c + k < cols) ? row[c + k] : (uint16_t)0;
+    }
+    uint32_t nz = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nz |= ((h[k] & 0x7FFFu) != 0 ? 1u : 0u) << k;
+    return nz;
+}
+
+// Exclusive max-scan of "last nonzero column" over lanes, seeded with `carry`; returns the
+// previous nonzero column before this lane's first column and updates carry to the warp max.
+__device__ __forceinline__ int prev_nonzero(int lane_last, int lane, int& carry) {
+    int incl = lane_last;
+#pragma unroll
+    for (int off = 1; off < kWarp; off <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl = max(incl, t);
+    }
+    int excl = __shfl_up_sync(kFull, incl, 1);
+    excl = lane == 0 ? carry : max(excl, carry);
+    carry = max(carry, __shfl_sync(kFull, incl, kWarp - 1));
+    return excl;
+}
+
+__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
+    count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
+               uint32_t* counts, int32_t* lastcol) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t nwarps = gridDim.x * kCompressWarpsPerCta;
+    const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
+    for (uint32_t r = blockIdx.x * kCompressWarpsPerCta + (threadIdx.x >> 5); r < rows; r += nwarps) {
+        const uint16_t* row = dense + (uint64_t)r * ld;
+        int carry = -1;
+        uint32_t cnt = 0;
+        for (uint32_t c0 = 0; c0 < cols; c0 += kWarp * 8) {
+            const uint32_t c = c0 + 8u * lane;
+            uint16_t h[8];
+            uint32_t nz = load8(row, c, cols, vec_base, h);
+            const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
+            int p = prev_nonzero(lane_last, lane, carry);
+            cnt += __popc(nz);
+            while (nz) {
+                const int k = __ffs(nz) - 1;
+                nz &= nz - 1;
+                const int cc = (int)c + k;
+                cnt += (uint32_t)(cc - p - 1) >> bits;
+                p = cc;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+        if (lane == 0) {
+            counts[r] = cnt;
+            lastcol[r] = carry;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) scan_counts(const uint32_t* counts, uint32_t rows, uint32_t* row_ptrs,
+                                                     unsigned long long* total) {
+    __shared__ unsigned long long warp_sums[32];
+    const uint32_t t = threadIdx.x, nt = blockDim.x;
+    const uint64_t lo = (uint64_t)rows * t / nt, hi = (uint64_t)rows * (t + 1) / nt;
+    unsigned long long mine = 0;
+    for (uint64_t i = lo; i < hi; ++i) mine += counts[i];
+    // block exclusive scan of `mine`
+    const int lane = t & 31, wid = t >> 5;
+    unsigned long long incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long v = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long ws = lane < (int)(nt / 32) ? warp_sums[lane] : 0ull;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long v = __shfl_up_sync(kFull, ws, off);
+            if (lane >= off) ws += v;
+        }
+        warp_sums[lane] = ws;
+    }
+    __syncthreads();
+    unsigned long long run = incl - mine + (wid ? warp_sums[wid - 1] : 0ull);
+    if (t == 0) row_ptrs[0] = 0;
+    for (uint64_t i = lo; i < hi; ++i) {
+        run += counts[i];
+        row_ptrs[i + 1] = (uint32_t)run;
+    }
+    if (t == nt - 1) *total = run;
+}
+
+__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
+    emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
+              const uint32_t* row_ptrs, const int32_t* lastcol, uint16_t* values, uint32_t* delta_words) {
+    __shared__ uint32_t stage_all[kCompressWarpsPerCta][kStageWords];
+    const int lane = threadIdx.x & (kWarp - 1);
+    uint32_t* stage = stage_all[threadIdx.x >> 5];
+    const uint32_t nwarps = gridDim.x * kCompressWarpsPerCta;
+    const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
+    const uint32_t maxd = 1u << bits;
+    for (uint32_t r = blockIdx.x * kCompressWarpsPerCta + (threadIdx.x >> 5); r < rows; r += nwarps) {
+        const uint32_t start = row_ptrs[r], end = row_ptrs[r + 1];
+        if (start == end) continue;
+        const int L = lastcol[r];
+        const uint16_t* row = dense + (uint64_t)r * ld;
+        const uint64_t row_first_word = ((uint64_t)start * bits) >> 5;
+        const bool first_shared = (((uint64_t)start * bits) & 31u) != 0;
+        for (int i = lane; i < kStageWords; i += kWarp) stage[i] = 0;
+        __syncwarp();
+        int carry = -1;
+        uint32_t emitted = 0;                // entries of this row written so far
+        uint64_t wb = row_first_word;        // global word held in stage[0]
+        for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kWarp * 8) {
+            const uint32_t c = c0 + 8u * lane;
+            uint16_t h[8];
+            const uint32_t nz = load8(row, c, cols, vec_base, h);
+            const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
+            int p = prev_nonzero(lane_last, lane, carry);
+            // classify the lane's 8 columns: nonzero entry, padding entry or nothing
+            uint32_t em = 0;       // entry mask
+            uint32_t code[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int cc = (int)c + k;
+                code[k] = 0;
+                if ((nz >> k) & 1u) {
+                    code[k] = (uint32_t)(cc - p - 1) & (maxd - 1);  // delta - 1
+                    em |= 1u << k;
+                    p = cc;
+                } else if (cc < L && cc > p && (((uint32_t)(cc - p)) & (maxd - 1)) == 0) {
+                    code[k] = maxd - 1;
+                    em |= 1u << k;
+                }
+            }
+            const uint32_t n = __popc(em);
+            uint64_t codes = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if ((em >> k) & 1u) codes |= (uint64_t)code[k] << (__popc(em & ((1u << k) - 1u)) * bits);
+            // lane offsets of the entries
+            uint32_t incl = n;
+#pragma unroll
+            for (int off = 1; off < kWarp; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += t;
+            }
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            const uint64_t o = (uint64_t)start + emitted + (incl - n);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if ((em >> k) & 1u) values[o + __popc(em & ((1u << k) - 1u))] = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;
+            if (n) {
+                const uint64_t bit0 = o * bits;
+                const uint32_t sh = (uint32_t)(bit0 & 31u);
+                const int rel = (int)((bit0 >> 5) - wb);
+                // codes (<= 64 bits) shifted left by sh (< 32) spans up to 3 words
+                const uint64_t lo64 = codes << sh;
+                const uint32_t hi_bits = sh ? (uint32_t)(codes >> (64 - sh)) : 0u;
+                atomicOr(&stage[rel], (uint32_t)lo64);
+                if ((uint32_t)(lo64 >> 32)) atomicOr(&stage[rel + 1], (uint32_t)(lo64 >> 32));
+                if (hi_bits) atomicOr(&stage[rel + 2], hi_bits);
+            }
+            __syncwarp();
+            emitted += tot;
+            const uint64_t end_bit = ((uint64_t)start + emitted) * bits;
+            const uint64_t wend = end_bit >> 5;  // words [wb, wend) are complete
+            const int ncomplete = (int)(wend - wb);
+            for (int i = lane; i < ncomplete; i += kWarp) {
+                const uint64_t gw = wb + i;
+                if (gw == row_first_word && first_shared)
+                    atomicOr(delta_words + gw, stage[i]);
+                else
+                    delta_words[gw] = stage[i];
+            }
+            __syncwarp();
+            // move the partial word (and anything after it, all zero) to the front
+            const uint32_t partial = (end_bit & 31u) ? stage[ncomplete] : 0u;
+            __syncwarp();
+            for (int i = lane; i < kStageWords; i += kWarp) stage[i] = 0;
+            __syncwarp();
+            if (lane == 0) stage[0] = partial;
+            __syncwarp();
+            wb = wend;
+        }
+        // the row's last partial word is shared with the next row
+        if (lane == 0 && ((((uint64_t)start + emitted) * bits) & 31u)) atomicOr(delta_words + wb, stage[0]);
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
+                              uint32_t* counts, int32_t* lastcol, int sms, cudaStream_t s) {
+    const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
+    if (grid > 0) count_rows<<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_counts(const uint32_t* counts, uint32_t rows, uint32_t* row_ptrs, unsigned long long* total,
+                               cudaStream_t s) {
+    scan_counts<<<1, 1024, 0, s>>>(counts, rows, row_ptrs, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
+                             const uint32_t* row_ptrs, const int32_t* lastcol, uint16_t* values, uint32_t* delta_words,
+                             int sms, cudaStream_t s) {
+    const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
+    if (grid > 0)
+        emit_rows<<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values,
+                                                                delta_words);
+    return cudaGetLastError();
+}
+
+}  // namespace mk

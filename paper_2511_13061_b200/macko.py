@@ -1,0 +1,227 @@
+"""Host-side mirror of the reference MACKO interface over the B200 C-ABI.
+
+Reference operation (file:line)                     -> here (runs on the GPU through libmacko_cuda)
+  csr_from_dense + macko_from_csr (convert.hpp:8-16) -> macko_from_dense(dense)        [GPU compressor]
+  MackoMatrix (matrix.hpp:57-81)                     -> MackoMatrix (host arrays, same bytes)
+  host MackoMatrix as SpMV operand                   -> DeviceMatrix.upload(MackoMatrix)
+  reference_spmv / warp_spmv       -> spmv(dm, x)                    [sm_100a kernel]
+  validate_macko (convert.hpp:25-27)                 -> DeviceMatrix.validate()
+  macko_values_bytes / macko_delta_bytes (matrix.hpp:77-81) -> values_bytes / delta_bytes
+  spmv_traffic                     -> DeviceMatrix.traffic_bytes
+
+Arguments follow the reference's meaning (fp16 payloads as raw uint16 bits, b_delta in
+{1,2,4,8}, row pointers as u32 element offsets) and its error behaviour (ValueError for
+std::invalid_argument, FormatError / IoError / InfeasibleError for the reference exceptions).
+Device tensors may be torch CUDA tensors; streams default to torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import CudaError, FormatError, InfeasibleError, IoError, check  # noqa: F401
+
+
+def values_bytes(pad_nnz: int) -> int:
+    """macko_values_bytes (matrix.hpp:77)."""
+    return (pad_nnz * 2 + 15) // 16 * 16
+
+
+def delta_bytes(pad_nnz: int, b_delta: int) -> int:
+    """macko_delta_bytes (matrix.hpp:78-81)."""
+    return ((pad_nnz * b_delta + 7) // 8 + 15) // 16 * 16
+
+
+@dataclass
+class MackoMatrix:
+    """Host copy of the reference MackoMatrix (matrix.hpp:57-67): identical byte layout."""
+
+    rows: int
+    cols: int
+    b_delta: int
+    values: np.ndarray      # uint16 fp16 bits, >= pad_nnz (16-byte zero tail)
+    packed_deltas: np.ndarray  # uint8, >= ceil(pad_nnz*b_delta/8) (16-byte zero tail)
+    row_pointers: np.ndarray   # uint32, rows+1
+
+    def pad_nnz(self) -> int:
+        return int(self.row_pointers[-1]) if len(self.row_pointers) else 0
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover - torch absent
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+def _ptr(t) -> int:
+    """Device pointer of a torch tensor (or an int pointer)."""
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+class DeviceMatrix:
+    """A MACKO matrix resident in HBM (opaque macko_dev_matrix handle)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        info = _lib.DevInfo()
+        check(_lib.load().macko_dev_get_info(self._h, C.byref(info)))
+        self.info = info
+
+    # -- construction -----------------------------------------------------------------------
+    @classmethod
+    def upload(cls, m: MackoMatrix, device: int = 0, stream=None) -> "DeviceMatrix":
+        vals = np.ascontiguousarray(m.values, np.uint16)
+        dl = np.ascontiguousarray(m.packed_deltas, np.uint8)
+        rp = np.ascontiguousarray(m.row_pointers, np.uint32)
+        h = C.c_void_p()
+        check(_lib.load().macko_dev_upload(device, m.rows, m.cols, m.b_delta, vals.ctypes.data, len(vals),
+                                           dl.ctypes.data, len(dl), rp.ctypes.data, _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_dense(cls, dense, rows: int | None = None, cols: int | None = None, ld: int | None = None,
+                   b_delta: int = 4, device: int | None = None, stream=None) -> "DeviceMatrix":
+        """GPU compressor from a dense fp16 device tensor (torch, row-major) or device pointer."""
+        if not isinstance(dense, int):
+            rows, cols = dense.shape
+            ld = dense.stride(0)
+            if device is None:
+                device = dense.device.index
+        if device is None:
+            device = 0
+        h = C.c_void_p()
+        check(_lib.load().macko_dev_from_dense(device, _ptr(dense), rows, cols, ld if ld is not None else cols, b_delta,
+                                               _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    # -- properties -------------------------------------------------------------------------
+    @property
+    def rows(self) -> int:
+        return self.info.rows
+
+    @property
+    def cols(self) -> int:
+        return self.info.cols
+
+    @property
+    def pad_nnz(self) -> int:
+        return self.info.pad_nnz
+
+    @property
+    def b_delta(self) -> int:
+        return self.info.b_delta
+
+    @property
+    def traffic_bytes(self) -> int:
+        """Algorithmic bytes of one SpMV (spmv_traffic)."""
+        return self.info.traffic_bytes
+
+    def launch_info(self) -> _lib.LaunchInfo:
+        li = _lib.LaunchInfo()
+        check(_lib.load().macko_dev_launch_info(self._h, C.byref(li)))
+        return li
+
+    # -- operations -------------------------------------------------------------------------
+    def download(self, stream=None) -> MackoMatrix:
+        i = self.info
+        vals = np.zeros(i.values_bytes // 2, np.uint16)
+        dl = np.zeros(i.delta_bytes, np.uint8)
+        rp = np.zeros(i.rows + 1, np.uint32)
+        check(_lib.load().macko_dev_download(self._h, vals.ctypes.data if vals.size else None,
+                                             dl.ctypes.data if dl.size else None, rp.ctypes.data, _stream_ptr(stream)))
+        return MackoMatrix(i.rows, i.cols, i.b_delta, vals, dl, rp)
+
+    def validate(self, stream=None) -> None:
+        check(_lib.load().macko_dev_validate(self._h, _stream_ptr(stream)))
+
+    def spmv_into(self, x, y, stream=None) -> None:
+        """y = A*x with device tensors / pointers (stream-ordered, asynchronous)."""
+        check(_lib.load().macko_dev_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+
+    def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
+        """End-to-end call with host buffers (H2D x, kernel, D2H y, synchronise)."""
+        x = np.ascontiguousarray(x, np.uint16)
+        if x.shape != (self.cols,):
+            raise ValueError("dimension mismatch: x must have cols entries")
+        if y is None:
+            y = np.zeros(self.rows, np.uint16)
+        check(_lib.load().macko_spmv_host(self._h, x.ctypes.data, y.ctypes.data, _stream_ptr(stream)))
+        return y
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().macko_dev_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def macko_from_dense(dense, b_delta: int = 4, stream=None) -> DeviceMatrix:
+    """csr_from_dense + macko_from_csr (convert.hpp:8-16) on the GPU."""
+    return DeviceMatrix.from_dense(dense, b_delta=b_delta, stream=stream)
+
+
+def spmv(m: DeviceMatrix, x, y=None, stream=None):
+    """reference_spmv on the GPU for a torch CUDA fp16/uint16 vector x."""
+    import torch
+
+    if x.shape[-1] != m.cols:
+        raise ValueError("dimension mismatch: x must have cols entries")
+    if y is None:
+        y = torch.empty(m.rows, dtype=x.dtype, device=x.device)
+    m.spmv_into(x, y, stream)
+    return y
+
+
+def density_threshold(d: float) -> int:
+    return _lib.load().macko_density_threshold(d)
+
+
+def gen_dense(out, rows: int, cols: int, density: float, seed: int, int_mode: bool = False, row0: int = 0,
+              device: int | None = None, stream=None) -> None:
+    """Fill a device fp16 matrix with the counter-hash generator (bit-identical to the oracle)."""
+    ld = out.stride(0) if not isinstance(out, int) else cols
+    if device is None:
+        device = out.device.index if not isinstance(out, int) else 0
+    check(_lib.load().macko_gen_dense(device, _ptr(out), rows, cols, ld, row0, density_threshold(density), seed,
+                                      int(int_mode), _stream_ptr(stream)))
+
+
+def gen_vector(out, n: int, seed: int, int_mode: bool = False, device: int | None = None, stream=None) -> None:
+    if device is None:
+        device = out.device.index if not isinstance(out, int) else 0
+    check(_lib.load().macko_gen_vector(device, _ptr(out), n, seed, int(int_mode), _stream_ptr(stream)))
+
+
+def shard_rows(rows: int, n_shards: int, shard: int) -> tuple[int, int]:
+    """Contiguous equal-row slab [r0, r1) of shard `shard`."""
+    r0, r1 = C.c_uint64(), C.c_uint64()
+    check(_lib.load().macko_shard_rows(rows, n_shards, shard, C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
+def kernel_launches() -> int:
+    return _lib.load().macko_kernel_launches()
+
+
+def version() -> str:
+    return _lib.load().macko_version().decode()

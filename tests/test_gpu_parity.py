@@ -1,0 +1,278 @@
+"""GPU parity: libmacko_cuda.so on cuda:0 against the CPU oracle and the reference's golden
+vectors.  Every check here goes through the C-ABI (ctypes) — the same entry points a C/C++
+caller binds.
+
+Bars: format (values / packed deltas / row pointers, tails included) bit-exact; y bit-exact in
+integer mode; in float mode bit-exact against the oracle's emulation of the kernel's summation
+order (oracle mo_b200_order_spmv) AND within the stated bound of the sequential reference.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2511_13061_b200 import macko as M
+from tests.helpers import UNIT_STEPS, to_dev, to_host_u16, within_bound
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_encode(dense: np.ndarray, bits: int = 4, ld_pad: int = 0) -> M.DeviceMatrix:
+    R, C = dense.shape
+    if ld_pad:
+        buf = np.zeros((R, C + ld_pad), np.uint16)
+        buf[:, :C] = dense
+        t = to_dev(buf)[:, :C]
+    else:
+        t = to_dev(dense)
+    dm = M.DeviceMatrix.from_dense(t, b_delta=bits)
+    torch.cuda.synchronize()
+    return dm
+
+
+def assert_same_format(dm: M.DeviceMatrix, m: O.Macko, ctx=""):
+    h = dm.download()
+    assert np.array_equal(h.row_pointers, m.row_ptrs), ctx
+    assert np.array_equal(h.values, m.values), ctx
+    assert np.array_equal(h.packed_deltas, m.deltas), ctx
+
+
+def gpu_spmv(dm: M.DeviceMatrix, x: np.ndarray) -> np.ndarray:
+    xd = to_dev(x)
+    y = M.spmv(dm, xd)
+    torch.cuda.synchronize()
+    return to_host_u16(y)
+
+
+def check_y(dense, m, x, y, int_mode, ctx=""):
+    if int_mode:
+        assert np.array_equal(y, O.reference_spmv(m, x, 8)), ctx
+    else:
+        assert np.array_equal(y, O.b200_order_spmv(m, x, UNIT_STEPS)), ctx
+        assert within_bound(dense, x, y, O.reference_spmv(m, x, 8)), ctx
+
+
+# ------------------------------------------------------------------------------ generator
+@pytest.mark.parametrize("int_mode", [False, True])
+def test_generator_bit_identical(cuda, int_mode):
+    for R, C, d, row0 in ((7, 37, 0.5, 0), (64, 4096, 0.3, 5), (3, 8, 1.0, 1000), (16, 1000, 0.05, 0)):
+        t = torch.empty((R, C + 3), dtype=torch.float16, device=cuda)[:, :C]
+        M.gen_dense(t, R, C, d, seed=42, int_mode=int_mode, row0=row0)
+        ref = O.gen_dense(row0 + R, C, d, 42, int_mode)[row0:]
+        assert np.array_equal(to_host_u16(t), ref)
+    v = torch.empty(12345, dtype=torch.float16, device=cuda)
+    M.gen_vector(v, 12345, 7, int_mode)
+    assert np.array_equal(to_host_u16(v), O.gen_vector(12345, 7, int_mode))
+
+
+# ------------------------------------------------------------------------------ compressor
+def test_compressor_reproduces_reference_golden_vectors(cuda, golden):
+    for name, c in golden.items():
+        bits = int(c["bits"])
+        dm = gpu_encode(c["dense"], bits)
+        h = dm.download()
+        assert np.array_equal(h.row_pointers, c["row_ptrs"]), name
+        assert np.array_equal(h.values, c["values"]), name
+        assert np.array_equal(h.packed_deltas, c["deltas"]), name
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_compressor_random_vs_oracle(cuda, bits):
+    rng = np.random.default_rng(bits)
+    shapes = [(1, 1), (1, 7), (2, 9), (31, 255), (33, 257), (5, 4096), (200, 513), (64, 1000)]
+    for i, (R, C) in enumerate(shapes):
+        for d in (0.0, 0.02, 0.3, 0.5, 0.9, 1.0):
+            A = O.gen_dense(R, C, d, 1000 * bits + i, bool(i & 1))
+            if R > 4:
+                A[rng.integers(0, R, R // 4)] = 0  # empty rows
+            m = O.encode_dense(A, bits)
+            dm = gpu_encode(A, bits, ld_pad=(i % 3) * 8 + (i % 2))
+            assert_same_format(dm, m, (R, C, d, bits))
+
+
+def test_compressor_edge_patterns(cuda):
+    one = O.float_to_half(1.0)
+    pats = []
+    wc = O.gen_worst_case(64, 4096 * 17 // 16, 16)  # Eq. 9 worst case
+    pats.append(wc)
+    r = np.zeros((3, 64), np.uint16)
+    r[0, 63] = one      # single far nonzero (3 pads)
+    r[1, 0] = one       # first column
+    r[2, 16] = 0x8000   # -0 is dropped
+    pats.append(r)
+    alt = np.zeros((4, 300), np.uint16)
+    alt[:, ::17] = one  # every gap forces exactly one pad
+    pats.append(alt)
+    for A in pats:
+        for bits in (1, 2, 4, 8):
+            assert_same_format(gpu_encode(A, bits), O.encode_dense(A, bits), (A.shape, bits))
+
+
+# ------------------------------------------------------------------------------ SpMV
+def test_spmv_on_reference_golden_vectors(cuda, golden):
+    n = 0
+    for name, c in golden.items():
+        if int(c["bits"]) != 4:
+            continue
+        m = O.Macko(c["dense"].shape[0], c["dense"].shape[1], 4, c["values"], c["deltas"], c["row_ptrs"])
+        dm = M.DeviceMatrix.upload(M.MackoMatrix(m.rows, m.cols, 4, m.values, m.deltas, m.row_ptrs))
+        y = gpu_spmv(dm, c["x"])
+        if name.endswith("_int") or name in ("fig3_b2", "diag", "zeros3", "dense16", "single31", "worst1x32"):
+            assert np.array_equal(y, c["y_ref"]), name
+        else:
+            assert np.array_equal(y, O.b200_order_spmv(m, c["x"], UNIT_STEPS)), name
+            assert within_bound(c["dense"], c["x"], y, c["y_ref"]), name
+        n += 1
+    assert n >= 10
+
+
+@pytest.mark.parametrize("int_mode", [True, False])
+def test_spmv_random_shapes(cuda, int_mode):
+    cases = [
+        (1, 1, 1.0), (1, 5, 0.5), (3, 16, 1.0), (7, 37, 0.5), (100, 100, 0.3), (33, 4097, 0.5),
+        (1, 65536, 0.5),       # one long row split across many warps
+        (2, 30000, 0.9),       # two long rows
+        (17, 20000, 0.02),     # sparse long rows (padding heavy)
+        (512, 300, 0.7), (4096, 64, 0.5),  # many short rows
+        (1000, 2048, 0.0),     # all-empty matrix
+    ]
+    for i, (R, C, d) in enumerate(cases):
+        A = O.gen_dense(R, C, d, 77 + i, int_mode)
+        if R >= 8:
+            A[3::7] = 0
+        x = O.gen_vector(C, 99 + i, int_mode)
+        m = O.encode_dense(A)
+        dm = gpu_encode(A)
+        y = gpu_spmv(dm, x)
+        check_y(A, m, x, y, int_mode, (R, C, d))
+
+
+@pytest.mark.parametrize("R,C", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_spmv_llama_shapes(cuda, R, C):
+    for int_mode in (False, True):
+        t = torch.empty((R, C), dtype=torch.float16, device=cuda)
+        M.gen_dense(t, R, C, 0.5, seed=5, int_mode=int_mode)
+        dm = M.DeviceMatrix.from_dense(t)
+        A = O.gen_dense(R, C, 0.5, 5, int_mode)
+        m = O.encode_dense(A)
+        assert_same_format(dm, m, (R, C))
+        x = O.gen_vector(C, 6, int_mode)
+        check_y(A, m, x, gpu_spmv(dm, x), int_mode, (R, C))
+
+
+@pytest.mark.parametrize("density", [0.5, 0.7, 0.3, 0.1])
+def test_spmv_headline_shape(cuda, density):
+    """36864 x 12288 (BASELINE.json configs[1]); full size at 50 %, 4608-row slabs elsewhere."""
+    R, C = (36864, 12288) if density == 0.5 else (4608, 12288)
+    t = torch.empty((R, C), dtype=torch.float16, device=cuda)
+    M.gen_dense(t, R, C, density, seed=1234)
+    dm = M.DeviceMatrix.from_dense(t)
+    A = O.gen_dense(R, C, density, 1234)
+    m = O.encode_dense(A)
+    assert_same_format(dm, m, (R, C, density))
+    x = O.gen_vector(C, 4321)
+    y = gpu_spmv(dm, x)
+    assert np.array_equal(y, O.b200_order_spmv(m, x, UNIT_STEPS))
+    assert within_bound(A, x, y, O.reference_spmv(m, x, 16))
+
+
+def test_spmv_x_in_global_memory_path(cuda):
+    # C beyond the shared-memory staging limit: x is gathered through L1
+    R, C = 6, 120000
+    A = O.gen_dense(R, C, 0.3, 3)
+    x = O.gen_vector(C, 4)
+    dm = gpu_encode(A)
+    assert dm.launch_info().x_in_smem == 0
+    check_y(A, O.encode_dense(A), x, gpu_spmv(dm, x), False)
+
+
+def test_spmv_deterministic_graph_and_unaligned_x(cuda):
+    A = O.gen_dense(3000, 5000, 0.5, 8)
+    x = O.gen_vector(5000, 9)
+    dm = gpu_encode(A)
+    assert dm.launch_info().n_split_rows > 0
+    y0 = gpu_spmv(dm, x)
+    for _ in range(5):
+        assert np.array_equal(gpu_spmv(dm, x), y0)
+    # x at a 2-byte (not 16-byte) aligned address
+    xb = to_dev(np.concatenate([np.zeros(1, np.uint16), x]))
+    y = torch.empty(3000, dtype=torch.float16, device=cuda)
+    dm.spmv_into(xb[1:], y)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host_u16(y), y0)
+    # CUDA graph capture / replay (split-row counters must reset between launches)
+    xd = to_dev(x)
+    yg = torch.empty(3000, dtype=torch.float16, device=cuda)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        dm.spmv_into(xd, yg, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            dm.spmv_into(xd, yg, stream=s)
+    for _ in range(3):
+        yg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host_u16(yg), y0)
+
+
+def test_spmv_host_buffers_e2e(cuda):
+    A = O.gen_dense(777, 3333, 0.5, 10)
+    x = O.gen_vector(3333, 11)
+    dm = gpu_encode(A)
+    y_host = dm.spmv_host(x)
+    assert np.array_equal(y_host, gpu_spmv(dm, x))
+    assert np.array_equal(y_host, O.b200_order_spmv(O.encode_dense(A), x, UNIT_STEPS))
+
+
+def test_split_points_do_not_change_y(cuda):
+    # the summation order is a function of the row only: a slab encoded and multiplied on its
+    # own gives bit-identical rows to the full matrix (row-sharding invariance)
+    R, C = 4096, 8192
+    A = O.gen_dense(R, C, 0.5, 21)
+    x = O.gen_vector(C, 22)
+    y_full = gpu_spmv(gpu_encode(A), x)
+    for r0, r1 in ((0, 512), (512, 1536), (1536, 4096), (100, 101)):
+        assert np.array_equal(gpu_spmv(gpu_encode(A[r0:r1]), x), y_full[r0:r1])
+    # device-generated slab with a row offset equals the slab of the global matrix
+    t = torch.empty((1024, C), dtype=torch.float16, device=cuda)
+    M.gen_dense(t, 1024, C, 0.5, seed=21, row0=2048)
+    dm = M.DeviceMatrix.from_dense(t)
+    assert np.array_equal(gpu_spmv(dm, x), y_full[2048:3072])
+
+
+def test_error_behaviour(cuda):
+    A = O.gen_dense(4, 64, 0.5, 1)
+    m = O.encode_dense(A)
+    # corrupt: decoded column walks past C -> FormatError
+    bad = m.deltas.copy()
+    bad[: m.pad_nnz // 2] = 0xFF
+    with pytest.raises(M.FormatError):
+        M.DeviceMatrix.upload(M.MackoMatrix(4, 64, 4, m.values, bad, m.row_ptrs))
+    # -0 padding value -> FormatError
+    v = m.values.copy()
+    v[np.flatnonzero(v[: m.pad_nnz] == 0)[:1]] = 0x8000
+    if (v != m.values).any():
+        with pytest.raises(M.FormatError):
+            M.DeviceMatrix.upload(M.MackoMatrix(4, 64, 4, v, m.deltas, m.row_ptrs))
+    # b_delta = 2: the compressor supports it, the SpMV kernel is b_delta = 4 only
+    dm2 = gpu_encode(A, 2)
+    with pytest.raises(ValueError, match="b_delta"):
+        gpu_spmv(dm2, O.gen_vector(64, 1))
+    dm = gpu_encode(A)
+    with pytest.raises(ValueError):
+        M.spmv(dm, torch.zeros(65, dtype=torch.float16, device=cuda))
+
+
+def test_native_library_is_the_code_path(cuda):
+    before = M.kernel_launches()
+    A = O.gen_dense(64, 512, 0.5, 1)
+    dm = gpu_encode(A)
+    gpu_spmv(dm, O.gen_vector(512, 2))
+    assert M.kernel_launches() > before
+    import re
+
+    maps = open("/proc/self/maps").read()
+    assert re.search(r"libmacko_cuda\.so", maps)
