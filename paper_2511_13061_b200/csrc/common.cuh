@@ -15,8 +15,8 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // unit and unit sums are added sequentially into the row sum.
 constexpr int kEltsPerLane = 8;
 constexpr int kStepElts = kWarp * kEltsPerLane;  // 256
-constexpr int kUnitSteps = 4;
-constexpr int kUnitElts = kStepElts * kUnitSteps;  // 1024
+constexpr int kUnitSteps = 8;
+constexpr int kUnitElts = kStepElts * kUnitSteps;  // 2048
 
 // ---- streaming loads (read-once data: no L1 allocation) ----
 __device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {

@@ -1,7 +1,7 @@
 """Shared test helpers (tolerance bound, torch <-> numpy fp16-bit transfers)."""
 import numpy as np
 
-UNIT_STEPS = 4  # csrc/common.cuh kUnitSteps: the kernel's canonical reduction granularity
+UNIT_STEPS = 8  # csrc/common.cuh kUnitSteps: the kernel's canonical reduction granularity
 
 
 def tol_bound(dense: np.ndarray, x: np.ndarray, y_ref: np.ndarray):
