@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="also report 30/50/70/90 %% sparsity and Llama shapes")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
+    p.add_argument("--x-mode", type=int, default=-1, help="x staging: -1 auto, 0 global, 1 fp16 smem, 2 pair smem")
+    p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs per SM (0 = occupancy maximum)")
     return p.parse_args()
 
 
@@ -207,6 +209,8 @@ def main():
     dm = M.DeviceMatrix.from_dense(dense)
     torch.cuda.synchronize()
     compress_s = time.perf_counter() - t0
+    if args.x_mode != -1 or args.ctas:
+        dm.configure(args.x_mode, args.ctas)
     x = torch.empty(C, dtype=torch.float16, device=dev)
     M.gen_vector(x, C, seed=SEED_X)
     y = torch.empty(R, dtype=torch.float16, device=dev)

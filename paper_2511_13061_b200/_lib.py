@@ -18,7 +18,7 @@ EXPORTS = (
     "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_get_info",
     "macko_dev_download", "macko_dev_spmv", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
-    "macko_dev_launch_info", "macko_kernel_launches",
+    "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
 )
 
 
@@ -106,6 +106,8 @@ def load() -> C.CDLL:
     L.macko_shard_rows.argtypes = [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]
     L.macko_dev_launch_info.restype = st
     L.macko_dev_launch_info.argtypes = [vp, C.POINTER(LaunchInfo)]
+    L.macko_dev_configure.restype = st
+    L.macko_dev_configure.argtypes = [vp, i32, i32, vp]
     L.macko_kernel_launches.restype = u64
     _lib = L
     return L

@@ -88,7 +88,8 @@ uint64_t values_bytes(uint64_t pad_nnz) { return align_up(pad_nnz * 2, 16); }
 uint64_t delta_bytes(uint64_t pad_nnz, unsigned bits) { return align_up((pad_nnz * bits + 7) / 8, 16); }
 
 constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (element equivalents)
-constexpr size_t kMaxSmemX = 200 * 1024;    // x staged in shared memory up to 100k columns
+constexpr size_t kMaxSmemX = 200 * 1024;     // fp16 x table in shared memory up to 100k columns
+constexpr size_t kMaxSmemPair = 100 * 1024;  // (x[c], x[c+1]) pair table while two CTAs still fit
 
 }  // namespace
 
@@ -102,7 +103,9 @@ struct macko_dev_matrix {
     DevBuf<uint32_t> row_ptrs;
     std::vector<uint32_t> h_row_ptrs;
     // SpMV plan
-    bool x_in_smem = false;
+    int x_mode = 1;             // 0 global x, 1 fp16 smem table, 2 pair smem table
+    int force_x_mode = -1;      // macko_dev_configure overrides (-1 / 0 = automatic)
+    int force_ctas = 0;
     size_t smem = 0;
     int grid = 0, ctas_per_sm = 0;
     uint32_t n_chunks = 0, n_split = 0;
@@ -131,10 +134,15 @@ void check_bits(uint32_t bits) {
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
-    m->x_in_smem = m->cols * 2 <= kMaxSmemX;
-    m->smem = m->x_in_smem ? align_up(m->cols * 2, 16) : 0;
-    ck(spmv_occupancy(m->x_in_smem, m->smem, &m->ctas_per_sm), "spmv occupancy");
+    if (m->force_x_mode >= 0) {
+        m->x_mode = m->force_x_mode;
+    } else {
+        m->x_mode = (m->cols * 4 <= kMaxSmemPair) ? 2 : (m->cols * 2 <= kMaxSmemX) ? 1 : 0;
+    }
+    m->smem = m->x_mode == 2 ? align_up(m->cols * 4, 16) : m->x_mode == 1 ? align_up(m->cols * 2, 16) : 0;
+    ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
+    if (m->force_ctas > 0) m->ctas_per_sm = std::min(m->ctas_per_sm, m->force_ctas);
     m->grid = m->sms * m->ctas_per_sm;
     const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
     m->n_chunks = W;
@@ -419,7 +427,7 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.rows = (uint32_t)m->rows;
         a.cols = (uint32_t)m->cols;
         a.plan = m->plan;
-        ck(mk::launch_spmv(a, m->grid, m->x_in_smem, m->smem, (cudaStream_t)stream), "macko_spmv launch");
+        ck(mk::launch_spmv(a, m->grid, m->x_mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
         g_launches.fetch_add(1);
     });
 }
@@ -484,6 +492,20 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
     });
 }
 
+macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        if (x_mode < -1 || x_mode > 2) fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 2");
+        if (x_mode == 2 && m->cols * 4 > 220 * 1024) fail(MACKO_EINVAL, "pair table does not fit shared memory");
+        if (x_mode == 1 && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
+        if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
+        DeviceGuard g(m->device);
+        m->force_x_mode = x_mode;
+        m->force_ctas = ctas_per_sm;
+        build_plan(m, (cudaStream_t)stream);
+    });
+}
+
 macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out) {
     return guarded([&] {
         if (!m || !out) fail(MACKO_EINVAL, "null argument");
@@ -492,7 +514,7 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
         out->warps = m->n_chunks;
         out->ctas_per_sm = (uint32_t)m->ctas_per_sm;
         out->n_split_rows = m->n_split;
-        out->x_in_smem = m->x_in_smem;
+        out->x_in_smem = (uint32_t)m->x_mode;
         out->n_units = m->n_units;
         out->smem_bytes = m->smem;
     });

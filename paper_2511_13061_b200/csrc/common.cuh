@@ -53,6 +53,18 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
+// Same scan with the shuffle's in-range predicate driving a predicated add (2 SASS per level).
+__device__ __forceinline__ uint32_t warp_incl_scan_p(uint32_t v) {
+    asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 2, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 4, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 8, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 16, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
+        : "+r"(v));
+    return v;
+}
+
 // xor-butterfly sum; every lane ends with identical bits (oracle lane_tree()).
 __device__ __forceinline__ float warp_tree_sum(float v) {
 #pragma unroll

@@ -10,14 +10,15 @@
 //     one integer multiply (byte-SIMD), then Algorithm 1's shfl_up scan gives the lane offset
 //     and lane 31's total advances the running column.  Two steps share one
 //     scan (their lane sums packed into 16-bit halves);
-//   * x is staged once per CTA in shared memory and gathered per element (PRMT + LEA + LDS);
-//     the multiply-add is FHFMA (fp16 x fp16 -> fp32 accumulate, exact product);
+//   * x is staged once per CTA in shared memory — as (x[c], x[c+1]) pairs when it fits, so an
+//     element pair at adjacent columns costs one 32-bit gather — and gathered per element; the
+//     multiply-add is FHFMA (fp16 x fp16 -> fp32 accumulate, exact product);
 //   * B200 work distribution and latency hiding: a persistent grid (SM count x occupancy)
 //     where every warp owns an equal-weight contiguous range of 2048-element units (a static
-//     plan built once per matrix).  A warp's loads run two step-pairs ahead of its math across
-//     row boundaries (a 4-slot register ring fed by a loader cursor that replays the same walk),
-//     so 4 x 640 B per warp are in flight.  Rows cut between warps are finished by the
-//     last-arriving warp, which adds the per-unit partials in unit order.
+//     plan built once per matrix).  A warp's loads run a step-pair ahead of its math across
+//     row boundaries (a 4-slot register ring fed by a loader cursor that replays the same
+//     walk).  Rows cut between warps are finished by the last-arriving warp, which adds the
+//     per-unit partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
 // lanes once per unit (8 steps), sequential over units — mirrored bit-exactly by
 // oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  The order depends on a row's elements
@@ -42,6 +43,20 @@ __device__ __forceinline__ uint16_t lds_u16(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// x gather: kXMode 0 = global (L1), 1 = fp16 table in smem, 2 = pair table in smem
+template <int kXMode>
+__device__ __forceinline__ uint16_t xget(uint32_t xs_addr, const uint16_t* __restrict__ xg, int col) {
+    if constexpr (kXMode == 0) return __ldg(xg + col);
+    if constexpr (kXMode == 1) return lds_u16(xs_addr + 2u * (uint32_t)col);
+    return lds_u16(xs_addr + 4u * (uint32_t)col);
+}
+
 // valid-element mask of a lane whose first element is eb, for the row [s, e)
 __device__ __forceinline__ uint32_t lane_mask(uint32_t eb, uint32_t s, uint32_t e) {
     const int klo = (int)max(0LL, min(8LL, (long long)s - (long long)eb));
@@ -50,14 +65,15 @@ __device__ __forceinline__ uint32_t lane_mask(uint32_t eb, uint32_t s, uint32_t 
 }
 
 struct Dec {
-    uint32_t even, odd, local;  // inclusive in-lane column offsets (bytes m), lane total
+    uint32_t even, odd, dh, local;  // in-lane inclusive column offsets (byte m), odd deltas, total
 };
 
 // Nibbles -> byte deltas -> in-lane inclusive prefixes.  Masked elements get delta 0.
+template <bool kMasked>
 __device__ __forceinline__ Dec decode(uint32_t d, uint32_t vm) {
     uint32_t dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
     uint32_t dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
-    if (vm != 0xFFu) {
+    if constexpr (kMasked) {
         uint32_t me = 0, mo = 0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -68,30 +84,60 @@ __device__ __forceinline__ Dec decode(uint32_t d, uint32_t vm) {
         dh &= mo;
     }
     const uint32_t pp = (dl + dh) * 0x01010101u;
-    return Dec{pp - dh, pp, pp >> 24};
+    return Dec{pp - dh, pp, dh, pp >> 24};
 }
 
-// The 8 gathers + FHFMAs of one lane step.  `cb` = column of the element before the lane's
-// first element; col(k) = cb + in-lane prefix byte.
-template <bool kEdge, bool kSmemX>
-__device__ __forceinline__ float fma_step(float acc, const uint4& v, const Dec& dc, int cb, uint32_t vm,
-                                          uint32_t xs_addr, const uint16_t* xg) {
+// 8 gathers + FHFMAs of one unmasked lane step.  cb = column before the lane's first element.
+template <int kXMode>
+__device__ __forceinline__ float fma_fast(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
+                                          const uint16_t* __restrict__ xg) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    const uint32_t base = xs_addr + 2u * (uint32_t)cb;
+    // shared address of column cb: per element one PRMT (byte extract) + one LEA
+    uint32_t base = xs_addr + (uint32_t)cb * (kXMode == 2 ? 4u : 2u);
+    asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + (b << k) a single LEA per element
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         uint16_t v0, v1;
         split_halves(w[m], v0, v1);
         const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
         const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
-        if (!kEdge || ((vm >> (2 * m)) & 1u)) {
-            const uint16_t x0 = kSmemX ? lds_u16(base + 2u * b0) : __ldg(xg + cb + (int)b0);
+        if constexpr (kXMode == 2) {
+            // (x[c0], x[c0+1]) in one gather; the odd element reuses the high half when adjacent
+            const uint32_t xa = lds_u32(base + (b0 << 2));
+            acc = fma_f16f16f32(v0, (uint16_t)(xa & 0xFFFFu), acc);
+            if (((dc.dh >> (8 * m)) & 0xFFu) == 1u)
+                acc = fma_f16f16f32(v1, (uint16_t)(xa >> 16), acc);
+            else
+                acc = fma_f16f16f32(v1, lds_u16(base + (b1 << 2)), acc);
+        } else if constexpr (kXMode == 1) {
+            const uint16_t x0 = lds_u16(base + (b0 << 1));
+            const uint16_t x1 = lds_u16(base + (b1 << 1));
             acc = fma_f16f16f32(v0, x0, acc);
-        }
-        if (!kEdge || ((vm >> (2 * m + 1)) & 1u)) {
-            const uint16_t x1 = kSmemX ? lds_u16(base + 2u * b1) : __ldg(xg + cb + (int)b1);
+            acc = fma_f16f16f32(v1, x1, acc);
+        } else {
+            const int c0 = cb + (int)b0, c1 = cb + (int)b1;
+            const uint16_t x0 = xget<kXMode>(xs_addr, xg, c0);
+            const uint16_t x1 = xget<kXMode>(xs_addr, xg, c1);
+            acc = fma_f16f16f32(v0, x0, acc);
             acc = fma_f16f16f32(v1, x1, acc);
         }
+    }
+    return acc;
+}
+
+// Masked lane step (row edges): only valid elements gather and accumulate.
+template <int kXMode>
+__device__ __forceinline__ float fma_masked(float acc, const uint4& v, const Dec& dc, int cb, uint32_t vm,
+                                            uint32_t xs_addr, const uint16_t* __restrict__ xg) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        uint16_t v0, v1;
+        split_halves(w[m], v0, v1);
+        if ((vm >> (2 * m)) & 1u)
+            acc = fma_f16f16f32(v0, xget<kXMode>(xs_addr, xg, cb + (int)__byte_perm(dc.even, 0u, 0x4440u + m)), acc);
+        if ((vm >> (2 * m + 1)) & 1u)
+            acc = fma_f16f16f32(v1, xget<kXMode>(xs_addr, xg, cb + (int)__byte_perm(dc.odd, 0u, 0x4440u + m)), acc);
     }
     return acc;
 }
@@ -108,12 +154,11 @@ struct Slot {
     uint32_t d;
 };
 
-__device__ __forceinline__ bool loader_next(Loader& c, const uint32_t* __restrict__ rp, const uint16_t* __restrict__ values,
-                                            const uint8_t* __restrict__ deltas, int lane, Slot& sl) {
+__device__ __forceinline__ bool loader_next(Loader& c, const SpmvArgs& a, int lane, Slot& sl) {
     while (c.t >= c.tend) {
         if (c.units_left == 0) return false;
         ++c.r;
-        const uint32_t s = __ldg(rp + c.r), e = __ldg(rp + c.r + 1);
+        const uint32_t s = __ldg(a.row_ptrs + c.r), e = __ldg(a.row_ptrs + c.r + 1);
         if (s == e) {
             c.units_left -= 1;
             continue;
@@ -127,12 +172,11 @@ __device__ __forceinline__ bool loader_next(Loader& c, const uint32_t* __restric
         c.tend = min(T, nu * kUnitSteps);
     }
     const uint32_t eb = c.al + c.t * kStepElts + 8u * lane;
+    sl.v = make_uint4(0, 0, 0, 0);
+    sl.d = 0;
     if (eb < c.e) {
-        sl.v = ldg_stream_v4(values + eb);
-        sl.d = ldg_stream_u32(deltas + eb / 2);
-    } else {
-        sl.v = make_uint4(0, 0, 0, 0);
-        sl.d = 0;
+        sl.v = ldg_stream_v4(a.values + eb);
+        sl.d = ldg_stream_u32(a.deltas + eb / 2);
     }
     ++c.t;
     return true;
@@ -149,15 +193,8 @@ struct RowState {
     float acc, row_acc;
 };
 
-struct Ctx {
-    const SpmvArgs* a;
-    uint32_t w;
-    int lane;
-};
-
-// Set up the piece of row rs.r starting at unit j0 (units_left = chunk units not yet placed).
-__device__ __forceinline__ void begin_piece(RowState& rs, const Ctx& cx, uint32_t j0, int colbase) {
-    const SpmvArgs& a = *cx.a;
+// Set up the piece of row rs.r starting at unit j0.
+__device__ __forceinline__ void begin_piece(RowState& rs, const SpmvArgs& a, uint32_t w, uint32_t j0, int colbase) {
     rs.s = __ldg(a.row_ptrs + rs.r);
     rs.e = __ldg(a.row_ptrs + rs.r + 1);
     rs.al = rs.s & ~7u;
@@ -172,7 +209,7 @@ __device__ __forceinline__ void begin_piece(RowState& rs, const Ctx& cx, uint32_
     rs.sid = -1;
     rs.slot = 0;
     if (rs.split) {
-        rs.sid = rs.first_row ? a.plan.chunk_sid[2 * cx.w] : a.plan.chunk_sid[2 * cx.w + 1];
+        rs.sid = rs.first_row ? a.plan.chunk_sid[2 * w] : a.plan.chunk_sid[2 * w + 1];
         rs.slot = a.plan.split_slot[rs.sid];
     }
     rs.col_base = colbase;
@@ -181,126 +218,46 @@ __device__ __forceinline__ void begin_piece(RowState& rs, const Ctx& cx, uint32_
 }
 
 // Finish the current piece (write y or hand the split row to its last arrival).
-__device__ __forceinline__ void finish_piece(RowState& rs, const Ctx& cx) {
-    const SpmvArgs& a = *cx.a;
-    const SpmvPlanDev& P = a.plan;
-    if (!rs.split) {
-        if (cx.lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
-        return;
-    }
+__device__ __noinline__ void finish_split(uint32_t r, uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot,
+                                          int32_t sid, float row_acc, const SpmvPlanDev P, uint16_t* y, int lane) {
     uint32_t last = 0;
-    if (cx.lane == 0) {
-        if (rs.j0 == 0) P.partials[rs.slot + (rs.tend - 1) / kUnitSteps] = rs.row_acc;
+    if (lane == 0) {
+        if (j0 == 0) P.partials[slot + (tend - 1) / kUnitSteps] = row_acc;
         __threadfence();
-        const uint32_t prev = atomicAdd(P.counters + rs.sid, 1u);
-        last = prev + 1 == P.split_pieces[rs.sid];
+        const uint32_t prev = atomicAdd(P.counters + sid, 1u);
+        last = prev + 1 == P.split_pieces[sid];
     }
     last = __shfl_sync(kFull, last, 0);
-    if (last && cx.lane == 0) {
+    if (last && lane == 0) {
         __threadfence();
-        const uint32_t f = P.split_first[rs.sid];
-        float tot = __ldcg(P.partials + rs.slot + f - 1);
-        for (uint32_t q = f; q < rs.n_r; ++q) tot += __ldcg(P.partials + rs.slot + q);
-        a.y[rs.r] = f32_to_f16_rn(tot);
-        P.counters[rs.sid] = 0;  // ready for the next launch (stream order)
+        const uint32_t f = P.split_first[sid];
+        float tot = __ldcg(P.partials + slot + f - 1);
+        for (uint32_t q = f; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
+        y[r] = f32_to_f16_rn(tot);
+        P.counters[sid] = 0;  // ready for the next launch (stream order)
     }
 }
 
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
 // when the chunk is exhausted.
-__device__ __forceinline__ bool next_piece(RowState& rs, const Ctx& cx) {
+__device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint32_t w, int lane) {
     for (;;) {
         if (rs.units_left == 0) return false;
         ++rs.r;
         rs.first_row = false;
-        begin_piece(rs, cx, 0, -1);
+        begin_piece(rs, a, w, 0, -1);
         if (rs.T) return true;
-        if (cx.lane == 0) cx.a->y[rs.r] = 0;  // empty row: fp16(+0.0)
+        if (lane == 0) a.y[rs.r] = 0;  // empty row: fp16(+0.0)
     }
 }
 
-// Account one finished step at (old) index t: unit end -> tree reduce; piece end -> finish.
-// Returns false when the chunk is exhausted.
-__device__ __forceinline__ bool end_step(RowState& rs, const Ctx& cx) {
-    ++rs.t;
-    if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
-        const float red = warp_tree_sum(rs.acc);
-        rs.acc = 0.0f;
-        if (rs.split && rs.j0 > 0 && cx.lane == 0) cx.a->plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
-        rs.row_acc += red;
-    }
-    if (rs.t == rs.tend) {
-        finish_piece(rs, cx);
-        return next_piece(rs, cx);
-    }
-    return true;
-}
-
-__device__ __forceinline__ bool is_edge(const RowState& rs, uint32_t t) { return t == 0 || t + 1 == rs.T; }
-
-// One step alone (used when a pair would cross a piece boundary).
-template <bool kSmemX>
-__device__ __forceinline__ bool single_step(RowState& rs, const Ctx& cx, const Slot& sl, uint32_t xs_addr) {
-    const uint32_t eb = rs.al + rs.t * kStepElts + 8u * cx.lane;
-    const bool edge = is_edge(rs, rs.t);
-    const uint32_t vm = edge ? lane_mask(eb, rs.s, rs.e) : 0xFFu;
-    const Dec dc = decode(sl.d, vm);
-    const uint32_t incl = warp_incl_scan(dc.local, cx.lane);
-    const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-    const int cb = rs.col_base + (int)(incl - dc.local);
-    if (edge)
-        rs.acc = fma_step<true, kSmemX>(rs.acc, sl.v, dc, cb, vm, xs_addr, cx.a->x);
-    else
-        rs.acc = fma_step<false, kSmemX>(rs.acc, sl.v, dc, cb, vm, xs_addr, cx.a->x);
-    rs.col_base += (int)tot;
-    return end_step(rs, cx);
-}
-
-// Two consecutive steps of the same piece with one packed scan.
-template <bool kSmemX>
-__device__ __forceinline__ bool pair_step(RowState& rs, const Ctx& cx, const Slot& A, const Slot& B, uint32_t xs_addr) {
-    const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * cx.lane;
-    const uint32_t ebB = ebA + kStepElts;
-    const bool eA = is_edge(rs, rs.t), eB = is_edge(rs, rs.t + 1);
-    const uint32_t vmA = eA ? lane_mask(ebA, rs.s, rs.e) : 0xFFu;
-    const uint32_t vmB = eB ? lane_mask(ebB, rs.s, rs.e) : 0xFFu;
-    const Dec dA = decode(A.d, vmA), dB = decode(B.d, vmB);
-    const uint32_t packed = dA.local | (dB.local << 16);
-    const uint32_t incl = warp_incl_scan(packed, cx.lane);
-    const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-    const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-    const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-    if (eA)
-        rs.acc = fma_step<true, kSmemX>(rs.acc, A.v, dA, cbA, vmA, xs_addr, cx.a->x);
-    else
-        rs.acc = fma_step<false, kSmemX>(rs.acc, A.v, dA, cbA, vmA, xs_addr, cx.a->x);
-    rs.col_base += (int)(tot & 0xFFFFu);
-    if (!end_step(rs, cx)) return false;  // cannot happen: B is in the same piece
-    if (eB)
-        rs.acc = fma_step<true, kSmemX>(rs.acc, B.v, dB, cbB, vmB, xs_addr, cx.a->x);
-    else
-        rs.acc = fma_step<false, kSmemX>(rs.acc, B.v, dB, cbB, vmB, xs_addr, cx.a->x);
-    rs.col_base += (int)(tot >> 16);
-    return end_step(rs, cx);
-}
-
-// Consume a loaded pair (A always valid; B valid iff hasB).
-template <bool kSmemX>
-__device__ __forceinline__ bool consume(RowState& rs, const Ctx& cx, const Slot& A, const Slot& B, bool hasB,
-                                        uint32_t xs_addr) {
-    if (hasB && rs.t + 1 < rs.tend) return pair_step<kSmemX>(rs, cx, A, B, xs_addr);
-    if (!single_step<kSmemX>(rs, cx, A, xs_addr)) return false;
-    if (hasB) return single_step<kSmemX>(rs, cx, B, xs_addr);
-    return true;
-}
-
-template <bool kSmemX>
+template <int kXMode>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
     macko_spmv_b4(const SpmvArgs a) {
     extern __shared__ __align__(16) uint16_t xs[];
     const int lane = threadIdx.x & (kWarp - 1);
-    if constexpr (kSmemX) {
-        const uint32_t C = a.cols;
+    const uint32_t C = a.cols;
+    if constexpr (kXMode == 1) {
         if ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0) {
             const uint32_t nv = C / 8;
             for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
@@ -309,42 +266,94 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
         } else {
             for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) xs[i] = a.x[i];
         }
-        __syncthreads();
+    } else if constexpr (kXMode == 2) {
+        uint32_t* xp = reinterpret_cast<uint32_t*>(xs);
+        for (uint32_t i = threadIdx.x; i < C; i += blockDim.x)
+            xp[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
     }
-    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+    if constexpr (kXMode != 0) __syncthreads();
+    uint32_t xs_addr;
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(xs_addr) : "l"(xs));
     const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + (threadIdx.x >> 5);
-    const SpmvPlanDev& P = a.plan;
-    const uint32_t u0 = P.chunk_unit[w], u_end = P.chunk_unit[w + 1];
+    const uint32_t u0 = a.plan.chunk_unit[w], u_end = a.plan.chunk_unit[w + 1];
     if (u0 >= u_end) return;
-    const Ctx cx{&a, w, lane};
 
     RowState rs;
-    rs.r = P.chunk_row[w];
+    rs.r = a.plan.chunk_row[w];
     rs.units_left = u_end - u0;
     rs.first_row = true;
-    const uint32_t j0 = P.chunk_j[w];
-    begin_piece(rs, cx, j0, j0 ? P.chunk_colbase[w] : -1);
-
+    const uint32_t j0 = a.plan.chunk_j[w];
+    begin_piece(rs, a, w, j0, j0 ? a.plan.chunk_colbase[w] : -1);
     Loader ld{rs.r, rs.t, rs.tend, rs.al, rs.e, rs.units_left};
     if (rs.T == 0) {
         if (lane == 0) a.y[rs.r] = 0;
-        if (!next_piece(rs, cx)) return;
+        if (!next_piece(rs, a, w, lane)) return;
     }
 
     Slot s0, s1, s2, s3;
-    bool k0 = loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s0);
-    bool k1 = k0 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s1);
-    bool k2 = k1 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s2);
-    bool k3 = k2 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s3);
-    for (;;) {
-        if (!k0) break;
-        if (!consume<kSmemX>(rs, cx, s0, s1, k1, xs_addr)) break;
-        k0 = k3 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s0);
-        k1 = k0 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s1);
-        if (!k2) break;
-        if (!consume<kSmemX>(rs, cx, s2, s3, k3, xs_addr)) break;
-        k2 = k1 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s2);
-        k3 = k2 && loader_next(ld, a.row_ptrs, a.values, a.deltas, lane, s3);
+    bool k0 = loader_next(ld, a, lane, s0);
+    bool k1 = k0 && loader_next(ld, a, lane, s1);
+    bool k2 = k1 && loader_next(ld, a, lane, s2);
+    bool k3 = k2 && loader_next(ld, a, lane, s3);
+    while (k0) {
+        // -- consume one step (piece end) or an aligned pair of steps of the same piece
+        const bool hasB = k1 && rs.t + 1 < rs.tend;
+        const bool edge = rs.t == 0 || rs.t + (hasB ? 2u : 1u) >= rs.T;
+        const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * lane;
+        if (!edge) {
+            const Dec dA = decode<false>(s0.d, 0xFFu), dB = decode<false>(s1.d, 0xFFu);
+            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+            rs.acc = fma_fast<kXMode>(rs.acc, s0.v, dA, cbA, xs_addr, a.x);
+            rs.acc = fma_fast<kXMode>(rs.acc, s1.v, dB, cbB, xs_addr, a.x);
+            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+        } else {
+            const uint32_t vmA = lane_mask(ebA, rs.s, rs.e);
+            const uint32_t vmB = hasB ? lane_mask(ebA + kStepElts, rs.s, rs.e) : 0u;
+            const Dec dA = decode<true>(s0.d, vmA), dB = decode<true>(s1.d, vmB);
+            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+            rs.acc = fma_masked<kXMode>(rs.acc, s0.v, dA, cbA, vmA, xs_addr, a.x);
+            if (hasB) rs.acc = fma_masked<kXMode>(rs.acc, s1.v, dB, cbB, vmB, xs_addr, a.x);
+            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+        }
+        rs.t += hasB ? 2u : 1u;
+        // -- unit end (pairs start at even t, so a unit boundary never falls inside a pair)
+        if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
+            const float red = warp_tree_sum(rs.acc);
+            rs.acc = 0.0f;
+            if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
+            rs.row_acc += red;
+        }
+        // -- refill the ring
+        if (hasB) {
+            s0 = s2;
+            s1 = s3;
+            k0 = k2;
+            k1 = k3;
+            k2 = k1 && loader_next(ld, a, lane, s2);
+        } else {
+            s0 = s1;
+            s1 = s2;
+            s2 = s3;
+            k0 = k1;
+            k1 = k2;
+            k2 = k3;
+        }
+        k3 = k2 && loader_next(ld, a, lane, s3);
+        // -- piece end
+        if (rs.t == rs.tend) {
+            if (!rs.split) {
+                if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
+            } else {
+                finish_split(rs.r, rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, a.y, lane);
+            }
+            if (!next_piece(rs, a, w, lane)) break;
+        }
     }
 }
 
@@ -372,20 +381,31 @@ __global__ void plan_colbase_kernel(const uint8_t* deltas, const uint32_t* row_p
 
 }  // namespace
 
-cudaError_t spmv_occupancy(bool x_in_smem, size_t smem, int* ctas_per_sm) {
-    if (x_in_smem) {
-        cudaError_t e = cudaFuncSetAttribute(macko_spmv_b4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<true>, kSpmvWarpsPerCta * kWarp, smem);
+cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
+    const int threads = kSpmvWarpsPerCta * kWarp;
+    cudaError_t e = cudaSuccess;
+    switch (x_mode) {
+        case 2:
+            e = cudaFuncSetAttribute(macko_spmv_b4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<2>, threads, smem);
+            return e;
+        case 1:
+            e = cudaFuncSetAttribute(macko_spmv_b4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<1>, threads, smem);
+            return e;
+        default:
+            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<0>, threads, 0);
     }
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<false>, kSpmvWarpsPerCta * kWarp, 0);
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, bool x_in_smem, size_t smem, cudaStream_t s) {
-    if (x_in_smem)
-        macko_spmv_b4<true><<<grid, kSpmvWarpsPerCta * kWarp, smem, s>>>(a);
+cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s) {
+    const int threads = kSpmvWarpsPerCta * kWarp;
+    if (x_mode == 2)
+        macko_spmv_b4<2><<<grid, threads, smem, s>>>(a);
+    else if (x_mode == 1)
+        macko_spmv_b4<1><<<grid, threads, smem, s>>>(a);
     else
-        macko_spmv_b4<false><<<grid, kSpmvWarpsPerCta * kWarp, 0, s>>>(a);
+        macko_spmv_b4<0><<<grid, threads, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -35,8 +35,9 @@ struct SpmvArgs {
 constexpr int kSpmvWarpsPerCta = 16;
 
 // Launchers (return cudaGetLastError()).
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, bool x_in_smem, size_t smem, cudaStream_t s);
-cudaError_t spmv_occupancy(bool x_in_smem, size_t smem, int* ctas_per_sm);
+// x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table
+cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s);
+cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, const uint32_t* row_ptrs, const uint32_t* chunk_row,
                                 const uint32_t* chunk_j, int32_t* chunk_colbase, uint32_t n_chunks,
                                 cudaStream_t s);

@@ -136,6 +136,11 @@ class DeviceMatrix:
         check(_lib.load().macko_dev_launch_info(self._h, C.byref(li)))
         return li
 
+    def configure(self, x_mode: int = -1, ctas_per_sm: int = 0, stream=None) -> None:
+        """Re-plan the launch (x staging 0/1/2 or -1 = auto; CTA cap or 0 = auto).  y is
+        bit-identical for every setting."""
+        check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
+
     # -- operations -------------------------------------------------------------------------
     def download(self, stream=None) -> MackoMatrix:
         i = self.info

@@ -218,6 +218,21 @@ def test_spmv_deterministic_graph_and_unaligned_x(cuda):
         assert np.array_equal(to_host_u16(yg), y0)
 
 
+def test_plan_and_x_staging_do_not_change_y(cuda):
+    # SPEC.md:279 determinism across parallelism degree: every launch plan (CTAs per SM ->
+    # number of warps -> where rows are cut) and every x staging mode gives identical bits.
+    for R, C, d in ((3000, 5000, 0.5), (64, 20000, 0.3), (4096, 4096, 0.9)):
+        A = O.gen_dense(R, C, d, 31)
+        x = O.gen_vector(C, 32)
+        dm = gpu_encode(A)
+        y0 = gpu_spmv(dm, x)
+        assert np.array_equal(y0, O.b200_order_spmv(O.encode_dense(A), x, UNIT_STEPS))
+        for x_mode in (0, 1, 2):
+            for ctas in (1, 2, 0):
+                dm.configure(x_mode, ctas)
+                assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, x_mode, ctas)
+
+
 def test_spmv_host_buffers_e2e(cuda):
     A = O.gen_dense(777, 3333, 0.5, 10)
     x = O.gen_vector(3333, 11)
