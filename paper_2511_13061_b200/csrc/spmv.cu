@@ -154,7 +154,8 @@ struct Slot {
     uint32_t d;
 };
 
-__device__ __forceinline__ bool loader_next(Loader& c, const SpmvArgs& a, int lane, Slot& sl) {
+// Advance to the next non-empty row piece (rare path).  False when the chunk is exhausted.
+__device__ __forceinline__ bool loader_advance(Loader& c, const SpmvArgs& a) {
     while (c.t >= c.tend) {
         if (c.units_left == 0) return false;
         ++c.r;
@@ -171,14 +172,27 @@ __device__ __forceinline__ bool loader_next(Loader& c, const SpmvArgs& a, int la
         c.t = 0;
         c.tend = min(T, nu * kUnitSteps);
     }
+    return true;
+}
+
+// Load the next aligned step pair (t, t+1) of the walk; the second step is a phantom (zeros,
+// no load) when the piece has an odd number of steps.
+__device__ __forceinline__ bool loader_pair(Loader& c, const SpmvArgs& a, int lane, Slot& A, Slot& B) {
+    if (c.t >= c.tend && !loader_advance(c, a)) return false;
     const uint32_t eb = c.al + c.t * kStepElts + 8u * lane;
-    sl.v = make_uint4(0, 0, 0, 0);
-    sl.d = 0;
+    A.v = make_uint4(0, 0, 0, 0);
+    A.d = 0;
+    B.v = make_uint4(0, 0, 0, 0);
+    B.d = 0;
     if (eb < c.e) {
-        sl.v = ldg_stream_v4(a.values + eb);
-        sl.d = ldg_stream_u32(a.deltas + eb / 2);
+        A.v = ldg_stream_v4(a.values + eb);
+        A.d = ldg_stream_u32(a.deltas + eb / 2);
     }
-    ++c.t;
+    if (c.t + 1 < c.tend && eb + kStepElts < c.e) {
+        B.v = ldg_stream_v4(a.values + eb + kStepElts);
+        B.d = ldg_stream_u32(a.deltas + (eb + kStepElts) / 2);
+    }
+    c.t += 2;
     return true;
 }
 
@@ -252,7 +266,7 @@ __device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint
 }
 
 template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
     macko_spmv_b4(const SpmvArgs a) {
     extern __shared__ __align__(16) uint16_t xs[];
     const int lane = threadIdx.x & (kWarp - 1);
@@ -290,15 +304,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
         if (!next_piece(rs, a, w, lane)) return;
     }
 
-    Slot s0, s1, s2, s3;
-    bool k0 = loader_next(ld, a, lane, s0);
-    bool k1 = k0 && loader_next(ld, a, lane, s1);
-    bool k2 = k1 && loader_next(ld, a, lane, s2);
-    bool k3 = k2 && loader_next(ld, a, lane, s3);
-    while (k0) {
-        // -- consume one step (piece end) or an aligned pair of steps of the same piece
-        const bool hasB = k1 && rs.t + 1 < rs.tend;
-        const bool edge = rs.t == 0 || rs.t + (hasB ? 2u : 1u) >= rs.T;
+    // Ring of three step pairs: (s0, s1) is consumed while (s2, s3) and (s4, s5) are in flight.
+    Slot s0, s1, s2, s3, s4, s5;
+    bool kx = loader_pair(ld, a, lane, s0, s1);
+    bool ky = kx && loader_pair(ld, a, lane, s2, s3);
+    bool kz = ky && loader_pair(ld, a, lane, s4, s5);
+    while (kx) {
+        // -- consume the aligned pair (t, t+1) of the current piece; t+1 may be a phantom
+        const bool hasB = rs.t + 1 < rs.tend;
+        const bool edge = !hasB || rs.t == 0 || rs.t + 2u >= rs.T;
         const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * lane;
         if (!edge) {
             const Dec dA = decode<false>(s0.d, 0xFFu), dB = decode<false>(s1.d, 0xFFu);
@@ -318,10 +332,10 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
             const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
             const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
             rs.acc = fma_masked<kXMode>(rs.acc, s0.v, dA, cbA, vmA, xs_addr, a.x);
-            if (hasB) rs.acc = fma_masked<kXMode>(rs.acc, s1.v, dB, cbB, vmB, xs_addr, a.x);
+            rs.acc = fma_masked<kXMode>(rs.acc, s1.v, dB, cbB, vmB, xs_addr, a.x);
             rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
         }
-        rs.t += hasB ? 2u : 1u;
+        rs.t = min(rs.t + 2u, rs.tend);
         // -- unit end (pairs start at even t, so a unit boundary never falls inside a pair)
         if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
             const float red = warp_tree_sum(rs.acc);
@@ -330,21 +344,13 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp)
             rs.row_acc += red;
         }
         // -- refill the ring
-        if (hasB) {
-            s0 = s2;
-            s1 = s3;
-            k0 = k2;
-            k1 = k3;
-            k2 = k1 && loader_next(ld, a, lane, s2);
-        } else {
-            s0 = s1;
-            s1 = s2;
-            s2 = s3;
-            k0 = k1;
-            k1 = k2;
-            k2 = k3;
-        }
-        k3 = k2 && loader_next(ld, a, lane, s3);
+        s0 = s2;
+        s1 = s3;
+        s2 = s4;
+        s3 = s5;
+        kx = ky;
+        ky = kz;
+        kz = ky && loader_pair(ld, a, lane, s4, s5);
         // -- piece end
         if (rs.t == rs.tend) {
             if (!rs.split) {

@@ -32,7 +32,8 @@ struct SpmvArgs {
     SpmvPlanDev plan;
 };
 
-constexpr int kSpmvWarpsPerCta = 16;
+constexpr int kSpmvWarpsPerCta = 8;
+constexpr int kSpmvMinCtasPerSm = 3;  // 24 resident warps, <= 85 registers
 
 // Launchers (return cudaGetLastError()).
 // x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table
