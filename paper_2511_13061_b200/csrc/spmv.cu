@@ -304,62 +304,65 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
         if (!next_piece(rs, a, w, lane)) return;
     }
 
-    // Ring of three step pairs: (s0, s1) is consumed while (s2, s3) and (s4, s5) are in flight.
-    Slot s0, s1, s2, s3, s4, s5;
-    bool kx = loader_pair(ld, a, lane, s0, s1);
-    bool ky = kx && loader_pair(ld, a, lane, s2, s3);
-    bool kz = ky && loader_pair(ld, a, lane, s4, s5);
-    while (kx) {
-        // -- consume the aligned pair (t, t+1) of the current piece; t+1 may be a phantom
+    // Consume the aligned pair (t, t+1) of the current piece (t+1 may be a phantom); returns
+    // false when the chunk is exhausted.
+    auto consume = [&](const Slot& A, const Slot& B) -> bool {
         const bool hasB = rs.t + 1 < rs.tend;
         const bool edge = !hasB || rs.t == 0 || rs.t + 2u >= rs.T;
-        const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * lane;
         if (!edge) {
-            const Dec dA = decode<false>(s0.d, 0xFFu), dB = decode<false>(s1.d, 0xFFu);
+            const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
             const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
             const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
             const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
             const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_fast<kXMode>(rs.acc, s0.v, dA, cbA, xs_addr, a.x);
-            rs.acc = fma_fast<kXMode>(rs.acc, s1.v, dB, cbB, xs_addr, a.x);
+            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
+            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
             rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
         } else {
+            const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * lane;
             const uint32_t vmA = lane_mask(ebA, rs.s, rs.e);
             const uint32_t vmB = hasB ? lane_mask(ebA + kStepElts, rs.s, rs.e) : 0u;
-            const Dec dA = decode<true>(s0.d, vmA), dB = decode<true>(s1.d, vmB);
+            const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
             const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
             const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
             const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
             const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_masked<kXMode>(rs.acc, s0.v, dA, cbA, vmA, xs_addr, a.x);
-            rs.acc = fma_masked<kXMode>(rs.acc, s1.v, dB, cbB, vmB, xs_addr, a.x);
+            rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
+            rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
             rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
         }
         rs.t = min(rs.t + 2u, rs.tend);
-        // -- unit end (pairs start at even t, so a unit boundary never falls inside a pair)
+        // unit end (pairs start at even t, so a unit boundary never falls inside a pair)
         if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
             const float red = warp_tree_sum(rs.acc);
             rs.acc = 0.0f;
             if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
             rs.row_acc += red;
         }
-        // -- refill the ring
-        s0 = s2;
-        s1 = s3;
-        s2 = s4;
-        s3 = s5;
-        kx = ky;
-        ky = kz;
-        kz = ky && loader_pair(ld, a, lane, s4, s5);
-        // -- piece end
-        if (rs.t == rs.tend) {
+        if (rs.t == rs.tend) {  // piece end
             if (!rs.split) {
                 if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
             } else {
                 finish_split(rs.r, rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, a.y, lane);
             }
-            if (!next_piece(rs, a, w, lane)) break;
+            return next_piece(rs, a, w, lane);
         }
+        return true;
+    };
+
+    // Ring of three step pairs, unrolled so no slot ever moves between registers: pair P_i is
+    // consumed while P_{i+1}, P_{i+2} are in flight, then refilled with P_{i+3}.
+    Slot p0a, p0b, p1a, p1b, p2a, p2b;
+    bool k0 = loader_pair(ld, a, lane, p0a, p0b);
+    bool k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
+    bool k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
+    for (;;) {
+        if (!k0 || !consume(p0a, p0b)) break;
+        k0 = k2 && loader_pair(ld, a, lane, p0a, p0b);
+        if (!k1 || !consume(p1a, p1b)) break;
+        k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
+        if (!k2 || !consume(p2a, p2b)) break;
+        k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
     }
 }
 
