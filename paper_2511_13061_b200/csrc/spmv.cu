@@ -271,34 +271,79 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
     extern __shared__ __align__(16) uint16_t xs[];
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t C = a.cols;
-    if constexpr (kXMode == 1) {
-        if ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0) {
-            const uint32_t nv = C / 8;
-            for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
-                reinterpret_cast<uint4*>(xs)[i] = __ldg(reinterpret_cast<const uint4*>(a.x) + i);
-            for (uint32_t i = nv * 8 + threadIdx.x; i < C; i += blockDim.x) xs[i] = a.x[i];
-        } else {
-            for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) xs[i] = a.x[i];
-        }
-    } else if constexpr (kXMode == 2) {
-        uint32_t* xp = reinterpret_cast<uint32_t*>(xs);
-        for (uint32_t i = threadIdx.x; i < C; i += blockDim.x)
-            xp[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
-    }
-    if constexpr (kXMode != 0) __syncthreads();
-    uint32_t xs_addr;
-    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(xs_addr) : "l"(xs));
     const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + (threadIdx.x >> 5);
     const uint32_t u0 = a.plan.chunk_unit[w], u_end = a.plan.chunk_unit[w + 1];
-    if (u0 >= u_end) return;
+    const bool has_work = u0 < u_end;
 
+    // Set up the walk and put the first three step pairs in flight BEFORE staging x, so the
+    // HBM latency of the matrix stream overlaps the x copy.
     RowState rs;
-    rs.r = a.plan.chunk_row[w];
-    rs.units_left = u_end - u0;
-    rs.first_row = true;
-    const uint32_t j0 = a.plan.chunk_j[w];
-    begin_piece(rs, a, w, j0, j0 ? a.plan.chunk_colbase[w] : -1);
-    Loader ld{rs.r, rs.t, rs.tend, rs.al, rs.e, rs.units_left};
+    Loader ld;
+    Slot p0a, p0b, p1a, p1b, p2a, p2b;
+    bool k0 = false, k1 = false, k2 = false;
+    if (has_work) {
+        rs.r = a.plan.chunk_row[w];
+        rs.units_left = u_end - u0;
+        rs.first_row = true;
+        const uint32_t j0 = a.plan.chunk_j[w];
+        begin_piece(rs, a, w, j0, j0 ? a.plan.chunk_colbase[w] : -1);
+        ld = Loader{rs.r, rs.t, rs.tend, rs.al, rs.e, rs.units_left};
+        k0 = loader_pair(ld, a, lane, p0a, p0b);
+        k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
+        k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
+    }
+
+    // Stage x in shared memory: 16-byte loads, all issued before the stores.
+    if constexpr (kXMode != 0) {
+        const bool vec = (reinterpret_cast<uintptr_t>(a.x) & 15u) == 0;
+        const uint32_t nv = vec ? C / 8 : 0;
+        const uint4* x4 = reinterpret_cast<const uint4*>(a.x);
+        constexpr int kU = 2;
+        for (uint32_t b0 = threadIdx.x; b0 < nv; b0 += kU * blockDim.x) {
+            uint4 t[kU];
+            uint32_t nx[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t i = b0 + u * blockDim.x;
+                if (i < nv) {
+                    t[u] = __ldg(x4 + i);
+                    nx[u] = (kXMode == 2 && 8 * i + 8 < C) ? (uint32_t)__ldg(a.x + 8 * i + 8) : 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t i = b0 + u * blockDim.x;
+                if (i >= nv) continue;
+                if constexpr (kXMode == 1) {
+                    reinterpret_cast<uint4*>(xs)[i] = t[u];
+                } else {
+                    // pair words (x[c], x[c+1]) for c = 8i .. 8i+7
+                    const uint32_t h[4] = {t[u].x, t[u].y, t[u].z, t[u].w};
+                    uint4 lo, hi;
+                    lo.x = h[0];
+                    lo.y = __byte_perm(h[0], h[1], 0x5432);
+                    lo.z = h[1];
+                    lo.w = __byte_perm(h[1], h[2], 0x5432);
+                    hi.x = h[2];
+                    hi.y = __byte_perm(h[2], h[3], 0x5432);
+                    hi.z = h[3];
+                    hi.w = __byte_perm(h[3], nx[u], 0x5432);
+                    reinterpret_cast<uint4*>(xs)[2 * i] = lo;
+                    reinterpret_cast<uint4*>(xs)[2 * i + 1] = hi;
+                }
+            }
+        }
+        for (uint32_t i = nv * 8 + threadIdx.x; i < C; i += blockDim.x) {
+            if constexpr (kXMode == 1)
+                xs[i] = a.x[i];
+            else
+                reinterpret_cast<uint32_t*>(xs)[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
+        }
+        __syncthreads();
+    }
+    if (!has_work) return;
+    uint32_t xs_addr;
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(xs_addr) : "l"(xs));
     if (rs.T == 0) {
         if (lane == 0) a.y[rs.r] = 0;
         if (!next_piece(rs, a, w, lane)) return;
@@ -352,10 +397,6 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
 
     // Ring of three step pairs, unrolled so no slot ever moves between registers: pair P_i is
     // consumed while P_{i+1}, P_{i+2} are in flight, then refilled with P_{i+3}.
-    Slot p0a, p0b, p1a, p1b, p2a, p2b;
-    bool k0 = loader_pair(ld, a, lane, p0a, p0b);
-    bool k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
-    bool k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
     for (;;) {
         if (!k0 || !consume(p0a, p0b)) break;
         k0 = k2 && loader_pair(ld, a, lane, p0a, p0b);
