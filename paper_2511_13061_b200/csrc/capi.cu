@@ -106,6 +106,8 @@ struct macko_dev_matrix {
     int x_mode = 1;             // 0 global x, 1 fp16 smem table, 2 pair smem table
     int force_x_mode = -1;      // macko_dev_configure overrides (-1 / 0 = automatic)
     int force_ctas = 0;
+    uint32_t ring = 0;          // TMA ring slots per warp
+    size_t ring_offset = 0;     // x table bytes (rings follow it in dynamic smem)
     size_t smem = 0;
     int grid = 0, ctas_per_sm = 0;
     uint32_t n_chunks = 0, n_split = 0;
@@ -134,16 +136,34 @@ void check_bits(uint32_t bits) {
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
+    // Shared memory: x table (x_mode 1: fp16, 2: (x[c], x[c+1]) pairs) + per-warp TMA rings.
+    int optin = 0;
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
+    const size_t budget = (size_t)optin - kSpmvWarpsPerCta * kMaxRing * 8 - 1024;
+    const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunkDBytes);
+    auto x_bytes = [&](int mode) { return mode == 2 ? align_up(m->cols * 4, 128) : mode == 1 ? align_up(m->cols * 2, 128) : 0; };
+    auto ring_for = [&](int mode) -> uint32_t {
+        const size_t xb = x_bytes(mode);
+        if (xb >= budget) return 0;
+        for (uint32_t r = kMaxRing; r >= 2; r /= 2)
+            if (r * per_slot <= budget - xb) return r;
+        return 0;
+    };
     if (m->force_x_mode >= 0) {
         m->x_mode = m->force_x_mode;
     } else {
-        m->x_mode = (m->cols * 4 <= kMaxSmemPair) ? 2 : (m->cols * 2 <= kMaxSmemX) ? 1 : 0;
+        m->x_mode = ring_for(2) >= 4 ? 2 : ring_for(1) >= 4 ? 1 : ring_for(1) >= 2 ? 1 : 0;
     }
-    m->smem = m->x_mode == 2 ? align_up(m->cols * 4, 16) : m->x_mode == 1 ? align_up(m->cols * 2, 16) : 0;
+    m->ring = ring_for(m->x_mode);
+    if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
+    m->ring_offset = x_bytes(m->x_mode);
+    m->smem = m->ring_offset + m->ring * per_slot;
     ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
-    if (m->force_ctas > 0) m->ctas_per_sm = std::min(m->ctas_per_sm, m->force_ctas);
+    m->ctas_per_sm = 1;  // one persistent 32-warp CTA per SM
     m->grid = m->sms * m->ctas_per_sm;
+    // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the SMs (a different plan, same y)
+    if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->sms * m->force_ctas / 4));
     const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
     m->n_chunks = W;
     const uint64_t R = m->rows;
@@ -168,7 +188,9 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     m->n_units = U;
     if (U >= 0xFFFFFFFFull) fail(MACKO_EINVAL, "matrix too large for the u32 unit plan");
     std::vector<uint32_t> chunk_unit(W + 1, (uint32_t)U), chunk_row(W, 0), chunk_j(W, 0);
+    std::vector<uint32_t> chunk_e(2 * (size_t)W, 0);  // [first, end) element streamed by TMA
     std::vector<int32_t> chunk_sid(2 * (size_t)W, -1);
+    const uint64_t pad_nnz = rp[R];
     std::vector<uint32_t> split_slot, split_first, split_pieces;
     uint64_t slots = 0;
     int64_t prev_k = -1;
@@ -190,6 +212,13 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
                 chunk_j[q] = (uint32_t)j;
             }
             prev_k = k;
+            if (T) {  // element range of the unit's steps, clamped to the payload
+                const uint64_t al = rp[r] & ~7ull;
+                const uint32_t lo = (uint32_t)(al + j * kUnitElts);
+                const uint32_t hi = (uint32_t)std::min<uint64_t>(al + kStepElts * std::min<uint64_t>((j + 1) * kUnitSteps, T), pad_nnz);
+                if (chunk_e[2 * k + 1] == 0) chunk_e[2 * k] = lo;
+                chunk_e[2 * k + 1] = std::max(chunk_e[2 * k + 1], hi);
+            }
             if (j == 0) kf = k;
             if (k == kf) ++first_units;
             if (j == 0 || k != kl) ++pieces;  // distinct (non-empty) chunks touching the row
@@ -213,7 +242,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     const uint32_t S = (uint32_t)split_slot.size();
     m->n_split = S;
     // upload
-    const size_t n_u32 = (W + 1) + 2 * (size_t)W + 4 * (size_t)S + 1;
+    const size_t n_u32 = (W + 1) + 4 * (size_t)W + 4 * (size_t)S + 1;
     m->plan_u32.alloc(n_u32);
     m->plan_i32.alloc(3 * (size_t)W);
     m->partials.alloc(std::max<uint64_t>(slots, 1));
@@ -223,6 +252,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     hu.insert(hu.end(), chunk_unit.begin(), chunk_unit.end());
     hu.insert(hu.end(), chunk_row.begin(), chunk_row.end());
     hu.insert(hu.end(), chunk_j.begin(), chunk_j.end());
+    hu.insert(hu.end(), chunk_e.begin(), chunk_e.end());
     hu.insert(hu.end(), split_slot.begin(), split_slot.end());
     hu.insert(hu.end(), split_first.begin(), split_first.end());
     hu.insert(hu.end(), split_pieces.begin(), split_pieces.end());
@@ -234,10 +264,11 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     P.chunk_unit = pu;
     P.chunk_row = pu + (W + 1);
     P.chunk_j = pu + (W + 1) + W;
-    P.split_slot = pu + (W + 1) + 2 * (size_t)W;
+    P.chunk_e = pu + (W + 1) + 2 * (size_t)W;
+    P.split_slot = pu + (W + 1) + 4 * (size_t)W;
     P.split_first = P.split_slot + S;
     P.split_pieces = P.split_first + S;
-    P.counters = pu + (W + 1) + 2 * (size_t)W + 3 * (size_t)S;
+    P.counters = pu + (W + 1) + 4 * (size_t)W + 3 * (size_t)S;
     P.chunk_colbase = pi;
     P.chunk_sid = pi + W;
     P.partials = m->partials.p;
@@ -426,6 +457,10 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.y = d_y;
         a.rows = (uint32_t)m->rows;
         a.cols = (uint32_t)m->cols;
+        a.values_bytes = m->values.n * 2;
+        a.delta_bytes = m->deltas.n;
+        a.ring = m->ring;
+        a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
         ck(mk::launch_spmv(a, m->grid, m->x_mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
         g_launches.fetch_add(1);

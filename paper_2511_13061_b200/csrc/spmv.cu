@@ -2,8 +2,7 @@
 //
 // Realises the paper's warp kernel (SPEC.md:255-264 warp_spmv) natively:
 //   * one warp walks a row in steps of 256 elements, lane l owning elements 8l..8l+7 of the
-//     step: one 16-B streaming load of values and one 4-B load of packed deltas per lane
-//     (PAPER.md:318-323), both L1::no_allocate;
+//     step;
 //   * ROMA: the row start is aligned down to 8 elements and the elements
 //     before it are masked in the first step; lanes past the row end are masked in the last;
 //   * column reconstruction: the 8 nibbles are widened to bytes, paired and prefix-summed with
@@ -12,13 +11,15 @@
 //     scan (their lane sums packed into 16-bit halves);
 //   * x is staged once per CTA in shared memory — as (x[c], x[c+1]) pairs when it fits, so an
 //     element pair at adjacent columns costs one 32-bit gather — and gathered per element; the
-//     multiply-add is FHFMA (fp16 x fp16 -> fp32 accumulate, exact product);
-//   * B200 work distribution and latency hiding: a persistent grid (SM count x occupancy)
-//     where every warp owns an equal-weight contiguous range of 2048-element units (a static
-//     plan built once per matrix).  A warp's loads run a step-pair ahead of its math across
-//     row boundaries (a 4-slot register ring fed by a loader cursor that replays the same
-//     walk).  Rows cut between warps are finished by the last-arriving warp, which adds the
-//     per-unit partials in unit order.
+//     multiply-add is FHFMA (fp16 x fp16 -> fp32 accumulate, exact product).
+// B200 specifics (profiles/r01_pipes.md): the kernel is bound by the L1/LSU data pipe (x
+// gathers + shuffles + loads), not by HBM.  The matrix stream therefore arrives by TMA: every
+// warp owns a contiguous element range (static equal-weight plan of 2048-element units, built
+// once per matrix) and keeps a ring of 512-element chunks (1 KiB values + 256 B deltas) in
+// flight with cp.async.bulk + mbarrier, which costs no LSU wavefronts; values and deltas are
+// read back with one LDS.128 + one LDS.32 per lane step.  One persistent CTA of 32 warps per
+// SM.  Rows cut between warps are finished by the last-arriving warp, which adds the per-unit
+// partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
 // lanes once per unit (8 steps), sequential over units — mirrored bit-exactly by
 // oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  The order depends on a row's elements
@@ -143,60 +144,6 @@ __device__ __forceinline__ float fma_masked(float acc, const uint4& v, const Dec
 }
 
 // ------------------------------------------------------------------------------------------
-// Loader cursor: replays the warp's walk over (row, step) to issue loads ahead of the math.
-// ------------------------------------------------------------------------------------------
-struct Loader {
-    uint32_t r, t, tend, al, e, units_left;
-};
-
-struct Slot {
-    uint4 v;
-    uint32_t d;
-};
-
-// Advance to the next non-empty row piece (rare path).  False when the chunk is exhausted.
-__device__ __forceinline__ bool loader_advance(Loader& c, const SpmvArgs& a) {
-    while (c.t >= c.tend) {
-        if (c.units_left == 0) return false;
-        ++c.r;
-        const uint32_t s = __ldg(a.row_ptrs + c.r), e = __ldg(a.row_ptrs + c.r + 1);
-        if (s == e) {
-            c.units_left -= 1;
-            continue;
-        }
-        c.al = s & ~7u;
-        c.e = e;
-        const uint32_t T = (e - c.al + kStepElts - 1) / kStepElts;
-        const uint32_t nu = min((T + kUnitSteps - 1) / kUnitSteps, c.units_left);
-        c.units_left -= nu;
-        c.t = 0;
-        c.tend = min(T, nu * kUnitSteps);
-    }
-    return true;
-}
-
-// Load the next aligned step pair (t, t+1) of the walk; the second step is a phantom (zeros,
-// no load) when the piece has an odd number of steps.
-__device__ __forceinline__ bool loader_pair(Loader& c, const SpmvArgs& a, int lane, Slot& A, Slot& B) {
-    if (c.t >= c.tend && !loader_advance(c, a)) return false;
-    const uint32_t eb = c.al + c.t * kStepElts + 8u * lane;
-    A.v = make_uint4(0, 0, 0, 0);
-    A.d = 0;
-    B.v = make_uint4(0, 0, 0, 0);
-    B.d = 0;
-    if (eb < c.e) {
-        A.v = ldg_stream_v4(a.values + eb);
-        A.d = ldg_stream_u32(a.deltas + eb / 2);
-    }
-    if (c.t + 1 < c.tend && eb + kStepElts < c.e) {
-        B.v = ldg_stream_v4(a.values + eb + kStepElts);
-        B.d = ldg_stream_u32(a.deltas + (eb + kStepElts) / 2);
-    }
-    c.t += 2;
-    return true;
-}
-
-// ------------------------------------------------------------------------------------------
 // Compute-side row state
 // ------------------------------------------------------------------------------------------
 struct RowState {
@@ -265,35 +212,132 @@ __device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Per-warp TMA ring of 512-element chunks (values 1 KiB + deltas 256 B per chunk)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+struct Ring {
+    uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
+    uint32_t q_iss, q_rel, q_done, q_last;
+};
+
+__device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane) {
+    if (lane == 0) {
+        const uint32_t q = g.q_iss, slot = q & (a.ring - 1);
+        const uint64_t e0 = (uint64_t)q * kChunk;
+        const uint64_t vleft = a.values_bytes - 2 * e0, dleft = a.delta_bytes - e0 / 2;
+        const uint32_t vb = vleft < kChunkVBytes ? (uint32_t)vleft : kChunkVBytes;
+        const uint32_t db = dleft < kChunkDBytes ? (uint32_t)dleft : kChunkDBytes;
+        const uint32_t bar = g.bar0 + 8u * slot;
+        // order this warp's earlier generic reads of the slot before the async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb + db) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         g.vbase + slot * kChunkVBytes),
+                     "l"(a.values + e0), "r"(vb), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         g.dbase + slot * kChunkDBytes),
+                     "l"(a.deltas + e0 / 2), "r"(db), "r"(bar)
+                     : "memory");
+    }
+    ++g.q_iss;
+}
+
+// Chunks wholly below element S are no longer needed: refill their slots further ahead.
+__device__ __forceinline__ void ring_release(Ring& g, const SpmvArgs& a, uint32_t S, int lane) {
+    const uint32_t qlo = S / kChunk;
+    if (qlo > g.q_rel) g.q_rel = qlo;
+    if (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last) {
+        __syncwarp();
+        do ring_issue(g, a, lane);
+        while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);
+    }
+}
+
+__device__ __forceinline__ void ring_need(Ring& g, const SpmvArgs& a, uint32_t q_need) {
+    while (g.q_done <= q_need) {
+        mbar_wait(g.bar0 + 8u * (g.q_done & (a.ring - 1)), (g.q_done / a.ring) & 1u);
+        ++g.q_done;
+    }
+}
+
+struct Slot {
+    uint4 v;
+    uint32_t d;
+};
+
+// Lane data of the step whose lane-0 element is eb (zeros for lanes wholly past the row).
+__device__ __forceinline__ Slot ring_read(const Ring& g, const SpmvArgs& a, uint32_t eb, uint32_t e) {
+    Slot sl{make_uint4(0, 0, 0, 0), 0u};
+    if (eb < e) {
+        const uint32_t q = eb / kChunk, off = eb % kChunk, slot = q & (a.ring - 1);
+        const uint32_t va = g.vbase + slot * kChunkVBytes + 2u * off;
+        const uint32_t da = g.dbase + slot * kChunkDBytes + off / 2u;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
+                     : "r"(va));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(da));
+    }
+    return sl;
+}
+
 template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
-    macko_spmv_b4(const SpmvArgs a) {
-    extern __shared__ __align__(16) uint16_t xs[];
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(const SpmvArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
     const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t warp = threadIdx.x >> 5;
     const uint32_t C = a.cols;
-    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + (threadIdx.x >> 5);
+    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
     const uint32_t u0 = a.plan.chunk_unit[w], u_end = a.plan.chunk_unit[w + 1];
     const bool has_work = u0 < u_end;
 
-    // Set up the walk and put the first three step pairs in flight BEFORE staging x, so the
-    // HBM latency of the matrix stream overlaps the x copy.
+    // Walk set-up and the first ring fills go out BEFORE x is staged, so the HBM latency of
+    // the matrix stream overlaps the x copy.
     RowState rs;
-    Loader ld;
-    Slot p0a, p0b, p1a, p1b, p2a, p2b;
-    bool k0 = false, k1 = false, k2 = false;
+    Ring g;
     if (has_work) {
         rs.r = a.plan.chunk_row[w];
         rs.units_left = u_end - u0;
         rs.first_row = true;
         const uint32_t j0 = a.plan.chunk_j[w];
         begin_piece(rs, a, w, j0, j0 ? a.plan.chunk_colbase[w] : -1);
-        ld = Loader{rs.r, rs.t, rs.tend, rs.al, rs.e, rs.units_left};
-        k0 = loader_pair(ld, a, lane, p0a, p0b);
-        k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
-        k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
+        const uint32_t E0 = a.plan.chunk_e[2 * w], E1 = a.plan.chunk_e[2 * w + 1];
+        const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+        g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
+        g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
+        g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
+        g.q_iss = g.q_rel = g.q_done = E0 / kChunk;
+        g.q_last = E1 > E0 ? (E1 - 1) / kChunk : g.q_iss;
+        if (lane == 0) {
+            for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (E1 > E0) {
+            do ring_issue(g, a, lane);
+            while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);
+        }
     }
 
-    // Stage x in shared memory: 16-byte loads, all issued before the stores.
+    // Stage x in shared memory: 16-byte loads, issued before the stores.
     if constexpr (kXMode != 0) {
         const bool vec = (reinterpret_cast<uintptr_t>(a.x) & 15u) == 0;
         const uint32_t nv = vec ? C / 8 : 0;
@@ -339,8 +383,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
             else
                 reinterpret_cast<uint32_t*>(xs)[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (!has_work) return;
     uint32_t xs_addr;
     asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(xs_addr) : "l"(xs));
@@ -349,61 +393,54 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvMinCtasPerSm)
         if (!next_piece(rs, a, w, lane)) return;
     }
 
-    // Consume the aligned pair (t, t+1) of the current piece (t+1 may be a phantom); returns
-    // false when the chunk is exhausted.
-    auto consume = [&](const Slot& A, const Slot& B) -> bool {
-        const bool hasB = rs.t + 1 < rs.tend;
-        const bool edge = !hasB || rs.t == 0 || rs.t + 2u >= rs.T;
-        if (!edge) {
-            const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
-            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
-            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
-            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-        } else {
-            const uint32_t ebA = rs.al + rs.t * kStepElts + 8u * lane;
-            const uint32_t vmA = lane_mask(ebA, rs.s, rs.e);
-            const uint32_t vmB = hasB ? lane_mask(ebA + kStepElts, rs.s, rs.e) : 0u;
-            const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
-            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
-            rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
-            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-        }
-        rs.t = min(rs.t + 2u, rs.tend);
-        // unit end (pairs start at even t, so a unit boundary never falls inside a pair)
-        if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
-            const float red = warp_tree_sum(rs.acc);
-            rs.acc = 0.0f;
-            if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
-            rs.row_acc += red;
-        }
-        if (rs.t == rs.tend) {  // piece end
-            if (!rs.split) {
-                if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
-            } else {
-                finish_split(rs.r, rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, a.y, lane);
-            }
-            return next_piece(rs, a, w, lane);
-        }
-        return true;
-    };
-
-    // Ring of three step pairs, unrolled so no slot ever moves between registers: pair P_i is
-    // consumed while P_{i+1}, P_{i+2} are in flight, then refilled with P_{i+3}.
     for (;;) {
-        if (!k0 || !consume(p0a, p0b)) break;
-        k0 = k2 && loader_pair(ld, a, lane, p0a, p0b);
-        if (!k1 || !consume(p1a, p1b)) break;
-        k1 = k0 && loader_pair(ld, a, lane, p1a, p1b);
-        if (!k2 || !consume(p2a, p2b)) break;
-        k2 = k1 && loader_pair(ld, a, lane, p2a, p2b);
+        while (rs.t < rs.tend) {
+            // -- the aligned step pair (t, t+1) of the piece; t+1 may be a phantom
+            const uint32_t S = rs.al + rs.t * kStepElts;
+            const bool hasB = rs.t + 1 < rs.tend;
+            ring_release(g, a, S, lane);
+            ring_need(g, a, min((S + (hasB ? 2u : 1u) * kStepElts - 1) / kChunk, g.q_last));
+            const uint32_t eb = S + 8u * lane;
+            const Slot A = ring_read(g, a, eb, rs.e);
+            const Slot B = hasB ? ring_read(g, a, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};
+            const bool edge = !hasB || rs.t == 0 || rs.t + 2u >= rs.T;
+            if (!edge) {
+                const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
+                const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+                const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+                const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+                const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+                rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
+                rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
+                rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+            } else {
+                const uint32_t vmA = lane_mask(eb, rs.s, rs.e);
+                const uint32_t vmB = hasB ? lane_mask(eb + kStepElts, rs.s, rs.e) : 0u;
+                const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
+                const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+                const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+                const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+                const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+                rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
+                rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
+                rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+            }
+            rs.t = min(rs.t + 2u, rs.tend);
+            // unit end (pairs start at even t, so a unit boundary never falls inside a pair)
+            if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
+                const float red = warp_tree_sum(rs.acc);
+                rs.acc = 0.0f;
+                if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
+                rs.row_acc += red;
+            }
+        }
+        // -- piece end
+        if (!rs.split) {
+            if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
+        } else {
+            finish_split(rs.r, rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, a.y, lane);
+        }
+        if (!next_piece(rs, a, w, lane)) break;
     }
 }
 

@@ -6,13 +6,14 @@
 
 namespace mk {
 
-// Static work plan of one matrix (built once on the host by plan.cpp logic in capi.cu, kept on
-// the device).  The element stream of the matrix is cut into units of kUnitSteps warp steps
-// per row; each warp ("chunk") owns a contiguous range of units of roughly equal weight.
+// Static work plan of one matrix (built once on the host by build_plan in capi.cu, kept on the
+// device).  The element stream of the matrix is cut into units of kUnitSteps warp steps per
+// row; each warp ("chunk") owns a contiguous range of units of roughly equal weight.
 struct SpmvPlanDev {
     const uint32_t* chunk_unit;     // W+1: first global unit of chunk w
     const uint32_t* chunk_row;      // W:   row of that unit
     const uint32_t* chunk_j;        // W:   unit index of that unit inside its row
+    const uint32_t* chunk_e;        // 2W:  [first, end) element of the chunk's stream (TMA range)
     const int32_t* chunk_colbase;   // W:   decoded column just before that unit (-1 if j == 0)
     const int32_t* chunk_sid;       // 2W:  split-row id of the chunk's first / last row, or -1
     const uint32_t* split_slot;     // S:   first partial slot of split row s
@@ -28,12 +29,18 @@ struct SpmvArgs {
     const uint32_t* row_ptrs;
     const uint16_t* x;
     uint16_t* y;
+    uint64_t values_bytes, delta_bytes;  // allocated payload sizes (TMA clamp)
     uint32_t rows, cols;
+    uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
+    uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
     SpmvPlanDev plan;
 };
 
-constexpr int kSpmvWarpsPerCta = 8;
-constexpr int kSpmvMinCtasPerSm = 3;  // 24 resident warps, <= 85 registers
+constexpr int kSpmvWarpsPerCta = 32;          // one persistent 1024-thread CTA per SM
+constexpr uint32_t kChunk = 512;              // elements per TMA chunk
+constexpr uint32_t kChunkVBytes = 2 * kChunk; // 1 KiB of values
+constexpr uint32_t kChunkDBytes = kChunk / 2; // 256 B of 4-bit deltas
+constexpr uint32_t kMaxRing = 8;
 
 // Launchers (return cudaGetLastError()).
 // x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table
