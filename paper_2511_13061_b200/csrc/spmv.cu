@@ -219,25 +219,33 @@ __device__ __forceinline__ void mbar_init(uint32_t bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
     uint32_t done;
-    do {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+    return done != 0;
+}
+
+// Wait for a TMA chunk.  A chunk that never lands (a bug, or a fault in the copy) traps after
+// ~2 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity))
+        if (clock64() - t0 > 4000000000LL) __trap();
 }
 
 struct Ring {
     uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
-    uint32_t q_iss, q_rel, q_done, q_last;
+    uint32_t q_iss, q_rel, q_done, q_last;  // absolute chunk indices
+    uint32_t q_first;                       // slot / phase are relative to the warp's first chunk
 };
 
 __device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane) {
     if (lane == 0) {
-        const uint32_t q = g.q_iss, slot = q & (a.ring - 1);
+        const uint32_t q = g.q_iss, slot = (q - g.q_first) & (a.ring - 1);
         const uint64_t e0 = (uint64_t)q * kChunk;
         const uint64_t vleft = a.values_bytes - 2 * e0, dleft = a.delta_bytes - e0 / 2;
         const uint32_t vb = vleft < kChunkVBytes ? (uint32_t)vleft : kChunkVBytes;
@@ -263,6 +271,8 @@ __device__ __forceinline__ void ring_release(Ring& g, const SpmvArgs& a, uint32_
     const uint32_t qlo = S / kChunk;
     if (qlo > g.q_rel) g.q_rel = qlo;
     if (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last) {
+        // every lane's generic reads of the released slots precede the async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         do ring_issue(g, a, lane);
         while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);
@@ -271,7 +281,8 @@ __device__ __forceinline__ void ring_release(Ring& g, const SpmvArgs& a, uint32_
 
 __device__ __forceinline__ void ring_need(Ring& g, const SpmvArgs& a, uint32_t q_need) {
     while (g.q_done <= q_need) {
-        mbar_wait(g.bar0 + 8u * (g.q_done & (a.ring - 1)), (g.q_done / a.ring) & 1u);
+        const uint32_t rel = g.q_done - g.q_first;
+        mbar_wait(g.bar0 + 8u * (rel & (a.ring - 1)), (rel / a.ring) & 1u);
         ++g.q_done;
     }
 }
@@ -285,7 +296,7 @@ struct Slot {
 __device__ __forceinline__ Slot ring_read(const Ring& g, const SpmvArgs& a, uint32_t eb, uint32_t e) {
     Slot sl{make_uint4(0, 0, 0, 0), 0u};
     if (eb < e) {
-        const uint32_t q = eb / kChunk, off = eb % kChunk, slot = q & (a.ring - 1);
+        const uint32_t q = eb / kChunk, off = eb % kChunk, slot = (q - g.q_first) & (a.ring - 1);
         const uint32_t va = g.vbase + slot * kChunkVBytes + 2u * off;
         const uint32_t da = g.dbase + slot * kChunkDBytes + off / 2u;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -323,7 +334,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
         g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
         g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
-        g.q_iss = g.q_rel = g.q_done = E0 / kChunk;
+        g.q_iss = g.q_rel = g.q_done = g.q_first = E0 / kChunk;
         g.q_last = E1 > E0 ? (E1 - 1) / kChunk : g.q_iss;
         if (lane == 0) {
             for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
