@@ -492,7 +492,9 @@ cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
             if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<1>, threads, smem);
             return e;
         default:
-            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<0>, threads, 0);
+            e = cudaFuncSetAttribute(macko_spmv_b4<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<0>, threads, smem);
+            return e;
     }
 }
 
@@ -503,7 +505,7 @@ cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cu
     else if (x_mode == 1)
         macko_spmv_b4<1><<<grid, threads, smem, s>>>(a);
     else
-        macko_spmv_b4<0><<<grid, threads, 0, s>>>(a);
+        macko_spmv_b4<0><<<grid, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
