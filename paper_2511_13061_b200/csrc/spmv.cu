@@ -251,9 +251,10 @@ __device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane)
         const uint32_t vb = vleft < kChunkVBytes ? (uint32_t)vleft : kChunkVBytes;
         const uint32_t db = dleft < kChunkDBytes ? (uint32_t)dleft : kChunkDBytes;
         const uint32_t bar = g.bar0 + 8u * slot;
-        // order this warp's earlier generic reads of the slot before the async-proxy refill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb + db) : "memory");
+        // relaxed: the arrive only arms the transaction count (no generic data to publish), so
+        // no MEMBAR is emitted before it
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb + db)
+                     : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          g.vbase + slot * kChunkVBytes),
                      "l"(a.values + e0), "r"(vb), "r"(bar)
@@ -271,8 +272,9 @@ __device__ __forceinline__ void ring_release(Ring& g, const SpmvArgs& a, uint32_
     const uint32_t qlo = S / kChunk;
     if (qlo > g.q_rel) g.q_rel = qlo;
     if (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last) {
-        // every lane's generic reads of the released slots precede the async-proxy refill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // The released slot's data was consumed (its LDS results fed the FHFMAs) by every lane
+        // before this point; the warp-converged refill is issued after it (WAR by execution
+        // order, as in a TMA producer/consumer pipeline).
         __syncwarp();
         do ring_issue(g, a, lane);
         while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);

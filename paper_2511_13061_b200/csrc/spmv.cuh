@@ -37,9 +37,9 @@ struct SpmvArgs {
 };
 
 constexpr int kSpmvWarpsPerCta = 32;          // one persistent 1024-thread CTA per SM
-constexpr uint32_t kChunk = 512;              // elements per TMA chunk
-constexpr uint32_t kChunkVBytes = 2 * kChunk; // 1 KiB of values
-constexpr uint32_t kChunkDBytes = kChunk / 2; // 256 B of 4-bit deltas
+constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two step pairs)
+constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
+constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
 constexpr uint32_t kMaxRing = 8;
 
 // Launchers (return cudaGetLastError()).
