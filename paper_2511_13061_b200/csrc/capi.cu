@@ -152,7 +152,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     if (m->force_x_mode >= 0) {
         m->x_mode = m->force_x_mode;
     } else {
-        m->x_mode = ring_for(2) >= 4 ? 2 : ring_for(1) >= 4 ? 1 : ring_for(1) >= 2 ? 1 : 0;
+        // prefer the pair table (fewer gather wavefronts), then the fp16 table, then global x
+        m->x_mode = ring_for(2) >= 2 ? 2 : ring_for(1) >= 2 ? 1 : 0;
     }
     m->ring = ring_for(m->x_mode);
     if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");

@@ -59,10 +59,17 @@ __device__ __forceinline__ uint16_t xget(uint32_t xs_addr, const uint16_t* __res
 }
 
 // valid-element mask of a lane whose first element is eb, for the row [s, e)
+// (row offsets are < 2^32 and a row spans < 2^31 elements, so 32-bit differences suffice)
 __device__ __forceinline__ uint32_t lane_mask(uint32_t eb, uint32_t s, uint32_t e) {
-    const int klo = (int)max(0LL, min(8LL, (long long)s - (long long)eb));
-    const int khi = (int)max(0LL, min(8LL, (long long)e - (long long)eb));
+    const int klo = min(max((int)(s - eb), 0), 8);
+    const int khi = min(max((int)(e - eb), 0), 8);
     return (0xFFu << klo) & (0xFFu >> (8 - khi)) & 0xFFu;
+}
+
+// Byte masks for the even (0,2,4,6) / odd (1,3,5,7) elements of an 8-bit element mask: bit 2m
+// lands on bit 8m through one multiply (no carries reach the target bits), then * 0xFF.
+__device__ __forceinline__ uint32_t spread_even(uint32_t vm) {
+    return (((vm & 0x55u) * 0x41041u) & 0x01010101u) * 0xFFu;
 }
 
 struct Dec {
@@ -75,14 +82,8 @@ __device__ __forceinline__ Dec decode(uint32_t d, uint32_t vm) {
     uint32_t dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
     uint32_t dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
     if constexpr (kMasked) {
-        uint32_t me = 0, mo = 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            me |= ((vm >> (2 * m)) & 1u) ? (0xFFu << (8 * m)) : 0u;
-            mo |= ((vm >> (2 * m + 1)) & 1u) ? (0xFFu << (8 * m)) : 0u;
-        }
-        dl &= me;
-        dh &= mo;
+        dl &= spread_even(vm);
+        dh &= spread_even(vm >> 1);
     }
     const uint32_t pp = (dl + dh) * 0x01010101u;
     return Dec{pp - dh, pp, dh, pp >> 24};
@@ -238,55 +239,64 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 struct Ring {
-    uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
-    uint32_t q_iss, q_rel, q_done, q_last;  // absolute chunk indices
-    uint32_t q_first;                       // slot / phase are relative to the warp's first chunk
+    uint32_t vbase, dbase, bar0;   // this warp's value ring, delta ring, first mbarrier (smem)
+    uint32_t ebase;                // first element of the warp's first chunk
+    uint32_t q_iss, q_done, q_last;  // absolute chunk indices: next to issue, next to wait, last
+    uint32_t ready_end;            // chunks below q_done have landed: elements < ready_end
+    uint32_t release_mark;         // the next chunk boundary at which a slot can be refilled
 };
+
+// The ring is contiguous: chunk q sits at element offset (q*kChunk - ebase) mod (ring*kChunk),
+// so an element's shared address is one AND + one LEA away (ring*kChunk is a power of two).
+__device__ __forceinline__ uint32_t ring_rel(const Ring& g, const SpmvArgs& a, uint32_t elem) {
+    return (elem - g.ebase) & (a.ring * kChunk - 1u);
+}
 
 __device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane) {
     if (lane == 0) {
-        const uint32_t q = g.q_iss, slot = (q - g.q_first) & (a.ring - 1);
+        const uint32_t q = g.q_iss;
+        const uint32_t rel = ring_rel(g, a, q * kChunk);
         const uint64_t e0 = (uint64_t)q * kChunk;
-        const uint64_t vleft = a.values_bytes - 2 * e0, dleft = a.delta_bytes - e0 / 2;
-        const uint32_t vb = vleft < kChunkVBytes ? (uint32_t)vleft : kChunkVBytes;
-        const uint32_t db = dleft < kChunkDBytes ? (uint32_t)dleft : kChunkDBytes;
-        const uint32_t bar = g.bar0 + 8u * slot;
-        // relaxed: the arrive only arms the transaction count (no generic data to publish), so
-        // no MEMBAR is emitted before it
+        uint32_t vb = kChunkVBytes, db = kChunkDBytes;
+        if (2 * e0 + kChunkVBytes > a.values_bytes) {  // the payload's last chunk
+            vb = (uint32_t)(a.values_bytes - 2 * e0);
+            db = (uint32_t)(a.delta_bytes - e0 / 2 < kChunkDBytes ? a.delta_bytes - e0 / 2 : kChunkDBytes);
+        }
+        const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
+        // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
         asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb + db)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         g.vbase + slot * kChunkVBytes),
+                         g.vbase + 2u * rel),
                      "l"(a.values + e0), "r"(vb), "r"(bar)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         g.dbase + slot * kChunkDBytes),
+                         g.dbase + rel / 2u),
                      "l"(a.deltas + e0 / 2), "r"(db), "r"(bar)
                      : "memory");
     }
     ++g.q_iss;
 }
 
-// Chunks wholly below element S are no longer needed: refill their slots further ahead.
-__device__ __forceinline__ void ring_release(Ring& g, const SpmvArgs& a, uint32_t S, int lane) {
-    const uint32_t qlo = S / kChunk;
-    if (qlo > g.q_rel) g.q_rel = qlo;
-    if (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last) {
-        // The released slot's data was consumed (its LDS results fed the FHFMAs) by every lane
-        // before this point; the warp-converged refill is issued after it (WAR by execution
-        // order, as in a TMA producer/consumer pipeline).
+// Make elements [S, Send) resident: refill every slot whose chunk lies wholly below S (its
+// data was consumed by every lane: the LDS results fed the FHFMAs of earlier steps, and the
+// warp-converged refill is issued after them), then wait for the chunks covering Send.
+__device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_t S, uint32_t Send, int lane) {
+    const uint32_t q_rel = S / kChunk;
+    if (g.q_iss < q_rel + a.ring && g.q_iss <= g.q_last) {
         __syncwarp();
         do ring_issue(g, a, lane);
-        while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);
+        while (g.q_iss < q_rel + a.ring && g.q_iss <= g.q_last);
     }
-}
-
-__device__ __forceinline__ void ring_need(Ring& g, const SpmvArgs& a, uint32_t q_need) {
+    g.release_mark = (q_rel + 1) * kChunk;
+    const uint32_t q_need = min((Send - 1) / kChunk, g.q_last);
     while (g.q_done <= q_need) {
-        const uint32_t rel = g.q_done - g.q_first;
-        mbar_wait(g.bar0 + 8u * (rel & (a.ring - 1)), (rel / a.ring) & 1u);
+        const uint32_t slot = ring_rel(g, a, g.q_done * kChunk) / kChunk;
+        const uint32_t phase = ((g.q_done * kChunk - g.ebase) / (a.ring * kChunk)) & 1u;
+        mbar_wait(g.bar0 + 8u * slot, phase);
         ++g.q_done;
     }
+    g.ready_end = g.q_done * kChunk;
 }
 
 struct Slot {
@@ -294,17 +304,15 @@ struct Slot {
     uint32_t d;
 };
 
-// Lane data of the step whose lane-0 element is eb (zeros for lanes wholly past the row).
+// Lane data of the step whose lane element is eb (zeros for lanes wholly past the row).
 __device__ __forceinline__ Slot ring_read(const Ring& g, const SpmvArgs& a, uint32_t eb, uint32_t e) {
     Slot sl{make_uint4(0, 0, 0, 0), 0u};
     if (eb < e) {
-        const uint32_t q = eb / kChunk, off = eb % kChunk, slot = (q - g.q_first) & (a.ring - 1);
-        const uint32_t va = g.vbase + slot * kChunkVBytes + 2u * off;
-        const uint32_t da = g.dbase + slot * kChunkDBytes + off / 2u;
+        const uint32_t rel = ring_rel(g, a, eb);
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
-                     : "r"(va));
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(da));
+                     : "r"(g.vbase + 2u * rel));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(g.dbase + rel / 2u));
     }
     return sl;
 }
@@ -336,8 +344,11 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
         g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
         g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
-        g.q_iss = g.q_rel = g.q_done = g.q_first = E0 / kChunk;
+        g.q_iss = g.q_done = E0 / kChunk;
+        g.ebase = g.q_iss * kChunk;
         g.q_last = E1 > E0 ? (E1 - 1) / kChunk : g.q_iss;
+        g.ready_end = g.ebase;
+        g.release_mark = g.ebase + kChunk;
         if (lane == 0) {
             for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -346,7 +357,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         __syncwarp();
         if (E1 > E0) {
             do ring_issue(g, a, lane);
-            while (g.q_iss < g.q_rel + a.ring && g.q_iss <= g.q_last);
+            while (g.q_iss < E0 / kChunk + a.ring && g.q_iss <= g.q_last);
         }
     }
 
@@ -411,8 +422,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
             // -- the aligned step pair (t, t+1) of the piece; t+1 may be a phantom
             const uint32_t S = rs.al + rs.t * kStepElts;
             const bool hasB = rs.t + 1 < rs.tend;
-            ring_release(g, a, S, lane);
-            ring_need(g, a, min((S + (hasB ? 2u : 1u) * kStepElts - 1) / kChunk, g.q_last));
+            const uint32_t Send = S + (hasB ? 2u : 1u) * kStepElts;
+            if (Send > g.ready_end || S >= g.release_mark) ring_advance(g, a, S, Send, lane);
             const uint32_t eb = S + 8u * lane;
             const Slot A = ring_read(g, a, eb, rs.e);
             const Slot B = hasB ? ring_read(g, a, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};

@@ -229,7 +229,11 @@ def test_plan_and_x_staging_do_not_change_y(cuda):
         assert np.array_equal(y0, O.b200_order_spmv(O.encode_dense(A), x, UNIT_STEPS))
         for x_mode in (0, 1, 2):
             for ctas in (1, 2, 0):
-                dm.configure(x_mode, ctas)
+                try:
+                    dm.configure(x_mode, ctas)
+                except ValueError:  # the x table would not leave room for the TMA rings
+                    assert x_mode > 0 and C * 2 * x_mode > 100_000
+                    continue
                 assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, x_mode, ctas)
 
 
