@@ -458,7 +458,7 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.y = d_y;
         a.rows = (uint32_t)m->rows;
         a.cols = (uint32_t)m->cols;
-        a.values_bytes = m->values.n * 2;
+        a.value_elems = m->values.n;
         a.delta_bytes = m->deltas.n;
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;

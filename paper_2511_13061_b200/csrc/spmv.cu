@@ -239,28 +239,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 struct Ring {
-    uint32_t vbase, dbase, bar0;   // this warp's value ring, delta ring, first mbarrier (smem)
-    uint32_t ebase;                // first element of the warp's first chunk
-    uint32_t q_iss, q_done, q_last;  // absolute chunk indices: next to issue, next to wait, last
-    uint32_t ready_end;            // chunks below q_done have landed: elements < ready_end
-    uint32_t release_mark;         // the next chunk boundary at which a slot can be refilled
+    uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
+    uint32_t ebase, emask;        // element e lives at ring offset (e - ebase) & emask
+    uint32_t iss_elem;            // producer: first element of the next chunk to issue
+    uint32_t stream_end;          // end (exclusive, chunk aligned) of the warp's chunk stream
+    uint32_t ready_end;           // consumer: elements below this have landed
+    uint32_t wait_slot, wait_phase;
+    uint32_t release_mark;        // next chunk boundary at which a slot becomes refillable
 };
 
-// The ring is contiguous: chunk q sits at element offset (q*kChunk - ebase) mod (ring*kChunk),
-// so an element's shared address is one AND + one LEA away (ring*kChunk is a power of two).
-__device__ __forceinline__ uint32_t ring_rel(const Ring& g, const SpmvArgs& a, uint32_t elem) {
-    return (elem - g.ebase) & (a.ring * kChunk - 1u);
-}
-
+// Issue the TMA copies of the chunk starting at element g.iss_elem (lane 0).
 __device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane) {
     if (lane == 0) {
-        const uint32_t q = g.q_iss;
-        const uint32_t rel = ring_rel(g, a, q * kChunk);
-        const uint64_t e0 = (uint64_t)q * kChunk;
+        const uint32_t e0 = g.iss_elem;
+        const uint32_t rel = (e0 - g.ebase) & g.emask;
         uint32_t vb = kChunkVBytes, db = kChunkDBytes;
-        if (2 * e0 + kChunkVBytes > a.values_bytes) {  // the payload's last chunk
-            vb = (uint32_t)(a.values_bytes - 2 * e0);
-            db = (uint32_t)(a.delta_bytes - e0 / 2 < kChunkDBytes ? a.delta_bytes - e0 / 2 : kChunkDBytes);
+        if (e0 + kChunk > a.value_elems) {  // the payload's last chunk: clamp to the buffers
+            vb = 2u * (a.value_elems - e0);
+            const uint64_t dleft = a.delta_bytes - e0 / 2;
+            db = dleft < kChunkDBytes ? (uint32_t)dleft : kChunkDBytes;
         }
         const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
         // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
@@ -275,28 +272,28 @@ __device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane)
                      "l"(a.deltas + e0 / 2), "r"(db), "r"(bar)
                      : "memory");
     }
-    ++g.q_iss;
+    g.iss_elem += kChunk;
 }
 
-// Make elements [S, Send) resident: refill every slot whose chunk lies wholly below S (its
-// data was consumed by every lane: the LDS results fed the FHFMAs of earlier steps, and the
-// warp-converged refill is issued after them), then wait for the chunks covering Send.
+// Make elements [S, Send) resident: refill every slot whose chunk lies wholly below S (its data
+// was consumed by every lane — the LDS results fed earlier FHFMAs — and the warp-converged
+// refill is issued after them), then wait for the chunks covering Send.
 __device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_t S, uint32_t Send, int lane) {
-    const uint32_t q_rel = S / kChunk;
-    if (g.q_iss < q_rel + a.ring && g.q_iss <= g.q_last) {
+    const uint32_t floor_s = S & ~(kChunk - 1u);
+    const uint32_t limit = min(floor_s + a.ring * kChunk, g.stream_end);
+    if (g.iss_elem < limit) {
         __syncwarp();
         do ring_issue(g, a, lane);
-        while (g.q_iss < q_rel + a.ring && g.q_iss <= g.q_last);
+        while (g.iss_elem < limit);
     }
-    g.release_mark = (q_rel + 1) * kChunk;
-    const uint32_t q_need = min((Send - 1) / kChunk, g.q_last);
-    while (g.q_done <= q_need) {
-        const uint32_t slot = ring_rel(g, a, g.q_done * kChunk) / kChunk;
-        const uint32_t phase = ((g.q_done * kChunk - g.ebase) / (a.ring * kChunk)) & 1u;
-        mbar_wait(g.bar0 + 8u * slot, phase);
-        ++g.q_done;
+    g.release_mark = floor_s + kChunk;
+    const uint32_t need = min(Send, g.stream_end);
+    while (g.ready_end < need) {
+        mbar_wait(g.bar0 + 8u * g.wait_slot, g.wait_phase);
+        g.wait_slot = (g.wait_slot + 1u) & (a.ring - 1u);
+        g.wait_phase ^= g.wait_slot == 0 ? 1u : 0u;
+        g.ready_end += kChunk;
     }
-    g.ready_end = g.q_done * kChunk;
 }
 
 struct Slot {
@@ -304,17 +301,19 @@ struct Slot {
     uint32_t d;
 };
 
-// Lane data of the step whose lane element is eb (zeros for lanes wholly past the row).
-__device__ __forceinline__ Slot ring_read(const Ring& g, const SpmvArgs& a, uint32_t eb, uint32_t e) {
-    Slot sl{make_uint4(0, 0, 0, 0), 0u};
-    if (eb < e) {
-        const uint32_t rel = ring_rel(g, a, eb);
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
-                     : "r"(g.vbase + 2u * rel));
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(g.dbase + rel / 2u));
-    }
+__device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
+    Slot sl;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
+                 : "r"(g.vbase + 2u * rel));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(g.dbase + rel / 2u));
     return sl;
+}
+
+// Lane data of the step whose lane element is eb (zeros for lanes wholly past the row).
+__device__ __forceinline__ Slot ring_read(const Ring& g, uint32_t eb, uint32_t e) {
+    if (eb < e) return lds_slot(g, (eb - g.ebase) & g.emask);
+    return Slot{make_uint4(0, 0, 0, 0), 0u};
 }
 
 template <int kXMode>
@@ -344,10 +343,13 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
         g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
         g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
-        g.q_iss = g.q_done = E0 / kChunk;
-        g.ebase = g.q_iss * kChunk;
-        g.q_last = E1 > E0 ? (E1 - 1) / kChunk : g.q_iss;
+        g.ebase = E0 & ~(kChunk - 1u);
+        g.emask = a.ring * kChunk - 1u;
+        g.iss_elem = g.ebase;
+        g.stream_end = E1 > E0 ? ((E1 - 1u) & ~(kChunk - 1u)) + kChunk : g.ebase;
         g.ready_end = g.ebase;
+        g.wait_slot = 0;
+        g.wait_phase = 0;
         g.release_mark = g.ebase + kChunk;
         if (lane == 0) {
             for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
@@ -355,10 +357,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (E1 > E0) {
-            do ring_issue(g, a, lane);
-            while (g.q_iss < E0 / kChunk + a.ring && g.q_iss <= g.q_last);
-        }
+        const uint32_t limit = min(g.ebase + a.ring * kChunk, g.stream_end);
+        while (g.iss_elem < limit) ring_issue(g, a, lane);
     }
 
     // Stage x in shared memory: 16-byte loads, issued before the stores.
@@ -417,47 +417,66 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         if (!next_piece(rs, a, w, lane)) return;
     }
 
+    // Unit end after the step pair that ends at step t_after (t_after multiple of 8 or piece end).
+    auto unit_end = [&](uint32_t t_after) {
+        const float red = warp_tree_sum(rs.acc);
+        rs.acc = 0.0f;
+        if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (t_after - 1) / kUnitSteps] = red;
+        rs.row_acc += red;
+    };
+
+    // A step pair at a row edge (ROMA first step, tail step, or a phantom second step).
+    auto edge_pair = [&](uint32_t t) {
+        const uint32_t S = rs.al + t * kStepElts;
+        const bool hasB = t + 1 < rs.tend;
+        const uint32_t Send = S + (hasB ? 2u : 1u) * kStepElts;
+        if (Send > g.ready_end || S >= g.release_mark) ring_advance(g, a, S, Send, lane);
+        const uint32_t eb = S + 8u * lane;
+        const Slot A = ring_read(g, eb, rs.e);
+        const Slot B = hasB ? ring_read(g, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};
+        const uint32_t vmA = lane_mask(eb, rs.s, rs.e);
+        const uint32_t vmB = hasB ? lane_mask(eb + kStepElts, rs.s, rs.e) : 0u;
+        const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
+        const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+        const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+        const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+        const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+        rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
+        rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
+        rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+        const uint32_t t_after = min(t + 2u, rs.tend);
+        if ((t_after % kUnitSteps) == 0 || t_after == rs.tend) unit_end(t_after);
+    };
+
     for (;;) {
-        while (rs.t < rs.tend) {
-            // -- the aligned step pair (t, t+1) of the piece; t+1 may be a phantom
-            const uint32_t S = rs.al + rs.t * kStepElts;
-            const bool hasB = rs.t + 1 < rs.tend;
-            const uint32_t Send = S + (hasB ? 2u : 1u) * kStepElts;
-            if (Send > g.ready_end || S >= g.release_mark) ring_advance(g, a, S, Send, lane);
-            const uint32_t eb = S + 8u * lane;
-            const Slot A = ring_read(g, a, eb, rs.e);
-            const Slot B = hasB ? ring_read(g, a, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};
-            const bool edge = !hasB || rs.t == 0 || rs.t + 2u >= rs.T;
-            if (!edge) {
-                const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
-                const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-                const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-                const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-                const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-                rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
-                rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
-                rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-            } else {
-                const uint32_t vmA = lane_mask(eb, rs.s, rs.e);
-                const uint32_t vmB = hasB ? lane_mask(eb + kStepElts, rs.s, rs.e) : 0u;
-                const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
-                const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-                const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-                const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-                const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-                rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
-                rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
-                rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-            }
-            rs.t = min(rs.t + 2u, rs.tend);
-            // unit end (pairs start at even t, so a unit boundary never falls inside a pair)
-            if ((rs.t % kUnitSteps) == 0 || rs.t == rs.tend) {
-                const float red = warp_tree_sum(rs.acc);
-                rs.acc = 0.0f;
-                if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (rs.t - 1) / kUnitSteps] = red;
-                rs.row_acc += red;
-            }
+        // -- the piece's steps [t0, tend) in aligned pairs; pair p = steps (t0+2p, t0+2p+1)
+        const uint32_t t0 = rs.t;
+        const uint32_t np = (rs.tend - t0 + 1u) / 2u;
+        const bool first_edge = t0 == 0;
+        const bool last_edge = rs.tend == rs.T || ((rs.tend - t0) & 1u);
+        const uint32_t p_lo = first_edge ? 1u : 0u;
+        const uint32_t p_hi = last_edge ? np - 1u : np;
+        if (first_edge) edge_pair(t0);
+        // interior pairs: every lane valid, no masks, no bounds checks
+        uint32_t S = rs.al + (t0 + 2u * p_lo) * kStepElts;
+        for (uint32_t p = p_lo; p < p_hi; ++p, S += 2u * kStepElts) {
+            if (S + 2u * kStepElts > g.ready_end || S >= g.release_mark)
+                ring_advance(g, a, S, S + 2u * kStepElts, lane);
+            const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
+            const Slot A = lds_slot(g, relA);
+            const Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
+            const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
+            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
+            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
+            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+            // t0 is a multiple of 8: a unit ends after every 4th pair (or at the piece end)
+            if ((p & 3u) == 3u || t0 + 2u * p + 2u == rs.tend) unit_end(t0 + 2u * p + 2u);
         }
+        if (last_edge && (np > 1u || !first_edge)) edge_pair(t0 + 2u * (np - 1u));
         // -- piece end
         if (!rs.split) {
             if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);

@@ -29,7 +29,7 @@ struct SpmvArgs {
     const uint32_t* row_ptrs;
     const uint16_t* x;
     uint16_t* y;
-    uint64_t values_bytes, delta_bytes;  // allocated payload sizes (TMA clamp)
+    uint64_t value_elems, delta_bytes;  // allocated payload sizes (TMA clamp)
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)

@@ -232,7 +232,7 @@ def test_plan_and_x_staging_do_not_change_y(cuda):
                 try:
                     dm.configure(x_mode, ctas)
                 except ValueError:  # the x table would not leave room for the TMA rings
-                    assert x_mode > 0 and C * 2 * x_mode > 100_000
+                    assert x_mode > 0 and C * 2 * x_mode >= 64_000
                     continue
                 assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, x_mode, ctas)
 
