@@ -190,6 +190,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2511_13061_b200 import macko as M
+    from paper_2511_13061_b200.sharded import RowShardedSpmv, device_local_spmv
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -214,7 +215,6 @@ def main():
     x = torch.empty(C, dtype=torch.float16, device=dev)
     M.gen_vector(x, C, seed=SEED_X)
     y = torch.empty(R, dtype=torch.float16, device=dev)
-    y_all = torch.empty(R * world, dtype=torch.float16, device=dev) if world > 1 else None
     bytes_rank = dm.traffic_bytes
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.int32, device=dev)
@@ -223,14 +223,15 @@ def main():
     def l2_flush():
         flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back
 
-    def step():
-        if world > 1:
-            dist.broadcast(x, src=0)
-        dm.spmv_into(x, y, stream)
-        if world > 1:
-            dist.all_gather_into_tensor(y_all, y)
+    # N > 1: rows [rank*R, (rank+1)*R) of an (N*R) x C matrix; NCCL broadcast(x) + SpMV + all_gather(y)
+    sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev) if world > 1 else None
 
-    # ---- compressor timing (K2a/b/c + host readback), reported as a side number
+    def step():
+        if sharded is not None:
+            sharded(x)
+        else:
+            dm.spmv_into(x, y, stream)
+
     # ---- dense cuBLAS GEMV on the same matrix (before freeing the dense copy)
     dense_us = None
     if rank == 0:

@@ -1,0 +1,72 @@
+"""Row sharding over torch.distributed with world_size 2 on CPU (gloo).
+
+The per-rank product is the CPU oracle on the rank's slab (test infrastructure); the plumbing
+under test — slab bounds, x broadcast, ordered y gather, uneven slabs — is the same
+RowShardedSpmv the GPU bench uses over NCCL.  Slab encodings must equal the global encoding
+sliced, and the gathered y must equal the single-process y bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, R, C, d, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2511_13061_b200.sharded import RowShardedSpmv, slab_bounds
+
+        r0, r1 = slab_bounds(R, world, rank)
+        A = O.gen_dense(R, C, d, 7)[r0:r1]
+        m = O.encode_dense(A)
+
+        def local(x, y):
+            xh = x.view(torch.int16).numpy().view(np.uint16)
+            y.view(torch.int16).copy_(torch.from_numpy(O.reference_spmv(m, xh).view(np.int16)))
+
+        sh = RowShardedSpmv(R, C, local)
+        x = torch.zeros(C, dtype=torch.float16)
+        if rank == 0:
+            x.view(torch.int16).copy_(torch.from_numpy(O.gen_vector(C, 8).view(np.int16)))
+        y = sh(x)
+        if rank == 0:
+            np.save(out_path, y.view(torch.int16).numpy().view(np.uint16))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("R,C,d", [(64, 300, 0.5), (37, 1000, 0.3)])  # even and uneven slabs
+def test_row_sharded_spmv_gloo_world2(tmp_path, R, C, d):
+    from oracle import oracle as O
+
+    out = str(tmp_path / "y.npy")
+    mp.spawn(_worker, args=(2, _free_port(), R, C, d, out), nprocs=2, join=True)
+    y = np.load(out)
+    A = O.gen_dense(R, C, d, 7)
+    y_ref = O.reference_spmv(O.encode_dense(A), O.gen_vector(C, 8))
+    assert np.array_equal(y, y_ref)
+
+
+def test_slab_bounds_cover_rows():
+    from paper_2511_13061_b200.sharded import slab_bounds
+
+    for R, N in ((131072, 8), (36864, 4), (37, 2), (5, 8)):
+        b = [slab_bounds(R, N, g) for g in range(N)]
+        assert b[0][0] == 0 and b[-1][1] == R
+        assert all(b[i][1] == b[i + 1][0] for i in range(N - 1))
+        assert max(y - x for x, y in b) - min(y - x for x, y in b) <= 1
