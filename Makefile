@@ -27,3 +27,14 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib oracle clean
+
+# C++ drop-in test (reference headers + our header); needs /root/reference at build time.
+REF_SRC ?= /root/reference/proj/src
+cpptest: lib oracle
+	@if [ -d "$(REF_SRC)" ]; then \
+	  $(NVCC) $(ARCH) -std=c++20 -O2 -I include -I $(REF_SRC) tests/cpp/dropin_test.cpp -o tests/cpp/dropin_test \
+	    -L $(PKG) -L oracle/_ref -lmacko_cuda -lmacko_ref \
+	    -Xlinker -rpath,'$$ORIGIN/../../$(PKG)' -Xlinker -rpath,'$$ORIGIN/../../oracle/_ref'; \
+	else echo "cpptest: $(REF_SRC) absent, keeping prebuilt tests/cpp/dropin_test"; fi
+
+.PHONY: cpptest
