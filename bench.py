@@ -217,8 +217,7 @@ def main():
     y = torch.empty(R, dtype=torch.float16, device=dev)
     bytes_rank = dm.traffic_bytes
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.int32, device=dev)
-    flush.fill_(1)
+    flush = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
 
     def l2_flush():
         flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back

@@ -440,9 +440,12 @@ int mo_warp_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* va
     return MO_OK;
 }
 
-/* The B200 kernel's order: as warp_spmv, but every `unit_steps` steps the lane
- * accumulators are tree-reduced and the unit sum is added to a sequential row accumulator
- * that starts at +0.  unit_steps = 0 means "one unit per row" (= warp_spmv). */
+/* The B200 kernel's order: as warp_spmv, but the row's steps (256 elements from
+ * the ROMA-aligned start) are grouped into units of `unit_steps` steps, the last unit absorbing
+ * a remainder shorter than `unit_steps` (a row of T steps has max(1, T / unit_steps) units).
+ * At every unit end the lane accumulators are tree-reduced and the unit sum is added to a
+ * sequential row accumulator that starts at +0.  unit_steps = 0 means "one unit per row"
+ * (= warp_spmv). */
 int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values,
                        const uint8_t* deltas, const uint32_t* rp, const uint16_t* x, uint16_t* y,
                        unsigned unit_steps) {
@@ -450,13 +453,17 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
     for (uint64_t r = 0; r < rows; ++r) {
         const uint64_t s = rp[r], e = rp[r + 1];
         const uint64_t a0 = s & ~(uint64_t)7;
+        const uint64_t T = e > s ? (e - a0 + 255) / 256 : 0;
+        uint64_t n_units = 1;
+        if (unit_steps && T >= unit_steps) n_units = T / unit_steps;
         float row_acc = 0.0f;
         int64_t col = -1;
         uint64_t i = s;
-        for (uint64_t a = a0, step = 0; a < e; ++step) {
+        for (uint64_t j = 0; j < n_units && T; ++j) {
             float acc[32] = {0};
-            const uint64_t nsteps = unit_steps ? unit_steps : ~(uint64_t)0;
-            for (uint64_t t = 0; t < nsteps && a < e; ++t, a += 256) {
+            const uint64_t t_end = (j + 1 == n_units) ? T : (j + 1) * unit_steps;
+            for (uint64_t t = unit_steps ? j * unit_steps : 0; t < t_end; ++t) {
+                const uint64_t a = a0 + 256 * t;
                 const uint64_t hi = a + 256 < e ? a + 256 : e;
                 for (; i < hi; ++i) {
                     col += code_at(deltas, i, bits) + 1;
@@ -465,7 +472,6 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
                 }
             }
             row_acc += lane_tree(acc);
-            (void)step;
         }
         y[r] = mo_float_to_half(row_acc);
     }

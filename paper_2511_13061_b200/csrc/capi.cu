@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -112,12 +113,19 @@ struct macko_dev_matrix {
     int grid = 0, ctas_per_sm = 0;
     uint32_t n_chunks = 0, n_split = 0;
     uint64_t n_units = 0;
-    DevBuf<uint32_t> plan_u32;   // chunk_unit | chunk_row | chunk_j | split_slot | split_first | split_pieces | counters
-    DevBuf<int32_t> plan_i32;    // chunk_colbase | chunk_sid
+    DevBuf<uint32_t> plan_recs;  // W mk::WarpPlan records
+    DevBuf<uint32_t> plan_u32;   // S split records {slot, first, pieces, 0} | S counters
     DevBuf<float> partials;
     mk::SpmvPlanDev plan{};
     // scratch for macko_spmv_host
     DevBuf<uint16_t> hx, hy;
+    // x as a 1-D fp16 texture for x_mode >= 3 (created per x buffer, reused while it stays the same)
+    mutable std::mutex tex_mu;
+    mutable const void* tex_ptr = nullptr;
+    mutable cudaTextureObject_t tex = 0;
+    ~macko_dev_matrix() {
+        if (tex) cudaDestroyTextureObject(tex);
+    }
 };
 
 namespace {
@@ -141,7 +149,9 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     const size_t budget = (size_t)optin - kSpmvWarpsPerCta * kMaxRing * 8 - 1024;
     const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunkDBytes);
-    auto x_bytes = [&](int mode) { return mode == 2 ? align_up(m->cols * 4, 128) : mode == 1 ? align_up(m->cols * 2, 128) : 0; };
+    auto x_bytes = [&](int mode) {
+        return (mode >= 2 && mode <= 5) ? align_up(m->cols * 4, 128) : (mode == 1 || mode >= 6) ? align_up(m->cols * 2, 128) : 0;
+    };
     auto ring_for = [&](int mode) -> uint32_t {
         const size_t xb = x_bytes(mode);
         if (xb >= budget) return 0;
@@ -153,12 +163,16 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         m->x_mode = m->force_x_mode;
     } else {
         // prefer the pair table (fewer gather wavefronts), then the fp16 table, then global x
-        m->x_mode = ring_for(2) >= 2 ? 2 : ring_for(1) >= 2 ? 1 : 0;
+        m->x_mode = ring_for(6) >= 2 ? 6 : ring_for(1) >= 2 ? 1 : 0;
     }
     m->ring = ring_for(m->x_mode);
     if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
     m->ring_offset = x_bytes(m->x_mode);
     m->smem = m->ring_offset + m->ring * per_slot;
+    if (m->x_mode >= 3) {  // the no-texture fallback (unaligned x) launches with the same smem
+        int dummy = 0;
+        ck(spmv_occupancy(m->x_mode >= 6 ? 1 : 2, m->smem, &dummy), "spmv occupancy");
+    }
     ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
     m->ctas_per_sm = 1;  // one persistent 32-warp CTA per SM
@@ -173,17 +187,18 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     auto row_geom = [&](uint64_t r, uint64_t& T, uint64_t& n_r) {
         const uint64_t s = rp[r], e = rp[r + 1], al = s & ~7ull;
         T = e > s ? (e - al + kStepElts - 1) / kStepElts : 0;
-        n_r = T ? (T + kUnitSteps - 1) / kUnitSteps : 1;
+        n_r = T >= (uint64_t)kUnitSteps ? T / kUnitSteps : 1;  // the last unit absorbs a short remainder
     };
-    auto unit_weight = [&](uint64_t T, uint64_t j) {
-        const uint64_t steps = T ? std::min<uint64_t>(kUnitSteps, T - j * kUnitSteps) : 0;
+    auto unit_end_step = [&](uint64_t T, uint64_t n_r, uint64_t j) { return j + 1 == n_r ? T : (j + 1) * kUnitSteps; };
+    auto unit_weight = [&](uint64_t T, uint64_t n_r, uint64_t j) {
+        const uint64_t steps = unit_end_step(T, n_r, j) - std::min<uint64_t>(T, j * kUnitSteps);
         return steps * kStepElts + (j == 0 ? kRowOverhead : 0);
     };
     uint64_t total_w = 0, U = 0;
     for (uint64_t r = 0; r < R; ++r) {
         uint64_t T, n_r;
         row_geom(r, T, n_r);
-        for (uint64_t j = 0; j < n_r; ++j) total_w += unit_weight(T, j);
+        for (uint64_t j = 0; j < n_r; ++j) total_w += unit_weight(T, n_r, j);
         U += n_r;
     }
     m->n_units = U;
@@ -202,7 +217,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         int64_t kf = -1, kl = -1;
         uint64_t first_units = 0, pieces = 0;
         for (uint64_t j = 0; j < n_r; ++j, ++u) {
-            const uint64_t w = unit_weight(T, j);
+            const uint64_t w = unit_weight(T, n_r, j);
             const uint64_t mid2 = 2 * cw + w;  // twice the unit midpoint
             int64_t k = (int64_t)((unsigned __int128)mid2 * W / (2 * (unsigned __int128)std::max<uint64_t>(total_w, 1)));
             if (k >= (int64_t)W) k = W - 1;
@@ -216,7 +231,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
             if (T) {  // element range of the unit's steps, clamped to the payload
                 const uint64_t al = rp[r] & ~7ull;
                 const uint32_t lo = (uint32_t)(al + j * kUnitElts);
-                const uint32_t hi = (uint32_t)std::min<uint64_t>(al + kStepElts * std::min<uint64_t>((j + 1) * kUnitSteps, T), pad_nnz);
+                const uint32_t hi = (uint32_t)std::min<uint64_t>(al + kStepElts * unit_end_step(T, n_r, j), pad_nnz);
                 if (chunk_e[2 * k + 1] == 0) chunk_e[2 * k] = lo;
                 chunk_e[2 * k + 1] = std::max(chunk_e[2 * k + 1], hi);
             }
@@ -242,38 +257,41 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     }
     const uint32_t S = (uint32_t)split_slot.size();
     m->n_split = S;
-    // upload
-    const size_t n_u32 = (W + 1) + 4 * (size_t)W + 4 * (size_t)S + 1;
-    m->plan_u32.alloc(n_u32);
-    m->plan_i32.alloc(3 * (size_t)W);
+    // upload: one 48-byte record per warp, one 16-byte record per split row, counters
+    std::vector<mk::WarpPlan> recs(W);
+    for (uint32_t k = 0; k < W; ++k) {
+        mk::WarpPlan& c = recs[k];
+        c.units_left = chunk_unit[k + 1] - chunk_unit[k];
+        c.row = chunk_row[k];
+        c.j = chunk_j[k];
+        c.e0 = chunk_e[2 * (size_t)k];
+        c.e1 = chunk_e[2 * (size_t)k + 1];
+        c.s = c.units_left ? rp[c.row] : 0;
+        c.e = c.units_left ? rp[c.row + 1] : 0;
+        c.colbase = -1;  // plan_colbase_kernel
+        c.sid0 = chunk_sid[2 * (size_t)k];
+        c.sid1 = chunk_sid[2 * (size_t)k + 1];
+        c.slot0 = c.sid0 >= 0 ? split_slot[c.sid0] : 0;
+        c.slot1 = c.sid1 >= 0 ? split_slot[c.sid1] : 0;
+    }
+    std::vector<uint32_t> sp(4 * (size_t)S + 4 * (size_t)((S + 3) / 4 + 1), 0);  // splits, then counters
+    for (uint32_t q = 0; q < S; ++q) {
+        sp[4 * (size_t)q] = split_slot[q];
+        sp[4 * (size_t)q + 1] = split_first[q];
+        sp[4 * (size_t)q + 2] = split_pieces[q];
+    }
+    m->plan_recs.alloc(recs.size() * sizeof(mk::WarpPlan) / 4);
+    m->plan_u32.alloc(sp.size());
     m->partials.alloc(std::max<uint64_t>(slots, 1));
-    uint32_t* pu = m->plan_u32.p;
-    std::vector<uint32_t> hu;
-    hu.reserve(n_u32);
-    hu.insert(hu.end(), chunk_unit.begin(), chunk_unit.end());
-    hu.insert(hu.end(), chunk_row.begin(), chunk_row.end());
-    hu.insert(hu.end(), chunk_j.begin(), chunk_j.end());
-    hu.insert(hu.end(), chunk_e.begin(), chunk_e.end());
-    hu.insert(hu.end(), split_slot.begin(), split_slot.end());
-    hu.insert(hu.end(), split_first.begin(), split_first.end());
-    hu.insert(hu.end(), split_pieces.begin(), split_pieces.end());
-    hu.resize(n_u32, 0);  // counters (S) zeroed + 1 spare
-    ck(cudaMemcpyAsync(pu, hu.data(), n_u32 * 4, cudaMemcpyHostToDevice, st), "plan upload");
-    int32_t* pi = m->plan_i32.p;
-    ck(cudaMemcpyAsync(pi + W, chunk_sid.data(), chunk_sid.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
+    ck(cudaMemcpyAsync(m->plan_recs.p, recs.data(), recs.size() * sizeof(mk::WarpPlan), cudaMemcpyHostToDevice, st),
+       "plan upload");
+    ck(cudaMemcpyAsync(m->plan_u32.p, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
     mk::SpmvPlanDev& P = m->plan;
-    P.chunk_unit = pu;
-    P.chunk_row = pu + (W + 1);
-    P.chunk_j = pu + (W + 1) + W;
-    P.chunk_e = pu + (W + 1) + 2 * (size_t)W;
-    P.split_slot = pu + (W + 1) + 4 * (size_t)W;
-    P.split_first = P.split_slot + S;
-    P.split_pieces = P.split_first + S;
-    P.counters = pu + (W + 1) + 4 * (size_t)W + 3 * (size_t)S;
-    P.chunk_colbase = pi;
-    P.chunk_sid = pi + W;
+    P.warps = reinterpret_cast<const mk::WarpPlan*>(m->plan_recs.p);
+    P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
+    P.counters = m->plan_u32.p + 4 * (size_t)S;
     P.partials = m->partials.p;
-    ck(launch_plan_colbase(m->deltas.p, m->row_ptrs.p, P.chunk_row, P.chunk_j, pi, W, st), "plan colbase");
+    ck(launch_plan_colbase(m->deltas.p, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st), "plan colbase");
     g_launches.fetch_add(1);
     ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
 }
@@ -292,6 +310,31 @@ void device_validate(macko_dev_matrix* m, cudaStream_t st) {
     if (h & 4u) fail(MACKO_EFORMAT, "row_pointers not monotone");
     if (h & 1u) fail(MACKO_EFORMAT, "decoded column index past the column bound");
     if (h & 2u) fail(MACKO_EFORMAT, "padding value must be +0");
+}
+
+// Texture view of x for the TEX-pipe gathers; 0 when x is not suitably aligned (the kernel then
+// falls back to the pair table alone, x_mode 2, which uses the same shared-memory layout).
+cudaTextureObject_t x_texture(const macko_dev_matrix* m, const uint16_t* d_x) {
+    std::lock_guard<std::mutex> lk(m->tex_mu);
+    if (m->tex && m->tex_ptr == d_x) return m->tex;
+    int align = 0;
+    ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
+    if (align > 0 && reinterpret_cast<uintptr_t>(d_x) % (uintptr_t)align != 0) return 0;
+    if (m->tex) {
+        cudaDestroyTextureObject(m->tex);
+        m->tex = 0;
+        m->tex_ptr = nullptr;
+    }
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = const_cast<uint16_t*>(d_x);
+    rd.res.linear.desc = cudaCreateChannelDesc<unsigned short>();
+    rd.res.linear.sizeInBytes = m->cols * 2;
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    ck(cudaCreateTextureObject(&m->tex, &rd, &td, nullptr), "x texture");
+    m->tex_ptr = d_x;
+    return m->tex;
 }
 
 void check_shape(uint64_t rows, uint64_t cols) {
@@ -339,8 +382,9 @@ macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t
         m->pad_nnz = pad_nnz;
         m->b_delta = b_delta;
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
-        m->values.alloc(std::max<uint64_t>(vb / 2, 8));
-        m->deltas.alloc(std::max<uint64_t>(db, 16));
+        // one zeroed TMA chunk of slack past the payload: the SpMV's ring copies are never clamped
+        m->values.alloc(vb / 2 + mk::kChunk);
+        m->deltas.alloc(db + mk::kChunkDBytes);
         m->row_ptrs.alloc(rows + 1);
         ck(cudaMemsetAsync(m->values.p, 0, m->values.n * 2, st), "memset");
         ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
@@ -392,8 +436,8 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         if (pad_nnz > 0xFFFFFFFFull) fail(MACKO_EINVAL, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
         m->pad_nnz = pad_nnz;
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
-        m->values.alloc(std::max<uint64_t>(vb / 2, 8));
-        m->deltas.alloc(std::max<uint64_t>(align_up(db, 16), 16));
+        m->values.alloc(vb / 2 + mk::kChunk);  // + one zeroed TMA chunk of slack (see upload)
+        m->deltas.alloc(db + mk::kChunkDBytes);
         ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
         if (m->values.n * 2 > pad_nnz * 2)
             ck(cudaMemsetAsync(m->values.p + pad_nnz, 0, m->values.n * 2 - pad_nnz * 2, st), "memset");
@@ -463,7 +507,13 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
-        ck(mk::launch_spmv(a, m->grid, m->x_mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
+        a.xtex = 0;
+        int mode = m->x_mode;
+        if (mode >= 3) {
+            a.xtex = x_texture(m, d_x);
+            if (!a.xtex) mode = mode >= 6 ? 1 : 2;  // same shared-memory layout, no TEX
+        }
+        ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
         g_launches.fetch_add(1);
     });
 }
@@ -531,9 +581,9 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream) {
     return guarded([&] {
         if (!m) fail(MACKO_EINVAL, "null handle");
-        if (x_mode < -1 || x_mode > 2) fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 2");
-        if (x_mode == 2 && m->cols * 4 > 220 * 1024) fail(MACKO_EINVAL, "pair table does not fit shared memory");
-        if (x_mode == 1 && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
+        if (x_mode < -1 || x_mode > 9) fail(MACKO_EINVAL, "x_mode must be -1 (auto) or 0..9");
+        if (x_mode >= 2 && x_mode <= 5 && m->cols * 4 > 220 * 1024) fail(MACKO_EINVAL, "pair table does not fit shared memory");
+        if ((x_mode == 1 || x_mode >= 6) && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
         if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
         DeviceGuard g(m->device);
         m->force_x_mode = x_mode;

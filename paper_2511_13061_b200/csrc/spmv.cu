@@ -50,12 +50,36 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     return v;
 }
 
-// x gather: kXMode 0 = global (L1), 1 = fp16 table in smem, 2 = pair table in smem
+// x gather: kXMode 0 = global (L1), 1 = fp16 table in smem, 2 = pair table in smem,
+// 3..5 = pair table + texture fetches (TEX pipe) for the odd elements of pairs m >= tex_from.
 template <int kXMode>
 __device__ __forceinline__ uint16_t xget(uint32_t xs_addr, const uint16_t* __restrict__ xg, int col) {
     if constexpr (kXMode == 0) return __ldg(xg + col);
-    if constexpr (kXMode == 1) return lds_u16(xs_addr + 2u * (uint32_t)col);
+    if constexpr (kXMode == 1 || kXMode >= 6) return lds_u16(xs_addr + 2u * (uint32_t)col);
     return lds_u16(xs_addr + 4u * (uint32_t)col);
+}
+
+template <int kXMode>
+constexpr int tex_from() {
+    return kXMode == 3 ? 1 : kXMode == 4 ? 0 : kXMode == 5 ? 2 : 4;
+}
+
+// x_mode >= 6: fp16 table in smem + fp16 texture; lane element slot k (0..7) of every step is
+// gathered by TEX when bit k of tex_slots is set, else by LDS.  The split balances the LSU
+// data pipe (values/deltas, shuffles, LDS gathers) against the TEX data pipe (~1 wavefront per
+// 128-B line a gather touches) — profiles/r01_pipes.md.
+template <int kXMode>
+constexpr uint32_t tex_slots() {
+    return kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 9 ? 0x92u : 0u;
+}
+
+template <int kXMode>
+constexpr bool pair_table() {
+    return kXMode >= 2 && kXMode <= 5;
+}
+
+__device__ __forceinline__ uint16_t xtex(cudaTextureObject_t t, int col) {
+    return tex1Dfetch<unsigned short>(t, col);
 }
 
 // valid-element mask of a lane whose first element is eb, for the row [s, e)
@@ -92,10 +116,10 @@ __device__ __forceinline__ Dec decode(uint32_t d, uint32_t vm) {
 // 8 gathers + FHFMAs of one unmasked lane step.  cb = column before the lane's first element.
 template <int kXMode>
 __device__ __forceinline__ float fma_fast(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
-                                          const uint16_t* __restrict__ xg) {
+                                          const uint16_t* __restrict__ xg, cudaTextureObject_t xt) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     // shared address of column cb: per element one PRMT (byte extract) + one LEA
-    uint32_t base = xs_addr + (uint32_t)cb * (kXMode == 2 ? 4u : 2u);
+    uint32_t base = xs_addr + (uint32_t)cb * (pair_table<kXMode>() ? 4u : 2u);
     asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + (b << k) a single LEA per element
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -103,12 +127,20 @@ __device__ __forceinline__ float fma_fast(float acc, const uint4& v, const Dec& 
         split_halves(w[m], v0, v1);
         const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
         const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
-        if constexpr (kXMode == 2) {
-            // (x[c0], x[c0+1]) in one gather; the odd element reuses the high half when adjacent
+        if constexpr (kXMode >= 6) {
+            const uint16_t x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + (b0 << 1));
+            const uint16_t x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + (b1 << 1));
+            acc = fma_f16f16f32(v0, x0, acc);
+            acc = fma_f16f16f32(v1, x1, acc);
+        } else if constexpr (kXMode >= 2) {
+            // (x[c0], x[c0+1]) in one gather; the odd element reuses the high half when adjacent,
+            // else gathers from the pair table (LSU pipe) or the texture (TEX pipe)
             const uint32_t xa = lds_u32(base + (b0 << 2));
             acc = fma_f16f16f32(v0, (uint16_t)(xa & 0xFFFFu), acc);
             if (((dc.dh >> (8 * m)) & 0xFFu) == 1u)
                 acc = fma_f16f16f32(v1, (uint16_t)(xa >> 16), acc);
+            else if (m >= tex_from<kXMode>())
+                acc = fma_f16f16f32(v1, xtex(xt, cb + (int)b1), acc);
             else
                 acc = fma_f16f16f32(v1, lds_u16(base + (b1 << 2)), acc);
         } else if constexpr (kXMode == 1) {
@@ -148,73 +180,82 @@ __device__ __forceinline__ float fma_masked(float acc, const uint4& v, const Dec
 // Compute-side row state
 // ------------------------------------------------------------------------------------------
 struct RowState {
-    uint32_t r, s, e, al, T, t, tend, j0, n_r, units_left, slot;
+    uint32_t r, s, e, e_next, al, T, t, tend, j0, n_r, last_b, units_left, slot;
     int32_t sid;
-    bool split, first_row;
+    bool split;
     int col_base;
     float acc, row_acc;
 };
 
-// Set up the piece of row rs.r starting at unit j0.
-__device__ __forceinline__ void begin_piece(RowState& rs, const SpmvArgs& a, uint32_t w, uint32_t j0, int colbase) {
-    rs.s = __ldg(a.row_ptrs + rs.r);
-    rs.e = __ldg(a.row_ptrs + rs.r + 1);
+// Set up the piece of row rs.r = [rs.s, rs.e) starting at unit j0.  sid / slot: the chunk's
+// split-row id for this piece (used only if the piece turns out to be split).
+__device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colbase, int32_t sid, uint32_t slot) {
     rs.al = rs.s & ~7u;
     rs.T = rs.e > rs.s ? (rs.e - rs.al + kStepElts - 1) / kStepElts : 0u;
-    rs.n_r = rs.T ? (rs.T + kUnitSteps - 1) / kUnitSteps : 1u;
+    // units of kUnitSteps steps; the last unit absorbs a remainder shorter than a unit
+    rs.n_r = rs.T >= (uint32_t)kUnitSteps ? rs.T / kUnitSteps : 1u;
+    rs.last_b = (rs.n_r - 1u) * kUnitSteps;
     const uint32_t nu = min(rs.n_r - j0, rs.units_left);
     rs.units_left -= nu;
     rs.j0 = j0;
     rs.t = j0 * kUnitSteps;
-    rs.tend = min(rs.T, (j0 + nu) * kUnitSteps);
+    rs.tend = j0 + nu == rs.n_r ? rs.T : (j0 + nu) * kUnitSteps;
     rs.split = !(j0 == 0 && j0 + nu == rs.n_r);
-    rs.sid = -1;
-    rs.slot = 0;
-    if (rs.split) {
-        rs.sid = rs.first_row ? a.plan.chunk_sid[2 * w] : a.plan.chunk_sid[2 * w + 1];
-        rs.slot = a.plan.split_slot[rs.sid];
-    }
+    rs.sid = sid;
+    rs.slot = slot;
     rs.col_base = colbase;
     rs.acc = 0.0f;
     rs.row_acc = 0.0f;
 }
 
-// Finish the current piece (write y or hand the split row to its last arrival).
+// Finish the current piece (write y or hand the split row to its last arrival).  Lane 0 wrote
+// the piece's unit partials; the release atomic orders them before its arrival (no full fence,
+// no L1 invalidation), and the last arrival reads every partial from L2 (ld.cg).
 __device__ __noinline__ void finish_split(uint32_t r, uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot,
                                           int32_t sid, float row_acc, const SpmvPlanDev P, uint16_t* y, int lane) {
-    uint32_t last = 0;
+    uint32_t last = 0, first = 0;
     if (lane == 0) {
-        if (j0 == 0) P.partials[slot + (tend - 1) / kUnitSteps] = row_acc;
-        __threadfence();
-        const uint32_t prev = atomicAdd(P.counters + sid, 1u);
-        last = prev + 1 == P.split_pieces[sid];
+        if (j0 == 0) P.partials[slot + tend / kUnitSteps - 1u] = row_acc;  // a first piece ends on a unit boundary
+        const uint4 sp = P.splits[sid];
+        first = sp.y;
+        uint32_t prev;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
+        last = prev + 1 == sp.z;
     }
     last = __shfl_sync(kFull, last, 0);
     if (last && lane == 0) {
-        __threadfence();
-        const uint32_t f = P.split_first[sid];
-        float tot = __ldcg(P.partials + slot + f - 1);
-        for (uint32_t q = f; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
+        float tot = __ldcg(P.partials + slot + first - 1);
+        for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
         y[r] = f32_to_f16_rn(tot);
         P.counters[sid] = 0;  // ready for the next launch (stream order)
     }
 }
 
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
-// when the chunk is exhausted.
+// when the chunk is exhausted.  The row pointer after the next row is prefetched one row ahead.
 __device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint32_t w, int lane) {
     for (;;) {
         if (rs.units_left == 0) return false;
         ++rs.r;
-        rs.first_row = false;
-        begin_piece(rs, a, w, 0, -1);
+        rs.s = rs.e;
+        rs.e = rs.e_next;
+        if (rs.r + 2u <= a.rows) rs.e_next = __ldg(a.row_ptrs + rs.r + 2u);
+        begin_piece(rs, 0, -1, -1, 0);
+        if (rs.split) {  // only the chunk's last row can be cut here: its split id is in the record
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.plan.warps + w) + 2);
+            rs.sid = (int32_t)q.y;
+            rs.slot = q.w;
+        }
         if (rs.T) return true;
         if (lane == 0) a.y[rs.r] = 0;  // empty row: fp16(+0.0)
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// Per-warp TMA ring of 512-element chunks (values 1 KiB + deltas 256 B per chunk)
+// Per-warp TMA ring of kChunk-element chunks (values 2 KiB + deltas 512 B per chunk).  The warp
+// streams its contiguous element range through the ring with cp.async.bulk + mbarrier
+// complete_tx; a slot is refilled (chunk k -> chunk k + ring) as soon as the walk has moved past
+// chunk k.  The payload buffers carry one zeroed chunk of slack, so copies are never clamped.
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
@@ -241,57 +282,54 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 struct Ring {
     uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
     uint32_t ebase, emask;        // element e lives at ring offset (e - ebase) & emask
-    uint32_t iss_elem;            // producer: first element of the next chunk to issue
+    uint32_t iss;                 // first element of the next chunk to issue
     uint32_t stream_end;          // end (exclusive, chunk aligned) of the warp's chunk stream
-    uint32_t ready_end;           // consumer: elements below this have landed
-    uint32_t wait_slot, wait_phase;
-    uint32_t release_mark;        // next chunk boundary at which a slot becomes refillable
+    uint32_t ready_end;           // elements below this have landed
+    uint32_t rel_mark;            // once S >= rel_mark, the oldest resident chunk's slot is refilled
+    uint32_t wslot, wphase;
 };
 
-// Issue the TMA copies of the chunk starting at element g.iss_elem (lane 0).
-__device__ __forceinline__ void ring_issue(Ring& g, const SpmvArgs& a, int lane) {
+// Copy the chunk starting at element g.iss into its slot (lane 0; full-size, never clamped).
+__device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int lane) {
     if (lane == 0) {
-        const uint32_t e0 = g.iss_elem;
+        const uint32_t e0 = g.iss;
         const uint32_t rel = (e0 - g.ebase) & g.emask;
-        uint32_t vb = kChunkVBytes, db = kChunkDBytes;
-        if (e0 + kChunk > a.value_elems) {  // the payload's last chunk: clamp to the buffers
-            vb = 2u * (a.value_elems - e0);
-            const uint64_t dleft = a.delta_bytes - e0 / 2;
-            db = dleft < kChunkDBytes ? (uint32_t)dleft : kChunkDBytes;
-        }
         const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
         // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
-        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb + db)
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "n"(kChunkVBytes + kChunkDBytes)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          g.vbase + 2u * rel),
-                     "l"(a.values + e0), "r"(vb), "r"(bar)
+                     "l"(a.values + e0), "n"(kChunkVBytes), "r"(bar)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          g.dbase + rel / 2u),
-                     "l"(a.deltas + e0 / 2), "r"(db), "r"(bar)
+                     "l"(a.deltas + e0 / 2), "n"(kChunkDBytes), "r"(bar)
                      : "memory");
     }
-    g.iss_elem += kChunk;
 }
 
-// Make elements [S, Send) resident: refill every slot whose chunk lies wholly below S (its data
-// was consumed by every lane — the LDS results fed earlier FHFMAs — and the warp-converged
-// refill is issued after them), then wait for the chunks covering Send.
-__device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_t S, uint32_t Send, int lane) {
-    const uint32_t floor_s = S & ~(kChunk - 1u);
-    const uint32_t limit = min(floor_s + a.ring * kChunk, g.stream_end);
-    if (g.iss_elem < limit) {
-        __syncwarp();
-        do ring_issue(g, a, lane);
-        while (g.iss_elem < limit);
-    }
-    g.release_mark = floor_s + kChunk;
+// The walk is at S: every chunk wholly below S was consumed by all lanes (their LDS results fed
+// earlier FHFMAs; __syncwarp orders them before lane 0's copy), so its slot takes a new chunk.
+__device__ __forceinline__ void ring_refill(Ring& g, const SpmvArgs& a, uint32_t S, int lane) {
+    __syncwarp();
+    do {
+        if (g.iss < g.stream_end) {
+            ring_issue(g, a, lane);
+            g.iss += kChunk;
+        }
+        g.rel_mark += kChunk;
+    } while (S >= g.rel_mark);
+}
+
+// Make elements below Send resident (chunk granularity).
+__device__ __forceinline__ void ring_wait(Ring& g, uint32_t Send, uint32_t nslots) {
     const uint32_t need = min(Send, g.stream_end);
     while (g.ready_end < need) {
-        mbar_wait(g.bar0 + 8u * g.wait_slot, g.wait_phase);
-        g.wait_slot = (g.wait_slot + 1u) & (a.ring - 1u);
-        g.wait_phase ^= g.wait_slot == 0 ? 1u : 0u;
+        mbar_wait(g.bar0 + 8u * g.wslot, g.wphase);
+        g.wslot = (g.wslot + 1u) & (nslots - 1u);
+        g.wphase ^= g.wslot == 0 ? 1u : 0u;
         g.ready_end += kChunk;
     }
 }
@@ -325,32 +363,27 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t C = a.cols;
     const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
-    const uint32_t u0 = a.plan.chunk_unit[w], u_end = a.plan.chunk_unit[w + 1];
-    const bool has_work = u0 < u_end;
+    const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + w);
+    const uint4 q0 = __ldg(rec), q1 = __ldg(rec + 1), q2 = __ldg(rec + 2);
+    const bool has_work = q0.x != 0;
 
-    // Walk set-up and the first ring fills go out BEFORE x is staged, so the HBM latency of
-    // the matrix stream overlaps the x copy.
+    // The first ring fills go out first; x staging overlaps their HBM latency.
     RowState rs;
     Ring g;
     if (has_work) {
-        rs.r = a.plan.chunk_row[w];
-        rs.units_left = u_end - u0;
-        rs.first_row = true;
-        const uint32_t j0 = a.plan.chunk_j[w];
-        begin_piece(rs, a, w, j0, j0 ? a.plan.chunk_colbase[w] : -1);
-        const uint32_t E0 = a.plan.chunk_e[2 * w], E1 = a.plan.chunk_e[2 * w + 1];
+        const uint32_t E0 = q0.w, E1 = q1.x;
         const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
         g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
         g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
         g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
         g.ebase = E0 & ~(kChunk - 1u);
         g.emask = a.ring * kChunk - 1u;
-        g.iss_elem = g.ebase;
+        g.iss = g.ebase;
         g.stream_end = E1 > E0 ? ((E1 - 1u) & ~(kChunk - 1u)) + kChunk : g.ebase;
         g.ready_end = g.ebase;
-        g.wait_slot = 0;
-        g.wait_phase = 0;
-        g.release_mark = g.ebase + kChunk;
+        g.rel_mark = g.ebase + kChunk;
+        g.wslot = 0;
+        g.wphase = 0;
         if (lane == 0) {
             for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -358,7 +391,18 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         }
         __syncwarp();
         const uint32_t limit = min(g.ebase + a.ring * kChunk, g.stream_end);
-        while (g.iss_elem < limit) ring_issue(g, a, lane);
+        for (; g.iss < limit; g.iss += kChunk) ring_issue(g, a, lane);
+        rs.r = q0.y;
+        rs.units_left = q0.x;
+        rs.s = q1.y;
+        rs.e = q1.z;
+        rs.e_next = rs.r + 2u <= a.rows ? __ldg(a.row_ptrs + rs.r + 2u) : 0u;
+        const uint32_t j0 = q0.z;
+        begin_piece(rs, j0, j0 ? (int)q1.w : -1, (int32_t)q2.x, q2.z);
+        if (rs.split && rs.units_left == 0 && (int32_t)q2.x < 0) {  // first row = last row of the chunk
+            rs.sid = (int32_t)q2.y;
+            rs.slot = q2.w;
+        }
     }
 
     // Stage x in shared memory: 16-byte loads, issued before the stores.
@@ -375,14 +419,14 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
                 const uint32_t i = b0 + u * blockDim.x;
                 if (i < nv) {
                     t[u] = __ldg(x4 + i);
-                    nx[u] = (kXMode == 2 && 8 * i + 8 < C) ? (uint32_t)__ldg(a.x + 8 * i + 8) : 0u;
+                    nx[u] = (kXMode >= 2 && kXMode <= 5 && 8 * i + 8 < C) ? (uint32_t)__ldg(a.x + 8 * i + 8) : 0u;
                 }
             }
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 const uint32_t i = b0 + u * blockDim.x;
                 if (i >= nv) continue;
-                if constexpr (kXMode == 1) {
+                if constexpr (kXMode == 1 || kXMode >= 6) {
                     reinterpret_cast<uint4*>(xs)[i] = t[u];
                 } else {
                     // pair words (x[c], x[c+1]) for c = 8i .. 8i+7
@@ -402,7 +446,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
             }
         }
         for (uint32_t i = nv * 8 + threadIdx.x; i < C; i += blockDim.x) {
-            if constexpr (kXMode == 1)
+            if constexpr (kXMode == 1 || kXMode >= 6)
                 xs[i] = a.x[i];
             else
                 reinterpret_cast<uint32_t*>(xs)[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
@@ -421,7 +465,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
     auto unit_end = [&](uint32_t t_after) {
         const float red = warp_tree_sum(rs.acc);
         rs.acc = 0.0f;
-        if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + (t_after - 1) / kUnitSteps] = red;
+        if (rs.split && rs.j0 > 0 && lane == 0)
+            a.plan.partials[rs.slot + min((t_after - 1u) / kUnitSteps, rs.n_r - 1u)] = red;
         rs.row_acc += red;
     };
 
@@ -430,22 +475,24 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         const uint32_t S = rs.al + t * kStepElts;
         const bool hasB = t + 1 < rs.tend;
         const uint32_t Send = S + (hasB ? 2u : 1u) * kStepElts;
-        if (Send > g.ready_end || S >= g.release_mark) ring_advance(g, a, S, Send, lane);
+        if (S >= g.rel_mark) ring_refill(g, a, S, lane);
+        if (Send > g.ready_end) ring_wait(g, Send, a.ring);
         const uint32_t eb = S + 8u * lane;
         const Slot A = ring_read(g, eb, rs.e);
         const Slot B = hasB ? ring_read(g, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};
         const uint32_t vmA = lane_mask(eb, rs.s, rs.e);
         const uint32_t vmB = hasB ? lane_mask(eb + kStepElts, rs.s, rs.e) : 0u;
         const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
-        const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-        const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+        const uint32_t pk = dA.local | (dB.local << 16);
+        const uint32_t incl = warp_incl_scan_p(pk);
+        const uint32_t tot = __reduce_add_sync(kFull, pk);
         const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
         const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
         rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
         rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
         rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
         const uint32_t t_after = min(t + 2u, rs.tend);
-        if ((t_after % kUnitSteps) == 0 || t_after == rs.tend) unit_end(t_after);
+        if (((t_after % kUnitSteps) == 0 && t_after <= rs.last_b) || t_after == rs.tend) unit_end(t_after);
     };
 
     for (;;) {
@@ -460,21 +507,24 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         // interior pairs: every lane valid, no masks, no bounds checks
         uint32_t S = rs.al + (t0 + 2u * p_lo) * kStepElts;
         for (uint32_t p = p_lo; p < p_hi; ++p, S += 2u * kStepElts) {
-            if (S + 2u * kStepElts > g.ready_end || S >= g.release_mark)
-                ring_advance(g, a, S, S + 2u * kStepElts, lane);
+            if (S >= g.rel_mark) ring_refill(g, a, S, lane);
+            if (S + 2u * kStepElts > g.ready_end) ring_wait(g, S + 2u * kStepElts, a.ring);
             const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
             const Slot A = lds_slot(g, relA);
             const Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
             const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
-            const uint32_t incl = warp_incl_scan_p(dA.local | (dB.local << 16));
-            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            const uint32_t pk = dA.local | (dB.local << 16);
+            const uint32_t incl = warp_incl_scan_p(pk);
+            const uint32_t tot = __reduce_add_sync(kFull, pk);
             const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
             const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x);
-            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x);
+            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x, a.xtex);
+            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x, a.xtex);
             rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-            // t0 is a multiple of 8: a unit ends after every 4th pair (or at the piece end)
-            if ((p & 3u) == 3u || t0 + 2u * p + 2u == rs.tend) unit_end(t0 + 2u * p + 2u);
+            // t0 is a multiple of 8: a unit ends after every 4th pair up to the last unit's start
+            // (the last unit may run up to 15 steps), and at the piece end
+            const uint32_t ta = t0 + 2u * p + 2u;
+            if (((p & 3u) == 3u && ta <= rs.last_b) || ta == rs.tend) unit_end(ta);
         }
         if (last_edge && (np > 1u || !first_edge)) edge_pair(t0 + 2u * (np - 1u));
         // -- piece end
@@ -489,63 +539,69 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
 
 // Column just before the first unit of every chunk that starts inside a row:
 // sum of the row's deltas over [row start, unit start) minus one.  Setup only.
-__global__ void plan_colbase_kernel(const uint8_t* deltas, const uint32_t* row_ptrs, const uint32_t* chunk_row,
-                                    const uint32_t* chunk_j, int32_t* chunk_colbase, uint32_t n_chunks) {
+__global__ void plan_colbase_kernel(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
     if (w >= n_chunks) return;
-    const uint32_t j = chunk_j[w];
-    if (j == 0) {
-        if (lane == 0) chunk_colbase[w] = -1;
+    const uint32_t j = warps[w].j;
+    if (warps[w].units_left == 0 || j == 0) {
+        if (lane == 0) warps[w].colbase = -1;
         return;
     }
-    const uint32_t r = chunk_row[w];
-    const uint32_t s = row_ptrs[r];
+    const uint32_t s = warps[w].s;
     const uint32_t lim = (s & ~7u) + j * kUnitElts;
     uint32_t sum = 0;
     for (uint32_t i = s + lane; i < lim; i += kWarp) sum += ((deltas[i >> 1] >> ((i & 1u) * 4)) & 15u) + 1u;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
-    if (lane == 0) chunk_colbase[w] = (int32_t)sum - 1;
+    if (lane == 0) warps[w].colbase = (int32_t)sum - 1;
 }
 
 }  // namespace
 
-cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
+template <int kXMode>
+static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     const int threads = kSpmvWarpsPerCta * kWarp;
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(macko_spmv_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<kXMode>, threads, smem);
+    return e;
+}
+
+cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
     switch (x_mode) {
-        case 2:
-            e = cudaFuncSetAttribute(macko_spmv_b4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<2>, threads, smem);
-            return e;
-        case 1:
-            e = cudaFuncSetAttribute(macko_spmv_b4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<1>, threads, smem);
-            return e;
-        default:
-            e = cudaFuncSetAttribute(macko_spmv_b4<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<0>, threads, smem);
-            return e;
+        case 9: return occ_one<9>(smem, ctas_per_sm);
+        case 8: return occ_one<8>(smem, ctas_per_sm);
+        case 7: return occ_one<7>(smem, ctas_per_sm);
+        case 6: return occ_one<6>(smem, ctas_per_sm);
+        case 5: return occ_one<5>(smem, ctas_per_sm);
+        case 4: return occ_one<4>(smem, ctas_per_sm);
+        case 3: return occ_one<3>(smem, ctas_per_sm);
+        case 2: return occ_one<2>(smem, ctas_per_sm);
+        case 1: return occ_one<1>(smem, ctas_per_sm);
+        default: return occ_one<0>(smem, ctas_per_sm);
     }
 }
 
 cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s) {
     const int threads = kSpmvWarpsPerCta * kWarp;
-    if (x_mode == 2)
-        macko_spmv_b4<2><<<grid, threads, smem, s>>>(a);
-    else if (x_mode == 1)
-        macko_spmv_b4<1><<<grid, threads, smem, s>>>(a);
-    else
-        macko_spmv_b4<0><<<grid, threads, smem, s>>>(a);
+    switch (x_mode) {
+        case 9: macko_spmv_b4<9><<<grid, threads, smem, s>>>(a); break;
+        case 8: macko_spmv_b4<8><<<grid, threads, smem, s>>>(a); break;
+        case 7: macko_spmv_b4<7><<<grid, threads, smem, s>>>(a); break;
+        case 6: macko_spmv_b4<6><<<grid, threads, smem, s>>>(a); break;
+        case 5: macko_spmv_b4<5><<<grid, threads, smem, s>>>(a); break;
+        case 4: macko_spmv_b4<4><<<grid, threads, smem, s>>>(a); break;
+        case 3: macko_spmv_b4<3><<<grid, threads, smem, s>>>(a); break;
+        case 2: macko_spmv_b4<2><<<grid, threads, smem, s>>>(a); break;
+        case 1: macko_spmv_b4<1><<<grid, threads, smem, s>>>(a); break;
+        default: macko_spmv_b4<0><<<grid, threads, smem, s>>>(a); break;
+    }
     return cudaGetLastError();
 }
-
-cudaError_t launch_plan_colbase(const uint8_t* deltas, const uint32_t* row_ptrs, const uint32_t* chunk_row,
-                                const uint32_t* chunk_j, int32_t* chunk_colbase, uint32_t n_chunks, cudaStream_t s) {
+cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s) {
     const int threads = 256;
     const int blocks = (int)((n_chunks * (uint64_t)kWarp + threads - 1) / threads);
-    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, row_ptrs, chunk_row, chunk_j, chunk_colbase, n_chunks);
+    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, warps, n_chunks);
     return cudaGetLastError();
 }
 

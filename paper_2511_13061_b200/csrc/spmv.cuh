@@ -7,20 +7,26 @@
 namespace mk {
 
 // Static work plan of one matrix (built once on the host by build_plan in capi.cu, kept on the
-// device).  The element stream of the matrix is cut into units of kUnitSteps warp steps per
-// row; each warp ("chunk") owns a contiguous range of units of roughly equal weight.
+// device).  The element stream of the matrix is cut into units of kUnitSteps warp steps per row
+// (the last unit of a row absorbs a remainder shorter than a unit); each warp ("chunk") owns a
+// contiguous range of units of roughly equal weight.  Everything a warp needs to start is in one
+// 48-byte record, so its prologue is a single memory round trip.
+struct WarpPlan {
+    uint32_t units_left;   // units in the chunk (0 = idle warp)
+    uint32_t row, j;       // first unit: its row and its unit index inside the row
+    uint32_t e0, e1;       // [first, end) element of the chunk's TMA stream
+    uint32_t s, e;         // row_ptrs[row], row_ptrs[row + 1]
+    int32_t colbase;       // decoded column just before unit j (-1 if j == 0; set on the device)
+    int32_t sid0, sid1;    // split-row id of the chunk's first / last row piece, or -1
+    uint32_t slot0, slot1; // first partial slot of those split rows
+};
+static_assert(sizeof(WarpPlan) == 48, "WarpPlan is loaded as three 16-byte vectors");
+
 struct SpmvPlanDev {
-    const uint32_t* chunk_unit;     // W+1: first global unit of chunk w
-    const uint32_t* chunk_row;      // W:   row of that unit
-    const uint32_t* chunk_j;        // W:   unit index of that unit inside its row
-    const uint32_t* chunk_e;        // 2W:  [first, end) element of the chunk's stream (TMA range)
-    const int32_t* chunk_colbase;   // W:   decoded column just before that unit (-1 if j == 0)
-    const int32_t* chunk_sid;       // 2W:  split-row id of the chunk's first / last row, or -1
-    const uint32_t* split_slot;     // S:   first partial slot of split row s
-    const uint32_t* split_first;    // S:   units handled by the row's first piece
-    const uint32_t* split_pieces;   // S:   number of chunks touching the row
-    float* partials;                // per split row, one slot per unit
-    uint32_t* counters;             // S:   arrival counters (zero between launches)
+    const WarpPlan* warps;   // W records
+    const uint4* splits;     // S: {first partial slot, units of the first piece, pieces, 0}
+    float* partials;         // per split row, one slot per unit
+    uint32_t* counters;      // S: arrival counters (zero between launches)
 };
 
 struct SpmvArgs {
@@ -29,7 +35,8 @@ struct SpmvArgs {
     const uint32_t* row_ptrs;
     const uint16_t* x;
     uint16_t* y;
-    uint64_t value_elems, delta_bytes;  // allocated payload sizes (TMA clamp)
+    cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode >= 3)
+    uint64_t value_elems, delta_bytes;  // allocated sizes (payload + one zeroed chunk of slack)
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
@@ -43,11 +50,10 @@ constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
 constexpr uint32_t kMaxRing = 8;
 
 // Launchers (return cudaGetLastError()).
-// x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table
+// x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table,
+// 3..5 = pair table + texture gathers for odd elements (TEX pipe in parallel with the LSU pipe)
 cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s);
 cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
-cudaError_t launch_plan_colbase(const uint8_t* deltas, const uint32_t* row_ptrs, const uint32_t* chunk_row,
-                                const uint32_t* chunk_j, int32_t* chunk_colbase, uint32_t n_chunks,
-                                cudaStream_t s);
+cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);
 
 }  // namespace mk
