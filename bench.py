@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="also report 30/50/70/90 %% sparsity and Llama shapes")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
-    p.add_argument("--x-mode", type=int, default=-1, help="x staging: -1 auto, 0 global, 1 fp16 smem, 2 pair smem")
+    p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture only, 1 smem table only, 6..9 smem + texture split")
     p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs per SM (0 = occupancy maximum)")
     return p.parse_args()
 
@@ -218,9 +218,14 @@ def main():
     bytes_rank = dm.traffic_bytes
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    # Inputs several times larger than L2 stream from HBM on every step (verified with ncu on
+    # back-to-back launches: L2 hit rate < 1 %, DRAM bytes = algorithmic bytes); smaller inputs
+    # get an L2 flush (a read of a 2xL2 buffer) before every step, outside the step events.
+    need_flush = bytes_rank < 3 * l2
 
-    def l2_flush():
-        flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back
+    def l2_flush(force=False):
+        if need_flush or force:
+            flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back
 
     # N > 1: rows [rank*R, (rank+1)*R) of an (N*R) x C matrix; NCCL broadcast(x) + SpMV + all_gather(y)
     sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev) if world > 1 else None
@@ -349,7 +354,9 @@ def main():
                 + (f" per rank, {R * world}x{C} row-sharded, NCCL broadcast x + all_gather y" if world > 1 else ""),
                 "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4, "pad_nnz": dm.pad_nnz,
                 "bytes_per_spmv_per_rank": bytes_rank, "parallelism": f"row-shard x{world}",
-                "l2": "flushed before every step (sum over a 2xL2 buffer, outside the step events)",
+                "l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush else
+                       f"not flushed: inputs larger than L2 ({bytes_rank / 2**20:.0f} MiB per step vs {l2 / 2**20:.0f} MiB L2; "
+                       "ncu: L2 hit rate < 1 % back to back)"),
                 "grid": li.grid, "block": li.block, "ctas_per_sm": li.ctas_per_sm, "split_rows": li.n_split_rows,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -433,12 +440,15 @@ def run_sweep(M, torch, dev, stream, l2_flush, peak):
         y = torch.empty(R, dtype=torch.float16, device=dev)
         yd = torch.empty(R, dtype=torch.float16, device=dev)
 
+        big = dm.traffic_bytes >= 3 * torch.cuda.get_device_properties(dev).L2_cache_size
+
         def timeit(fn, n=50):
             for _ in range(5):
                 fn()
             ts = []
             for _ in range(n):
-                l2_flush()
+                if not big:
+                    l2_flush(force=True)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 fn()
@@ -451,6 +461,7 @@ def run_sweep(M, torch, dev, stream, l2_flush, peak):
         dus = timeit(lambda: torch.mv(dense, x, out=yd))
         gbs = dm.traffic_bytes / (us * 1e-6) / 1e9
         out.append({"shape": f"{R}x{C}", "sparsity": round(1 - d, 2), "us": round(us, 2), "GBps": round(gbs, 1),
+                    "x_mode": dm.launch_info().x_in_smem, "l2_flush": not big,
                     "frac": round(gbs / peak, 4), "cublas_us": round(dus, 2), "speedup": round(dus / us, 3),
                     "bytes": dm.traffic_bytes})
         del dense, dm

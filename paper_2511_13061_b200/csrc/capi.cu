@@ -123,6 +123,8 @@ struct macko_dev_matrix {
     mutable std::mutex tex_mu;
     mutable const void* tex_ptr = nullptr;
     mutable cudaTextureObject_t tex = 0;
+    mutable int tex_align = 0;
+    mutable DevBuf<uint16_t> xcopy;  // aligned copy of a misaligned x
     ~macko_dev_matrix() {
         if (tex) cudaDestroyTextureObject(tex);
     }
@@ -149,8 +151,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     const size_t budget = (size_t)optin - kSpmvWarpsPerCta * kMaxRing * 8 - 1024;
     const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunkDBytes);
-    auto x_bytes = [&](int mode) {
-        return (mode >= 2 && mode <= 5) ? align_up(m->cols * 4, 128) : (mode == 1 || mode >= 6) ? align_up(m->cols * 2, 128) : 0;
+    auto x_bytes = [&](int mode) -> size_t {
+        return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
     };
     auto ring_for = [&](int mode) -> uint32_t {
         const size_t xb = x_bytes(mode);
@@ -163,16 +165,18 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         m->x_mode = m->force_x_mode;
     } else {
         // prefer the pair table (fewer gather wavefronts), then the fp16 table, then global x
-        m->x_mode = ring_for(6) >= 2 ? 6 : ring_for(1) >= 2 ? 1 : 0;
+        // TEX gathers cost ~1 wavefront per 128-B line a warp gather touches, which grows with the
+        // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
+        // density.  Measured best split (profiles/r01_v12_modes.md): 4 of 8 slots by TEX at
+        // d >= 0.4, 3 at 0.25 <= d < 0.4, 2 below.
+        const double d = (double)m->pad_nnz / ((double)m->rows * (double)m->cols);
+        const int split = d >= 0.4 ? 7 : d >= 0.25 ? 6 : 8;
+        m->x_mode = ring_for(split) >= 2 ? split : 0;
     }
     m->ring = ring_for(m->x_mode);
     if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
     m->ring_offset = x_bytes(m->x_mode);
     m->smem = m->ring_offset + m->ring * per_slot;
-    if (m->x_mode >= 3) {  // the no-texture fallback (unaligned x) launches with the same smem
-        int dummy = 0;
-        ck(spmv_occupancy(m->x_mode >= 6 ? 1 : 2, m->smem, &dummy), "spmv occupancy");
-    }
     ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
     m->ctas_per_sm = 1;  // one persistent 32-warp CTA per SM
@@ -312,14 +316,25 @@ void device_validate(macko_dev_matrix* m, cudaStream_t st) {
     if (h & 2u) fail(MACKO_EFORMAT, "padding value must be +0");
 }
 
-// Texture view of x for the TEX-pipe gathers; 0 when x is not suitably aligned (the kernel then
-// falls back to the pair table alone, x_mode 2, which uses the same shared-memory layout).
-cudaTextureObject_t x_texture(const macko_dev_matrix* m, const uint16_t* d_x) {
+// x as the kernel reads it: 16-byte aligned for the shared-memory staging and texture-aligned
+// for the TEX gathers; a misaligned x is first copied into the matrix's aligned scratch buffer.
+// The texture object is cached per x buffer.
+const uint16_t* x_view(const macko_dev_matrix* m, const uint16_t* d_x, bool need_tex, cudaTextureObject_t* tex,
+                       cudaStream_t st) {
     std::lock_guard<std::mutex> lk(m->tex_mu);
-    if (m->tex && m->tex_ptr == d_x) return m->tex;
-    int align = 0;
-    ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
-    if (align > 0 && reinterpret_cast<uintptr_t>(d_x) % (uintptr_t)align != 0) return 0;
+    if (!m->tex_align) ck(cudaDeviceGetAttribute(&m->tex_align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
+    const uintptr_t align = std::max<uintptr_t>(16, (uintptr_t)m->tex_align);
+    if (reinterpret_cast<uintptr_t>(d_x) % align != 0) {
+        if (!m->xcopy.p) m->xcopy.alloc(m->cols);
+        ck(cudaMemcpyAsync(m->xcopy.p, d_x, m->cols * 2, cudaMemcpyDeviceToDevice, st), "x copy");
+        d_x = m->xcopy.p;
+    }
+    *tex = 0;
+    if (!need_tex) return d_x;
+    if (m->tex && m->tex_ptr == d_x) {
+        *tex = m->tex;
+        return d_x;
+    }
     if (m->tex) {
         cudaDestroyTextureObject(m->tex);
         m->tex = 0;
@@ -334,7 +349,8 @@ cudaTextureObject_t x_texture(const macko_dev_matrix* m, const uint16_t* d_x) {
     td.readMode = cudaReadModeElementType;
     ck(cudaCreateTextureObject(&m->tex, &rd, &td, nullptr), "x texture");
     m->tex_ptr = d_x;
-    return m->tex;
+    *tex = m->tex;
+    return d_x;
 }
 
 void check_shape(uint64_t rows, uint64_t cols) {
@@ -498,7 +514,8 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.values = m->values.p;
         a.deltas = m->deltas.p;
         a.row_ptrs = m->row_ptrs.p;
-        a.x = d_x;
+        const int mode = m->x_mode;
+        a.x = x_view(m, d_x, mode != 1, &a.xtex, (cudaStream_t)stream);
         a.y = d_y;
         a.rows = (uint32_t)m->rows;
         a.cols = (uint32_t)m->cols;
@@ -507,12 +524,6 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
-        a.xtex = 0;
-        int mode = m->x_mode;
-        if (mode >= 3) {
-            a.xtex = x_texture(m, d_x);
-            if (!a.xtex) mode = mode >= 6 ? 1 : 2;  // same shared-memory layout, no TEX
-        }
         ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
         g_launches.fetch_add(1);
     });
@@ -581,9 +592,8 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream) {
     return guarded([&] {
         if (!m) fail(MACKO_EINVAL, "null handle");
-        if (x_mode < -1 || x_mode > 9) fail(MACKO_EINVAL, "x_mode must be -1 (auto) or 0..9");
-        if (x_mode >= 2 && x_mode <= 5 && m->cols * 4 > 220 * 1024) fail(MACKO_EINVAL, "pair table does not fit shared memory");
-        if ((x_mode == 1 || x_mode >= 6) && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
+        if (x_mode != -1 && !mk::spmv_valid_x_mode(x_mode)) fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 6..11");
+        if (x_mode > 0 && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
         if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
         DeviceGuard g(m->device);
         m->force_x_mode = x_mode;

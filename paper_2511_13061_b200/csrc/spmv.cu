@@ -3,29 +3,35 @@
 // Realises the paper's warp kernel (SPEC.md:255-264 warp_spmv) natively:
 //   * one warp walks a row in steps of 256 elements, lane l owning elements 8l..8l+7 of the
 //     step;
-//   * ROMA: the row start is aligned down to 8 elements and the elements
-//     before it are masked in the first step; lanes past the row end are masked in the last;
+//   * ROMA: the row start is aligned down to 8 elements; elements outside
+//     the row (before its start in the first step, past its end in the last) are masked;
 //   * column reconstruction: the 8 nibbles are widened to bytes, paired and prefix-summed with
 //     one integer multiply (byte-SIMD), then Algorithm 1's shfl_up scan gives the lane offset
-//     and lane 31's total advances the running column.  Two steps share one
-//     scan (their lane sums packed into 16-bit halves);
-//   * x is staged once per CTA in shared memory — as (x[c], x[c+1]) pairs when it fits, so an
-//     element pair at adjacent columns costs one 32-bit gather — and gathered per element; the
-//     multiply-add is FHFMA (fp16 x fp16 -> fp32 accumulate, exact product).
-// B200 specifics (profiles/r01_pipes.md): the kernel is bound by the L1/LSU data pipe (x
-// gathers + shuffles + loads), not by HBM.  The matrix stream therefore arrives by TMA: every
-// warp owns a contiguous element range (static equal-weight plan of 2048-element units, built
-// once per matrix) and keeps a ring of 512-element chunks (1 KiB values + 256 B deltas) in
-// flight with cp.async.bulk + mbarrier, which costs no LSU wavefronts; values and deltas are
-// read back with one LDS.128 + one LDS.32 per lane step.  One persistent CTA of 32 warps per
-// SM.  Rows cut between warps are finished by the last-arriving warp, which adds the per-unit
-// partials in unit order.
+//     and the warp total advances the running column.  Two steps share one
+//     scan (their lane sums packed into 16-bit halves); the total comes from REDUX;
+//   * every element's x value is gathered and multiply-added with FHFMA (fp16 x fp16 -> fp32
+//     accumulate, exact product).
+// B200 specifics (profiles/r01_pipes.md): the kernel is bound by on-chip data pipes, not HBM.
+//   * The matrix stream arrives by TMA: every warp owns a contiguous element range (static
+//     equal-weight plan of 2048-element units, built once per matrix) and keeps a ring of
+//     1024-element chunks in flight with cp.async.bulk + mbarrier (no LSU wavefronts); values
+//     and deltas are read back with one LDS.128 + one LDS.32 per lane step.
+//   * x gathers are split between two pipes that run in parallel: an fp16 copy of x in shared
+//     memory (LDS, LSU pipe) and x as a 1-D texture (TEX pipe, L1-resident); which of a lane's
+//     8 element slots use the texture is a compile-time mask (x_mode).
+//   * Masked elements cost no predication: their codewords are forced to 0 (delta 1) and their
+//     values to +0, and they gather from zero guards around the shared table (or out-of-range
+//     texels, which read 0), so row edges run the same code as interior steps.
+//   * One persistent CTA of 32 warps per SM.  Rows cut between warps are finished by the
+//     last-arriving warp, which adds the per-unit partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
-// lanes once per unit (8 steps), sequential over units — mirrored bit-exactly by
-// oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  The order depends on a row's elements
-// and on its start offset mod 8 (ROMA), never on the plan.
+// lanes once per unit (8 steps; the row's last unit absorbs a shorter remainder), sequential
+// over units — mirrored bit-exactly by oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  It
+// depends on a row's elements and on its start offset mod 8 (ROMA), never on the plan.
 #include "common.cuh"
 #include "spmv.cuh"
+
+#include <type_traits>
 
 namespace mk {
 
@@ -44,136 +50,62 @@ __device__ __forceinline__ uint16_t lds_u16(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-
-// x gather: kXMode 0 = global (L1), 1 = fp16 table in smem, 2 = pair table in smem,
-// 3..5 = pair table + texture fetches (TEX pipe) for the odd elements of pairs m >= tex_from.
-template <int kXMode>
-__device__ __forceinline__ uint16_t xget(uint32_t xs_addr, const uint16_t* __restrict__ xg, int col) {
-    if constexpr (kXMode == 0) return __ldg(xg + col);
-    if constexpr (kXMode == 1 || kXMode >= 6) return lds_u16(xs_addr + 2u * (uint32_t)col);
-    return lds_u16(xs_addr + 4u * (uint32_t)col);
-}
-
-template <int kXMode>
-constexpr int tex_from() {
-    return kXMode == 3 ? 1 : kXMode == 4 ? 0 : kXMode == 5 ? 2 : 4;
-}
-
-// x_mode >= 6: fp16 table in smem + fp16 texture; lane element slot k (0..7) of every step is
-// gathered by TEX when bit k of tex_slots is set, else by LDS.  The split balances the LSU
-// data pipe (values/deltas, shuffles, LDS gathers) against the TEX data pipe (~1 wavefront per
-// 128-B line a gather touches) — profiles/r01_pipes.md.
-template <int kXMode>
-constexpr uint32_t tex_slots() {
-    return kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 9 ? 0x92u : 0u;
-}
-
-template <int kXMode>
-constexpr bool pair_table() {
-    return kXMode >= 2 && kXMode <= 5;
-}
-
 __device__ __forceinline__ uint16_t xtex(cudaTextureObject_t t, int col) {
     return tex1Dfetch<unsigned short>(t, col);
 }
 
-// valid-element mask of a lane whose first element is eb, for the row [s, e)
-// (row offsets are < 2^32 and a row spans < 2^31 elements, so 32-bit differences suffice)
-__device__ __forceinline__ uint32_t lane_mask(uint32_t eb, uint32_t s, uint32_t e) {
-    const int klo = min(max((int)(s - eb), 0), 8);
-    const int khi = min(max((int)(e - eb), 0), 8);
-    return (0xFFu << klo) & (0xFFu >> (8 - khi)) & 0xFFu;
+// Lane element slots k (0..7) gathered through the texture (bit k set) rather than the shared
+// table.  x_mode 0: texture only (x too large for shared memory); 1: shared table only;
+// 6..9: split between the LSU and TEX data pipes (profiles/r01_pipes.md).
+template <int kXMode>
+constexpr uint32_t tex_slots() {
+    return kXMode == 0 ? 0xFFu : kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 9 ? 0x92u
+         : kXMode == 10 ? 0xABu : kXMode == 11 ? 0xBBu : 0u;
 }
 
-// Byte masks for the even (0,2,4,6) / odd (1,3,5,7) elements of an 8-bit element mask: bit 2m
-// lands on bit 8m through one multiply (no carries reach the target bits), then * 0xFF.
-__device__ __forceinline__ uint32_t spread_even(uint32_t vm) {
-    return (((vm & 0x55u) * 0x41041u) & 0x01010101u) * 0xFFu;
+template <int kXMode>
+constexpr bool x_table() {
+    return kXMode != 0;
 }
 
 struct Dec {
-    uint32_t even, odd, dh, local;  // in-lane inclusive column offsets (byte m), odd deltas, total
+    uint32_t even, odd, local;  // in-lane inclusive column offsets of elements 0,2,4,6 / 1,3,5,7; lane total
 };
 
-// Nibbles -> byte deltas -> in-lane inclusive prefixes.  Masked elements get delta 0.
-template <bool kMasked>
-__device__ __forceinline__ Dec decode(uint32_t d, uint32_t vm) {
-    uint32_t dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
-    uint32_t dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
-    if constexpr (kMasked) {
-        dl &= spread_even(vm);
-        dh &= spread_even(vm >> 1);
-    }
+// Nibbles -> byte deltas (codeword + 1) -> in-lane inclusive prefixes (byte m of even/odd).
+__device__ __forceinline__ Dec decode(uint32_t d) {
+    const uint32_t dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
+    const uint32_t dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
     const uint32_t pp = (dl + dh) * 0x01010101u;
-    return Dec{pp - dh, pp, dh, pp >> 24};
+    return Dec{pp - dh, pp, pp >> 24};
 }
 
-// 8 gathers + FHFMAs of one unmasked lane step.  cb = column before the lane's first element.
+// 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.
 template <int kXMode>
-__device__ __forceinline__ float fma_fast(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
-                                          const uint16_t* __restrict__ xg, cudaTextureObject_t xt) {
+__device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
+                                           cudaTextureObject_t xt) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    // shared address of column cb: per element one PRMT (byte extract) + one LEA
-    uint32_t base = xs_addr + (uint32_t)cb * (pair_table<kXMode>() ? 4u : 2u);
-    asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + (b << k) a single LEA per element
+    // shared address of column cb: per element one PRMT (byte extract) + one IADD3
+    uint32_t base = xs_addr + 2u * (uint32_t)cb;
+    asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + 2b a single IADD3 per element
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         uint16_t v0, v1;
         split_halves(w[m], v0, v1);
         const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
         const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
-        if constexpr (kXMode >= 6) {
-            const uint16_t x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + (b0 << 1));
-            const uint16_t x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + (b1 << 1));
-            acc = fma_f16f16f32(v0, x0, acc);
-            acc = fma_f16f16f32(v1, x1, acc);
-        } else if constexpr (kXMode >= 2) {
-            // (x[c0], x[c0+1]) in one gather; the odd element reuses the high half when adjacent,
-            // else gathers from the pair table (LSU pipe) or the texture (TEX pipe)
-            const uint32_t xa = lds_u32(base + (b0 << 2));
-            acc = fma_f16f16f32(v0, (uint16_t)(xa & 0xFFFFu), acc);
-            if (((dc.dh >> (8 * m)) & 0xFFu) == 1u)
-                acc = fma_f16f16f32(v1, (uint16_t)(xa >> 16), acc);
-            else if (m >= tex_from<kXMode>())
-                acc = fma_f16f16f32(v1, xtex(xt, cb + (int)b1), acc);
-            else
-                acc = fma_f16f16f32(v1, lds_u16(base + (b1 << 2)), acc);
-        } else if constexpr (kXMode == 1) {
-            const uint16_t x0 = lds_u16(base + (b0 << 1));
-            const uint16_t x1 = lds_u16(base + (b1 << 1));
-            acc = fma_f16f16f32(v0, x0, acc);
-            acc = fma_f16f16f32(v1, x1, acc);
-        } else {
-            const int c0 = cb + (int)b0, c1 = cb + (int)b1;
-            const uint16_t x0 = xget<kXMode>(xs_addr, xg, c0);
-            const uint16_t x1 = xget<kXMode>(xs_addr, xg, c1);
-            acc = fma_f16f16f32(v0, x0, acc);
-            acc = fma_f16f16f32(v1, x1, acc);
-        }
+        const uint16_t x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
+        const uint16_t x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
+        acc = fma_f16f16f32(v0, x0, acc);
+        acc = fma_f16f16f32(v1, x1, acc);
     }
     return acc;
 }
 
-// Masked lane step (row edges): only valid elements gather and accumulate.
-template <int kXMode>
-__device__ __forceinline__ float fma_masked(float acc, const uint4& v, const Dec& dc, int cb, uint32_t vm,
-                                            uint32_t xs_addr, const uint16_t* __restrict__ xg) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        uint16_t v0, v1;
-        split_halves(w[m], v0, v1);
-        if ((vm >> (2 * m)) & 1u)
-            acc = fma_f16f16f32(v0, xget<kXMode>(xs_addr, xg, cb + (int)__byte_perm(dc.even, 0u, 0x4440u + m)), acc);
-        if ((vm >> (2 * m + 1)) & 1u)
-            acc = fma_f16f16f32(v1, xget<kXMode>(xs_addr, xg, cb + (int)__byte_perm(dc.odd, 0u, 0x4440u + m)), acc);
-    }
-    return acc;
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -190,6 +122,9 @@ struct RowState {
 // Set up the piece of row rs.r = [rs.s, rs.e) starting at unit j0.  sid / slot: the chunk's
 // split-row id for this piece (used only if the piece turns out to be split).
 __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colbase, int32_t sid, uint32_t slot) {
+    // A row's first step starts at the 8-aligned al (ROMA); its k = s - al leading elements
+    // belong to the previous row and are decoded as codeword 0 (delta 1) after masking, so the
+    // column before the row is -1 - k (the masked elements land on guard zeros at -k..-1).
     rs.al = rs.s & ~7u;
     rs.T = rs.e > rs.s ? (rs.e - rs.al + kStepElts - 1) / kStepElts : 0u;
     // units of kUnitSteps steps; the last unit absorbs a remainder shorter than a unit
@@ -203,7 +138,7 @@ __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colba
     rs.split = !(j0 == 0 && j0 + nu == rs.n_r);
     rs.sid = sid;
     rs.slot = slot;
-    rs.col_base = colbase;
+    rs.col_base = j0 ? colbase : -1 - (int)(rs.s - rs.al);
     rs.acc = 0.0f;
     rs.row_acc = 0.0f;
 }
@@ -348,17 +283,26 @@ __device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
     return sl;
 }
 
-// Lane data of the step whose lane element is eb (zeros for lanes wholly past the row).
-__device__ __forceinline__ Slot ring_read(const Ring& g, uint32_t eb, uint32_t e) {
-    if (eb < e) return lds_slot(g, (eb - g.ebase) & g.emask);
-    return Slot{make_uint4(0, 0, 0, 0), 0u};
+// Keep only the lane's elements inside [s, e) (eb = the lane's first element): the others get
+// codeword 0 (delta 1) and value +0, and their columns fall on zero guards / out-of-range texels,
+// so they add exactly +0 (also when the masked values or x hold inf / NaN).
+__device__ __forceinline__ void mask_slot(Slot& sl, uint32_t eb, uint32_t s, uint32_t e) {
+    const int klo = min(max((int)(s - eb), 0), 8);
+    const int khi = min(max((int)(e - eb), klo), 8);
+    const uint32_t nm = (uint32_t)(((1ull << (4 * khi)) - 1ull) & ~((1ull << (4 * klo)) - 1ull));
+    sl.d &= nm;
+    // value masks: 16-bit halves replicate the msb of their element's nibble (PRMT sign mode)
+    const uint32_t lo = nm << 4;
+    sl.v.x &= prmt(lo, nm, 0xCC88u);
+    sl.v.y &= prmt(lo, nm, 0xDD99u);
+    sl.v.z &= prmt(lo, nm, 0xEEAAu);
+    sl.v.w &= prmt(lo, nm, 0xFFBBu);
 }
 
 template <int kXMode>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t C = a.cols;
@@ -397,136 +341,79 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         rs.s = q1.y;
         rs.e = q1.z;
         rs.e_next = rs.r + 2u <= a.rows ? __ldg(a.row_ptrs + rs.r + 2u) : 0u;
-        const uint32_t j0 = q0.z;
-        begin_piece(rs, j0, j0 ? (int)q1.w : -1, (int32_t)q2.x, q2.z);
-        if (rs.split && rs.units_left == 0 && (int32_t)q2.x < 0) {  // first row = last row of the chunk
-            rs.sid = (int32_t)q2.y;
-            rs.slot = q2.w;
-        }
+        begin_piece(rs, q0.z, (int)q1.w, (int32_t)q2.x, q2.z);
     }
 
-    // Stage x in shared memory: 16-byte loads, issued before the stores.
-    if constexpr (kXMode != 0) {
-        const bool vec = (reinterpret_cast<uintptr_t>(a.x) & 15u) == 0;
-        const uint32_t nv = vec ? C / 8 : 0;
-        const uint4* x4 = reinterpret_cast<const uint4*>(a.x);
-        constexpr int kU = 2;
-        for (uint32_t b0 = threadIdx.x; b0 < nv; b0 += kU * blockDim.x) {
-            uint4 t[kU];
-            uint32_t nx[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const uint32_t i = b0 + u * blockDim.x;
-                if (i < nv) {
-                    t[u] = __ldg(x4 + i);
-                    nx[u] = (kXMode >= 2 && kXMode <= 5 && 8 * i + 8 < C) ? (uint32_t)__ldg(a.x + 8 * i + 8) : 0u;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const uint32_t i = b0 + u * blockDim.x;
-                if (i >= nv) continue;
-                if constexpr (kXMode == 1 || kXMode >= 6) {
-                    reinterpret_cast<uint4*>(xs)[i] = t[u];
-                } else {
-                    // pair words (x[c], x[c+1]) for c = 8i .. 8i+7
-                    const uint32_t h[4] = {t[u].x, t[u].y, t[u].z, t[u].w};
-                    uint4 lo, hi;
-                    lo.x = h[0];
-                    lo.y = __byte_perm(h[0], h[1], 0x5432);
-                    lo.z = h[1];
-                    lo.w = __byte_perm(h[1], h[2], 0x5432);
-                    hi.x = h[2];
-                    hi.y = __byte_perm(h[2], h[3], 0x5432);
-                    hi.z = h[3];
-                    hi.w = __byte_perm(h[3], nx[u], 0x5432);
-                    reinterpret_cast<uint4*>(xs)[2 * i] = lo;
-                    reinterpret_cast<uint4*>(xs)[2 * i + 1] = hi;
-                }
-            }
-        }
-        for (uint32_t i = nv * 8 + threadIdx.x; i < C; i += blockDim.x) {
-            if constexpr (kXMode == 1 || kXMode >= 6)
-                xs[i] = a.x[i];
-            else
-                reinterpret_cast<uint32_t*>(xs)[i] = (uint32_t)a.x[i] | ((i + 1 < C ? (uint32_t)a.x[i + 1] : 0u) << 16);
-        }
+    // Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries).
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    if constexpr (x_table<kXMode>()) {
+        const uint4* x4 = reinterpret_cast<const uint4*>(a.x);  // 16-byte aligned (capi guarantees)
+        const uint32_t nv = C / 8;
+        for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4*>(xs)[i] = __ldg(x4 + i);
+        for (uint32_t i = nv * 8 + threadIdx.x; i < C + kXGuardHi; i += blockDim.x) xs[i] = i < C ? a.x[i] : 0;
+        if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
     }
     __syncthreads();
     if (!has_work) return;
-    uint32_t xs_addr;
-    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(xs_addr) : "l"(xs));
+    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
     if (rs.T == 0) {
         if (lane == 0) a.y[rs.r] = 0;
         if (!next_piece(rs, a, w, lane)) return;
     }
+    // ring event: refill once the walk passes rel_mark, wait once a pair reaches ready_end
+    uint32_t ev = 0;
 
-    // Unit end after the step pair that ends at step t_after (t_after multiple of 8 or piece end).
-    auto unit_end = [&](uint32_t t_after) {
-        const float red = warp_tree_sum(rs.acc);
-        rs.acc = 0.0f;
-        if (rs.split && rs.j0 > 0 && lane == 0)
-            a.plan.partials[rs.slot + min((t_after - 1u) / kUnitSteps, rs.n_r - 1u)] = red;
-        rs.row_acc += red;
-    };
-
-    // A step pair at a row edge (ROMA first step, tail step, or a phantom second step).
-    auto edge_pair = [&](uint32_t t) {
+    // One step pair (steps t, t+1 of the current row).  Masked pairs: the row's first pair
+    // (ROMA) and its last (partial / phantom second step).
+    auto pair = [&](auto masked, uint32_t t) {
+        constexpr bool kMasked = decltype(masked)::value;
         const uint32_t S = rs.al + t * kStepElts;
-        const bool hasB = t + 1 < rs.tend;
-        const uint32_t Send = S + (hasB ? 2u : 1u) * kStepElts;
-        if (S >= g.rel_mark) ring_refill(g, a, S, lane);
-        if (Send > g.ready_end) ring_wait(g, Send, a.ring);
-        const uint32_t eb = S + 8u * lane;
-        const Slot A = ring_read(g, eb, rs.e);
-        const Slot B = hasB ? ring_read(g, eb + kStepElts, rs.e) : Slot{make_uint4(0, 0, 0, 0), 0u};
-        const uint32_t vmA = lane_mask(eb, rs.s, rs.e);
-        const uint32_t vmB = hasB ? lane_mask(eb + kStepElts, rs.s, rs.e) : 0u;
-        const Dec dA = decode<true>(A.d, vmA), dB = decode<true>(B.d, vmB);
+        if (S >= ev) {
+            const uint32_t Send = S + ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts;
+            if (S >= g.rel_mark) ring_refill(g, a, S, lane);
+            if (Send > g.ready_end) ring_wait(g, Send, a.ring);
+            ev = min(g.rel_mark, g.ready_end > 2u * kStepElts - 1u ? g.ready_end - (2u * kStepElts - 1u) : 0u);
+        }
+        const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
+        Slot A = lds_slot(g, relA);
+        Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
+        if constexpr (kMasked) {
+            const uint32_t eb = S + 8u * lane;
+            mask_slot(A, eb, rs.s, rs.e);
+            mask_slot(B, eb + kStepElts, rs.s, rs.e);
+        }
+        const Dec dA = decode(A.d), dB = decode(B.d);
         const uint32_t pk = dA.local | (dB.local << 16);
         const uint32_t incl = warp_incl_scan_p(pk);
         const uint32_t tot = __reduce_add_sync(kFull, pk);
-        const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-        const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-        rs.acc = fma_masked<kXMode>(rs.acc, A.v, dA, cbA, vmA, xs_addr, a.x);
-        rs.acc = fma_masked<kXMode>(rs.acc, B.v, dB, cbB, vmB, xs_addr, a.x);
+        int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+        int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+        if constexpr (kMasked) {  // lanes wholly past the row gather from the guard at C..C+8
+            const uint32_t eb = S + 8u * lane;
+            if (eb >= rs.e) cbA = (int)C;
+            if (eb + kStepElts >= rs.e) cbB = (int)C;
+        }
+        rs.acc = lane_step<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex);
+        rs.acc = lane_step<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex);
         rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-        const uint32_t t_after = min(t + 2u, rs.tend);
-        if (((t_after % kUnitSteps) == 0 && t_after <= rs.last_b) || t_after == rs.tend) unit_end(t_after);
     };
 
     for (;;) {
-        // -- the piece's steps [t0, tend) in aligned pairs; pair p = steps (t0+2p, t0+2p+1)
-        const uint32_t t0 = rs.t;
-        const uint32_t np = (rs.tend - t0 + 1u) / 2u;
-        const bool first_edge = t0 == 0;
-        const bool last_edge = rs.tend == rs.T || ((rs.tend - t0) & 1u);
-        const uint32_t p_lo = first_edge ? 1u : 0u;
-        const uint32_t p_hi = last_edge ? np - 1u : np;
-        if (first_edge) edge_pair(t0);
-        // interior pairs: every lane valid, no masks, no bounds checks
-        uint32_t S = rs.al + (t0 + 2u * p_lo) * kStepElts;
-        for (uint32_t p = p_lo; p < p_hi; ++p, S += 2u * kStepElts) {
-            if (S >= g.rel_mark) ring_refill(g, a, S, lane);
-            if (S + 2u * kStepElts > g.ready_end) ring_wait(g, S + 2u * kStepElts, a.ring);
-            const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
-            const Slot A = lds_slot(g, relA);
-            const Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
-            const Dec dA = decode<false>(A.d, 0xFFu), dB = decode<false>(B.d, 0xFFu);
-            const uint32_t pk = dA.local | (dB.local << 16);
-            const uint32_t incl = warp_incl_scan_p(pk);
-            const uint32_t tot = __reduce_add_sync(kFull, pk);
-            const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-            const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-            rs.acc = fma_fast<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.x, a.xtex);
-            rs.acc = fma_fast<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.x, a.xtex);
-            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
-            // t0 is a multiple of 8: a unit ends after every 4th pair up to the last unit's start
-            // (the last unit may run up to 15 steps), and at the piece end
-            const uint32_t ta = t0 + 2u * p + 2u;
-            if (((p & 3u) == 3u && ta <= rs.last_b) || ta == rs.tend) unit_end(ta);
+        // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T)
+        for (uint32_t t = rs.t; t < rs.tend;) {
+            const uint32_t ue = t < rs.last_b ? t + kUnitSteps : rs.tend;
+            for (; t < ue; t += 2u) {
+                if (t == 0u || t + 2u >= rs.T)
+                    pair(std::true_type{}, t);
+                else
+                    pair(std::false_type{}, t);
+            }
+            const float red = warp_tree_sum(rs.acc);
+            rs.acc = 0.0f;
+            if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + min((ue - 1u) / kUnitSteps, rs.n_r - 1u)] = red;
+            rs.row_acc += red;
+            t = ue;
         }
-        if (last_edge && (np > 1u || !first_edge)) edge_pair(t0 + 2u * (np - 1u));
         // -- piece end
         if (!rs.split) {
             if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
@@ -567,37 +454,38 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     return e;
 }
 
+bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 11); }
+
 cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
     switch (x_mode) {
+        case 11: return occ_one<11>(smem, ctas_per_sm);
+        case 10: return occ_one<10>(smem, ctas_per_sm);
         case 9: return occ_one<9>(smem, ctas_per_sm);
         case 8: return occ_one<8>(smem, ctas_per_sm);
         case 7: return occ_one<7>(smem, ctas_per_sm);
         case 6: return occ_one<6>(smem, ctas_per_sm);
-        case 5: return occ_one<5>(smem, ctas_per_sm);
-        case 4: return occ_one<4>(smem, ctas_per_sm);
-        case 3: return occ_one<3>(smem, ctas_per_sm);
-        case 2: return occ_one<2>(smem, ctas_per_sm);
         case 1: return occ_one<1>(smem, ctas_per_sm);
-        default: return occ_one<0>(smem, ctas_per_sm);
+        case 0: return occ_one<0>(smem, ctas_per_sm);
+        default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s) {
     const int threads = kSpmvWarpsPerCta * kWarp;
     switch (x_mode) {
+        case 11: macko_spmv_b4<11><<<grid, threads, smem, s>>>(a); break;
+        case 10: macko_spmv_b4<10><<<grid, threads, smem, s>>>(a); break;
         case 9: macko_spmv_b4<9><<<grid, threads, smem, s>>>(a); break;
         case 8: macko_spmv_b4<8><<<grid, threads, smem, s>>>(a); break;
         case 7: macko_spmv_b4<7><<<grid, threads, smem, s>>>(a); break;
         case 6: macko_spmv_b4<6><<<grid, threads, smem, s>>>(a); break;
-        case 5: macko_spmv_b4<5><<<grid, threads, smem, s>>>(a); break;
-        case 4: macko_spmv_b4<4><<<grid, threads, smem, s>>>(a); break;
-        case 3: macko_spmv_b4<3><<<grid, threads, smem, s>>>(a); break;
-        case 2: macko_spmv_b4<2><<<grid, threads, smem, s>>>(a); break;
         case 1: macko_spmv_b4<1><<<grid, threads, smem, s>>>(a); break;
-        default: macko_spmv_b4<0><<<grid, threads, smem, s>>>(a); break;
+        case 0: macko_spmv_b4<0><<<grid, threads, smem, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
+
 cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s) {
     const int threads = 256;
     const int blocks = (int)((n_chunks * (uint64_t)kWarp + threads - 1) / threads);

@@ -35,7 +35,7 @@ struct SpmvArgs {
     const uint32_t* row_ptrs;
     const uint16_t* x;
     uint16_t* y;
-    cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode >= 3)
+    cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode 0, 6..9)
     uint64_t value_elems, delta_bytes;  // allocated sizes (payload + one zeroed chunk of slack)
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
@@ -47,11 +47,18 @@ constexpr int kSpmvWarpsPerCta = 32;          // one persistent 1024-thread CTA 
 constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two step pairs)
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
 constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
-constexpr uint32_t kMaxRing = 8;
+constexpr uint32_t kMaxRing = 4;
+// fp16 x table in shared memory: kXGuardLo zero entries before x[0] (the ROMA-masked elements of
+// a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (the masked elements
+// of a row's last step decode to at most 7 columns past its last element; lanes wholly past the
+// row are pointed at column C, so their elements land on C+1..C+8).
+constexpr int kXGuardLo = 8;
+constexpr int kXGuardHi = 16;
 
 // Launchers (return cudaGetLastError()).
-// x_mode: 0 = x gathered from global (L1), 1 = fp16 table in smem, 2 = (x[c], x[c+1]) pair table,
-// 3..5 = pair table + texture gathers for odd elements (TEX pipe in parallel with the LSU pipe)
+// x_mode: 0 = texture gathers only, 1 = fp16 shared-memory table only, 6..9 = table + texture
+// gathers for a fixed subset of element slots (TEX pipe in parallel with the LSU pipe)
+bool spmv_valid_x_mode(int x_mode);
 cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s);
 cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);

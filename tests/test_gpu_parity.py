@@ -177,7 +177,7 @@ def test_spmv_headline_shape(cuda, density):
 
 
 def test_spmv_x_in_global_memory_path(cuda):
-    # C beyond the shared-memory staging limit: x is gathered through L1
+    # C beyond the shared-memory staging limit: every x gather goes through the texture (TEX pipe)
     R, C = 6, 120000
     A = O.gen_dense(R, C, 0.3, 3)
     x = O.gen_vector(C, 4)
@@ -228,12 +228,12 @@ def test_plan_and_x_staging_do_not_change_y(cuda):
         dm = gpu_encode(A)
         y0 = gpu_spmv(dm, x)
         assert np.array_equal(y0, O.b200_order_spmv(O.encode_dense(A), x, UNIT_STEPS))
-        for x_mode in (0, 1, 2, 3, 6, 7, 8, 9):
+        for x_mode in (0, 1, 6, 7, 8, 9):
             for ctas in (1, 2, 0):
                 try:
                     dm.configure(x_mode, ctas)
                 except ValueError:  # the x table would not leave room for the TMA rings
-                    assert x_mode > 0 and C * (4 if 2 <= x_mode <= 5 else 2) >= 64_000
+                    assert x_mode > 0 and C * 2 >= 64_000
                     continue
                 assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, x_mode, ctas)
 
