@@ -28,6 +28,15 @@ clean:
 
 .PHONY: all lib oracle clean
 
+# opt-in trace build (per-warp %globaltimer stamps; tools/trace_spmv.py), never the product .so
+trace: $(PKG)/libmacko_cuda_trace.so
+build/trace/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build/trace
+	$(NVCC) $(NVFLAGS) -DMACKO_TRACE -c $< -o $@ 2> /dev/null
+$(PKG)/libmacko_cuda_trace.so: $(patsubst $(CSRC)/%.cu,build/trace/%.o,$(SRCS))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+.PHONY: trace
+
 # C++ drop-in test (reference headers + our header); needs /root/reference at build time.
 REF_SRC ?= /root/reference/proj/src
 cpptest: lib oracle

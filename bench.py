@@ -42,6 +42,9 @@ def parse():
     p.add_argument("--cols", type=int, default=HEADLINE["cols"])
     p.add_argument("--density", type=float, default=HEADLINE["density"])
     p.add_argument("--sweep", action="store_true", help="also report 30/50/70/90 %% sparsity and Llama shapes")
+    p.add_argument("--chain", action="store_true",
+                   help="also report the Llama2-7B 32-layer decode SpMV chain (config 4) vs a dense cuBLAS chain")
+    p.add_argument("--chain-tokens", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
     p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture only, 1 smem table only, 6..9 smem + texture split")
@@ -332,17 +335,25 @@ def main():
         e2e_mean = t.item()
     e2e_val = total_bytes / (e2e_mean * 1e-3) / 1e9
 
+    cpu_src = dm.download() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    li = dm.launch_info()
+    pad_nnz = dm.pad_nnz
     sweep = None
     if args.sweep and rank == 0:
         sweep = run_sweep(M, torch, dev, stream, l2_flush, peak)
 
+    chain = None
+    if args.chain:
+        del dm
+        torch.cuda.empty_cache()
+        chain = run_chain(args, torch, dist, dev, world, rank, peak)
+
     # ---- CPU baseline (rank 0, N = 1): reference SpMV on the same matrix, host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(dm, C, d)
+        cpu = cpu_baseline(cpu_src, C, d)
 
     if rank == 0:
-        li = dm.launch_info()
         traffic = load_traffic(R, C, d)
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -352,7 +363,7 @@ def main():
             "config": {
                 "workload": f"{R}x{C} fp16 @{sparsity_pct}% sparsity (random unstructured), single SpMV"
                 + (f" per rank, {R * world}x{C} row-sharded, NCCL broadcast x + all_gather y" if world > 1 else ""),
-                "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4, "pad_nnz": dm.pad_nnz,
+                "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4, "pad_nnz": pad_nnz,
                 "bytes_per_spmv_per_rank": bytes_rank, "parallelism": f"row-shard x{world}",
                 "l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush else
                        f"not flushed: inputs larger than L2 ({bytes_rank / 2**20:.0f} MiB per step vs {l2 / 2**20:.0f} MiB L2; "
@@ -375,6 +386,8 @@ def main():
         }
         if sweep is not None:
             line["sweep"] = sweep
+        if chain is not None:
+            line["chain"] = chain
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -394,6 +407,70 @@ def load_traffic(R, C, d):
     return None
 
 
+def run_chain(args, torch, dist, dev, world, rank, peak):
+    """Config 4: Llama2-7B decode chain (32 layers x {qkv, o, gate_up, down}) at 50 % sparsity,
+    PDL-chained SpMVs in one CUDA graph per token; N > 1: row slabs + NCCL all_gather per SpMV.
+    Weights stream from HBM (8.1 GB per token >> L2): no flush.  Beside it (N = 1) the same
+    chain with dense fp16 weights through torch.mv (cuBLAS GEMV), also graph-captured."""
+    from paper_2511_13061_b200 import decoder_chain as D
+    from paper_2511_13061_b200 import macko as M
+
+    t0 = time.time()
+    ch = D.SparseDecoderChain(D.LLAMA2_7B, density=0.5, keep_dense=(world == 1))
+    build_s = time.time() - t0
+    M.gen_vector(ch.acts["h"], D.LLAMA2_7B.hidden, seed=SEED_X)
+    g = ch.capture(pdl=True)
+
+    def time_graph(graph, n):
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for a, b in evs:
+            a.record()
+            graph.replay()
+            b.record()
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / n
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    n = max(3, args.chain_tokens)
+    launches0 = M.kernel_launches()
+    ms = time_graph(g, n)
+    bytes_rank = ch.traffic_bytes
+    total_bytes = bytes_rank * world
+    out = {
+        "workload": "Llama2-7B decoder stack, 32 layers x {qkv 12288x4096, o 4096x4096, gate_up 22016x4096, "
+                    "down 4096x11008} @50% sparsity, batch-1 decode (q/k/v and gate/up row-stacked), random-init",
+        "n_gpus": world, "parallelism": f"row-shard x{world}" + (" + NCCL all_gather per SpMV" if world > 1 else ""),
+        "kernels_per_token": ch.kernels_per_token, "launch": "PDL-chained SpMVs, one CUDA graph per token",
+        "us_per_token": round(ms * 1e3, 2), "tokens_per_s": round(1e3 / ms, 2),
+        "bytes_per_token": total_bytes, "GBps": round(total_bytes / (ms * 1e-3) / 1e9, 1),
+        "frac_per_gpu": round(bytes_rank / (ms * 1e-3) / 1e9 / peak, 4), "build_s": round(build_s, 2),
+        "l2": "not flushed: 8.1 GB of weights per token streams from HBM",
+        "timed_tokens": n, "host_launch_calls_in_timed_region": M.kernel_launches() - launches0,
+    }
+    if world == 1:
+        dch = D.DenseDecoderChain(ch)
+        dch.acts["h"].copy_(ch.acts["h"])
+        dg = dch.capture()
+        dms = time_graph(dg, n)
+        out.update({"cublas_us_per_token": round(dms * 1e3, 2), "cublas_tokens_per_s": round(1e3 / dms, 2),
+                    "cublas_GBps": round(dch.traffic_bytes / (dms * 1e-3) / 1e9, 1),
+                    "speedup_vs_cublas": round(dms / ms, 3)})
+        del dch, dg
+    ch.close()
+    del ch, g
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline(dm, C, d):
     try:
         from oracle import oracle as O
@@ -401,7 +478,7 @@ def cpu_baseline(dm, C, d):
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "port", "sample": f"oracle unavailable: {e}"}
     kind = "reference" if O.ref_available() else "port"
     threads = host_cores()
-    h = dm.download()
+    h = dm  # host MackoMatrix downloaded from the GPU
     m = O.Macko(h.rows, h.cols, 4, h.values, h.packed_deltas, h.row_pointers)
     x = O.gen_vector(C, SEED_X)
     if kind == "reference":
@@ -419,7 +496,7 @@ def cpu_baseline(dm, C, d):
         if time.time() - t_start > 30:
             break
     ms = statistics.median(ts) * 1e3
-    bytes_step = dm.traffic_bytes
+    bytes_step = O.spmv_traffic_bytes(m.rows, C, m.pad_nnz, 4)
     return {"value": round(bytes_step / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
             "ms_per_spmv": round(ms, 3),
             "sample": f"the same {m.rows}x{C} matrix (downloaded from the GPU), reference_spmv, median of {len(ts)} "

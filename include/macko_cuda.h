@@ -87,6 +87,13 @@ macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uin
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y,
                             void* stream);
 
+/* macko_dev_spmv with launch flags.  MACKO_SPMV_PDL: programmatic dependent launch — the kernel
+ * may begin (plan load, first matrix fills) while the previous kernel on the stream drains, and
+ * waits for it before reading x.  For chains of SpMVs (decoder stacks); CUDA-graph capturable. */
+#define MACKO_SPMV_PDL 1u
+macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
+                               uint32_t flags);
+
 /* End-to-end call with HOST buffers (what a CPU caller of reference_spmv would bind): copies
  * x host->device, runs macko_dev_spmv, copies y device->host, synchronises the stream.
  * Pinned host buffers make the copies asynchronous DMA. */

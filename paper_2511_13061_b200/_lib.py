@@ -9,14 +9,15 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmacko_cuda.so")
+# MACKO_LIB overrides the library path (the opt-in trace build, `make trace`); default in-tree .so
+LIB_PATH = os.environ.get("MACKO_LIB") or os.path.join(HERE, "libmacko_cuda.so")
 
 MACKO_OK, MACKO_EINVAL, MACKO_EFORMAT, MACKO_EIO, MACKO_EINFEASIBLE, MACKO_ECUDA, MACKO_ENCCL, MACKO_ENOMEM = range(8)
 
 # Every symbol include/macko_cuda.h declares (tests check the library exports all of them).
 EXPORTS = (
     "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_get_info",
-    "macko_dev_download", "macko_dev_spmv", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
+    "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
 )
@@ -90,6 +91,8 @@ def load() -> C.CDLL:
     L.macko_dev_download.argtypes = [vp, vp, vp, vp, vp]
     L.macko_dev_spmv.restype = st
     L.macko_dev_spmv.argtypes = [vp, vp, vp, vp]
+    L.macko_dev_spmv_ex.restype = st
+    L.macko_dev_spmv_ex.argtypes = [vp, vp, vp, vp, C.c_uint32]
     L.macko_spmv_host.restype = st
     L.macko_spmv_host.argtypes = [vp, vp, vp, vp]
     L.macko_dev_validate.restype = st

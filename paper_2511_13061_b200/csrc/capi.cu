@@ -504,9 +504,11 @@ macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uin
     });
 }
 
-macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
+macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
+                               uint32_t flags) {
     return guarded([&] {
         if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
+        if (flags & ~(uint32_t)MACKO_SPMV_PDL) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
         if (m->b_delta != 4)
             fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only; got " + std::to_string(m->b_delta));
         DeviceGuard g(m->device);
@@ -524,9 +526,14 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
-        ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream), "macko_spmv launch");
+        ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0),
+           "macko_spmv launch");
         g_launches.fetch_add(1);
     });
+}
+
+macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
+    return macko_dev_spmv_ex(m, d_x, d_y, stream, 0);
 }
 
 macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream) {
@@ -615,5 +622,10 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
         out->smem_bytes = m->smem;
     });
 }
+
+#ifdef MACKO_TRACE
+// trace build only (not declared in include/macko_cuda.h): per-warp prologue timestamps
+int macko_trace_read(unsigned long long* host, size_t n) { return (int)mk::trace_read(host, n); }
+#endif
 
 }  // extern "C"

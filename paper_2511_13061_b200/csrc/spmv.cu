@@ -33,6 +33,24 @@
 
 #include <type_traits>
 
+#ifdef MACKO_TRACE
+// Opt-in trace build (`make trace` -> libmacko_cuda_trace.so): per warp, %globaltimer at each
+// prologue phase and at the end, for latency studies of small SpMVs (tools/trace_spmv.py).
+__device__ unsigned long long g_macko_trace[148 * 32 * 8];
+#define MK_TRACE(i)                                                                                    \
+    do {                                                                                                \
+        if ((threadIdx.x & 31) == 0 && blockIdx.x < 148) {                                              \
+            unsigned long long t_;                                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+            g_macko_trace[(blockIdx.x * 32 + (threadIdx.x >> 5)) * 8 + (i)] = t_;                       \
+        }                                                                                               \
+    } while (0)
+#else
+#define MK_TRACE(i) \
+    do {            \
+    } while (0)
+#endif
+
 namespace mk {
 
 namespace {
@@ -307,9 +325,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t C = a.cols;
     const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
+    MK_TRACE(0);
     const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + w);
     const uint4 q0 = __ldg(rec), q1 = __ldg(rec + 1), q2 = __ldg(rec + 2);
     const bool has_work = q0.x != 0;
+    MK_TRACE(1);
+    // Programmatic dependent launch (chains of SpMVs): the next kernel in the stream may start
+    // its prologue (plan record, first matrix ring fills) on SMs this grid has left; everything
+    // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     // The first ring fills go out first; x staging overlaps their HBM latency.
     RowState rs;
@@ -328,14 +352,38 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         g.rel_mark = g.ebase + kChunk;
         g.wslot = 0;
         g.wphase = 0;
-        if (lane == 0) {
-            for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncwarp();
         const uint32_t limit = min(g.ebase + a.ring * kChunk, g.stream_end);
-        for (; g.iss < limit; g.iss += kChunk) ring_issue(g, a, lane);
+        if (lane == 0) {
+            // The barriers are used by this warp and its own bulk copies only (no cluster): the
+            // async-proxy fence orders their initialisation before the copies' complete_tx.
+            for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            MK_TRACE(5);
+            // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so
+            // one copy per array fills them all and completes on barrier 0; the other barriers
+            // complete their first phase with a plain arrive (the consumer passes barrier 0 first).
+            const uint32_t n = (limit - g.ebase) / kChunk;
+            if (n) {
+                asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
+                             "r"(n * (kChunkVBytes + kChunkDBytes))
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        g.vbase),
+                    "l"(a.values + g.ebase), "r"(n * kChunkVBytes), "r"(g.bar0)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        g.dbase),
+                    "l"(a.deltas + g.ebase / 2), "r"(n * kChunkDBytes), "r"(g.bar0)
+                    : "memory");
+                for (uint32_t i = 1; i < n; ++i)
+                    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
+            }
+            MK_TRACE(7);
+        }
+        g.iss = limit;
+        __syncwarp();
         rs.r = q0.y;
         rs.units_left = q0.x;
         rs.s = q1.y;
@@ -344,16 +392,27 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         begin_piece(rs, q0.z, (int)q1.w, (int32_t)q2.x, q2.z);
     }
 
+    MK_TRACE(2);
+    // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    MK_TRACE(3);
     // Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries).
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
     if constexpr (x_table<kXMode>()) {
         const uint4* x4 = reinterpret_cast<const uint4*>(a.x);  // 16-byte aligned (capi guarantees)
         const uint32_t nv = C / 8;
-        for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4*>(xs)[i] = __ldg(x4 + i);
+        // every CTA reads all of x: start each CTA at a different place so the 148 concurrent
+        // streams spread over the L2 slices instead of queueing on the same lines
+        const uint32_t rot = nv ? (blockIdx.x * 97u) % nv : 0u;
+        for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+            const uint32_t k = i + rot < nv ? i + rot : i + rot - nv;
+            reinterpret_cast<uint4*>(xs)[k] = __ldg(x4 + k);
+        }
         for (uint32_t i = nv * 8 + threadIdx.x; i < C + kXGuardHi; i += blockDim.x) xs[i] = i < C ? a.x[i] : 0;
         if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
     }
     __syncthreads();
+    MK_TRACE(4);
     if (!has_work) return;
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
     if (rs.T == 0) {
@@ -422,6 +481,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         }
         if (!next_piece(rs, a, w, lane)) break;
     }
+    MK_TRACE(6);
 }
 
 // Column just before the first unit of every chunk that starts inside a row:
@@ -470,21 +530,41 @@ cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
     }
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s) {
-    const int threads = kSpmvWarpsPerCta * kWarp;
+template <int kXMode>
+static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSpmvWarpsPerCta * kWarp);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, macko_spmv_b4<kXMode>, a);
+}
+
+cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
     switch (x_mode) {
-        case 11: macko_spmv_b4<11><<<grid, threads, smem, s>>>(a); break;
-        case 10: macko_spmv_b4<10><<<grid, threads, smem, s>>>(a); break;
-        case 9: macko_spmv_b4<9><<<grid, threads, smem, s>>>(a); break;
-        case 8: macko_spmv_b4<8><<<grid, threads, smem, s>>>(a); break;
-        case 7: macko_spmv_b4<7><<<grid, threads, smem, s>>>(a); break;
-        case 6: macko_spmv_b4<6><<<grid, threads, smem, s>>>(a); break;
-        case 1: macko_spmv_b4<1><<<grid, threads, smem, s>>>(a); break;
-        case 0: macko_spmv_b4<0><<<grid, threads, smem, s>>>(a); break;
+        case 11: return launch_one<11>(a, grid, smem, s, pdl);
+        case 10: return launch_one<10>(a, grid, smem, s, pdl);
+        case 9: return launch_one<9>(a, grid, smem, s, pdl);
+        case 8: return launch_one<8>(a, grid, smem, s, pdl);
+        case 7: return launch_one<7>(a, grid, smem, s, pdl);
+        case 6: return launch_one<6>(a, grid, smem, s, pdl);
+        case 1: return launch_one<1>(a, grid, smem, s, pdl);
+        case 0: return launch_one<0>(a, grid, smem, s, pdl);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
+
+#ifdef MACKO_TRACE
+cudaError_t trace_read(unsigned long long* host, size_t n) {
+    n = n < sizeof(g_macko_trace) / 8 ? n : sizeof(g_macko_trace) / 8;
+    return cudaMemcpyFromSymbol(host, g_macko_trace, n * 8);
+}
+#endif
 
 cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s) {
     const int threads = 256;

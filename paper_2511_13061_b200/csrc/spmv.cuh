@@ -59,7 +59,11 @@ constexpr int kXGuardHi = 16;
 // x_mode: 0 = texture gathers only, 1 = fp16 shared-memory table only, 6..9 = table + texture
 // gathers for a fixed subset of element slots (TEX pipe in parallel with the LSU pipe)
 bool spmv_valid_x_mode(int x_mode);
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s);
+#ifdef MACKO_TRACE
+cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
+#endif
+// pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
+cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
 cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);
 

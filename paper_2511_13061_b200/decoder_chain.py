@@ -1,0 +1,193 @@
+"""Batch-1 decode chain of sparse linears — BASELINE.json config 4: "Llama2-7B full decoder stack
+of 32 layers' sparse linears at 50 %, batch-1 decode SpMV chain, row-sharded over 1/2/4/8 B200".
+
+The paper's end-to-end use: every linear of a decoder layer is a MACKO
+matrix and one generated token is a chain of SpMVs.  Per layer (the stand-in for
+attention and the MLP activation — only the SpMV chain is timed):
+
+    qkv = W_qkv h          W_qkv = [W_q; W_k; W_v]   (3H x H, rows stacked: rows are independent,
+    o   = W_o v            v = qkv[2H:3H]              so the stacked encoding is the three
+    gu  = W_gu o           W_gu = [W_gate; W_up]       encodings concatenated)
+    h'  = W_down u         u = gu[I:2I]
+
+so a token is 4 dependent SpMVs per layer (128 for Llama2-7B: H = 4096, I = 11008, 8.1 GB of
+MACKO data at 50 % sparsity).  The chain is launched with programmatic dependent launch (each
+SpMV's plan load and first matrix fills overlap the previous kernel's tail) and captured into a
+CUDA graph.  Row sharding (N > 1): rank g owns the row slab g of every linear and the outputs are
+all-gathered (NCCL) after each SpMV, so every rank holds the full activation.
+
+`DenseDecoderChain` is the same chain over dense fp16 weights with torch.mv (cuBLAS GEMV, fp32
+compute) — the baseline the paper compares against.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import macko as M
+
+LINEARS = ("qkv", "o", "gate_up", "down")
+
+
+@dataclass(frozen=True)
+class ChainShape:
+    layers: int = 32
+    hidden: int = 4096
+    inter: int = 11008
+
+    def shape(self, name: str) -> Tuple[int, int]:
+        H, I = self.hidden, self.inter
+        return {"qkv": (3 * H, H), "o": (H, H), "gate_up": (2 * I, H), "down": (H, I)}[name]
+
+
+LLAMA2_7B = ChainShape(32, 4096, 11008)
+
+
+def weight_seed(base: int, layer: int, name: str) -> int:
+    return base + 16 * layer + LINEARS.index(name)
+
+
+def _x_slice(shape: ChainShape, name: str, acts: Dict[str, torch.Tensor]) -> torch.Tensor:
+    H, I = shape.hidden, shape.inter
+    if name == "qkv":
+        return acts["h"]
+    if name == "o":
+        return acts["qkv"][2 * H: 3 * H]
+    if name == "gate_up":
+        return acts["o"]
+    return acts["gate_up"][I: 2 * I]
+
+
+def _out_name(name: str) -> str:
+    return "h" if name == "down" else name
+
+
+class SparseDecoderChain:
+    """The decode chain over MACKO matrices built on the GPU (generator -> GPU compressor)."""
+
+    def __init__(self, shape: ChainShape = LLAMA2_7B, density: float = 0.5, seed: int = 0x5EEDA000,
+                 device: Optional[torch.device] = None, keep_dense: bool = False, group=None):
+        self.shape = shape
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.mats: List[Dict[str, M.DeviceMatrix]] = []
+        self.dense: List[Dict[str, torch.Tensor]] = []
+        self.bounds: Dict[str, Tuple[int, int]] = {}
+        H, I = shape.hidden, shape.inter
+        self.acts = {"h": torch.zeros(H, dtype=torch.float16, device=self.device),
+                     "qkv": torch.zeros(3 * H, dtype=torch.float16, device=self.device),
+                     "o": torch.zeros(H, dtype=torch.float16, device=self.device),
+                     "gate_up": torch.zeros(2 * I, dtype=torch.float16, device=self.device)}
+        self.local = {}
+        for name in LINEARS:
+            R, C = shape.shape(name)
+            r0, r1 = M.shard_rows(R, self.world, self.rank)
+            self.bounds[name] = (r0, r1)
+            if self.world > 1:
+                self.local[name] = torch.zeros(r1 - r0, dtype=torch.float16, device=self.device)
+        for layer in range(shape.layers):
+            mats, dense = {}, {}
+            for name in LINEARS:
+                R, C = shape.shape(name)
+                r0, r1 = self.bounds[name]
+                w = torch.empty((r1 - r0, C), dtype=torch.float16, device=self.device)
+                M.gen_dense(w, r1 - r0, C, density, seed=weight_seed(seed, layer, name), row0=r0)
+                mats[name] = M.DeviceMatrix.from_dense(w)
+                if keep_dense:
+                    dense[name] = w
+                else:
+                    del w
+            self.mats.append(mats)
+            self.dense.append(dense)
+        torch.cuda.synchronize(self.device)
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+
+    # -- accounting -------------------------------------------------------------------------
+    @property
+    def traffic_bytes(self) -> int:
+        """Algorithmic bytes of one token on this rank (sum of spmv_traffic of its slabs)."""
+        return sum(m.traffic_bytes for mats in self.mats for m in mats.values())
+
+    @property
+    def kernels_per_token(self) -> int:
+        return self.shape.layers * len(LINEARS)
+
+    # -- execution --------------------------------------------------------------------------
+    def _spmv(self, layer: int, name: str, stream, pdl: bool) -> None:
+        x = _x_slice(self.shape, name, self.acts)
+        out = self.acts[_out_name(name)]
+        if self.world == 1:
+            self.mats[layer][name].spmv_into(x, out, stream, pdl=pdl)
+        else:
+            self.mats[layer][name].spmv_into(x, self.local[name], stream, pdl=pdl)
+            dist.all_gather_into_tensor(out, self.local[name], group=self.group)
+
+    def forward_token(self, stream=None, pdl: bool = True) -> torch.Tensor:
+        """One token through every layer (stream-ordered; h is updated in place)."""
+        for layer in range(self.shape.layers):
+            for name in LINEARS:
+                # the first kernel of a token follows the previous token's last SpMV: chained too
+                self._spmv(layer, name, stream, pdl)
+        return self.acts["h"]
+
+    def capture(self, pdl: bool = True) -> torch.cuda.CUDAGraph:
+        """Capture forward_token into a CUDA graph (kernel nodes keep their PDL edges)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward_token(s, pdl)  # warm-up: texture objects for each x buffer, allocations
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward_token(s, pdl)
+        self.graph = g
+        return g
+
+    def close(self) -> None:
+        for mats in self.mats:
+            for m in mats.values():
+                m.close()
+        self.mats = []
+        self.dense = []
+
+
+class DenseDecoderChain:
+    """The same chain over dense fp16 weights: torch.mv = cuBLAS GEMV with fp32 compute."""
+
+    def __init__(self, sparse: SparseDecoderChain):
+        if not sparse.dense or not sparse.dense[0]:
+            raise ValueError("build the SparseDecoderChain with keep_dense=True")
+        self.sparse = sparse
+        self.shape = sparse.shape
+        self.acts = {k: torch.zeros_like(v) for k, v in sparse.acts.items()}
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+
+    @property
+    def traffic_bytes(self) -> int:
+        return sum(2 * w.numel() + 2 * w.shape[0] + 2 * w.shape[1] for d in self.sparse.dense for w in d.values())
+
+    def forward_token(self) -> torch.Tensor:
+        for layer in range(self.shape.layers):
+            for name in LINEARS:
+                torch.mv(self.sparse.dense[layer][name], _x_slice(self.shape, name, self.acts),
+                         out=self.acts[_out_name(name)])
+        return self.acts["h"]
+
+    def capture(self) -> torch.cuda.CUDAGraph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.forward_token()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward_token()
+        self.graph = g
+        return g

@@ -154,9 +154,13 @@ class DeviceMatrix:
     def validate(self, stream=None) -> None:
         check(_lib.load().macko_dev_validate(self._h, _stream_ptr(stream)))
 
-    def spmv_into(self, x, y, stream=None) -> None:
-        """y = A*x with device tensors / pointers (stream-ordered, asynchronous)."""
-        check(_lib.load().macko_dev_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+    def spmv_into(self, x, y, stream=None, pdl: bool = False) -> None:
+        """y = A*x with device tensors / pointers (stream-ordered, asynchronous).  pdl: launch as
+        a programmatic dependent of the previous kernel on the stream (SpMV chains)."""
+        if pdl:
+            check(_lib.load().macko_dev_spmv_ex(self._h, _ptr(x), _ptr(y), _stream_ptr(stream), 1))
+        else:
+            check(_lib.load().macko_dev_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
 
     def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
         """End-to-end call with host buffers (H2D x, kernel, D2H y, synchronise)."""
