@@ -19,9 +19,10 @@
 //   * x gathers are split between two pipes that run in parallel: an fp16 copy of x in shared
 //     memory (LDS, LSU pipe) and x as a 1-D texture (TEX pipe, L1-resident); which of a lane's
 //     8 element slots use the texture is a compile-time mask (x_mode).
-//   * Masked elements cost no predication: their codewords are forced to 0 (delta 1) and their
-//     values to +0, and they gather from zero guards around the shared table (or out-of-range
-//     texels, which read 0), so row edges run the same code as interior steps.
+//   * Row edges run the interior code with cheap masks: elements outside the row get codeword 0
+//     (delta 1, so the scan stays exact) and value +0, and they gather x = +0 (zero guards /
+//     out-of-range texels, or a predicated-off gather in the step holding the row end), so
+//     nothing outside the row reaches the sum, not even 0 * inf.
 //   * One persistent CTA of 32 warps per SM.  Rows cut between warps are finished by the
 //     last-arriving warp, which adds the per-unit partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
@@ -98,10 +99,12 @@ __device__ __forceinline__ Dec decode(uint32_t d) {
     return Dec{pp - dh, pp, pp >> 24};
 }
 
-// 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.
-template <int kXMode>
+// 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.  Masked
+// steps (row edges): element m gathers only if bit m of vm is set, else it multiplies x = +0
+// (its value is already +0), so nothing outside the row reaches the sum, not even 0 * inf.
+template <int kXMode, bool kMasked>
 __device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
-                                           cudaTextureObject_t xt) {
+                                           cudaTextureObject_t xt, uint32_t vm) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     // shared address of column cb: per element one PRMT (byte extract) + one IADD3
     uint32_t base = xs_addr + 2u * (uint32_t)cb;
@@ -112,8 +115,11 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec&
         split_halves(w[m], v0, v1);
         const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
         const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
-        const uint16_t x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
-        const uint16_t x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
+        uint16_t x0 = 0, x1 = 0;
+        if (!kMasked || ((vm >> (2 * m)) & 1u))
+            x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
+        if (!kMasked || ((vm >> (2 * m + 1)) & 1u))
+            x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
         acc = fma_f16f16f32(v0, x0, acc);
         acc = fma_f16f16f32(v1, x1, acc);
     }
@@ -142,7 +148,7 @@ struct RowState {
 __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colbase, int32_t sid, uint32_t slot) {
     // A row's first step starts at the 8-aligned al (ROMA); its k = s - al leading elements
     // belong to the previous row and are decoded as codeword 0 (delta 1) after masking, so the
-    // column before the row is -1 - k (the masked elements land on guard zeros at -k..-1).
+    // column before the row is -1 - k (the masked elements sit at columns -k..-1).
     rs.al = rs.s & ~7u;
     rs.T = rs.e > rs.s ? (rs.e - rs.al + kStepElts - 1) / kStepElts : 0u;
     // units of kUnitSteps steps; the last unit absorbs a remainder shorter than a unit
@@ -304,7 +310,7 @@ __device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
 // Keep only the lane's elements inside [s, e) (eb = the lane's first element): the others get
 // codeword 0 (delta 1) and value +0, and their columns fall on zero guards / out-of-range texels,
 // so they add exactly +0 (also when the masked values or x hold inf / NaN).
-__device__ __forceinline__ void mask_slot(Slot& sl, uint32_t eb, uint32_t s, uint32_t e) {
+__device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s, uint32_t e) {
     const int klo = min(max((int)(s - eb), 0), 8);
     const int khi = min(max((int)(e - eb), klo), 8);
     const uint32_t nm = (uint32_t)(((1ull << (4 * khi)) - 1ull) & ~((1ull << (4 * klo)) - 1ull));
@@ -315,6 +321,7 @@ __device__ __forceinline__ void mask_slot(Slot& sl, uint32_t eb, uint32_t s, uin
     sl.v.y &= prmt(lo, nm, 0xDD99u);
     sl.v.z &= prmt(lo, nm, 0xEEAAu);
     sl.v.w &= prmt(lo, nm, 0xFFBBu);
+    return (0xFFu >> (8 - khi)) & (0xFFu << klo) & 0xFFu;  // valid-element mask
 }
 
 template <int kXMode>
@@ -436,24 +443,37 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
         Slot A = lds_slot(g, relA);
         Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
+        uint32_t vmA = 0xFFu, vmB = 0xFFu;
         if constexpr (kMasked) {
             const uint32_t eb = S + 8u * lane;
-            mask_slot(A, eb, rs.s, rs.e);
-            mask_slot(B, eb + kStepElts, rs.s, rs.e);
+            vmA = mask_slot(A, eb, rs.s, rs.e);
+            vmB = mask_slot(B, eb + kStepElts, rs.s, rs.e);
         }
         const Dec dA = decode(A.d), dB = decode(B.d);
         const uint32_t pk = dA.local | (dB.local << 16);
         const uint32_t incl = warp_incl_scan_p(pk);
         const uint32_t tot = __reduce_add_sync(kFull, pk);
-        int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-        int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
-        if constexpr (kMasked) {  // lanes wholly past the row gather from the guard at C..C+8
-            const uint32_t eb = S + 8u * lane;
-            if (eb >= rs.e) cbA = (int)C;
-            if (eb + kStepElts >= rs.e) cbB = (int)C;
+        const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
+        const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+        if constexpr (kMasked) {
+            // Only the step holding the row end (step T-1) predicates its gathers: its masked
+            // elements decode to columns right after the row's last one.  Leading ROMA elements
+            // decode to -7..-1 and a phantom step is pointed at column C: both read zero guards
+            // (or out-of-range texels) with value +0.
+            if (t + 1u == rs.T) {
+                rs.acc = lane_step<kXMode, true>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+                rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, (int)C, xs_addr, a.xtex, vmB);
+            } else if (t + 2u == rs.T) {
+                rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+                rs.acc = lane_step<kXMode, true>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            } else {
+                rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+                rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            }
+        } else {
+            rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+            rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
         }
-        rs.acc = lane_step<kXMode>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex);
-        rs.acc = lane_step<kXMode>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex);
         rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
     };
 

@@ -48,10 +48,9 @@ constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two ste
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
 constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
 constexpr uint32_t kMaxRing = 4;
-// fp16 x table in shared memory: kXGuardLo zero entries before x[0] (the ROMA-masked elements of
-// a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (the masked elements
-// of a row's last step decode to at most 7 columns past its last element; lanes wholly past the
-// row are pointed at column C, so their elements land on C+1..C+8).
+// fp16 x table in shared memory with zero guards: kXGuardLo entries before x[0] (the ROMA-masked
+// elements of a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (a phantom
+// step past the row end is pointed at column C, its elements land on C+1..C+8).
 constexpr int kXGuardLo = 8;
 constexpr int kXGuardHi = 16;
 

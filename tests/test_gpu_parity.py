@@ -308,3 +308,40 @@ def test_native_library_is_the_code_path(cuda):
 
     maps = open("/proc/self/maps").read()
     assert re.search(r"libmacko_cuda\.so", maps)
+
+
+def _same_or_both_nan(a: np.ndarray, b: np.ndarray) -> bool:
+    fa, fb = a.view(np.float16), b.view(np.float16)
+    nan = np.isnan(fa) & np.isnan(fb)
+    return bool(np.all(nan | (a == b)))
+
+
+@pytest.mark.parametrize("x_mode", [-1, 0, 1, 6, 7, 8])
+def test_masked_edges_do_not_leak_inf_nan(cuda, x_mode):
+    # Row edges are masked (codeword 0, value +0, x = +0).  Even rows are finite and end exactly
+    # at column 699 (so masked elements after their end decode to columns 700..706); x is inf /
+    # NaN from column 700 on, and the odd rows hold inf / NaN values (the ROMA-masked elements at
+    # the start of every even row belong to them).  reference_spmv multiplies only a row's own
+    # stored elements and pads: the even rows must come out finite and bit-exact.
+    R, C = 240, 1500
+    A = O.gen_dense(R, C, 0.35, 21)
+    A[0::2, 700:] = 0
+    A[0::2, 699] = 0x3C00  # 1.0
+    for r in range(1, R, 2):
+        cols = np.nonzero(A[r])[0]
+        A[r, cols[:: max(1, cols.size // 4)]] = np.uint16(0x7C00)
+        A[r, cols[1]] = np.uint16(0x7E00)
+    x = O.gen_vector(C, 22)
+    x[700::3] = np.uint16(0x7C00)
+    x[701::3] = np.uint16(0xFC00)
+    x[702::3] = np.uint16(0x7E00)
+    dm = gpu_encode(A)
+    if x_mode >= 0:
+        dm.configure(x_mode)
+    m = O.encode_dense(A)
+    y = gpu_spmv(dm, x)
+    y_ref = O.b200_order_spmv(m, x, UNIT_STEPS)
+    assert _same_or_both_nan(y, y_ref)
+    assert np.isfinite(y_ref[0::2].view(np.float16)).all()
+    assert np.array_equal(y[0::2], y_ref[0::2])
+    assert not np.isfinite(y[1::2].view(np.float16)).any()

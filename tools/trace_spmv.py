@@ -53,3 +53,12 @@ for i, name in [(0, "start"), (1, "record"), (5, "mbar init"), (7, "ring issued"
     col = rel[:, i][t[ok, i] > 0]
     if col.size:
         print(f"{name:10s} min {col.min():7.2f}  med {np.median(col):7.2f}  p90 {np.percentile(col, 90):7.2f}  max {col.max():7.2f} us")
+# tail analysis: per-CTA spread of the done stamps
+done = np.where(t[:, 6] > 0, (t[:, 6] - t0) / 1e3, np.nan).reshape(148, 32)
+cta_max = np.nanmax(done, axis=1)
+cta_min = np.nanmin(done, axis=1)
+print(f"per-CTA last warp: min {np.nanmin(cta_max):.2f} med {np.nanmedian(cta_max):.2f} max {np.nanmax(cta_max):.2f} us; "
+      f"within-CTA spread med {np.nanmedian(cta_max - cta_min):.2f} max {np.nanmax(cta_max - cta_min):.2f} us")
+order = np.argsort(cta_max)
+print("slowest CTAs:", [(int(i), round(float(cta_max[i]), 1)) for i in order[-6:]])
+print("fastest CTAs:", [(int(i), round(float(cta_max[i]), 1)) for i in order[:6]])
