@@ -111,8 +111,9 @@ class DeviceMatrix {
     void validate(void* stream = nullptr) const { check(macko_dev_validate(h_, stream)); }
 
     // y = A*x on device buffers (stream ordered).
-    void spmv(const uint16_t* d_x, uint16_t* d_y, void* stream = nullptr) const {
-        check(macko_dev_spmv(h_, d_x, d_y, stream));
+    // pdl: programmatic dependent launch after the previous kernel on the stream (SpMV chains)
+    void spmv(const uint16_t* d_x, uint16_t* d_y, void* stream = nullptr, bool pdl = false) const {
+        check(macko_dev_spmv_ex(h_, d_x, d_y, stream, pdl ? MACKO_SPMV_PDL : 0u));
     }
 
     // reference_spmv drop-in on host vectors: H2D x, kernel, D2H y.
