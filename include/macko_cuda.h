@@ -104,6 +104,32 @@ macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
 
 macko_status macko_dev_free(macko_dev_matrix* m);
 
+/* ---- MCKO container (io.cpp write_macko / read_macko are absent) ----------
+ * File: 32-byte little-endian header "MCKO" | u16 version=1 | u8 b_val=16 | u8 b_delta | u64 R |
+ * u64 C | u64 pad_nnz, then row_pointers ((R+1) x u32), packed_deltas (macko_delta_bytes) and
+ * values (u16, macko_values_bytes).  read(write(m)) is bit-identical.  Errors: bad magic /
+ * version / truncated section -> MACKO_EIO (IoError); invariant violation after decode ->
+ * MACKO_EFORMAT (FormatError). */
+macko_status macko_mcko_write(const char* path, uint64_t rows, uint64_t cols, uint32_t b_delta, const uint16_t* values,
+                              uint64_t n_values, const uint8_t* deltas, uint64_t n_delta_bytes, const uint32_t* row_ptrs);
+/* Header only: rows, cols, pad_nnz, b_delta and the array sizes (values_bytes, delta_bytes) a
+ * caller allocates for macko_mcko_read; device = -1. */
+macko_status macko_mcko_read_info(const char* path, macko_dev_info* out);
+/* read_macko into caller arrays (sizes from macko_mcko_read_info); fully validated on the host. */
+macko_status macko_mcko_read(const char* path, uint16_t* values, uint8_t* deltas, uint32_t* row_ptrs);
+/* Device matrix -> file (pinned staging, synchronous). */
+macko_status macko_mcko_write_dev(const macko_dev_matrix* m, const char* path, void* stream);
+/* File -> device matrix without a host copy of the payload: the sections stream through two
+ * pinned buffers (disk read overlapped with the H2D copy), then validate_macko runs on the
+ * device and the SpMV plan is built.  Synchronises `stream`. */
+macko_status macko_mcko_read_dev(int device, const char* path, void* stream, macko_dev_matrix** out);
+
+/* Matrix Market reader: "%%MatrixMarket matrix coordinate real|integer
+ * general" -> dense row-major fp16 (1-based indices, entries rounded to fp16 RNE).  Call with
+ * dense = NULL to get the dimensions, then with rows*cols uint16 of storage.  Unsupported
+ * header / parse errors -> MACKO_EIO; out-of-range index / duplicate coordinate -> MACKO_EFORMAT. */
+macko_status macko_mm_read_dense(const char* path, uint64_t* rows, uint64_t* cols, uint16_t* dense);
+
 /* ---- synthetic inputs (counter-hash generator, bit-identical to oracle/macko_oracle.c) ---- */
 uint32_t macko_density_threshold(double density);
 /* Dense rows [row0, row0+rows) of a conceptual (row0+rows) x cols matrix; element (r, c) is

@@ -351,3 +351,20 @@ class RefMatrix:
         if getattr(self, "h", None) is not None and self.h.value and _ref is not None:
             _ref.ref_matrix_free(self.h)
             self.h = None
+
+
+# ---------------------------------------------------------------- MCKO container
+def mcko_bytes(m: Macko) -> bytes:
+    """write_macko restated from SPEC.md:376-386 (io.cpp is absent): 32-byte LE header "MCKO",
+    u16 version 1, u8 b_val 16, u8 b_delta, u64 R, u64 C, u64 pad_nnz; then row_pointers
+    ((R+1) x u32 LE), packed_deltas (tail-padded to 16 B), values (u16 LE, tail-padded to 16 B)."""
+    import struct
+
+    pad_nnz = m.pad_nnz
+    db, vb = delta_bytes(pad_nnz, m.b_delta), values_bytes(pad_nnz)
+    d = np.zeros(db, np.uint8)
+    d[: min(db, m.deltas.size)] = m.deltas[:db]
+    v = np.zeros(vb // 2, np.uint16)
+    v[: min(vb // 2, m.values.size)] = m.values[: vb // 2]
+    head = b"MCKO" + struct.pack("<HBBQQQ", 1, 16, m.b_delta, m.rows, m.cols, pad_nnz)
+    return head + np.asarray(m.row_ptrs, "<u4").tobytes() + d.tobytes() + v.astype("<u2").tobytes()

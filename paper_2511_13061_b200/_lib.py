@@ -20,6 +20,8 @@ EXPORTS = (
     "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
+    "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
+    "macko_mm_read_dense",
 )
 
 
@@ -107,6 +109,19 @@ def load() -> C.CDLL:
     L.macko_gen_vector.argtypes = [i32, vp, u64, u64, i32, vp]
     L.macko_shard_rows.restype = st
     L.macko_shard_rows.argtypes = [u64, u32, u32, C.POINTER(u64), C.POINTER(u64)]
+    cp = C.c_char_p
+    L.macko_mcko_write.restype = st
+    L.macko_mcko_write.argtypes = [cp, u64, u64, u32, vp, u64, vp, u64, vp]
+    L.macko_mcko_read_info.restype = st
+    L.macko_mcko_read_info.argtypes = [cp, C.POINTER(DevInfo)]
+    L.macko_mcko_read.restype = st
+    L.macko_mcko_read.argtypes = [cp, vp, vp, vp]
+    L.macko_mcko_write_dev.restype = st
+    L.macko_mcko_write_dev.argtypes = [vp, cp, vp]
+    L.macko_mcko_read_dev.restype = st
+    L.macko_mcko_read_dev.argtypes = [C.c_int, cp, vp, C.POINTER(vp)]
+    L.macko_mm_read_dense.restype = st
+    L.macko_mm_read_dense.argtypes = [cp, C.POINTER(u64), C.POINTER(u64), vp]
     L.macko_dev_launch_info.restype = st
     L.macko_dev_launch_info.argtypes = [vp, C.POINTER(LaunchInfo)]
     L.macko_dev_configure.restype = st

@@ -6,7 +6,10 @@
 // C boundary; the C++ wrapper include/macko/macko_cuda.hpp rethrows the reference types).
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <set>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -353,6 +356,198 @@ const uint16_t* x_view(const macko_dev_matrix* m, const uint16_t* d_x, bool need
     return d_x;
 }
 
+// ------------------------------------------------------------------------------------------
+// MCKO container (io.cpp absent): 32-byte little-endian header
+//   "MCKO" | u16 version = 1 | u8 b_val = 16 | u8 b_delta | u64 R | u64 C | u64 pad_nnz
+// then row_pointers ((R+1) x u32 LE), packed_deltas (macko_delta_bytes), values (u16 LE,
+// macko_values_bytes) back to back.  Readers reject a bad magic / version / truncated section
+// (MACKO_EIO = IoError) and any invariant violation after decode (MACKO_EFORMAT = FormatError).
+// ------------------------------------------------------------------------------------------
+constexpr size_t kMckoHeader = 32;
+
+struct MckoHeader {
+    uint32_t b_delta = 4;
+    uint64_t rows = 0, cols = 0, pad_nnz = 0;
+};
+
+void put_u16(uint8_t* p, uint16_t v) {
+    p[0] = (uint8_t)v;
+    p[1] = (uint8_t)(v >> 8);
+}
+void put_u64(uint8_t* p, uint64_t v) {
+    for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+uint16_t get_u16(const uint8_t* p) { return (uint16_t)(p[0] | (p[1] << 8)); }
+uint64_t get_u64(const uint8_t* p) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+bool host_little_endian() {
+    const uint16_t one = 1;
+    return *reinterpret_cast<const uint8_t*>(&one) == 1;
+}
+
+struct File {
+    FILE* f = nullptr;
+    File(const char* path, const char* mode) {
+        if (!path) fail(MACKO_EINVAL, "null path");
+        f = std::fopen(path, mode);
+        if (!f) fail(MACKO_EIO, std::string("cannot open ") + path);
+    }
+    ~File() {
+        if (f) std::fclose(f);
+    }
+    void write(const void* p, size_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n) fail(MACKO_EIO, "short write");
+    }
+    void read(void* p, size_t n, const char* what) {
+        if (n && std::fread(p, 1, n, f) != n) fail(MACKO_EIO, std::string("truncated ") + what + " section");
+    }
+    void zeros(size_t n) {
+        static const uint8_t z[16] = {0};
+        while (n) {
+            const size_t k = std::min<size_t>(n, 16);
+            write(z, k);
+            n -= k;
+        }
+    }
+};
+
+void write_header(File& f, const MckoHeader& h) {
+    uint8_t b[kMckoHeader] = {'M', 'C', 'K', 'O'};
+    put_u16(b + 4, 1);
+    b[6] = 16;
+    b[7] = (uint8_t)h.b_delta;
+    put_u64(b + 8, h.rows);
+    put_u64(b + 16, h.cols);
+    put_u64(b + 24, h.pad_nnz);
+    f.write(b, sizeof b);
+}
+
+MckoHeader read_header(File& f) {
+    uint8_t b[kMckoHeader];
+    f.read(b, sizeof b, "header");
+    if (std::memcmp(b, "MCKO", 4) != 0) fail(MACKO_EIO, "bad magic (not an MCKO file)");
+    if (get_u16(b + 4) != 1) fail(MACKO_EIO, "unsupported MCKO version " + std::to_string(get_u16(b + 4)));
+    if (b[6] != 16) fail(MACKO_EFORMAT, "value width must be 16 bits");
+    MckoHeader h;
+    h.b_delta = b[7];
+    h.rows = get_u64(b + 8);
+    h.cols = get_u64(b + 16);
+    h.pad_nnz = get_u64(b + 24);
+    if (!(h.b_delta == 1 || h.b_delta == 2 || h.b_delta == 4 || h.b_delta == 8))
+        fail(MACKO_EFORMAT, "delta width must be one of 1, 2, 4, 8 bits; got " + std::to_string(h.b_delta));
+    if (h.rows == 0 || h.cols == 0 || h.rows >= 0x7FFFFFFFull || h.cols >= 0x7FFFFFFFull)
+        fail(MACKO_EFORMAT, "matrix dimensions out of range");
+    if (h.pad_nnz > 0xFFFFFFFFull) fail(MACKO_EFORMAT, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
+    return h;
+}
+
+// Row pointers section: read + check (row_pointers[0] = 0, monotone, row_pointers[R] = pad_nnz).
+std::vector<uint32_t> read_row_ptrs(File& f, const MckoHeader& h) {
+    std::vector<uint32_t> rp(h.rows + 1);
+    std::vector<uint8_t> raw((h.rows + 1) * 4);
+    f.read(raw.data(), raw.size(), "row_pointers");
+    for (uint64_t i = 0; i <= h.rows; ++i)
+        rp[i] = raw[4 * i] | (raw[4 * i + 1] << 8) | (raw[4 * i + 2] << 16) | ((uint32_t)raw[4 * i + 3] << 24);
+    if (rp[0] != 0) fail(MACKO_EFORMAT, "row_pointers[0] must be 0");
+    for (uint64_t r = 0; r < h.rows; ++r)
+        if (rp[r + 1] < rp[r]) fail(MACKO_EFORMAT, "row_pointers not monotone");
+    if (rp[h.rows] != h.pad_nnz) fail(MACKO_EFORMAT, "row_pointers[R] != pad_nnz in the header");
+    return rp;
+}
+
+// validate_macko (convert.hpp:25-27) on host arrays: codewords decode to strictly increasing
+// columns < C, padding entries (codeword all-ones followed by... any entry with value +/-0) are +0.
+void host_validate(const MckoHeader& h, const std::vector<uint32_t>& rp, const uint8_t* deltas, const uint16_t* values) {
+    const uint32_t bits = h.b_delta, per = 8 / bits, mask = (1u << bits) - 1u;
+    for (uint64_t r = 0; r < h.rows; ++r) {
+        int64_t col = -1;
+        for (uint64_t e = rp[r]; e < rp[r + 1]; ++e) {
+            col += ((deltas[e / per] >> ((e % per) * bits)) & mask) + 1;
+            if ((uint64_t)col >= h.cols) fail(MACKO_EFORMAT, "decoded column index past the column bound");
+            if ((values[e] & 0x7FFFu) == 0 && values[e] != 0) fail(MACKO_EFORMAT, "padding value must be +0");
+        }
+    }
+}
+
+// Streams `bytes` from the file into device memory through two pinned staging buffers, so the
+// disk read of one block overlaps the H2D copy of the previous one.
+void stream_to_device(File& f, void* dst, uint64_t bytes, cudaStream_t st, const char* what) {
+    constexpr size_t kBlock = 32u << 20;
+    uint8_t* pinned[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    struct Cleanup {
+        uint8_t** p;
+        cudaEvent_t* e;
+        ~Cleanup() {
+            for (int i = 0; i < 2; ++i) {
+                if (e[i]) {
+                    cudaEventSynchronize(e[i]);
+                    cudaEventDestroy(e[i]);
+                }
+                if (p[i]) cudaFreeHost(p[i]);
+            }
+        }
+    } cleanup{pinned, done};
+    const size_t blk = (size_t)std::min<uint64_t>(bytes, kBlock);
+    if (!blk) return;
+    for (int i = 0; i < 2; ++i) {
+        ck(cudaMallocHost(&pinned[i], blk), "pinned staging buffer");
+        ck(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "event");
+    }
+    bool used[2] = {false, false};
+    uint64_t off = 0;
+    for (int i = 0; off < bytes; i ^= 1) {
+        const size_t n = (size_t)std::min<uint64_t>(bytes - off, blk);
+        if (used[i]) ck(cudaEventSynchronize(done[i]), "staging wait");
+        f.read(pinned[i], n, what);
+        ck(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, pinned[i], n, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaEventRecord(done[i], st), "event");
+        used[i] = true;
+        off += n;
+    }
+}
+
+// Matrix Market coordinate real/integer general -> dense fp16 (row-major), entries converted
+// like the reference's float_to_half (fp16.cpp:37-73: RNE) from the parsed value.
+void read_mm(const char* path, uint64_t* rows, uint64_t* cols, uint16_t* dense) {
+    File f(path, "r");
+    char line[4096];
+    if (!std::fgets(line, sizeof line, f.f)) fail(MACKO_EIO, "empty Matrix Market file");
+    std::string hdr(line);
+    for (auto& c : hdr) c = (char)std::tolower((unsigned char)c);
+    if (hdr.rfind("%%matrixmarket", 0) != 0) fail(MACKO_EIO, "missing %%MatrixMarket banner");
+    if (hdr.find("matrix") == std::string::npos || hdr.find("coordinate") == std::string::npos ||
+        (hdr.find("real") == std::string::npos && hdr.find("integer") == std::string::npos) ||
+        hdr.find("general") == std::string::npos)
+        fail(MACKO_EIO, "unsupported Matrix Market kind (need: matrix coordinate real|integer general)");
+    unsigned long long R = 0, C = 0, nnz = 0;
+    for (;;) {
+        if (!std::fgets(line, sizeof line, f.f)) fail(MACKO_EIO, "missing size line");
+        if (line[0] == '%' || line[strspn(line, " \t\r\n")] == 0) continue;
+        if (std::sscanf(line, "%llu %llu %llu", &R, &C, &nnz) != 3) fail(MACKO_EIO, "bad size line");
+        break;
+    }
+    if (R == 0 || C == 0 || R >= 0x7FFFFFFFull || C >= 0x7FFFFFFFull) fail(MACKO_EFORMAT, "matrix dimensions out of range");
+    *rows = R;
+    *cols = C;
+    if (!dense) return;
+    std::memset(dense, 0, R * C * 2);
+    std::set<std::pair<uint64_t, uint64_t>> seen;
+    for (unsigned long long k = 0; k < nnz; ++k) {
+        if (!std::fgets(line, sizeof line, f.f)) fail(MACKO_EIO, "truncated Matrix Market entries");
+        unsigned long long i = 0, j = 0;
+        double v = 0;
+        if (std::sscanf(line, "%llu %llu %lf", &i, &j, &v) != 3) fail(MACKO_EIO, "bad entry line");
+        if (i < 1 || j < 1 || i > R || j > C) fail(MACKO_EFORMAT, "Matrix Market index out of range");
+        if (!seen.insert({i, j}).second) fail(MACKO_EFORMAT, "duplicate Matrix Market coordinate");
+        const __half hv = __float2half_rn((float)v);
+        dense[(i - 1) * C + (j - 1)] = __half_as_ushort(hv);
+    }
+}
+
 void check_shape(uint64_t rows, uint64_t cols) {
     if (rows == 0 || cols == 0) fail(MACKO_EINVAL, "matrix dimensions must be >= 1");
     if (rows >= 0x7FFFFFFFull || cols >= 0x7FFFFFFFull) fail(MACKO_EINVAL, "rows/cols must be < 2^31");
@@ -585,6 +780,145 @@ macko_status macko_gen_vector(int device, uint16_t* d_out, uint64_t n, uint64_t 
         DeviceGuard g(device);
         ck(mk::launch_gen_vector(d_out, n, seed, int_mode, (cudaStream_t)stream), "gen_vector");
         g_launches.fetch_add(1);
+    });
+}
+
+
+// ---- MCKO container ----------------------------------------------------------------------
+macko_status macko_mcko_write(const char* path, uint64_t rows, uint64_t cols, uint32_t b_delta, const uint16_t* values,
+                              uint64_t n_values, const uint8_t* deltas, uint64_t n_delta_bytes, const uint32_t* row_ptrs) {
+    return guarded([&] {
+        if (!row_ptrs) fail(MACKO_EINVAL, "null row_pointers");
+        if (!host_little_endian()) fail(MACKO_EIO, "big-endian host");
+        check_bits(b_delta);
+        check_shape(rows, cols);
+        const uint64_t pad_nnz = row_ptrs[rows];
+        if (n_values < pad_nnz || n_delta_bytes * 8 < pad_nnz * b_delta) fail(MACKO_EFORMAT, "arrays shorter than pad_nnz");
+        if (pad_nnz && (!values || !deltas)) fail(MACKO_EINVAL, "null payload");
+        MckoHeader h;
+        h.b_delta = b_delta;
+        h.rows = rows;
+        h.cols = cols;
+        h.pad_nnz = pad_nnz;
+        File f(path, "wb");
+        write_header(f, h);
+        f.write(row_ptrs, (rows + 1) * 4);
+        const uint64_t db = delta_bytes(pad_nnz, b_delta), vb = values_bytes(pad_nnz);
+        const uint64_t dn = std::min<uint64_t>(n_delta_bytes, db), vn = std::min<uint64_t>(n_values * 2, vb);
+        f.write(deltas, dn);
+        f.zeros(db - dn);
+        f.write(values, vn);
+        f.zeros(vb - vn);
+    });
+}
+
+macko_status macko_mcko_read_info(const char* path, macko_dev_info* out) {
+    return guarded([&] {
+        if (!out) fail(MACKO_EINVAL, "null argument");
+        File f(path, "rb");
+        const MckoHeader h = read_header(f);
+        std::memset(out, 0, sizeof *out);
+        out->rows = h.rows;
+        out->cols = h.cols;
+        out->pad_nnz = h.pad_nnz;
+        out->b_delta = h.b_delta;
+        out->values_bytes = values_bytes(h.pad_nnz);
+        out->delta_bytes = delta_bytes(h.pad_nnz, h.b_delta);
+        out->row_ptr_bytes = 4 * (h.rows + 1);
+        out->traffic_bytes = out->values_bytes + out->delta_bytes + out->row_ptr_bytes + 2 * h.cols + 2 * h.rows;
+        out->device = -1;
+    });
+}
+
+macko_status macko_mcko_read(const char* path, uint16_t* values, uint8_t* deltas, uint32_t* row_ptrs) {
+    return guarded([&] {
+        if (!host_little_endian()) fail(MACKO_EIO, "big-endian host");
+        File f(path, "rb");
+        const MckoHeader h = read_header(f);
+        const std::vector<uint32_t> rp = read_row_ptrs(f, h);
+        const uint64_t db = delta_bytes(h.pad_nnz, h.b_delta), vb = values_bytes(h.pad_nnz);
+        std::vector<uint8_t> d(db);
+        std::vector<uint16_t> v(vb / 2);
+        f.read(d.data(), db, "packed_deltas");
+        f.read(v.data(), vb, "values");
+        host_validate(h, rp, d.data(), v.data());
+        if (row_ptrs) std::memcpy(row_ptrs, rp.data(), rp.size() * 4);
+        if (deltas) std::memcpy(deltas, d.data(), db);
+        if (values) std::memcpy(values, v.data(), vb);
+    });
+}
+
+macko_status macko_mcko_write_dev(const macko_dev_matrix* m, const char* path, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        if (!host_little_endian()) fail(MACKO_EIO, "big-endian host");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        MckoHeader h;
+        h.b_delta = m->b_delta;
+        h.rows = m->rows;
+        h.cols = m->cols;
+        h.pad_nnz = m->pad_nnz;
+        File f(path, "wb");
+        write_header(f, h);
+        f.write(m->h_row_ptrs.data(), (m->rows + 1) * 4);
+        constexpr size_t kBlock = 32u << 20;
+        uint8_t* pinned = nullptr;
+        ck(cudaMallocHost(&pinned, kBlock), "pinned staging buffer");
+        std::unique_ptr<uint8_t, cudaError_t (*)(void*)> hold(pinned, cudaFreeHost);
+        auto dump = [&](const void* src, uint64_t bytes) {
+            for (uint64_t off = 0; off < bytes; off += kBlock) {
+                const size_t n = (size_t)std::min<uint64_t>(bytes - off, kBlock);
+                ck(cudaMemcpyAsync(pinned, static_cast<const uint8_t*>(src) + off, n, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaStreamSynchronize(st), "sync");
+                f.write(pinned, n);
+            }
+        };
+        dump(m->deltas.p, delta_bytes(m->pad_nnz, m->b_delta));
+        dump(m->values.p, values_bytes(m->pad_nnz));
+    });
+}
+
+macko_status macko_mcko_read_dev(int device, const char* path, void* stream, macko_dev_matrix** out) {
+    return guarded([&] {
+        if (!out) fail(MACKO_EINVAL, "null argument");
+        *out = nullptr;
+        if (!host_little_endian()) fail(MACKO_EIO, "big-endian host");
+        File f(path, "rb");
+        const MckoHeader h = read_header(f);
+        std::vector<uint32_t> rp = read_row_ptrs(f, h);
+        DeviceGuard g(device);
+        cudaStream_t st = (cudaStream_t)stream;
+        auto* m = new macko_dev_matrix;
+        std::unique_ptr<macko_dev_matrix> hold(m);
+        m->device = device;
+        m->sms = sm_count(device);
+        m->rows = h.rows;
+        m->cols = h.cols;
+        m->pad_nnz = h.pad_nnz;
+        m->b_delta = h.b_delta;
+        const uint64_t vb = values_bytes(h.pad_nnz), db = delta_bytes(h.pad_nnz, h.b_delta);
+        m->values.alloc(vb / 2 + mk::kChunk);
+        m->deltas.alloc(db + mk::kChunkDBytes);
+        m->row_ptrs.alloc(h.rows + 1);
+        ck(cudaMemsetAsync(m->values.p + vb / 2, 0, mk::kChunk * 2, st), "memset");
+        ck(cudaMemsetAsync(m->deltas.p + db, 0, mk::kChunkDBytes, st), "memset");
+        ck(cudaMemcpyAsync(m->row_ptrs.p, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, st), "upload row_ptrs");
+        stream_to_device(f, m->deltas.p, db, st, "packed_deltas");
+        stream_to_device(f, m->values.p, vb, st, "values");
+        ck(cudaStreamSynchronize(st), "sync");
+        m->h_row_ptrs = std::move(rp);
+        device_validate(m, st);
+        if (m->b_delta == 4) build_plan(m, st);
+        *out = hold.release();
+    });
+}
+
+// ---- Matrix Market ------------------------------------------------------------------------
+macko_status macko_mm_read_dense(const char* path, uint64_t* rows, uint64_t* cols, uint16_t* dense) {
+    return guarded([&] {
+        if (!rows || !cols) fail(MACKO_EINVAL, "null argument");
+        read_mm(path, rows, cols, dense);
     });
 }
 

@@ -8,6 +8,8 @@ Reference operation (file:line)                     -> here (runs on the GPU thr
   validate_macko (convert.hpp:25-27)                 -> DeviceMatrix.validate()
   macko_values_bytes / macko_delta_bytes (matrix.hpp:77-81) -> values_bytes / delta_bytes
   spmv_traffic (SPEC.md:333-341)                     -> DeviceMatrix.traffic_bytes
+  write_macko / read_macko (SPEC.md:380-390)          -> write_mcko / read_mcko_host / read_mcko (-> device)
+  read_matrix_market (SPEC.md:391-397)                -> read_matrix_market
 
 Arguments follow the reference's meaning (fp16 payloads as raw uint16 bits, b_delta in
 {1,2,4,8}, row pointers as u32 element offsets) and its error behaviour (ValueError for
@@ -199,6 +201,59 @@ def spmv(m: DeviceMatrix, x, y=None, stream=None):
         y = torch.empty(m.rows, dtype=x.dtype, device=x.device)
     m.spmv_into(x, y, stream)
     return y
+
+
+def _path(path) -> bytes:
+    import os
+
+    return os.fsencode(path)
+
+
+def write_mcko(m, path) -> None:
+    """write_macko: a DeviceMatrix (streamed from HBM) or a host MackoMatrix."""
+    L = _lib.load()
+    if isinstance(m, DeviceMatrix):
+        check(L.macko_mcko_write_dev(m._h, _path(path), None))
+        return
+    vals = np.ascontiguousarray(m.values, np.uint16)
+    dl = np.ascontiguousarray(m.packed_deltas, np.uint8)
+    rp = np.ascontiguousarray(m.row_pointers, np.uint32)
+    check(L.macko_mcko_write(_path(path), m.rows, m.cols, m.b_delta, vals.ctypes.data if vals.size else None, len(vals),
+                             dl.ctypes.data if dl.size else None, len(dl), rp.ctypes.data))
+
+
+def mcko_info(path) -> _lib.DevInfo:
+    info = _lib.DevInfo()
+    check(_lib.load().macko_mcko_read_info(_path(path), C.byref(info)))
+    return info
+
+
+def read_mcko_host(path) -> MackoMatrix:
+    """read_macko into host arrays (validated like validate_macko)."""
+    i = mcko_info(path)
+    vals = np.zeros(i.values_bytes // 2, np.uint16)
+    dl = np.zeros(i.delta_bytes, np.uint8)
+    rp = np.zeros(i.rows + 1, np.uint32)
+    check(_lib.load().macko_mcko_read(_path(path), vals.ctypes.data if vals.size else None,
+                                      dl.ctypes.data if dl.size else None, rp.ctypes.data))
+    return MackoMatrix(i.rows, i.cols, i.b_delta, vals, dl, rp)
+
+
+def read_mcko(path, device: int = 0, stream=None) -> DeviceMatrix:
+    """MCKO file -> device matrix (sections streamed through pinned buffers, validated on the GPU)."""
+    h = C.c_void_p()
+    check(_lib.load().macko_mcko_read_dev(device, _path(path), _stream_ptr(stream), C.byref(h)))
+    return DeviceMatrix(h.value)
+
+
+def read_matrix_market(path) -> np.ndarray:
+    """read_matrix_market -> dense fp16 bits (rows x cols uint16)."""
+    L = _lib.load()
+    r, c = C.c_uint64(), C.c_uint64()
+    check(L.macko_mm_read_dense(_path(path), C.byref(r), C.byref(c), None))
+    out = np.zeros((r.value, c.value), np.uint16)
+    check(L.macko_mm_read_dense(_path(path), C.byref(r), C.byref(c), out.ctypes.data))
+    return out
 
 
 def density_threshold(d: float) -> int:
