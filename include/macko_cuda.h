@@ -104,6 +104,19 @@ macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
 
 macko_status macko_dev_free(macko_dev_matrix* m);
 
+/* ---- persistent SpMV chains (decoder stacks) ------------------------------------------------
+ * A fixed sequence of dependent SpMVs y_k = A_k x_k, where x_k may be (a slice of) an earlier
+ * y_j, run by ONE persistent cooperative kernel: each warp sets up op k+1 (plan record, first
+ * matrix ring fills) as soon as its part of op k is done and a grid barrier orders x_k after
+ * the op that wrote it, so the weight stream keeps HBM busy across the dependencies.  The
+ * matrices and vectors must outlive the chain; x buffers must be texture-aligned (512 B).
+ * Results are bit-identical to running the ops one by one with macko_dev_spmv. */
+typedef struct macko_chain macko_chain;
+macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint16_t* const* xs, uint16_t* const* ys,
+                                uint32_t n_ops, macko_chain** out);
+macko_status macko_chain_run(macko_chain* c, void* stream); /* one launch; CUDA-graph capturable */
+macko_status macko_chain_free(macko_chain* c);
+
 /* ---- MCKO container (io.cpp write_macko / read_macko are absent) ----------
  * File: 32-byte little-endian header "MCKO" | u16 version=1 | u8 b_val=16 | u8 b_delta | u64 R |
  * u64 C | u64 pad_nnz, then row_pointers ((R+1) x u32), packed_deltas (macko_delta_bytes) and

@@ -21,7 +21,7 @@ EXPORTS = (
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
-    "macko_mm_read_dense",
+    "macko_mm_read_dense", "macko_chain_create", "macko_chain_run", "macko_chain_free",
 )
 
 
@@ -120,6 +120,12 @@ def load() -> C.CDLL:
     L.macko_mcko_write_dev.argtypes = [vp, cp, vp]
     L.macko_mcko_read_dev.restype = st
     L.macko_mcko_read_dev.argtypes = [C.c_int, cp, vp, C.POINTER(vp)]
+    L.macko_chain_create.restype = st
+    L.macko_chain_create.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), u32, C.POINTER(vp)]
+    L.macko_chain_run.restype = st
+    L.macko_chain_run.argtypes = [vp, vp]
+    L.macko_chain_free.restype = st
+    L.macko_chain_free.argtypes = [vp]
     L.macko_mm_read_dense.restype = st
     L.macko_mm_read_dense.argtypes = [cp, C.POINTER(u64), C.POINTER(u64), vp]
     L.macko_dev_launch_info.restype = st

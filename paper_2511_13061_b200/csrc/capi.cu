@@ -133,6 +133,20 @@ struct macko_dev_matrix {
     }
 };
 
+struct macko_chain {
+    int device = 0;
+    int grid = 0, x_mode = 0;
+    size_t smem = 0;
+    uint32_t n_ops = 0;
+    DevBuf<uint8_t> ops;     // n_ops mk::SpmvArgs
+    DevBuf<uint32_t> bar;    // grid barrier {count, generation}
+    std::vector<cudaTextureObject_t> tex;
+    ~macko_chain() {
+        for (auto t : tex)
+            if (t) cudaDestroyTextureObject(t);
+    }
+};
+
 namespace {
 
 int sm_count(int dev) {
@@ -919,6 +933,105 @@ macko_status macko_mm_read_dense(const char* path, uint64_t* rows, uint64_t* col
     return guarded([&] {
         if (!rows || !cols) fail(MACKO_EINVAL, "null argument");
         read_mm(path, rows, cols, dense);
+    });
+}
+
+
+// ---- persistent SpMV chains -----------------------------------------------------------------
+macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint16_t* const* xs, uint16_t* const* ys,
+                                uint32_t n_ops, macko_chain** out) {
+    return guarded([&] {
+        if (!out || !mats || !xs || !ys || n_ops == 0) fail(MACKO_EINVAL, "bad chain arguments");
+        *out = nullptr;
+        const int dev = mats[0]->device;
+        DeviceGuard g(dev);
+        auto* c = new macko_chain;
+        std::unique_ptr<macko_chain> hold(c);
+        c->device = dev;
+        c->n_ops = n_ops;
+        c->grid = mats[0]->grid;
+        // one x_mode for all ops (a template parameter): the op with the most bytes decides
+        uint64_t best = 0;
+        size_t xtab = 0;
+        for (uint32_t k = 0; k < n_ops; ++k) {
+            const macko_dev_matrix* m = mats[k];
+            if (!m || !xs[k] || !ys[k]) fail(MACKO_EINVAL, "null matrix or vector in the chain");
+            if (m->device != dev) fail(MACKO_EINVAL, "chain ops must live on one device");
+            if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
+            if (m->grid != c->grid || m->ring != mats[0]->ring) fail(MACKO_EINVAL, "chain ops must share the launch plan geometry");
+            const uint64_t tb = values_bytes(m->pad_nnz) + delta_bytes(m->pad_nnz, 4);
+            if (tb >= best) {
+                best = tb;
+                c->x_mode = m->x_mode;
+            }
+            xtab = std::max<size_t>(xtab, align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128));
+        }
+        if (c->x_mode == 0) xtab = 0;
+        const uint32_t ring = mats[0]->ring;
+        c->smem = xtab + (size_t)ring * mk::kSpmvWarpsPerCta * (mk::kChunkVBytes + mk::kChunkDBytes);
+        int optin = 0;
+        ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attribute");
+        if (c->smem + 2048 > (size_t)optin) fail(MACKO_EINVAL, "chain x table + rings exceed shared memory");
+        int align = 0;
+        ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev), "texture alignment");
+        std::vector<mk::SpmvArgs> ops(n_ops);
+        for (uint32_t k = 0; k < n_ops; ++k) {
+            const macko_dev_matrix* m = mats[k];
+            if (reinterpret_cast<uintptr_t>(xs[k]) % std::max<uintptr_t>(16, (uintptr_t)align) != 0)
+                fail(MACKO_EINVAL, "chain x buffers must be texture-aligned (no staging copy inside a chain)");
+            mk::SpmvArgs& a = ops[k];
+            std::memset(&a, 0, sizeof a);
+            a.values = m->values.p;
+            a.deltas = m->deltas.p;
+            a.row_ptrs = m->row_ptrs.p;
+            a.x = xs[k];
+            a.y = ys[k];
+            a.rows = (uint32_t)m->rows;
+            a.cols = (uint32_t)m->cols;
+            a.value_elems = m->values.n;
+            a.delta_bytes = m->deltas.n;
+            a.ring = ring;
+            a.ring_offset = (uint32_t)xtab;
+            a.plan = m->plan;
+            a.xtex = 0;
+            if (c->x_mode != 1) {
+                cudaResourceDesc rd{};
+                rd.resType = cudaResourceTypeLinear;
+                rd.res.linear.devPtr = const_cast<uint16_t*>(xs[k]);
+                rd.res.linear.desc = cudaCreateChannelDesc<unsigned short>();
+                rd.res.linear.sizeInBytes = m->cols * 2;
+                cudaTextureDesc td{};
+                td.readMode = cudaReadModeElementType;
+                cudaTextureObject_t t = 0;
+                ck(cudaCreateTextureObject(&t, &rd, &td, nullptr), "x texture");
+                c->tex.push_back(t);
+                a.xtex = t;
+            }
+        }
+        c->ops.alloc(n_ops * sizeof(mk::SpmvArgs));
+        c->bar.alloc(2);
+        ck(cudaMemcpy(c->ops.p, ops.data(), n_ops * sizeof(mk::SpmvArgs), cudaMemcpyHostToDevice), "chain upload");
+        ck(cudaMemset(c->bar.p, 0, 8), "chain barrier");
+        *out = hold.release();
+    });
+}
+
+macko_status macko_chain_run(macko_chain* c, void* stream) {
+    return guarded([&] {
+        if (!c) fail(MACKO_EINVAL, "null chain");
+        DeviceGuard g(c->device);
+        ck(mk::launch_chain(reinterpret_cast<const mk::SpmvArgs*>(c->ops.p), c->n_ops, c->bar.p, c->grid, c->x_mode,
+                            c->smem, (cudaStream_t)stream),
+           "macko_chain launch");
+        g_launches.fetch_add(1);
+    });
+}
+
+macko_status macko_chain_free(macko_chain* c) {
+    return guarded([&] {
+        if (!c) return;
+        DeviceGuard g(c->device);
+        delete c;
     });
 }
 

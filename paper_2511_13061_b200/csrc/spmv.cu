@@ -38,6 +38,14 @@
 // Opt-in trace build (`make trace` -> libmacko_cuda_trace.so): per warp, %globaltimer at each
 // prologue phase and at the end, for latency studies of small SpMVs (tools/trace_spmv.py).
 __device__ unsigned long long g_macko_trace[148 * 32 * 8];
+#define MK_CTRACE(k, i)                                                                                \
+    do {                                                                                                \
+        if (threadIdx.x == 0 && (k) < 32) {                                                             \
+            unsigned long long t_;                                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+            g_macko_trace[(blockIdx.x * 32 + (k)) * 8 + (i)] = t_;                                      \
+        }                                                                                               \
+    } while (0)
 #define MK_TRACE(i)                                                                                    \
     do {                                                                                                \
         if ((threadIdx.x & 31) == 0 && blockIdx.x < 148) {                                              \
@@ -47,6 +55,9 @@ __device__ unsigned long long g_macko_trace[148 * 32 * 8];
         }                                                                                               \
     } while (0)
 #else
+#define MK_CTRACE(k, i) \
+    do {                \
+    } while (0)
 #define MK_TRACE(i) \
     do {            \
     } while (0)
@@ -324,42 +335,34 @@ __device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s,
     return (0xFFu >> (8 - khi)) & (0xFFu << klo) & 0xFFu;  // valid-element mask
 }
 
-template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(const SpmvArgs a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t C = a.cols;
-    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
-    MK_TRACE(0);
+// ------------------------------------------------------------------------------------------
+// Per-op building blocks (shared by the single-SpMV kernel and the persistent chain kernel)
+// ------------------------------------------------------------------------------------------
+// Set up the warp's ring and walk for one SpMV and issue the first ring fills.  `fresh`: the
+// barriers are initialised here and the first fill is one copy per array (single-SpMV kernel);
+// otherwise (chain) the ring continues where the previous op left it — the first chunk goes to
+// the slot after the last one consumed, each chunk on its own barrier phase.
+template <bool kFresh>
+__device__ __forceinline__ bool op_begin(const SpmvArgs& a, uint32_t w, uint32_t warp, int lane, uint32_t smem_base,
+                                         uint32_t bar0, Ring& g, RowState& rs) {
     const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + w);
     const uint4 q0 = __ldg(rec), q1 = __ldg(rec + 1), q2 = __ldg(rec + 2);
-    const bool has_work = q0.x != 0;
     MK_TRACE(1);
-    // Programmatic dependent launch (chains of SpMVs): the next kernel in the stream may start
-    // its prologue (plan record, first matrix ring fills) on SMs this grid has left; everything
-    // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-    // The first ring fills go out first; x staging overlaps their HBM latency.
-    RowState rs;
-    Ring g;
-    if (has_work) {
-        const uint32_t E0 = q0.w, E1 = q1.x;
-        const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-        g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
-        g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
-        g.bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
-        g.ebase = E0 & ~(kChunk - 1u);
-        g.emask = a.ring * kChunk - 1u;
-        g.iss = g.ebase;
-        g.stream_end = E1 > E0 ? ((E1 - 1u) & ~(kChunk - 1u)) + kChunk : g.ebase;
-        g.ready_end = g.ebase;
-        g.rel_mark = g.ebase + kChunk;
+    if (q0.x == 0) return false;
+    const uint32_t E0 = q0.w, E1 = q1.x;
+    g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
+    g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
+    g.bar0 = bar0;
+    const uint32_t e0 = E0 & ~(kChunk - 1u);
+    g.emask = a.ring * kChunk - 1u;
+    g.stream_end = E1 > E0 ? ((E1 - 1u) & ~(kChunk - 1u)) + kChunk : e0;
+    g.ready_end = e0;
+    g.rel_mark = e0 + kChunk;
+    const uint32_t limit = min(e0 + a.ring * kChunk, g.stream_end);
+    if constexpr (kFresh) {
+        g.ebase = e0;
         g.wslot = 0;
         g.wphase = 0;
-        const uint32_t limit = min(g.ebase + a.ring * kChunk, g.stream_end);
         if (lane == 0) {
             // The barriers are used by this warp and its own bulk copies only (no cluster): the
             // async-proxy fence orders their initialisation before the copies' complete_tx.
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
             // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so
             // one copy per array fills them all and completes on barrier 0; the other barriers
             // complete their first phase with a plain arrive (the consumer passes barrier 0 first).
-            const uint32_t n = (limit - g.ebase) / kChunk;
+            const uint32_t n = (limit - e0) / kChunk;
             if (n) {
                 asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
                              "r"(n * (kChunkVBytes + kChunkDBytes))
@@ -377,12 +380,12 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         g.vbase),
-                    "l"(a.values + g.ebase), "r"(n * kChunkVBytes), "r"(g.bar0)
+                    "l"(a.values + e0), "r"(n * kChunkVBytes), "r"(g.bar0)
                     : "memory");
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         g.dbase),
-                    "l"(a.deltas + g.ebase / 2), "r"(n * kChunkDBytes), "r"(g.bar0)
+                    "l"(a.deltas + e0 / 2), "r"(n * kChunkDBytes), "r"(g.bar0)
                     : "memory");
                 for (uint32_t i = 1; i < n; ++i)
                     asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
@@ -390,22 +393,28 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
             MK_TRACE(7);
         }
         g.iss = limit;
-        __syncwarp();
-        rs.r = q0.y;
-        rs.units_left = q0.x;
-        rs.s = q1.y;
-        rs.e = q1.z;
-        rs.e_next = rs.r + 2u <= a.rows ? __ldg(a.row_ptrs + rs.r + 2u) : 0u;
-        begin_piece(rs, q0.z, (int)q1.w, (int32_t)q2.x, q2.z);
+    } else {
+        // element e0 maps to the slot the consumer waits on next (all earlier chunks consumed)
+        g.ebase = e0 - g.wslot * kChunk;
+        for (g.iss = e0; g.iss < limit; g.iss += kChunk) ring_issue(g, a, lane);
     }
+    __syncwarp();
+    rs.r = q0.y;
+    rs.units_left = q0.x;
+    rs.s = q1.y;
+    rs.e = q1.z;
+    rs.e_next = rs.r + 2u <= a.rows ? __ldg(a.row_ptrs + rs.r + 2u) : 0u;
+    begin_piece(rs, q0.z, (int)q1.w, (int32_t)q2.x, q2.z);
+    return true;
+}
 
-    MK_TRACE(2);
-    // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    MK_TRACE(3);
-    // Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries).
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+// Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries); all
+// threads of the CTA, the caller synchronises.  kCoherent: read x from L2 (ld.cg) — x was
+// written earlier in the same launch (chain kernel).
+template <int kXMode, bool kCoherent>
+__device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
     if constexpr (x_table<kXMode>()) {
+        const uint32_t C = a.cols;
         const uint4* x4 = reinterpret_cast<const uint4*>(a.x);  // 16-byte aligned (capi guarantees)
         const uint32_t nv = C / 8;
         // every CTA reads all of x: start each CTA at a different place so the 148 concurrent
@@ -413,15 +422,19 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         const uint32_t rot = nv ? (blockIdx.x * 97u) % nv : 0u;
         for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
             const uint32_t k = i + rot < nv ? i + rot : i + rot - nv;
-            reinterpret_cast<uint4*>(xs)[k] = __ldg(x4 + k);
+            reinterpret_cast<uint4*>(xs)[k] = kCoherent ? __ldcg(x4 + k) : __ldg(x4 + k);
         }
-        for (uint32_t i = nv * 8 + threadIdx.x; i < C + kXGuardHi; i += blockDim.x) xs[i] = i < C ? a.x[i] : 0;
+        for (uint32_t i = nv * 8 + threadIdx.x; i < C + kXGuardHi; i += blockDim.x)
+            xs[i] = i < C ? (kCoherent ? __ldcg(a.x + i) : a.x[i]) : (uint16_t)0;
         if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
     }
-    __syncthreads();
-    MK_TRACE(4);
-    if (!has_work) return;
-    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+}
+
+// The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
+template <int kXMode>
+__device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr, Ring& g,
+                                         RowState& rs) {
+    const uint32_t C = a.cols;
     if (rs.T == 0) {
         if (lane == 0) a.y[rs.r] = 0;
         if (!next_piece(rs, a, w, lane)) return;
@@ -501,7 +514,116 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(con
         }
         if (!next_piece(rs, a, w, lane)) break;
     }
+}
+
+template <int kXMode>
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(const SpmvArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
+    const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    MK_TRACE(0);
+    // Programmatic dependent launch (chains of SpMVs): the next kernel in the stream may start
+    // its prologue (plan record, first matrix ring fills) on SMs this grid has left; everything
+    // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // The first ring fills go out first; x staging overlaps their HBM latency.
+    RowState rs;
+    Ring g;
+    const bool has_work = op_begin<true>(a, w, warp, lane, smem_base,
+                                         static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
+    MK_TRACE(2);
+    // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    MK_TRACE(3);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    stage_x<kXMode, false>(a, xs);
+    __syncthreads();
+    MK_TRACE(4);
+    if (!has_work) return;
+    run_rows<kXMode>(a, w, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g, rs);
     MK_TRACE(6);
+}
+
+// Grid-wide barrier for the persistent chain kernel (all CTAs co-resident: cooperative launch).
+// Sense-reversing and self-resetting, so it works across launches and CUDA-graph replays.  The
+// fences around it are the cooperative-groups pattern: the first releases this CTA's y writes
+// (ordered before it by bar.sync), the second acquires the other CTAs' writes and invalidates
+// this SM's L1 / texture lines, so the next op's x (staged with ld.cg, gathered through TEX)
+// is never stale.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t* gen = bar + 1;
+        const uint32_t g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1u) {
+            bar[0] = 0;
+            __threadfence();
+            *gen = g0 + 1u;
+        } else {
+            const long long t0 = clock64();
+            while (*gen == g0) {
+                __nanosleep(20);
+                if (clock64() - t0 > 8000000000LL) __trap();  // ~4 s: never hang the GPU
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Persistent chain of dependent SpMVs (decoder stacks): op k+1 reads op k's y.  Each warp sets up
+// op k+1 (plan record, first ring fills) as soon as its part of op k is done — BEFORE the grid
+// barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
+template <int kXMode>
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1)
+    macko_chain_b4(const SpmvArgs* __restrict__ ops, uint32_t n_ops, uint32_t* bar) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
+    __shared__ __align__(16) SpmvArgs args[2];  // op k and op k+1 (double buffer)
+    constexpr uint32_t kArgWords = sizeof(SpmvArgs) / 4;
+    static_assert(sizeof(SpmvArgs) % 4 == 0 && kArgWords <= 64, "SpmvArgs is copied word by word");
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
+    const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+    auto load_args = [&](uint32_t k) {  // whole CTA; caller synchronises
+        if (threadIdx.x < kArgWords)
+            reinterpret_cast<uint32_t*>(&args[k & 1])[threadIdx.x] = __ldg(reinterpret_cast<const uint32_t*>(ops + k) + threadIdx.x);
+    };
+    load_args(0);
+    if (n_ops > 1) load_args(1);
+    if (lane == 0) {
+        for (uint32_t i = 0; i < kMaxRing; ++i) mbar_init(bar0 + 8u * i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    RowState rs;
+    Ring g;
+    g.wslot = 0;
+    g.wphase = 0;
+    bool has_work = op_begin<false>(args[0], w, warp, lane, smem_base, bar0, g, rs);
+    for (uint32_t k = 0; k < n_ops; ++k) {
+        const SpmvArgs& a = args[k & 1];
+        MK_CTRACE(k, 0);
+        if (k) grid_barrier(bar);  // op k-1's y (this op's x) is complete everywhere
+        MK_CTRACE(k, 1);
+        stage_x<kXMode, true>(a, xs);
+        __syncthreads();
+        MK_CTRACE(k, 2);
+        if (has_work) run_rows<kXMode>(a, w, lane, xs_addr, g, rs);
+        MK_CTRACE(k, 3);
+        if (k + 1 < n_ops) has_work = op_begin<false>(args[(k + 1) & 1], w, warp, lane, smem_base, bar0, g, rs);
+        MK_CTRACE(k, 4);
+        __syncthreads();  // every warp is done with op k's x table and arguments
+        if (k + 2 < n_ops) load_args(k + 2);  // into op k's slot (visible after the next barrier)
+    }
 }
 
 // Column just before the first unit of every chunk that starts inside a row:
@@ -575,6 +697,36 @@ cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cu
         case 6: return launch_one<6>(a, grid, smem, s, pdl);
         case 1: return launch_one<1>(a, grid, smem, s, pdl);
         case 0: return launch_one<0>(a, grid, smem, s, pdl);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int kXMode>
+static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSpmvWarpsPerCta * kWarp);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode>, ops, n, bar);
+}
+
+cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
+                         cudaStream_t s) {
+    switch (x_mode) {
+        case 9: return chain_one<9>(d_ops, n_ops, d_bar, grid, smem, s);
+        case 8: return chain_one<8>(d_ops, n_ops, d_bar, grid, smem, s);
+        case 7: return chain_one<7>(d_ops, n_ops, d_bar, grid, smem, s);
+        case 6: return chain_one<6>(d_ops, n_ops, d_bar, grid, smem, s);
+        case 1: return chain_one<1>(d_ops, n_ops, d_bar, grid, smem, s);
+        case 0: return chain_one<0>(d_ops, n_ops, d_bar, grid, smem, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -64,6 +64,10 @@ cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
 cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
 cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
+// Persistent chain of dependent SpMVs (d_ops: device array of n_ops SpmvArgs; d_bar: 2 zeroed u32
+// for the grid barrier).  Cooperative launch of `grid` CTAs; all ops share x_mode, ring and smem.
+cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
+                         cudaStream_t s);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);
 
 }  // namespace mk

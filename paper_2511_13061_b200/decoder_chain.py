@@ -5,10 +5,10 @@ The paper's end-to-end use: every linear of a decoder laye
 matrix and one generated token is a chain of SpMVs.  Per layer (the stand-in for
 attention and the MLP activation — only the SpMV chain is timed):
 
-    qkv = W_qkv h          W_qkv = [W_q; W_k; W_v]   (3H x H, rows stacked: rows are independent,
-    o   = W_o v            v = qkv[2H:3H]              so the stacked encoding is the three
-    gu  = W_gu o           W_gu = [W_gate; W_up]       encodings concatenated)
-    h'  = W_down u         u = gu[I:2I]
+    qkv = W_qkv h          W_qkv = [W_v; W_q; W_k]   (3H x H, rows stacked: rows are independent,
+    o   = W_o v            v = qkv[0:H]                so the stacked encoding is the three
+    gu  = W_gu o           W_gu = [W_up; W_gate]       encodings concatenated; the
+    h'  = W_down u         u = gu[0:I]                 consumed slice first keeps it 512-B aligned)
 
 so a token is 4 dependent SpMVs per layer (128 for Llama2-7B: H = 4096, I = 11008, 8.1 GB of
 MACKO data at 50 % sparsity).  The chain is launched with programmatic dependent launch (each
@@ -55,10 +55,10 @@ def _x_slice(shape: ChainShape, name: str, acts: Dict[str, torch.Tensor]) -> tor
     if name == "qkv":
         return acts["h"]
     if name == "o":
-        return acts["qkv"][2 * H: 3 * H]
+        return acts["qkv"][:H]  # v
     if name == "gate_up":
         return acts["o"]
-    return acts["gate_up"][I: 2 * I]
+    return acts["gate_up"][:I]  # up
 
 
 def _out_name(name: str) -> str:
@@ -135,6 +135,22 @@ class SparseDecoderChain:
                 self._spmv(layer, name, stream, pdl)
         return self.acts["h"]
 
+    def persistent(self) -> "M.Chain":
+        """The token as ONE persistent cooperative kernel (macko_chain_*): op k+1's plan load and
+        first weight fills are issued before the grid barrier that waits for op k's output, so
+        the weight stream keeps HBM busy across the dependencies (N = 1 only)."""
+        if self.world != 1:
+            raise ValueError("the persistent chain runs on one GPU (sharded chains all-gather between SpMVs)")
+        if getattr(self, "_chain", None) is None:
+            ops = [(self.mats[layer][name], _x_slice(self.shape, name, self.acts), self.acts[_out_name(name)])
+                   for layer in range(self.shape.layers) for name in LINEARS]
+            self._chain = M.Chain(ops)
+        return self._chain
+
+    def forward_token_persistent(self, stream=None) -> torch.Tensor:
+        self.persistent().run(stream)
+        return self.acts["h"]
+
     def capture(self, pdl: bool = True) -> torch.cuda.CUDAGraph:
         """Capture forward_token into a CUDA graph (kernel nodes keep their PDL edges)."""
         s = torch.cuda.Stream(device=self.device)
@@ -150,6 +166,9 @@ class SparseDecoderChain:
         return g
 
     def close(self) -> None:
+        if getattr(self, "_chain", None) is not None:
+            self._chain.close()
+            self._chain = None
         for mats in self.mats:
             for m in mats.values():
                 m.close()

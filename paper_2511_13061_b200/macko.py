@@ -186,6 +186,36 @@ class DeviceMatrix:
             pass
 
 
+class Chain:
+    """A persistent chain of dependent SpMVs (macko_chain_*): ops = [(DeviceMatrix, x, y), ...]
+    with device tensors; x_k may alias (a slice of) an earlier y_j.  run() is one cooperative
+    launch, bit-identical to the ops run one by one."""
+
+    def __init__(self, ops):
+        n = len(ops)
+        self._keep = ops  # matrices and vectors must outlive the chain
+        mats = (C.c_void_p * n)(*[m._h.value for m, _, _ in ops])
+        xs = (C.c_void_p * n)(*[_ptr(x) for _, x, _ in ops])
+        ys = (C.c_void_p * n)(*[_ptr(y) for _, _, y in ops])
+        h = C.c_void_p()
+        check(_lib.load().macko_chain_create(mats, xs, ys, n, C.byref(h)))
+        self._h = h
+
+    def run(self, stream=None) -> None:
+        check(_lib.load().macko_chain_run(self._h, _stream_ptr(stream)))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().macko_chain_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def macko_from_dense(dense, b_delta: int = 4, stream=None) -> DeviceMatrix:
     """csr_from_dense + macko_from_csr (convert.hpp:8-16) on the GPU."""
     return DeviceMatrix.from_dense(dense, b_delta=b_delta, stream=stream)

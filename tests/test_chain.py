@@ -36,9 +36,9 @@ def test_chain_matches_oracle(cuda):
             R, C = shape.shape(name)
             ws[name] = O.encode_dense(O.gen_dense(R, C, 0.5, D.weight_seed(seed, layer, name)))
         qkv = O.b200_order_spmv(ws["qkv"], h, UNIT_STEPS)
-        o = O.b200_order_spmv(ws["o"], qkv[2 * H:3 * H], UNIT_STEPS)
+        o = O.b200_order_spmv(ws["o"], qkv[:H], UNIT_STEPS)  # v = first H rows of [W_v; W_q; W_k]
         gu = O.b200_order_spmv(ws["gate_up"], o, UNIT_STEPS)
-        h = O.b200_order_spmv(ws["down"], gu[I:2 * I], UNIT_STEPS)
+        h = O.b200_order_spmv(ws["down"], gu[:I], UNIT_STEPS)  # up = first I rows of [W_up; W_gate]
     assert np.isfinite(h.view(np.float16).astype(np.float32)).all()
     assert np.array_equal(to_host_u16(ch.acts["h"]), h)
     ch.close()
@@ -66,3 +66,37 @@ def test_chain_pdl_graph_bit_identical(cuda):
         for k, v in ch.acts.items():
             assert np.array_equal(to_host_u16(v), ref[k]), ("graph", k)
     ch.close()
+
+
+def test_persistent_chain_bit_identical(cuda):
+    # one cooperative kernel per token (grid barrier between dependent SpMVs) == op-by-op launches,
+    # over several tokens (the activations are rewritten inside the launch: x staging and the
+    # texture gathers must never see stale lines)
+    for shape in (D.ChainShape(layers=2, hidden=4096, inter=11008), D.ChainShape(layers=3, hidden=256, inter=688)):
+        ch = D.SparseDecoderChain(shape, density=0.5, seed=9)
+        _h0(ch, 4)
+        h0 = ch.acts["h"].clone()
+        refs = []
+        for _ in range(3):
+            ch.forward_token(pdl=False)
+            torch.cuda.synchronize()
+            refs.append({k: to_host_u16(v) for k, v in ch.acts.items()})
+        ch.acts["h"].copy_(h0)
+        for tok in range(3):
+            ch.forward_token_persistent()
+            torch.cuda.synchronize()
+            for k, v in ch.acts.items():
+                assert np.array_equal(to_host_u16(v), refs[tok][k]), (shape, tok, k)
+        # CUDA-graph capture of the persistent launch
+        s = torch.cuda.Stream()
+        ch.acts["h"].copy_(h0)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ch.forward_token_persistent(s)
+        ch.acts["h"].copy_(h0)
+        for tok in range(2):
+            g.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host_u16(ch.acts["h"]), refs[tok]["h"]), ("graph", shape, tok)
+        ch.close()

@@ -62,3 +62,8 @@ print(f"per-CTA last warp: min {np.nanmin(cta_max):.2f} med {np.nanmedian(cta_ma
 order = np.argsort(cta_max)
 print("slowest CTAs:", [(int(i), round(float(cta_max[i]), 1)) for i in order[-6:]])
 print("fastest CTAs:", [(int(i), round(float(cta_max[i]), 1)) for i in order[:6]])
+# done time vs warp index within the CTA (scheduler priority?) and vs SMSP (warp % 4)
+rel_done = done - np.nanmedian(done, axis=1, keepdims=True)
+print("done - CTA median by warp index (us):", " ".join(f"{v:+.1f}" for v in np.nanmean(rel_done, axis=0)))
+print("by SMSP (warp % 4):", [round(float(np.nanmean(rel_done[:, k::4])), 2) for k in range(4)])
+print("percentiles of done - CTA median:", [round(float(np.nanpercentile(rel_done, q)), 2) for q in (1, 10, 50, 90, 99)])
