@@ -92,8 +92,6 @@ uint64_t values_bytes(uint64_t pad_nnz) { return align_up(pad_nnz * 2, 16); }
 uint64_t delta_bytes(uint64_t pad_nnz, unsigned bits) { return align_up((pad_nnz * bits + 7) / 8, 16); }
 
 constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (element equivalents)
-constexpr size_t kMaxSmemX = 200 * 1024;     // fp16 x table in shared memory up to 100k columns
-constexpr size_t kMaxSmemPair = 100 * 1024;  // (x[c], x[c+1]) pair table while two CTAs still fit
 
 }  // namespace
 
@@ -164,9 +162,13 @@ void check_bits(uint32_t bits) {
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
     // Shared memory: x table (x_mode 1: fp16, 2: (x[c], x[c+1]) pairs) + per-warp TMA rings.
-    int optin = 0;
+    int optin = 0, per_sm = 0;
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
-    const size_t budget = (size_t)optin - kSpmvWarpsPerCta * kMaxRing * 8 - 1024;
+    ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
+    // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
+    // the mbarriers and the chain kernel's argument buffers)
+    const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
+    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 2 * sizeof(mk::SpmvArgs) - 64;
     const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunkDBytes);
     auto x_bytes = [&](int mode) -> size_t {
         return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
@@ -196,10 +198,11 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     m->smem = m->ring_offset + m->ring * per_slot;
     ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
-    m->ctas_per_sm = 1;  // one persistent 32-warp CTA per SM
+    if (m->ctas_per_sm < kSpmvCtasPerSm) fail(MACKO_ECUDA, "SpMV CTAs do not fit kSpmvCtasPerSm per SM");
+    m->ctas_per_sm = kSpmvCtasPerSm;  // persistent: 32 warps per SM
     m->grid = m->sms * m->ctas_per_sm;
-    // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the SMs (a different plan, same y)
-    if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->sms * m->force_ctas / 4));
+    // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the CTAs (a different plan, same y)
+    if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->grid * m->force_ctas / 4));
     const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
     m->n_chunks = W;
     const uint64_t R = m->rows;
@@ -971,7 +974,11 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
         c->smem = xtab + (size_t)ring * mk::kSpmvWarpsPerCta * (mk::kChunkVBytes + mk::kChunkDBytes);
         int optin = 0;
         ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attribute");
-        if (c->smem + 2048 > (size_t)optin) fail(MACKO_EINVAL, "chain x table + rings exceed shared memory");
+        int per_sm = 0;
+        ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem attribute");
+        if (c->smem > std::min<size_t>((size_t)optin, (size_t)per_sm / mk::kSpmvCtasPerSm - 1024) -
+                          mk::kSpmvWarpsPerCta * mk::kMaxRing * 8 - 2 * sizeof(mk::SpmvArgs) - 64)
+            fail(MACKO_EINVAL, "chain x table + rings exceed shared memory");
         int align = 0;
         ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev), "texture alignment");
         std::vector<mk::SpmvArgs> ops(n_ops);

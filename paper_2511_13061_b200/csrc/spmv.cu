@@ -517,7 +517,7 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
 }
 
 template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1) macko_spmv_b4(const SpmvArgs a) {
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv_b4(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
     const int lane = threadIdx.x & (kWarp - 1);
@@ -579,7 +579,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar) {
 // op k+1 (plan record, first ring fills) as soon as its part of op k is done — BEFORE the grid
 // barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
 template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, 1)
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     macko_chain_b4(const SpmvArgs* __restrict__ ops, uint32_t n_ops, uint32_t* bar) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];

@@ -43,7 +43,14 @@ struct SpmvArgs {
     SpmvPlanDev plan;
 };
 
-constexpr int kSpmvWarpsPerCta = 32;          // one persistent 1024-thread CTA per SM
+#ifndef MACKO_WARPS_PER_CTA
+#define MACKO_WARPS_PER_CTA 32
+#endif
+// kSpmvCtasPerSm persistent CTAs of kSpmvWarpsPerCta warps per SM (32 warps per SM either way).
+// Measured: two 16-warp CTAs per SM (so the next SpMV of a PDL chain can start on half an SM) are
+// 8 % slower on 36864x12288 and no faster on the decode chain; one 32-warp CTA is the default.
+constexpr int kSpmvWarpsPerCta = MACKO_WARPS_PER_CTA;
+constexpr int kSpmvCtasPerSm = 32 / kSpmvWarpsPerCta;
 constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two step pairs)
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
 constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
