@@ -520,10 +520,13 @@ def cpu_baseline(dm, C, d):
 
 
 def run_sweep(M, torch, dev, stream, l2_flush, peak):
-    """30/50/70/90 % sparsity at 36864x12288 and the Llama2-7B linear shapes at 50 %."""
+    """30/50/70/90 % sparsity at 36864x12288, the Llama2-7B linear shapes at 50 % and the
+    131072x32768 shapes of config 5 (whole matrix and an N = 8 row slab) at 50 / 90 %."""
     out = []
     cfgs = [(36864, 12288, 0.7), (36864, 12288, 0.5), (36864, 12288, 0.3), (36864, 12288, 0.1),
-            (4096, 4096, 0.5), (11008, 4096, 0.5), (4096, 11008, 0.5)]
+            (4096, 4096, 0.5), (11008, 4096, 0.5), (4096, 11008, 0.5),
+            # config 5: 131072x32768 (whole matrix on one GPU, and the row slab of one rank at N = 8)
+            (131072, 32768, 0.5), (131072, 32768, 0.1), (16384, 32768, 0.5), (16384, 32768, 0.1)]
     for R, C, d in cfgs:
         dense = torch.empty((R, C), dtype=torch.float16, device=dev)
         M.gen_dense(dense, R, C, d, seed=SEED_A)

@@ -188,8 +188,13 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
         // density.  Measured best split (profiles/r01_v12_modes.md): 4 of 8 slots by TEX at
         // d >= 0.4, 3 at 0.25 <= d < 0.4, 2 below.
+        // At low density the texture gathers need x resident in L1: the unified 256 KB L1/shared
+        // memory keeps what the x table and the rings leave (C = 32768: ~28 KB < 64 KB of x), so
+        // there the shared table alone is faster (131072x32768 @90 %: 51 vs 78 us per 16k-row slab).
         const double d = (double)m->pad_nnz / ((double)m->rows * (double)m->cols);
-        const int split = d >= 0.4 ? 7 : d >= 0.25 ? 6 : 8;
+        const size_t smem_all = x_bytes(6) + (size_t)ring_for(6) * per_slot;
+        const bool x_in_l1 = (size_t)per_sm + 24 * 1024 >= smem_all + 2 * m->cols + 16 * 1024;
+        const int split = d >= 0.4 ? 7 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
         m->x_mode = ring_for(split) >= 2 ? split : 0;
     }
     m->ring = ring_for(m->x_mode);
@@ -724,7 +729,7 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         if (m->b_delta != 4)
             fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only; got " + std::to_string(m->b_delta));
         DeviceGuard g(m->device);
-        mk::SpmvArgs a;
+        mk::SpmvArgs a{};
         a.values = m->values.p;
         a.deltas = m->deltas.p;
         a.row_ptrs = m->row_ptrs.p;
@@ -738,6 +743,7 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
+        a.pdl = (flags & MACKO_SPMV_PDL) != 0;
         ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0),
            "macko_spmv launch");
         g_launches.fetch_add(1);

@@ -342,11 +342,19 @@ __device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s,
 // barriers are initialised here and the first fill is one copy per array (single-SpMV kernel);
 // otherwise (chain) the ring continues where the previous op left it — the first chunk goes to
 // the slot after the last one consumed, each chunk on its own barrier phase.
-template <bool kFresh>
-__device__ __forceinline__ bool op_begin(const SpmvArgs& a, uint32_t w, uint32_t warp, int lane, uint32_t smem_base,
-                                         uint32_t bar0, Ring& g, RowState& rs) {
+struct PlanRecord {
+    uint4 q0, q1, q2;  // the warp's WarpPlan (48 bytes)
+};
+
+__device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w) {
     const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + w);
-    const uint4 q0 = __ldg(rec), q1 = __ldg(rec + 1), q2 = __ldg(rec + 2);
+    return PlanRecord{__ldg(rec), __ldg(rec + 1), __ldg(rec + 2)};
+}
+
+template <bool kFresh>
+__device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
+                                         uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
+    const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
     MK_TRACE(1);
     if (q0.x == 0) return false;
     const uint32_t E0 = q0.w, E1 = q1.x;
@@ -529,17 +537,20 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     // its prologue (plan record, first matrix ring fills) on SMs this grid has left; everything
     // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // The first ring fills go out first; x staging overlaps their HBM latency.
+    const PlanRecord pr = load_record(a, w);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    // Without a PDL producer x is final at entry: its loads overlap the plan record's latency.
+    if (!a.pdl) stage_x<kXMode, false>(a, xs);
+    // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
     RowState rs;
     Ring g;
-    const bool has_work = op_begin<true>(a, w, warp, lane, smem_base,
+    const bool has_work = op_begin<true>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
     MK_TRACE(2);
     // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     MK_TRACE(3);
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
-    stage_x<kXMode, false>(a, xs);
+    if (a.pdl) stage_x<kXMode, false>(a, xs);
     __syncthreads();
     MK_TRACE(4);
     if (!has_work) return;
@@ -608,7 +619,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     Ring g;
     g.wslot = 0;
     g.wphase = 0;
-    bool has_work = op_begin<false>(args[0], w, warp, lane, smem_base, bar0, g, rs);
+    bool has_work = op_begin<false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
     for (uint32_t k = 0; k < n_ops; ++k) {
         const SpmvArgs& a = args[k & 1];
         MK_CTRACE(k, 0);
@@ -619,7 +630,10 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
         MK_CTRACE(k, 2);
         if (has_work) run_rows<kXMode>(a, w, lane, xs_addr, g, rs);
         MK_CTRACE(k, 3);
-        if (k + 1 < n_ops) has_work = op_begin<false>(args[(k + 1) & 1], w, warp, lane, smem_base, bar0, g, rs);
+        if (k + 1 < n_ops) {
+            const SpmvArgs& an = args[(k + 1) & 1];
+            has_work = op_begin<false>(an, load_record(an, w), warp, lane, smem_base, bar0, g, rs);
+        }
         MK_CTRACE(k, 4);
         __syncthreads();  // every warp is done with op k's x table and arguments
         if (k + 2 < n_ops) load_args(k + 2);  // into op k's slot (visible after the next barrier)

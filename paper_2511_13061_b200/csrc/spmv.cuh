@@ -40,6 +40,7 @@ struct SpmvArgs {
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
+    uint32_t pdl;          // launched as a PDL dependent: x may still be written by the producer
     SpmvPlanDev plan;
 };
 
