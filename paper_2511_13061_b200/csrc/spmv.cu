@@ -90,7 +90,14 @@ __device__ __forceinline__ uint16_t xtex(cudaTextureObject_t t, int col) {
 template <int kXMode>
 constexpr uint32_t tex_slots() {
     return kXMode == 0 ? 0xFFu : kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 9 ? 0x92u
-         : kXMode == 10 ? 0xABu : kXMode == 11 ? 0xBBu : 0u;
+         : kXMode == 10 ? 0xAAu : kXMode == 11 ? 0xABu : 0u;
+}
+
+// Second step of a pair: x_mode 10 alternates 4 and 3 texture slots between the two steps
+// (3.5 of 8 on average), x_mode 11 alternates 5 and 4.
+template <int kXMode>
+constexpr uint32_t tex_slots_b() {
+    return kXMode == 10 ? 0x2Au : kXMode == 11 ? 0xAAu : tex_slots<kXMode>();
 }
 
 template <int kXMode>
@@ -113,7 +120,7 @@ __device__ __forceinline__ Dec decode(uint32_t d) {
 // 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.  Masked
 // steps (row edges): element m gathers only if bit m of vm is set, else it multiplies x = +0
 // (its value is already +0), so nothing outside the row reaches the sum, not even 0 * inf.
-template <int kXMode, bool kMasked>
+template <int kXMode, bool kMasked, uint32_t kTex = tex_slots<kXMode>()>
 __device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
                                            cudaTextureObject_t xt, uint32_t vm) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -128,9 +135,9 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec&
         const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
         uint16_t x0 = 0, x1 = 0;
         if (!kMasked || ((vm >> (2 * m)) & 1u))
-            x0 = ((tex_slots<kXMode>() >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
+            x0 = ((kTex >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
         if (!kMasked || ((vm >> (2 * m + 1)) & 1u))
-            x1 = ((tex_slots<kXMode>() >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
+            x1 = ((kTex >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
         acc = fma_f16f16f32(v0, x0, acc);
         acc = fma_f16f16f32(v1, x1, acc);
     }
@@ -483,17 +490,17 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
             // (or out-of-range texels) with value +0.
             if (t + 1u == rs.T) {
                 rs.acc = lane_step<kXMode, true>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, (int)C, xs_addr, a.xtex, vmB);
+                rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, (int)C, xs_addr, a.xtex, vmB);
             } else if (t + 2u == rs.T) {
                 rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, true>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+                rs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
             } else {
                 rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+                rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
             }
         } else {
             rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-            rs.acc = lane_step<kXMode, false>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
         }
         rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
     };
