@@ -169,7 +169,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     // the mbarriers and the chain kernel's argument buffers)
     const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
     const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 2 * sizeof(mk::SpmvArgs) - 64;
-    const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunkDBytes);
+    const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunk * m->b_delta / 8);
     auto x_bytes = [&](int mode) -> size_t {
         return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
     };
@@ -201,7 +201,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
     m->ring_offset = x_bytes(m->x_mode);
     m->smem = m->ring_offset + m->ring * per_slot;
-    ck(spmv_occupancy(m->x_mode, m->smem, &m->ctas_per_sm), "spmv occupancy");
+    ck(spmv_occupancy(m->x_mode, (int)m->b_delta, m->smem, &m->ctas_per_sm), "spmv occupancy");
     if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
     if (m->ctas_per_sm < kSpmvCtasPerSm) fail(MACKO_ECUDA, "SpMV CTAs do not fit kSpmvCtasPerSm per SM");
     m->ctas_per_sm = kSpmvCtasPerSm;  // persistent: 32 warps per SM
@@ -320,7 +320,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
     P.counters = m->plan_u32.p + 4 * (size_t)S;
     P.partials = m->partials.p;
-    ck(launch_plan_colbase(m->deltas.p, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st), "plan colbase");
+    ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
+       "plan colbase");
     g_launches.fetch_add(1);
     ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
 }
@@ -580,7 +581,7 @@ void check_shape(uint64_t rows, uint64_t cols) {
 extern "C" {
 
 const char* macko_last_error(void) { return g_err.c_str(); }
-const char* macko_version(void) { return "macko-b200 0.1 (sm_100a, b_delta=4 SpMV, compressor b_delta in {1,2,4,8})"; }
+const char* macko_version(void) { return "macko-b200 0.2 (sm_100a; SpMV and compressor for b_delta in {1,2,4,8})"; }
 uint64_t macko_kernel_launches(void) { return g_launches.load(); }
 
 uint32_t macko_density_threshold(double d) {
@@ -617,7 +618,7 @@ macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
         // one zeroed TMA chunk of slack past the payload: the SpMV's ring copies are never clamped
         m->values.alloc(vb / 2 + mk::kChunk);
-        m->deltas.alloc(db + mk::kChunkDBytes);
+        m->deltas.alloc(db + mk::kChunk);  // one chunk of codewords at up to 8 bits
         m->row_ptrs.alloc(rows + 1);
         ck(cudaMemsetAsync(m->values.p, 0, m->values.n * 2, st), "memset");
         ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
@@ -630,7 +631,7 @@ macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t
         ck(cudaMemcpyAsync(m->row_ptrs.p, row_ptrs, (rows + 1) * 4, cudaMemcpyHostToDevice, st), "upload row_ptrs");
         m->h_row_ptrs.assign(row_ptrs, row_ptrs + rows + 1);
         device_validate(m, st);
-        if (b_delta == 4) build_plan(m, st);
+        build_plan(m, st);
         *out = hold.release();
     });
 }
@@ -670,7 +671,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         m->pad_nnz = pad_nnz;
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
         m->values.alloc(vb / 2 + mk::kChunk);  // + one zeroed TMA chunk of slack (see upload)
-        m->deltas.alloc(db + mk::kChunkDBytes);
+        m->deltas.alloc(db + mk::kChunk);  // one chunk of codewords at up to 8 bits
         ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
         if (m->values.n * 2 > pad_nnz * 2)
             ck(cudaMemsetAsync(m->values.p + pad_nnz, 0, m->values.n * 2 - pad_nnz * 2, st), "memset");
@@ -682,7 +683,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         m->h_row_ptrs.resize(rows + 1);
         ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
         ck(cudaStreamSynchronize(st), "sync");
-        if (b_delta == 4) build_plan(m, st);
+        build_plan(m, st);
         *out = hold.release();
     });
 }
@@ -726,8 +727,8 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
     return guarded([&] {
         if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
         if (flags & ~(uint32_t)MACKO_SPMV_PDL) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
-        if (m->b_delta != 4)
-            fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only; got " + std::to_string(m->b_delta));
+        if (!mk::spmv_valid_config(m->x_mode, (int)m->b_delta))
+            fail(MACKO_EINVAL, "no SpMV kernel for b_delta " + std::to_string(m->b_delta) + " with this x_mode");
         DeviceGuard g(m->device);
         mk::SpmvArgs a{};
         a.values = m->values.p;
@@ -744,7 +745,7 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
-        ck(mk::launch_spmv(a, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0),
+        ck(mk::launch_spmv(a, (int)m->b_delta, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0),
            "macko_spmv launch");
         g_launches.fetch_add(1);
     });
@@ -922,17 +923,17 @@ macko_status macko_mcko_read_dev(int device, const char* path, void* stream, mac
         m->b_delta = h.b_delta;
         const uint64_t vb = values_bytes(h.pad_nnz), db = delta_bytes(h.pad_nnz, h.b_delta);
         m->values.alloc(vb / 2 + mk::kChunk);
-        m->deltas.alloc(db + mk::kChunkDBytes);
+        m->deltas.alloc(db + mk::kChunk);  // one chunk of codewords at up to 8 bits
         m->row_ptrs.alloc(h.rows + 1);
         ck(cudaMemsetAsync(m->values.p + vb / 2, 0, mk::kChunk * 2, st), "memset");
-        ck(cudaMemsetAsync(m->deltas.p + db, 0, mk::kChunkDBytes, st), "memset");
+        ck(cudaMemsetAsync(m->deltas.p + db, 0, mk::kChunk, st), "memset");
         ck(cudaMemcpyAsync(m->row_ptrs.p, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, st), "upload row_ptrs");
         stream_to_device(f, m->deltas.p, db, st, "packed_deltas");
         stream_to_device(f, m->values.p, vb, st, "values");
         ck(cudaStreamSynchronize(st), "sync");
         m->h_row_ptrs = std::move(rp);
         device_validate(m, st);
-        if (m->b_delta == 4) build_plan(m, st);
+        build_plan(m, st);
         *out = hold.release();
     });
 }
@@ -1059,9 +1060,9 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream) {
     return guarded([&] {
         if (!m) fail(MACKO_EINVAL, "null handle");
-        if (x_mode != -1 && !mk::spmv_valid_x_mode(x_mode)) fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 6..11");
+        if (x_mode != -1 && !mk::spmv_valid_config(x_mode, (int)m->b_delta))
+            fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 6..11 (6..8, 10 for b_delta != 4)");
         if (x_mode > 0 && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
-        if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
         DeviceGuard g(m->device);
         m->force_x_mode = x_mode;
         m->force_ctas = ctas_per_sm;

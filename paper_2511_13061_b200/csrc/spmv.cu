@@ -105,34 +105,84 @@ constexpr bool x_table() {
     return kXMode != 0;
 }
 
+template <int kBits>
+constexpr uint32_t dbytes() {  // delta bytes of one kChunk-element chunk
+    return kChunk * kBits / 8;
+}
+
 struct Dec {
     uint32_t even, odd, local;  // in-lane inclusive column offsets of elements 0,2,4,6 / 1,3,5,7; lane total
 };
 
-// Nibbles -> byte deltas (codeword + 1) -> in-lane inclusive prefixes (byte m of even/odd).
+// b_delta <= 4: codewords -> byte deltas (codeword + 1) -> in-lane inclusive prefixes (byte m of
+// even/odd; at most 8 x 16 = 128, so bytes never carry).  Nibbles (b = 4) are split directly;
+// crumbs (b = 2) are first spread to one nibble per byte, bits (b = 1) to one per byte.
+template <int kBits>
 __device__ __forceinline__ Dec decode(uint32_t d) {
-    const uint32_t dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
-    const uint32_t dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
+    uint32_t dl, dh;
+    if constexpr (kBits == 4) {
+        dl = (d & 0x0F0F0F0Fu) + 0x01010101u;         // elements 0,2,4,6
+        dh = ((d >> 4) & 0x0F0F0F0Fu) + 0x01010101u;  // elements 1,3,5,7
+    } else if constexpr (kBits == 2) {
+        uint32_t nib;  // byte m = crumbs of elements 2m (bits 0-1) and 2m+1 (bits 2-3)
+        asm("prmt.b32 %0, %1, %2, 0x5140;" : "=r"(nib) : "r"(d & 0x0F0Fu), "r"((d >> 4) & 0x0F0Fu));
+        dl = (nib & 0x03030303u) + 0x01010101u;
+        dh = ((nib >> 2) & 0x03030303u) + 0x01010101u;
+    } else {  // kBits == 1: bit k = element k
+        dl = (((d & 0x55u) * 0x41041u) & 0x01010101u) + 0x01010101u;
+        dh = ((((d >> 1) & 0x55u) * 0x41041u) & 0x01010101u) + 0x01010101u;
+    }
     const uint32_t pp = (dl + dh) * 0x01010101u;
     return Dec{pp - dh, pp, pp >> 24};
+}
+
+// b_delta = 8: byte codewords, deltas up to 256, so prefixes (up to 2048) live in 16-bit halves:
+// p[j] = (offset of element 2j, offset of element 2j+1).
+struct Dec8 {
+    uint32_t p[4];
+    uint32_t local;
+};
+
+__device__ __forceinline__ Dec8 decode8(uint32_t w0, uint32_t w1) {
+    Dec8 r;
+    uint32_t h[4];
+    asm("prmt.b32 %0, %1, 0, 0x4140;" : "=r"(h[0]) : "r"(w0));
+    asm("prmt.b32 %0, %1, 0, 0x4342;" : "=r"(h[1]) : "r"(w0));
+    asm("prmt.b32 %0, %1, 0, 0x4140;" : "=r"(h[2]) : "r"(w1));
+    asm("prmt.b32 %0, %1, 0, 0x4342;" : "=r"(h[3]) : "r"(w1));
+    uint32_t carry = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t q = h[j] + 0x00010001u;         // (delta 2j, delta 2j+1)
+        r.p[j] = q + (q << 16) + carry * 0x00010001u;  // inclusive prefixes
+        carry = r.p[j] >> 16;
+    }
+    r.local = carry;
+    return r;
 }
 
 // 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.  Masked
 // steps (row edges): element m gathers only if bit m of vm is set, else it multiplies x = +0
 // (its value is already +0), so nothing outside the row reaches the sum, not even 0 * inf.
-template <int kXMode, bool kMasked, uint32_t kTex = tex_slots<kXMode>()>
-__device__ __forceinline__ float lane_step(float acc, const uint4& v, const Dec& dc, int cb, uint32_t xs_addr,
+template <int kXMode, bool kMasked, uint32_t kTex = tex_slots<kXMode>(), class D>
+__device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& dc, int cb, uint32_t xs_addr,
                                            cudaTextureObject_t xt, uint32_t vm) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    // shared address of column cb: per element one PRMT (byte extract) + one IADD3
+    // shared address of column cb: per element one PRMT (offset extract) + one IADD3
     uint32_t base = xs_addr + 2u * (uint32_t)cb;
     asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + 2b a single IADD3 per element
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         uint16_t v0, v1;
         split_halves(w[m], v0, v1);
-        const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
-        const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
+        uint32_t b0, b1;
+        if constexpr (std::is_same<D, Dec8>::value) {
+            b0 = __byte_perm(dc.p[m], 0u, 0x4410u);
+            b1 = __byte_perm(dc.p[m], 0u, 0x4432u);
+        } else {
+            b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
+            b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
+        }
         uint16_t x0 = 0, x1 = 0;
         if (!kMasked || ((vm >> (2 * m)) & 1u))
             x0 = ((kTex >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
@@ -267,6 +317,7 @@ struct Ring {
 };
 
 // Copy the chunk starting at element g.iss into its slot (lane 0; full-size, never clamped).
+template <int kBits>
 __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int lane) {
     if (lane == 0) {
         const uint32_t e0 = g.iss;
@@ -274,26 +325,27 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int
         const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
         // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
         asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "n"(kChunkVBytes + kChunkDBytes)
+                     "n"(kChunkVBytes + dbytes<kBits>())
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          g.vbase + 2u * rel),
                      "l"(a.values + e0), "n"(kChunkVBytes), "r"(bar)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         g.dbase + rel / 2u),
-                     "l"(a.deltas + e0 / 2), "n"(kChunkDBytes), "r"(bar)
+                         g.dbase + rel * kBits / 8u),
+                     "l"(a.deltas + e0 * kBits / 8u), "n"(dbytes<kBits>()), "r"(bar)
                      : "memory");
     }
 }
 
 // The walk is at S: every chunk wholly below S was consumed by all lanes (their LDS results fed
 // earlier FHFMAs; __syncwarp orders them before lane 0's copy), so its slot takes a new chunk.
+template <int kBits>
 __device__ __forceinline__ void ring_refill(Ring& g, const SpmvArgs& a, uint32_t S, int lane) {
     __syncwarp();
     do {
         if (g.iss < g.stream_end) {
-            ring_issue(g, a, lane);
+            ring_issue<kBits>(g, a, lane);
             g.iss += kChunk;
         }
         g.rel_mark += kChunk;
@@ -313,33 +365,66 @@ __device__ __forceinline__ void ring_wait(Ring& g, uint32_t Send, uint32_t nslot
 
 struct Slot {
     uint4 v;
-    uint32_t d;
+    uint32_t d, d2;  // the lane's 8 codewords (d2: elements 4..7 when b_delta = 8)
 };
 
+template <int kBits>
 __device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
     Slot sl;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
                  : "r"(g.vbase + 2u * rel));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(g.dbase + rel / 2u));
+    const uint32_t da = g.dbase + rel * kBits / 8u;
+    sl.d2 = 0;
+    if constexpr (kBits == 8) {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(sl.d), "=r"(sl.d2) : "r"(da));
+    } else if constexpr (kBits == 4) {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sl.d) : "r"(da));
+    } else if constexpr (kBits == 2) {
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(sl.d) : "r"(da));
+    } else {
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sl.d) : "r"(da));
+    }
     return sl;
 }
 
 // Keep only the lane's elements inside [s, e) (eb = the lane's first element): the others get
 // codeword 0 (delta 1) and value +0, and their columns fall on zero guards / out-of-range texels,
 // so they add exactly +0 (also when the masked values or x hold inf / NaN).
+template <int kBits>
 __device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s, uint32_t e) {
     const int klo = min(max((int)(s - eb), 0), 8);
     const int khi = min(max((int)(e - eb), klo), 8);
-    const uint32_t nm = (uint32_t)(((1ull << (4 * khi)) - 1ull) & ~((1ull << (4 * klo)) - 1ull));
-    sl.d &= nm;
-    // value masks: 16-bit halves replicate the msb of their element's nibble (PRMT sign mode)
-    const uint32_t lo = nm << 4;
-    sl.v.x &= prmt(lo, nm, 0xCC88u);
-    sl.v.y &= prmt(lo, nm, 0xDD99u);
-    sl.v.z &= prmt(lo, nm, 0xEEAAu);
-    sl.v.w &= prmt(lo, nm, 0xFFBBu);
-    return (0xFFu >> (8 - khi)) & (0xFFu << klo) & 0xFFu;  // valid-element mask
+    const uint32_t vm = (0xFFu >> (8 - khi)) & (0xFFu << klo) & 0xFFu;  // valid-element mask
+    if constexpr (kBits == 4) {
+        const uint32_t nm = (uint32_t)(((1ull << (4 * khi)) - 1ull) & ~((1ull << (4 * klo)) - 1ull));
+        sl.d &= nm;
+        // value masks: 16-bit halves replicate the msb of their element's nibble (PRMT sign mode)
+        const uint32_t lo = nm << 4;
+        sl.v.x &= prmt(lo, nm, 0xCC88u);
+        sl.v.y &= prmt(lo, nm, 0xDD99u);
+        sl.v.z &= prmt(lo, nm, 0xEEAAu);
+        sl.v.w &= prmt(lo, nm, 0xFFBBu);
+    } else {
+        if constexpr (kBits == 8) {
+            sl.d &= ((vm & 0x0Fu) * 0x204081u & 0x01010101u) * 0xFFu;
+            sl.d2 &= ((vm >> 4) * 0x204081u & 0x01010101u) * 0xFFu;
+        } else if constexpr (kBits == 2) {
+            uint32_t c = vm;  // bit k -> crumb k
+            c = (c | (c << 4)) & 0x0F0Fu;
+            c = (c | (c << 2)) & 0x3333u;
+            c = (c | (c << 1)) & 0x5555u;
+            sl.d &= c * 3u;
+        } else {
+            sl.d &= vm;
+        }
+        auto hm = [&](int k) { return ((vm >> k) & 1u) ? 0xFFFFu : 0u; };
+        sl.v.x &= hm(0) | (hm(1) << 16);
+        sl.v.y &= hm(2) | (hm(3) << 16);
+        sl.v.z &= hm(4) | (hm(5) << 16);
+        sl.v.w &= hm(6) | (hm(7) << 16);
+    }
+    return vm;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -358,7 +443,7 @@ __device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w)
     return PlanRecord{__ldg(rec), __ldg(rec + 1), __ldg(rec + 2)};
 }
 
-template <bool kFresh>
+template <int kBits, bool kFresh>
 __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
                                          uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
     const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
@@ -366,7 +451,7 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
     if (q0.x == 0) return false;
     const uint32_t E0 = q0.w, E1 = q1.x;
     g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
-    g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * kChunkDBytes;
+    g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * dbytes<kBits>();
     g.bar0 = bar0;
     const uint32_t e0 = E0 & ~(kChunk - 1u);
     g.emask = a.ring * kChunk - 1u;
@@ -390,7 +475,7 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
             const uint32_t n = (limit - e0) / kChunk;
             if (n) {
                 asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
-                             "r"(n * (kChunkVBytes + kChunkDBytes))
+                             "r"(n * (kChunkVBytes + dbytes<kBits>()))
                              : "memory");
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -400,7 +485,7 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         g.dbase),
-                    "l"(a.deltas + e0 / 2), "r"(n * kChunkDBytes), "r"(g.bar0)
+                    "l"(a.deltas + e0 * kBits / 8u), "r"(n * dbytes<kBits>()), "r"(g.bar0)
                     : "memory");
                 for (uint32_t i = 1; i < n; ++i)
                     asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
@@ -411,7 +496,7 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
     } else {
         // element e0 maps to the slot the consumer waits on next (all earlier chunks consumed)
         g.ebase = e0 - g.wslot * kChunk;
-        for (g.iss = e0; g.iss < limit; g.iss += kChunk) ring_issue(g, a, lane);
+        for (g.iss = e0; g.iss < limit; g.iss += kChunk) ring_issue<kBits>(g, a, lane);
     }
     __syncwarp();
     rs.r = q0.y;
@@ -446,7 +531,7 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
-template <int kXMode>
+template <int kXMode, int kBits>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr, Ring& g,
                                          RowState& rs) {
     const uint32_t C = a.cols;
@@ -464,25 +549,36 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         const uint32_t S = rs.al + t * kStepElts;
         if (S >= ev) {
             const uint32_t Send = S + ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts;
-            if (S >= g.rel_mark) ring_refill(g, a, S, lane);
+            if (S >= g.rel_mark) ring_refill<kBits>(g, a, S, lane);
             if (Send > g.ready_end) ring_wait(g, Send, a.ring);
             ev = min(g.rel_mark, g.ready_end > 2u * kStepElts - 1u ? g.ready_end - (2u * kStepElts - 1u) : 0u);
         }
         const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
-        Slot A = lds_slot(g, relA);
-        Slot B = lds_slot(g, (relA + kStepElts) & g.emask);
+        Slot A = lds_slot<kBits>(g, relA);
+        Slot B = lds_slot<kBits>(g, (relA + kStepElts) & g.emask);
         uint32_t vmA = 0xFFu, vmB = 0xFFu;
         if constexpr (kMasked) {
             const uint32_t eb = S + 8u * lane;
-            vmA = mask_slot(A, eb, rs.s, rs.e);
-            vmB = mask_slot(B, eb + kStepElts, rs.s, rs.e);
+            vmA = mask_slot<kBits>(A, eb, rs.s, rs.e);
+            vmB = mask_slot<kBits>(B, eb + kStepElts, rs.s, rs.e);
         }
-        const Dec dA = decode(A.d), dB = decode(B.d);
-        const uint32_t pk = dA.local | (dB.local << 16);
+        using D = typename std::conditional<kBits == 8, Dec8, Dec>::type;
+        D dA, dB;
+        uint32_t bias = 0;  // b = 8: lane totals reach 2048, so the packed scan runs on (total - 8)
+        if constexpr (kBits == 8) {
+            dA = decode8(A.d, A.d2);
+            dB = decode8(B.d, B.d2);
+            bias = 8;
+        } else {
+            dA = decode<kBits>(A.d);
+            dB = decode<kBits>(B.d);
+        }
+        const uint32_t pk = (dA.local - bias) | ((dB.local - bias) << 16);
         const uint32_t incl = warp_incl_scan_p(pk);
         const uint32_t tot = __reduce_add_sync(kFull, pk);
-        const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - dA.local);
-        const int cbB = rs.col_base + (int)(tot & 0xFFFFu) + (int)((incl >> 16) - dB.local);
+        const uint32_t lane_bias = bias * (uint32_t)lane, tot_bias = bias * kWarp;
+        const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - (dA.local - bias) + lane_bias);
+        const int cbB = rs.col_base + (int)((tot & 0xFFFFu) + tot_bias) + (int)((incl >> 16) - (dB.local - bias) + lane_bias);
         if constexpr (kMasked) {
             // Only the step holding the row end (step T-1) predicates its gathers: its masked
             // elements decode to columns right after the row's last one.  Leading ROMA elements
@@ -502,7 +598,7 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
             rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
             rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
         }
-        rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16);
+        rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16) + 2 * (int)tot_bias;
     };
 
     for (;;) {
@@ -531,8 +627,8 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     }
 }
 
-template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv_b4(const SpmvArgs a) {
+template <int kXMode, int kBits>
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
     const int lane = threadIdx.x & (kWarp - 1);
@@ -551,7 +647,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
     RowState rs;
     Ring g;
-    const bool has_work = op_begin<true>(a, pr, warp, lane, smem_base,
+    const bool has_work = op_begin<kBits, true>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
     MK_TRACE(2);
     // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
@@ -561,7 +657,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     __syncthreads();
     MK_TRACE(4);
     if (!has_work) return;
-    run_rows<kXMode>(a, w, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g, rs);
+    run_rows<kXMode, kBits>(a, w, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g, rs);
     MK_TRACE(6);
 }
 
@@ -626,7 +722,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     Ring g;
     g.wslot = 0;
     g.wphase = 0;
-    bool has_work = op_begin<false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
+    bool has_work = op_begin<4, false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
     for (uint32_t k = 0; k < n_ops; ++k) {
         const SpmvArgs& a = args[k & 1];
         MK_CTRACE(k, 0);
@@ -635,11 +731,11 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
         stage_x<kXMode, true>(a, xs);
         __syncthreads();
         MK_CTRACE(k, 2);
-        if (has_work) run_rows<kXMode>(a, w, lane, xs_addr, g, rs);
+        if (has_work) run_rows<kXMode, 4>(a, w, lane, xs_addr, g, rs);
         MK_CTRACE(k, 3);
         if (k + 1 < n_ops) {
             const SpmvArgs& an = args[(k + 1) & 1];
-            has_work = op_begin<false>(an, load_record(an, w), warp, lane, smem_base, bar0, g, rs);
+            has_work = op_begin<4, false>(an, load_record(an, w), warp, lane, smem_base, bar0, g, rs);
         }
         MK_CTRACE(k, 4);
         __syncthreads();  // every warp is done with op k's x table and arguments
@@ -649,7 +745,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
 
 // Column just before the first unit of every chunk that starts inside a row:
 // sum of the row's deltas over [row start, unit start) minus one.  Setup only.
-__global__ void plan_colbase_kernel(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks) {
+__global__ void plan_colbase_kernel(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
     if (w >= n_chunks) return;
@@ -660,8 +756,9 @@ __global__ void plan_colbase_kernel(const uint8_t* deltas, WarpPlan* warps, uint
     }
     const uint32_t s = warps[w].s;
     const uint32_t lim = (s & ~7u) + j * kUnitElts;
+    const uint32_t per = 8u / bits, mask = bits == 8 ? 0xFFu : (1u << bits) - 1u;
     uint32_t sum = 0;
-    for (uint32_t i = s + lane; i < lim; i += kWarp) sum += ((deltas[i >> 1] >> ((i & 1u) * 4)) & 15u) + 1u;
+    for (uint32_t i = s + lane; i < lim; i += kWarp) sum += ((deltas[i / per] >> ((i % per) * bits)) & mask) + 1u;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
     if (lane == 0) warps[w].colbase = (int32_t)sum - 1;
@@ -669,31 +766,16 @@ __global__ void plan_colbase_kernel(const uint8_t* deltas, WarpPlan* warps, uint
 
 }  // namespace
 
-template <int kXMode>
+template <int kXMode, int kBits>
 static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     const int threads = kSpmvWarpsPerCta * kWarp;
-    cudaError_t e = cudaFuncSetAttribute(macko_spmv_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv_b4<kXMode>, threads, smem);
+    cudaError_t e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
     return e;
 }
 
-bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 11); }
-
-cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm) {
-    switch (x_mode) {
-        case 11: return occ_one<11>(smem, ctas_per_sm);
-        case 10: return occ_one<10>(smem, ctas_per_sm);
-        case 9: return occ_one<9>(smem, ctas_per_sm);
-        case 8: return occ_one<8>(smem, ctas_per_sm);
-        case 7: return occ_one<7>(smem, ctas_per_sm);
-        case 6: return occ_one<6>(smem, ctas_per_sm);
-        case 1: return occ_one<1>(smem, ctas_per_sm);
-        case 0: return occ_one<0>(smem, ctas_per_sm);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template <int kXMode>
+template <int kXMode, int kBits>
 static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -705,19 +787,74 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, macko_spmv_b4<kXMode>, a);
+    return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
+// b_delta = 4 (the paper's format) gets every x_mode; the other widths the automatic ones.
+bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 11); }
+bool spmv_valid_config(int x_mode, int bits) {
+    if (bits == 4) return spmv_valid_x_mode(x_mode);
+    return (bits == 1 || bits == 2 || bits == 8) && (x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 8) || x_mode == 10);
+}
+
+template <int kBits>
+static cudaError_t occ_bits(int x_mode, size_t smem, int* c) {
     switch (x_mode) {
-        case 11: return launch_one<11>(a, grid, smem, s, pdl);
-        case 10: return launch_one<10>(a, grid, smem, s, pdl);
-        case 9: return launch_one<9>(a, grid, smem, s, pdl);
-        case 8: return launch_one<8>(a, grid, smem, s, pdl);
-        case 7: return launch_one<7>(a, grid, smem, s, pdl);
-        case 6: return launch_one<6>(a, grid, smem, s, pdl);
-        case 1: return launch_one<1>(a, grid, smem, s, pdl);
-        case 0: return launch_one<0>(a, grid, smem, s, pdl);
+        case 10: return occ_one<10, kBits>(smem, c);
+        case 8: return occ_one<8, kBits>(smem, c);
+        case 7: return occ_one<7, kBits>(smem, c);
+        case 6: return occ_one<6, kBits>(smem, c);
+        case 1: return occ_one<1, kBits>(smem, c);
+        case 0: return occ_one<0, kBits>(smem, c);
+        default: break;
+    }
+    if constexpr (kBits == 4) {
+        switch (x_mode) {
+            case 11: return occ_one<11, 4>(smem, c);
+            case 9: return occ_one<9, 4>(smem, c);
+            default: break;
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int kBits>
+static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
+    switch (x_mode) {
+        case 10: return launch_one<10, kBits>(a, grid, smem, s, pdl);
+        case 8: return launch_one<8, kBits>(a, grid, smem, s, pdl);
+        case 7: return launch_one<7, kBits>(a, grid, smem, s, pdl);
+        case 6: return launch_one<6, kBits>(a, grid, smem, s, pdl);
+        case 1: return launch_one<1, kBits>(a, grid, smem, s, pdl);
+        case 0: return launch_one<0, kBits>(a, grid, smem, s, pdl);
+        default: break;
+    }
+    if constexpr (kBits == 4) {
+        switch (x_mode) {
+            case 11: return launch_one<11, 4>(a, grid, smem, s, pdl);
+            case 9: return launch_one<9, 4>(a, grid, smem, s, pdl);
+            default: break;
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm) {
+    switch (bits) {
+        case 4: return occ_bits<4>(x_mode, smem, ctas_per_sm);
+        case 2: return occ_bits<2>(x_mode, smem, ctas_per_sm);
+        case 8: return occ_bits<8>(x_mode, smem, ctas_per_sm);
+        case 1: return occ_bits<1>(x_mode, smem, ctas_per_sm);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
+    switch (bits) {
+        case 4: return launch_bits<4>(a, grid, x_mode, smem, s, pdl);
+        case 2: return launch_bits<2>(a, grid, x_mode, smem, s, pdl);
+        case 8: return launch_bits<8>(a, grid, x_mode, smem, s, pdl);
+        case 1: return launch_bits<1>(a, grid, x_mode, smem, s, pdl);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -759,10 +896,11 @@ cudaError_t trace_read(unsigned long long* host, size_t n) {
 }
 #endif
 
-cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s) {
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks,
+                                cudaStream_t s) {
     const int threads = 256;
     const int blocks = (int)((n_chunks * (uint64_t)kWarp + threads - 1) / threads);
-    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, warps, n_chunks);
+    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, bits, warps, n_chunks);
     return cudaGetLastError();
 }
 

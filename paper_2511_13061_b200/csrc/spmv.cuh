@@ -54,7 +54,7 @@ constexpr int kSpmvWarpsPerCta = MACKO_WARPS_PER_CTA;
 constexpr int kSpmvCtasPerSm = 32 / kSpmvWarpsPerCta;
 constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two step pairs)
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
-constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas
+constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas (b_delta = 4; kChunk * b / 8 in general)
 constexpr uint32_t kMaxRing = 4;
 // fp16 x table in shared memory with zero guards: kXGuardLo entries before x[0] (the ROMA-masked
 // elements of a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (a phantom
@@ -70,12 +70,14 @@ bool spmv_valid_x_mode(int x_mode);
 cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
 #endif
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
-cudaError_t launch_spmv(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
-cudaError_t spmv_occupancy(int x_mode, size_t smem, int* ctas_per_sm);
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
+cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
+bool spmv_valid_config(int x_mode, int bits);
 // Persistent chain of dependent SpMVs (d_ops: device array of n_ops SpmvArgs; d_bar: 2 zeroed u32
 // for the grid barrier).  Cooperative launch of `grid` CTAs; all ops share x_mode, ring and smem.
 cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
                          cudaStream_t s);
-cudaError_t launch_plan_colbase(const uint8_t* deltas, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks,
+                                cudaStream_t s);
 
 }  // namespace mk

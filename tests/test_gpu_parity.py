@@ -289,10 +289,10 @@ def test_error_behaviour(cuda):
     if (v != m.values).any():
         with pytest.raises(M.FormatError):
             M.DeviceMatrix.upload(M.MackoMatrix(4, 64, 4, v, m.deltas, m.row_ptrs))
-    # b_delta = 2: the compressor supports it, the SpMV kernel is b_delta = 4 only
+    # b_delta = 2 has no x_mode 9 / 11 instantiation (b_delta = 4 only)
     dm2 = gpu_encode(A, 2)
-    with pytest.raises(ValueError, match="b_delta"):
-        gpu_spmv(dm2, O.gen_vector(64, 1))
+    with pytest.raises(ValueError, match="x_mode"):
+        dm2.configure(9)
     dm = gpu_encode(A)
     with pytest.raises(ValueError):
         M.spmv(dm, torch.zeros(65, dtype=torch.float16, device=cuda))
@@ -345,3 +345,26 @@ def test_masked_edges_do_not_leak_inf_nan(cuda, x_mode):
     assert np.isfinite(y_ref[0::2].view(np.float16)).all()
     assert np.array_equal(y[0::2], y_ref[0::2])
     assert not np.isfinite(y[1::2].view(np.float16)).any()
+
+
+@pytest.mark.parametrize("bits", [1, 2, 8])
+def test_spmv_other_delta_widths(cuda, bits):
+    # b_delta in {1, 2, 8}: the same kernel with the width's codeword loads / decode (b = 8: 16-bit
+    # prefixes, scan on total - 8).  Integer mode is bit-exact against reference_spmv; float mode
+    # bit-exact against the B200 order and within the bound of the sequential reference.
+    cases = ((300, 5000, 0.5), (64, 20000, 0.05), (1000, 3000, 0.9), (7, 70000, 0.02))
+    for R, C, d in cases:
+        for int_mode in (True, False):
+            A = O.gen_dense(R, C, d, 70 + bits, int_mode)
+            x = O.gen_vector(C, 71, int_mode)
+            m = O.encode_dense(A, bits)
+            dm = gpu_encode(A, bits)
+            assert_same_format(dm, m, (bits, R, C, d))
+            check_y(A, m, x, gpu_spmv(dm, x), int_mode, (bits, R, C, d, int_mode))
+    A = O.gen_dense(500, 9000, 0.3, 72)
+    x = O.gen_vector(9000, 73)
+    dm = gpu_encode(A, bits)
+    y0 = gpu_spmv(dm, x)
+    for x_mode in (0, 1, 6, 7, 8, 10):
+        dm.configure(x_mode)
+        assert np.array_equal(gpu_spmv(dm, x), y0), (bits, x_mode)

@@ -17,11 +17,12 @@ p.add_argument("--density", type=float, default=0.5)
 p.add_argument("--modes", default="-1")
 p.add_argument("--flush", type=int, default=1)
 p.add_argument("--n", type=int, default=40)
+p.add_argument("--bits", type=int, default=4)
 a = p.parse_args()
 R, C = a.rows, a.cols
 dense = torch.empty((R, C), dtype=torch.float16, device="cuda")
 M.gen_dense(dense, R, C, a.density, seed=1234)
-dm = M.DeviceMatrix.from_dense(dense)
+dm = M.DeviceMatrix.from_dense(dense, b_delta=a.bits)
 del dense
 x = torch.empty(C, dtype=torch.float16, device="cuda")
 M.gen_vector(x, C, seed=4321)
@@ -42,5 +43,5 @@ for mode in [int(m) for m in a.modes.split(",")]:
         e1.record(st)
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
-    print(f"mode {mode:2d} flush {a.flush}: median {statistics.median(ts):7.2f} us  min {min(ts):7.2f}  "
+    print(f"b{a.bits} d={a.density} mode {dm.launch_info().x_in_smem:2d} flush {a.flush}: median {statistics.median(ts):7.2f} us  min {min(ts):7.2f}  "
           f"GB/s {dm.traffic_bytes / statistics.median(ts) / 1e3:7.1f}")
