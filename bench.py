@@ -372,7 +372,7 @@ def main():
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "macko_spmv_b4", "us": round(kern_ms * 1e3, 2)},
+                         "kernel": f"macko_spmv<{li.x_in_smem},4>", "us": round(kern_ms * 1e3, 2)},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * C,
                     "d2h_bytes_per_step": 2 * R, "us_per_call": round(e2e_mean * 1e3, 2)},
             "dense_cublas_gemv": None if dense_us is None else {
