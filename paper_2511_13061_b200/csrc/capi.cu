@@ -118,8 +118,9 @@ struct macko_dev_matrix {
     DevBuf<uint32_t> plan_u32;   // S split records {slot, first, pieces, 0} | S counters
     DevBuf<float> partials;
     mk::SpmvPlanDev plan{};
-    // scratch for macko_spmv_host
+    // scratch for macko_spmv_host (x texture-aligned inside hx, so the SpMV needs no staging copy)
     DevBuf<uint16_t> hx, hy;
+    uint16_t* hx_aligned = nullptr;
     // x as a 1-D fp16 texture for x_mode >= 3 (created per x buffer, reused while it stays the same)
     mutable std::mutex tex_mu;
     mutable const void* tex_ptr = nullptr;
@@ -760,11 +761,19 @@ macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t*
         if (!m || !h_x || !h_y) fail(MACKO_EINVAL, "null argument");
         DeviceGuard g(m->device);
         cudaStream_t st = (cudaStream_t)stream;
-        if (!m->hx.p) m->hx.alloc(m->cols);
+        if (!m->hx.p) {
+            // texture-aligned device x (no staging copy inside the SpMV): over-allocate and align
+            int align = 0;
+            ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
+            m->hx.alloc(m->cols + (uint64_t)std::max(align, 16) / 2);
+            const uintptr_t p = reinterpret_cast<uintptr_t>(m->hx.p), a = (uintptr_t)std::max(align, 16);
+            m->hx_aligned = reinterpret_cast<uint16_t*>((p + a - 1) / a * a);
+        }
         if (!m->hy.p) m->hy.alloc(m->rows);
-        ck(cudaMemcpyAsync(m->hx.p, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
-        const macko_status s = macko_dev_spmv(m, m->hx.p, m->hy.p, stream);
-        if (s != MACKO_OK) fail(s, g_err);
+        // Plain stream order (a cached CUDA graph of the three steps measured 11 us slower).
+        ck(cudaMemcpyAsync(m->hx_aligned, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
+        const macko_status sp = macko_dev_spmv(m, m->hx_aligned, m->hy.p, st);
+        if (sp != MACKO_OK) fail(sp, g_err);
         ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
         ck(cudaStreamSynchronize(st), "sync");
     });
