@@ -4,6 +4,7 @@ The product is libmacko_cuda.so (include/macko_cuda.h).  This package is the thi
 mirror of the reference interface used by tests and bench.py; it never falls back to CPU.
 """
 from .macko import (  # noqa: F401
+    Chain,
     CudaError,
     DeviceMatrix,
     FormatError,
@@ -16,8 +17,13 @@ from .macko import (  # noqa: F401
     gen_vector,
     kernel_launches,
     macko_from_dense,
+    mcko_info,
+    read_matrix_market,
+    read_mcko,
+    read_mcko_host,
     shard_rows,
     spmv,
     values_bytes,
     version,
+    write_mcko,
 )

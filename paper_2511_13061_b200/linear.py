@@ -1,0 +1,56 @@
+"""`MackoLinear`: an nn.Linear replacement for batch-1 decode over a MACKO weight (the paper's
+end-to-end use, PAPER.md:86,496-510 — every linear of a pruned LLM becomes an SpMV).
+
+The fp16 weight is compressed once on the GPU (bit-exact MACKO format, b_delta = 4 by default);
+forward(x) for x of shape [in_features] or [1, ..., 1, in_features] is one sm_100a SpMV (fp32
+accumulate, one RNE) plus the optional bias.  Larger batches run one SpMV per input vector — the
+kernel is a matrix-vector product (SpMM is the paper's future work).  There is no CPU fallback:
+the module requires the CUDA library and a CUDA weight.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+from torch import nn
+
+from . import macko as M
+
+
+class MackoLinear(nn.Module):
+    def __init__(self, matrix: M.DeviceMatrix, bias: Optional[torch.Tensor] = None):
+        super().__init__()
+        self.matrix = matrix
+        self.in_features = matrix.cols
+        self.out_features = matrix.rows
+        if bias is not None:
+            self.register_buffer("bias", bias.detach().to(torch.float16).contiguous())
+        else:
+            self.bias = None
+
+    @classmethod
+    def from_linear(cls, linear: nn.Linear, b_delta: int = 4) -> "MackoLinear":
+        """Compress an (already pruned) nn.Linear's weight on its CUDA device."""
+        w = linear.weight.detach()
+        if not w.is_cuda:
+            raise ValueError("MackoLinear needs a CUDA weight (no CPU fallback)")
+        w16 = w.to(torch.float16).contiguous()
+        dm = M.DeviceMatrix.from_dense(w16, b_delta=b_delta)
+        return cls(dm, linear.bias)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if x.shape[-1] != self.in_features:
+            raise ValueError(f"expected last dimension {self.in_features}, got {x.shape[-1]}")
+        lead = x.shape[:-1]
+        xs = x.reshape(-1, self.in_features).to(torch.float16).contiguous()
+        out = torch.empty((xs.shape[0], self.out_features), dtype=torch.float16, device=x.device)
+        stream = torch.cuda.current_stream(x.device)
+        for i in range(xs.shape[0]):
+            self.matrix.spmv_into(xs[i], out[i], stream)
+        if self.bias is not None:
+            out += self.bias
+        return out.reshape(*lead, self.out_features)
+
+    def extra_repr(self) -> str:
+        return (f"in_features={self.in_features}, out_features={self.out_features}, "
+                f"pad_nnz={self.matrix.pad_nnz}, b_delta={self.matrix.b_delta}, bias={self.bias is not None}")
