@@ -211,6 +211,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->grid * m->force_ctas / 4));
     const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
     m->n_chunks = W;
+    // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
+    if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
     const uint64_t R = m->rows;
     const std::vector<uint32_t>& rp = m->h_row_ptrs;
 

@@ -333,7 +333,7 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          g.dbase + rel * kBits / 8u),
-                     "l"(a.deltas + e0 * kBits / 8u), "n"(dbytes<kBits>()), "r"(bar)
+                     "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "n"(dbytes<kBits>()), "r"(bar)
                      : "memory");
     }
 }
@@ -485,7 +485,7 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         g.dbase),
-                    "l"(a.deltas + e0 * kBits / 8u), "r"(n * dbytes<kBits>()), "r"(g.bar0)
+                    "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(n * dbytes<kBits>()), "r"(g.bar0)
                     : "memory");
                 for (uint32_t i = 1; i < n; ++i)
                     asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");

@@ -368,3 +368,43 @@ def test_spmv_other_delta_widths(cuda, bits):
     for x_mode in (0, 1, 6, 7, 8, 10):
         dm.configure(x_mode)
         assert np.array_equal(gpu_spmv(dm, x), y0), (bits, x_mode)
+
+
+def _codes(deltas: np.ndarray, first: int, n: int) -> np.ndarray:
+    """4-bit codewords of elements [first, first + n) (LSB-first nibbles, bitpack.cpp:18-32)."""
+    idx = np.arange(first, first + n, dtype=np.int64)
+    return (deltas[idx // 2] >> ((idx % 2) * 4).astype(np.uint8)) & 0xF
+
+
+def test_large_offsets_beyond_2_30(cuda):
+    # pad_nnz ~1.15e9 > 2^30: element offsets times 4 bits leave u32 range in the last ~7 % of rows.
+    # Integer mode (order-independent, exact): y of the big matrix == y of the same rows encoded
+    # as a standalone slab (small offsets) == reference_spmv on that slab; the big matrix's stored
+    # bytes for those rows decode to the oracle's encoding of them.
+    R, C = 70000, 32768
+    dense = torch.empty((R, C), dtype=torch.float16, device=cuda)
+    M.gen_dense(dense, R, C, 0.5, seed=91, int_mode=True)
+    dm = M.DeviceMatrix.from_dense(dense)
+    assert dm.pad_nnz > 2**30
+    x = torch.empty(C, dtype=torch.float16, device=cuda)
+    M.gen_vector(x, C, seed=92, int_mode=True)
+    y = M.spmv(dm, x)
+    torch.cuda.synchronize()
+    y_big = to_host_u16(y)
+    xh = to_host_u16(x)
+    h = dm.download()
+    for r0, r1 in ((R - 257, R), (0, 130)):
+        slab = dense[r0:r1]
+        dms = M.DeviceMatrix.from_dense(slab)
+        ys = to_host_u16(M.spmv(dms, x))
+        torch.cuda.synchronize()
+        assert np.array_equal(y_big[r0:r1], ys), (r0, r1)
+        A = to_host_u16(slab)
+        m = O.encode_dense(A)
+        assert np.array_equal(ys, O.reference_spmv(m, xh, 8)), (r0, r1)
+        e0, e1 = int(h.row_pointers[r0]), int(h.row_pointers[r1])
+        assert np.array_equal(h.row_pointers[r0:r1 + 1] - e0, m.row_ptrs)
+        assert np.array_equal(h.values[e0:e1], m.values[: e1 - e0])
+        assert np.array_equal(_codes(h.packed_deltas, e0, e1 - e0), _codes(m.deltas, 0, e1 - e0))
+        dms.close()
+    dm.close()
