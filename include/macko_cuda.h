@@ -159,12 +159,13 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
 /* ---- introspection ---- */
 typedef struct macko_launch_info {
     uint32_t grid, block, warps, ctas_per_sm, n_split_rows;
-    uint32_t x_in_smem; /* x staging: 0 global (L1), 1 fp16 table, 2 (x[c], x[c+1]) pair table */
+    uint32_t x_in_smem; /* x_mode: how x is gathered — 0 texture only, 1 fp16 shared-memory table
+                         * only, 6..11 table + texture split over the element slots */
     uint64_t n_units, smem_bytes;
 } macko_launch_info;
 macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out);
-/* Re-plan the SpMV launch: x staging mode (-1 automatic, 0/1/2 as above) and a cap on CTAs per
- * SM (0 automatic).  Results are identical for every setting (the summation order does not
+/* Re-plan the SpMV launch: x_mode (-1 automatic, else as above; 9 and 11 exist for b_delta = 4
+ * only) and a cap on CTAs (k > 0: use k/4 of the persistent CTAs; 0 automatic).  Results are identical for every setting (the summation order does not
  * depend on the plan); exposed for tuning and for the grid-independence tests.  Synchronous. */
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream);
 /* Number of kernels this library has launched in the process (for bench gpu_launches). */

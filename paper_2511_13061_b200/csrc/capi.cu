@@ -162,7 +162,7 @@ void check_bits(uint32_t bits) {
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
-    // Shared memory: x table (x_mode 1: fp16, 2: (x[c], x[c+1]) pairs) + per-warp TMA rings.
+    // Shared memory: fp16 x table with zero guards (every x_mode but 0) + per-warp TMA rings.
     int optin = 0, per_sm = 0;
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
@@ -184,10 +184,9 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     if (m->force_x_mode >= 0) {
         m->x_mode = m->force_x_mode;
     } else {
-        // prefer the pair table (fewer gather wavefronts), then the fp16 table, then global x
         // TEX gathers cost ~1 wavefront per 128-B line a warp gather touches, which grows with the
         // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
-        // density.  Measured best split (profiles/r01_v12_modes.md): 4 of 8 slots by TEX at
+        // density.  Measured best split (profiles/r01_v12_summary.md): 4 of 8 slots by TEX at
         // d >= 0.4 (alternating 4 / 3 at d >= 0.6), 3 at 0.25 <= d < 0.4, 2 below.
         // At low density the texture gathers need x resident in L1: the unified 256 KB L1/shared
         // memory keeps what the x table and the rings leave (C = 32768: ~28 KB < 64 KB of x), so

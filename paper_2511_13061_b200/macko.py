@@ -139,8 +139,8 @@ class DeviceMatrix:
         return li
 
     def configure(self, x_mode: int = -1, ctas_per_sm: int = 0, stream=None) -> None:
-        """Re-plan the launch (x staging 0/1/2 or -1 = auto; CTA cap or 0 = auto).  y is
-        bit-identical for every setting."""
+        """Re-plan the launch (x_mode: -1 auto, 0 texture only, 1 shared table only, 6..11 split;
+        CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""
         check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
 
     # -- operations -------------------------------------------------------------------------
