@@ -162,12 +162,18 @@ typedef struct macko_launch_info {
     uint32_t x_in_smem; /* x_mode: how x is gathered — 0 texture only, 1 fp16 shared-memory table
                          * only, 6..11 table + texture split over the element slots */
     uint64_t n_units, smem_bytes;
+    uint32_t order; /* 0: ROMA row-relative walk (oracle mo_b200_order_spmv, the default), 1: flat
+                     * global windows (oracle mo_b200_flat_spmv) — DESIGN.md §2.1 */
+    uint32_t reserved;
 } macko_launch_info;
 macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out);
 /* Re-plan the SpMV launch: x_mode (-1 automatic, else as above; 9 and 11 exist for b_delta = 4
  * only) and a cap on CTAs (k > 0: use k/4 of the persistent CTAs; 0 automatic).  Results are identical for every setting (the summation order does not
  * depend on the plan); exposed for tuning and for the grid-independence tests.  Synchronous. */
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream);
+/* Choose the SpMV walk (launch_info.order) and re-plan.  Both are deterministic and independent of
+ * the plan; they differ in where lane / unit boundaries sit, hence in the float summation order. */
+macko_status macko_dev_set_order(macko_dev_matrix* m, int order, void* stream);
 /* Number of kernels this library has launched in the process (for bench gpu_launches). */
 uint64_t macko_kernel_launches(void);
 

@@ -478,6 +478,30 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
     return MO_OK;
 }
 
+/* The flat-window kernel's order: lane = (e mod 256) / 8 by global position, units = global
+ * 2048-element blocks (see macko_oracle.h).  Independent of the launch plan by construction. */
+int mo_b200_flat_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values,
+                      const uint8_t* deltas, const uint32_t* rp, const uint16_t* x, uint16_t* y) {
+    if (!mo_is_valid_delta_bits(bits)) return fail(MO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits");
+    for (uint64_t r = 0; r < rows; ++r) {
+        const uint64_t s = rp[r], e = rp[r + 1];
+        float row_acc = 0.0f;
+        int64_t col = -1;
+        for (uint64_t u0 = s & ~(uint64_t)2047; u0 < e; u0 += 2048) {
+            float acc[32] = {0};
+            const uint64_t lo = u0 > s ? u0 : s, hi = u0 + 2048 < e ? u0 + 2048 : e;
+            for (uint64_t i = lo; i < hi; ++i) {
+                col += code_at(deltas, i, bits) + 1;
+                if ((uint64_t)col >= cols) return fail(MO_EFORMAT, "decoded column index past the column bound");
+                acc[(i % 256) / 8] += mo_half_to_float(values[i]) * mo_half_to_float(x[col]);
+            }
+            row_acc += lane_tree(acc);
+        }
+        y[r] = mo_float_to_half(row_acc);
+    }
+    return MO_OK;
+}
+
 /* ------------------------------------------------------------------------------------------
  * Synthetic inputs.  gen_random leaves the magnitude distribution and RNG
  * undocumented (generate.cpp is absent), so this generator is ours and identical on CPU and

@@ -95,6 +95,14 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
                        const uint8_t* deltas, const uint32_t* row_ptrs, const uint16_t* x,
                        uint16_t* y, unsigned unit_steps);
 
+/* The flat-window kernel's order: lanes, steps and units are aligned to GLOBAL
+ * element positions — element e of a row goes to lane (e mod 256)/8; the row's elements are
+ * split at global 2048-element unit boundaries; within a unit each lane sums its elements
+ * sequentially, the 32 lanes are xor-tree reduced, and the unit sums are added sequentially into
+ * the row accumulator (+0 start); one RNE at the end. */
+int mo_b200_flat_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values,
+                      const uint8_t* deltas, const uint32_t* row_ptrs, const uint16_t* x, uint16_t* y);
+
 /* ---- synthetic inputs (our counter-hash generator) ---- */
 uint32_t mo_density_threshold(double density);
 uint16_t mo_gen_value(uint64_t seed, uint64_t idx, uint32_t thr24, int int_mode);

@@ -76,6 +76,7 @@ def lib() -> C.CDLL:
         L.mo_warp_prefix_sum.argtypes = [_u32p, _u32p]
         L.mo_warp_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p]
         L.mo_b200_order_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p, C.c_uint]
+        L.mo_b200_flat_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p]
         L.mo_density_threshold.restype = C.c_uint32
         L.mo_density_threshold.argtypes = [C.c_double]
         L.mo_gen_dense.argtypes = [_u64, _u64, C.c_uint32, _u64, C.c_int, _u16p]
@@ -279,6 +280,14 @@ def b200_order_spmv(m: Macko, x: np.ndarray, unit_steps: int) -> np.ndarray:
     y = np.zeros(max(m.rows, 1), np.uint16)
     _check(lib().mo_b200_order_spmv(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), m.row_ptrs,
                                     _nz(np.ascontiguousarray(x, np.uint16)), y, unit_steps))
+    return y[: m.rows]
+
+
+def b200_flat_spmv(m: Macko, x: np.ndarray) -> np.ndarray:
+    """The flat-window kernel's order (global lane / unit alignment)."""
+    y = np.zeros(max(m.rows, 1), np.uint16)
+    _check(lib().mo_b200_flat_spmv(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), m.row_ptrs,
+                                   _nz(np.ascontiguousarray(x, np.uint16)), y))
     return y[: m.rows]
 
 

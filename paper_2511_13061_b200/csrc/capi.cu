@@ -108,6 +108,7 @@ struct macko_dev_matrix {
     int x_mode = 1;             // 0 global x, 1 fp16 smem table, 2 pair smem table
     int force_x_mode = -1;      // macko_dev_configure overrides (-1 / 0 = automatic)
     int force_ctas = 0;
+    int order = 0;              // 0: ROMA row-relative walk, 1: flat global windows
     uint32_t ring = 0;          // TMA ring slots per warp
     size_t ring_offset = 0;     // x table bytes (rings follow it in dynamic smem)
     size_t smem = 0;
@@ -134,7 +135,7 @@ struct macko_dev_matrix {
 
 struct macko_chain {
     int device = 0;
-    int grid = 0, x_mode = 0;
+    int grid = 0, x_mode = 0, order = 0;
     size_t smem = 0;
     uint32_t n_ops = 0;
     DevBuf<uint8_t> ops;     // n_ops mk::SpmvArgs
@@ -157,6 +158,108 @@ int sm_count(int dev) {
 void check_bits(uint32_t bits) {
     if (!(bits == 1 || bits == 2 || bits == 4 || bits == 8))
         fail(MACKO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits; got " + std::to_string(bits));
+}
+
+constexpr uint64_t kRowOverheadFlat = 384;  // flat-plan weight of a row start (element equivalents)
+
+// Flat plan (order 1): units are the global 2048-element blocks of the payload; warp k owns the
+// whole units [cu[k], cu[k+1]) of roughly equal weight and the rows that start there (plus the
+// row it continues into).  Rows cut at unit boundaries between warps get per-unit partial slots.
+void build_plan_flat(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
+    using namespace mk;
+    const std::vector<uint32_t>& rp = m->h_row_ptrs;
+    const uint64_t R = m->rows, N = m->pad_nnz;
+    const uint64_t U = (N + kUnitElts - 1) / kUnitElts;
+    std::vector<uint64_t> wpre(U + 1, 0);
+    {
+        std::vector<uint32_t> starts(U, 0);
+        for (uint64_t r = 0; r < R; ++r)
+            if (rp[r + 1] > rp[r]) ++starts[rp[r] / kUnitElts];
+        for (uint64_t u = 0; u < U; ++u)
+            wpre[u + 1] = wpre[u] + std::min<uint64_t>(kUnitElts, N - u * kUnitElts) + kRowOverheadFlat * starts[u];
+    }
+    const uint64_t total = wpre[U];
+    std::vector<uint64_t> cu(W + 1, U);
+    cu[0] = 0;
+    for (uint32_t k = 1; k < W; ++k) {
+        const uint64_t target = (uint64_t)((unsigned __int128)total * k / W);
+        cu[k] = (uint64_t)(std::lower_bound(wpre.begin(), wpre.end(), target) - wpre.begin());
+        cu[k] = std::min<uint64_t>(std::max<uint64_t>(cu[k], cu[k - 1]), U);
+    }
+    m->n_units = U;
+    std::vector<mk::WarpPlan> recs(W);
+    for (uint32_t k = 0; k < W; ++k) {
+        mk::WarpPlan& c = recs[k];
+        std::memset(&c, 0, sizeof c);
+        c.sid0 = c.sid1 = -1;
+        c.colbase = -1;
+        if (cu[k] >= cu[k + 1]) continue;
+        const uint64_t E0 = cu[k] * kUnitElts, E1 = std::min<uint64_t>(cu[k + 1] * kUnitElts, N);
+        c.units_left = (uint32_t)(cu[k + 1] - cu[k]);
+        c.e0 = (uint32_t)E0;
+        c.e1 = (uint32_t)E1;
+        // first row starting at or after E0; the row before it continues into this warp iff it ends past E0
+        uint64_t q = (uint64_t)(std::lower_bound(rp.begin(), rp.begin() + R, (uint32_t)E0) - rp.begin());
+        if (q > 0 && rp[q] > E0) --q;
+        c.row = (uint32_t)q;
+        c.s = rp[q];
+        c.e = rp[q + 1];
+    }
+    // split rows
+    std::vector<uint32_t> split_slot, split_first, split_pieces;
+    uint64_t slots = 0;
+    auto warp_of = [&](uint64_t elem) -> uint32_t {  // the non-idle warp whose units contain elem
+        const uint64_t u = elem / kUnitElts;
+        return (uint32_t)(std::upper_bound(cu.begin(), cu.end(), u) - cu.begin()) - 1u;
+    };
+    for (uint64_t r = 0; r < R; ++r) {
+        const uint64_t s = rp[r], e = rp[r + 1];
+        if (e <= s) continue;
+        const uint32_t kf = warp_of(s), kl = warp_of(e - 1);
+        if (kf == kl) continue;
+        const int32_t sid = (int32_t)split_slot.size();
+        const uint64_t n_r = (e - 1) / kUnitElts - s / kUnitElts + 1;
+        uint32_t pieces = 0;
+        for (uint32_t k = kf; k <= kl; ++k) pieces += cu[k] < cu[k + 1];
+        split_slot.push_back((uint32_t)slots);
+        split_first.push_back((uint32_t)(cu[kf + 1] - s / kUnitElts));
+        split_pieces.push_back(pieces);
+        for (uint32_t k = kf; k <= kl; ++k) {
+            if (cu[k] >= cu[k + 1]) continue;
+            if (k != kf) {
+                recs[k].sid0 = sid;
+                recs[k].slot0 = (uint32_t)slots;
+            }
+            if (k != kl) {
+                recs[k].sid1 = sid;
+                recs[k].slot1 = (uint32_t)slots;
+            }
+        }
+        slots += n_r;
+    }
+    const uint32_t S = (uint32_t)split_slot.size();
+    m->n_split = S;
+    std::vector<uint32_t> sp(4 * (size_t)S + 4 * (size_t)((S + 3) / 4 + 1), 0);
+    for (uint32_t q = 0; q < S; ++q) {
+        sp[4 * (size_t)q] = split_slot[q];
+        sp[4 * (size_t)q + 1] = split_first[q];
+        sp[4 * (size_t)q + 2] = split_pieces[q];
+    }
+    m->plan_recs.alloc(recs.size() * sizeof(mk::WarpPlan) / 4);
+    m->plan_u32.alloc(sp.size());
+    m->partials.alloc(std::max<uint64_t>(slots, 1));
+    ck(cudaMemcpyAsync(m->plan_recs.p, recs.data(), recs.size() * sizeof(mk::WarpPlan), cudaMemcpyHostToDevice, st),
+       "plan upload");
+    ck(cudaMemcpyAsync(m->plan_u32.p, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
+    mk::SpmvPlanDev& P = m->plan;
+    P.warps = reinterpret_cast<const mk::WarpPlan*>(m->plan_recs.p);
+    P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
+    P.counters = m->plan_u32.p + 4 * (size_t)S;
+    P.partials = m->partials.p;
+    ck(launch_plan_colbase(m->deltas.p, m->b_delta, 1, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
+       "plan colbase");
+    g_launches.fetch_add(1);
+    ck(cudaStreamSynchronize(st), "plan sync");
 }
 
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
@@ -212,6 +315,10 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     m->n_chunks = W;
     // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
     if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
+    if (m->order == 1) {
+        build_plan_flat(m, st, W);
+        return;
+    }
     const uint64_t R = m->rows;
     const std::vector<uint32_t>& rp = m->h_row_ptrs;
 
@@ -322,7 +429,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
     P.counters = m->plan_u32.p + 4 * (size_t)S;
     P.partials = m->partials.p;
-    ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
+    ck(launch_plan_colbase(m->deltas.p, m->b_delta, 0, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
        "plan colbase");
     g_launches.fetch_add(1);
     ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
@@ -747,7 +854,13 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
-        ck(mk::launch_spmv(a, (int)m->b_delta, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0),
+        a.value_count = (uint32_t)m->pad_nnz;
+        if (m->pad_nnz == 0) {  // no stored entries: every row is empty, y = +0
+            ck(cudaMemsetAsync(d_y, 0, m->rows * 2, (cudaStream_t)stream), "y = 0");
+            return;
+        }
+        ck(mk::launch_spmv(a, (int)m->b_delta, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0,
+                           m->order),
            "macko_spmv launch");
         g_launches.fetch_add(1);
     });
@@ -970,6 +1083,7 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
         c->device = dev;
         c->n_ops = n_ops;
         c->grid = mats[0]->grid;
+        c->order = mats[0]->order;
         // one x_mode for all ops (a template parameter): the op with the most bytes decides
         uint64_t best = 0;
         size_t xtab = 0;
@@ -978,7 +1092,8 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
             if (!m || !xs[k] || !ys[k]) fail(MACKO_EINVAL, "null matrix or vector in the chain");
             if (m->device != dev) fail(MACKO_EINVAL, "chain ops must live on one device");
             if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
-            if (m->grid != c->grid || m->ring != mats[0]->ring) fail(MACKO_EINVAL, "chain ops must share the launch plan geometry");
+            if (m->grid != c->grid || m->ring != mats[0]->ring || m->order != mats[0]->order)
+                fail(MACKO_EINVAL, "chain ops must share the launch plan geometry and order");
             const uint64_t tb = values_bytes(m->pad_nnz) + delta_bytes(m->pad_nnz, 4);
             if (tb >= best) {
                 best = tb;
@@ -1017,6 +1132,8 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
             a.ring = ring;
             a.ring_offset = (uint32_t)xtab;
             a.plan = m->plan;
+            a.value_count = (uint32_t)m->pad_nnz;
+            if (m->pad_nnz == 0) fail(MACKO_EINVAL, "chain ops need stored entries");
             a.xtex = 0;
             if (c->x_mode != 1) {
                 cudaResourceDesc rd{};
@@ -1045,7 +1162,7 @@ macko_status macko_chain_run(macko_chain* c, void* stream) {
         if (!c) fail(MACKO_EINVAL, "null chain");
         DeviceGuard g(c->device);
         ck(mk::launch_chain(reinterpret_cast<const mk::SpmvArgs*>(c->ops.p), c->n_ops, c->bar.p, c->grid, c->x_mode,
-                            c->smem, (cudaStream_t)stream),
+                            c->smem, (cudaStream_t)stream, c->order),
            "macko_chain launch");
         g_launches.fetch_add(1);
     });
@@ -1080,6 +1197,16 @@ macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_s
     });
 }
 
+macko_status macko_dev_set_order(macko_dev_matrix* m, int order, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        if (order != 0 && order != 1) fail(MACKO_EINVAL, "order must be 0 (ROMA) or 1 (flat)");
+        DeviceGuard g(m->device);
+        m->order = order;
+        build_plan(m, (cudaStream_t)stream);
+    });
+}
+
 macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out) {
     return guarded([&] {
         if (!m || !out) fail(MACKO_EINVAL, "null argument");
@@ -1091,6 +1218,8 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
         out->x_in_smem = (uint32_t)m->x_mode;
         out->n_units = m->n_units;
         out->smem_bytes = m->smem;
+        out->order = (uint32_t)m->order;
+        out->reserved = 0;
     });
 }
 

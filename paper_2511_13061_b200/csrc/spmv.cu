@@ -443,13 +443,13 @@ __device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w)
     return PlanRecord{__ldg(rec), __ldg(rec + 1), __ldg(rec + 2)};
 }
 
+// Ring set-up for the warp's element stream [E0, E1) and its first fills.  `fresh`: the
+// barriers are initialised here and the first fill is one copy per array (single-SpMV kernels);
+// otherwise (chain) the ring continues where the previous op left it — the first chunk goes to
+// the slot after the last one consumed, each chunk on its own barrier phase.
 template <int kBits, bool kFresh>
-__device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
-                                         uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
-    const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
-    MK_TRACE(1);
-    if (q0.x == 0) return false;
-    const uint32_t E0 = q0.w, E1 = q1.x;
+__device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint32_t E1, uint32_t warp, int lane,
+                                           uint32_t smem_base, uint32_t bar0, Ring& g) {
     g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
     g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * dbytes<kBits>();
     g.bar0 = bar0;
@@ -499,6 +499,16 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
         for (g.iss = e0; g.iss < limit; g.iss += kChunk) ring_issue<kBits>(g, a, lane);
     }
     __syncwarp();
+}
+
+// Set up the warp's ring and ROMA walk for one SpMV (plan record pr) and issue the first fills.
+template <int kBits, bool kFresh>
+__device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
+                                         uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
+    const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
+    MK_TRACE(1);
+    if (q0.x == 0) return false;
+    ring_begin<kBits, kFresh>(a, q0.w, q1.x, warp, lane, smem_base, bar0, g);
     rs.r = q0.y;
     rs.units_left = q0.x;
     rs.s = q1.y;
@@ -627,6 +637,221 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Flat-window walk (order 1): lanes, steps and units aligned to GLOBAL element positions
+// (oracle mo_b200_flat_spmv).  A warp owns whole 2048-element units [E0, E1) and walks them in
+// 512-element windows, two per 1024-element TMA chunk, so the ring is serviced once per chunk
+// at a fixed point.  A window inside one row is the interior pair; a window holding row
+// boundaries decodes and scans its 512 codewords once and gathers each row segment with masks.
+// ------------------------------------------------------------------------------------------
+struct FlatState {
+    uint32_t r, s, e, e_next;  // current row and its bounds; row_ptrs[r + 2] prefetched
+    int col_base;              // column of the element just before the current window (-1: none)
+    float acc, row_acc;
+};
+
+// Inclusive in-lane prefix of element m (0..7) of the lane's step.
+template <class D>
+__device__ __forceinline__ uint32_t incl_at(const D& d, uint32_t m) {
+    if constexpr (std::is_same<D, Dec8>::value) {
+        const uint32_t w = d.p[0] * (m < 2) + d.p[1] * (m >= 2 && m < 4) + d.p[2] * (m >= 4 && m < 6) + d.p[3] * (m >= 6);
+        return (m & 1u) ? (w >> 16) : (w & 0xFFFFu);
+    } else {
+        return __byte_perm((m & 1u) ? d.odd : d.even, 0u, 0x4440u + (m >> 1));
+    }
+}
+
+__device__ __forceinline__ uint4 mask_values(uint4 v, uint32_t vm) {
+    auto hm = [&](int k) { return ((vm >> k) & 1u) ? 0xFFFFu : 0u; };
+    v.x &= hm(0) | (hm(1) << 16);
+    v.y &= hm(2) | (hm(3) << 16);
+    v.z &= hm(4) | (hm(5) << 16);
+    v.w &= hm(6) | (hm(7) << 16);
+    return v;
+}
+
+// Finish a row cut between warps (flat plan): the first piece stores its sum at the slot of its
+// last unit, other pieces stored per-unit partials at their unit ends; the last arrival adds them
+// in unit order.
+__device__ __noinline__ void finish_split_flat(uint32_t r, bool first_piece, uint32_t n_r, const uint4* rec,
+                                               float row_acc, const SpmvPlanDev P, uint16_t* y, int lane) {
+    uint32_t last = 0, first = 0, slot = 0;
+    if (lane == 0) {
+        const uint4 q2 = __ldg(rec + 2);  // sid0, sid1, slot0, slot1 (spmv.cuh WarpPlan)
+        const int32_t sid = (int32_t)(first_piece ? q2.y : q2.x);
+        slot = first_piece ? q2.w : q2.z;
+        const uint4 sp = P.splits[sid];
+        first = sp.y;
+        if (first_piece) P.partials[slot + first - 1u] = row_acc;
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
+        last = prev + 1 == sp.z;
+        if (last) {
+            float tot = __ldcg(P.partials + slot + first - 1);
+            for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
+            y[r] = f32_to_f16_rn(tot);
+            P.counters[sid] = 0;
+        }
+    }
+    __syncwarp();
+}
+
+template <int kXMode, int kBits>
+__device__ __forceinline__ void run_flat(const SpmvArgs& a, const PlanRecord& pr, int lane, uint32_t xs_addr, Ring& g) {
+    using D = typename std::conditional<kBits == 8, Dec8, Dec>::type;
+    constexpr uint32_t kBias = kBits == 8 ? 8u : 0u;  // b = 8: the packed scan runs on (total - 8)
+    const uint32_t E0 = pr.q0.w, E1 = pr.q1.x;
+    // the warp's plan record: split ids / partial slots are re-read when a split row finishes
+    const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + blockIdx.x * kSpmvWarpsPerCta + (threadIdx.x >> 5));
+    FlatState fs;
+    fs.r = pr.q0.y;
+    fs.s = pr.q1.y;
+    fs.e = pr.q1.z;
+    fs.e_next = fs.r + 2u <= a.rows ? __ldg(a.row_ptrs + fs.r + 2u) : 0u;
+    fs.col_base = (int)pr.q1.w;
+    fs.acc = 0.0f;
+    fs.row_acc = 0.0f;
+    // a row that began before E0 (a continuation piece of a split row) stores per-unit partials
+    auto unit_end = [&](uint32_t unit) {  // tree over lanes
+        const float red = warp_tree_sum(fs.acc);
+        fs.acc = 0.0f;
+        if (fs.s < E0 && lane == 0) a.plan.partials[__ldg(&rec[2].z) + unit - fs.s / kUnitElts] = red;
+        fs.row_acc += red;
+    };
+    auto finish_row = [&]() {
+        if (fs.s >= E0 && fs.e <= E1) {
+            if (lane == 0) a.y[fs.r] = f32_to_f16_rn(fs.row_acc);
+        } else {
+            const uint32_t n_r = (fs.e - 1u) / kUnitElts - fs.s / kUnitElts + 1u;
+            finish_split_flat(fs.r, fs.s >= E0, n_r, rec, fs.row_acc, a.plan, a.y, lane);
+        }
+    };
+    // Move to the next row this warp owns (empty rows get +0).  Returns false when the walk is over.
+    auto next_row = [&]() -> bool {
+        for (;;) {
+            if (fs.r + 1u >= a.rows) return false;
+            ++fs.r;
+            fs.s = fs.e;
+            fs.e = fs.e_next;
+            if (fs.r + 2u <= a.rows) fs.e_next = __ldg(a.row_ptrs + fs.r + 2u);
+            if (fs.s >= E1 && E1 != a.value_count) return false;  // the next warp's row
+            fs.acc = 0.0f;
+            fs.row_acc = 0.0f;
+            fs.col_base = -1;  // a row starting at a window start
+            if (fs.e > fs.s) return true;
+            if (lane == 0) a.y[fs.r] = 0;  // empty row
+        }
+    };
+    // leading empty rows of this warp
+    if (fs.e == fs.s) {
+        if (lane == 0) a.y[fs.r] = 0;
+        if (!next_row()) return;
+    }
+
+    auto window = [&](uint32_t W) -> bool {  // false: the walk is over
+        const uint32_t relA0 = (W + 8u * lane - g.ebase) & g.emask;
+        const Slot A = lds_slot<kBits>(g, relA0);
+        const Slot B = lds_slot<kBits>(g, (relA0 + kStepElts) & g.emask);
+        D dA, dB;
+        if constexpr (kBits == 8) {
+            dA = decode8(A.d, A.d2);
+            dB = decode8(B.d, B.d2);
+        } else {
+            dA = decode<kBits>(A.d);
+            dB = decode<kBits>(B.d);
+        }
+        const uint32_t pk = (dA.local - kBias) | ((dB.local - kBias) << 16);
+        const uint32_t incl = warp_incl_scan_p(pk);
+        const uint32_t tot = __reduce_add_sync(kFull, pk);
+        const uint32_t lane_bias = kBias * (uint32_t)lane, tot_bias = kBias * kWarp;
+        const uint32_t totA = (tot & 0xFFFFu) + tot_bias, totAB = totA + (tot >> 16) + tot_bias;
+        const int relA = (int)((incl & 0xFFFFu) - (dA.local - kBias) + lane_bias);
+        const int relB = (int)totA + (int)((incl >> 16) - (dB.local - kBias) + lane_bias);
+        if (fs.e > W + 2u * kStepElts) {  // the whole window lies inside the current row
+            fs.acc = lane_step<kXMode, false>(fs.acc, A.v, dA, fs.col_base + relA, xs_addr, a.xtex, 0xFFu);
+            fs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(fs.acc, B.v, dB, fs.col_base + relB, xs_addr,
+                                                                     a.xtex, 0xFFu);
+            fs.col_base += (int)totAB;
+            if (((W + 2u * kStepElts) & (kUnitElts - 1u)) == 0) unit_end(W / kUnitElts);
+            return true;
+        }
+        // boundary window: row segments one after the other
+        for (;;) {
+            int base;
+            if (fs.s < W) {
+                base = fs.col_base;
+            } else if (fs.s == W) {
+                base = -1;
+            } else {  // the row starts inside the window: base = -1 - P(s - 1)
+                const uint32_t x = fs.s - 1u - W, m = x & 7u, L = (x >> 3) & 31u;
+                const uint32_t mine = (x < kStepElts) ? (uint32_t)relA + incl_at(dA, m) : (uint32_t)relB + incl_at(dB, m);
+                base = -1 - (int)__shfl_sync(kFull, mine, (int)L);
+            }
+            const uint32_t lo = max(fs.s, W), hi = min(fs.e, W + 2u * kStepElts);
+            const uint32_t eb = W + 8u * lane;
+            const uint32_t vmA = (0xFFu >> (8 - min(max((int)(hi - eb), 0), 8))) & (0xFFu << min(max((int)(lo - eb), 0), 8)) & 0xFFu;
+            const uint32_t ebB = eb + kStepElts;
+            const uint32_t vmB = (0xFFu >> (8 - min(max((int)(hi - ebB), 0), 8))) & (0xFFu << min(max((int)(lo - ebB), 0), 8)) & 0xFFu;
+            if (lo < W + kStepElts)
+                fs.acc = lane_step<kXMode, true>(fs.acc, mask_values(A.v, vmA), dA, base + relA, xs_addr, a.xtex, vmA);
+            if (hi > W + kStepElts)
+                fs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(fs.acc, mask_values(B.v, vmB), dB, base + relB,
+                                                                        xs_addr, a.xtex, vmB);
+            if (fs.e <= W + 2u * kStepElts) {  // the row ends in this window
+                unit_end((fs.e - 1u) / kUnitElts);
+                finish_row();
+                if (!next_row()) return false;
+                if (fs.s >= W + 2u * kStepElts) return true;  // next row starts at the next window
+                continue;
+            }
+            fs.col_base = base + (int)totAB;  // the row continues past the window
+            if (((W + 2u * kStepElts) & (kUnitElts - 1u)) == 0) unit_end(W / kUnitElts);
+            return true;
+        }
+    };
+
+    // Fixed ring schedule: chunk k of the warp's range lives in slot k mod ring (phase k / ring);
+    // consuming chunk k first refills the slot of chunk k - 1 with chunk k - 1 + ring.
+    const uint32_t rshift = a.ring == 4u ? 2u : 1u;
+    for (uint32_t cs = E0; cs < E1; cs += kChunk) {
+        const uint32_t k = (cs - E0) / kChunk;
+        if (k) {
+            __syncwarp();
+            g.iss = cs + (a.ring - 1u) * kChunk;
+            if (g.iss < E1) ring_issue<kBits>(g, a, lane);
+        }
+        mbar_wait(g.bar0 + 8u * (k & (a.ring - 1u)), (k >> rshift) & 1u);
+        if (!window(cs)) return;
+        if (cs + 2u * kStepElts < E1 && !window(cs + 2u * kStepElts)) return;
+    }
+    // the warp's range ends inside the current row (a split row)
+    if (fs.e > E1) finish_row();
+}
+
+template <int kXMode, int kBits>
+__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv_flat(const SpmvArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
+    const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const PlanRecord pr = load_record(a, w);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    if (!a.pdl) stage_x<kXMode, false>(a, xs);
+    Ring g;
+    const bool has_work = pr.q0.x != 0;
+    if (has_work)
+        ring_begin<kBits, true>(a, pr.q0.w, pr.q1.x, warp, lane, smem_base,
+                                static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pdl) stage_x<kXMode, false>(a, xs);
+    __syncthreads();
+    if (!has_work) return;
+    run_flat<kXMode, kBits>(a, pr, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g);
+}
+
 template <int kXMode, int kBits>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -692,7 +917,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar) {
 // Persistent chain of dependent SpMVs (decoder stacks): op k+1 reads op k's y.  Each warp sets up
 // op k+1 (plan record, first ring fills) as soon as its part of op k is done — BEFORE the grid
 // barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
-template <int kXMode>
+template <int kXMode, int kOrder>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     macko_chain_b4(const SpmvArgs* __restrict__ ops, uint32_t n_ops, uint32_t* bar) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -722,7 +947,17 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     Ring g;
     g.wslot = 0;
     g.wphase = 0;
-    bool has_work = op_begin<4, false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
+    PlanRecord pr = load_record(args[0], w);
+    auto begin = [&](const SpmvArgs& an) -> bool {
+        if constexpr (kOrder == 1) {
+            if (pr.q0.x == 0) return false;
+            ring_begin<4, false>(an, pr.q0.w, pr.q1.x, warp, lane, smem_base, bar0, g);
+            return true;
+        } else {
+            return op_begin<4, false>(an, pr, warp, lane, smem_base, bar0, g, rs);
+        }
+    };
+    bool has_work = begin(args[0]);
     for (uint32_t k = 0; k < n_ops; ++k) {
         const SpmvArgs& a = args[k & 1];
         MK_CTRACE(k, 0);
@@ -745,17 +980,19 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
 
 // Column just before the first unit of every chunk that starts inside a row:
 // sum of the row's deltas over [row start, unit start) minus one.  Setup only.
-__global__ void plan_colbase_kernel(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks) {
+// order 0 (ROMA): lim = the row's 8-aligned start + j units; order 1 (flat): lim = E0, the warp's
+// first element (-1 for rows starting at or after it).
+__global__ void plan_colbase_kernel(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
+                                    uint32_t n_chunks) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
     if (w >= n_chunks) return;
-    const uint32_t j = warps[w].j;
-    if (warps[w].units_left == 0 || j == 0) {
+    const uint32_t s = warps[w].s;
+    const uint32_t lim = order ? warps[w].e0 : (s & ~7u) + warps[w].j * kUnitElts;
+    if (warps[w].units_left == 0 || (order ? s >= lim : warps[w].j == 0)) {
         if (lane == 0) warps[w].colbase = -1;
         return;
     }
-    const uint32_t s = warps[w].s;
-    const uint32_t lim = (s & ~7u) + j * kUnitElts;
     const uint32_t per = 8u / bits, mask = bits == 8 ? 0xFFu : (1u << bits) - 1u;
     uint32_t sum = 0;
     for (uint32_t i = s + lane; i < lim; i += kWarp) sum += ((deltas[i / per] >> ((i % per) * bits)) & mask) + 1u;
@@ -771,12 +1008,18 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     const int threads = kSpmvWarpsPerCta * kWarp;
     cudaError_t e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(macko_spmv_flat<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
+    int flat = 0;
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&flat, macko_spmv_flat<kXMode, kBits>, threads, smem);
+    if (e == cudaSuccess) *ctas_per_sm = std::min(*ctas_per_sm, flat);
     return e;
 }
 
 template <int kXMode, int kBits>
-static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl) {
+static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl, int order) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kSpmvWarpsPerCta * kWarp);
@@ -787,6 +1030,7 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    if (order == 1) return cudaLaunchKernelEx(&cfg, macko_spmv_flat<kXMode, kBits>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 
@@ -819,20 +1063,21 @@ static cudaError_t occ_bits(int x_mode, size_t smem, int* c) {
 }
 
 template <int kBits>
-static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
+static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
+                               int order) {
     switch (x_mode) {
-        case 10: return launch_one<10, kBits>(a, grid, smem, s, pdl);
-        case 8: return launch_one<8, kBits>(a, grid, smem, s, pdl);
-        case 7: return launch_one<7, kBits>(a, grid, smem, s, pdl);
-        case 6: return launch_one<6, kBits>(a, grid, smem, s, pdl);
-        case 1: return launch_one<1, kBits>(a, grid, smem, s, pdl);
-        case 0: return launch_one<0, kBits>(a, grid, smem, s, pdl);
+        case 10: return launch_one<10, kBits>(a, grid, smem, s, pdl, order);
+        case 8: return launch_one<8, kBits>(a, grid, smem, s, pdl, order);
+        case 7: return launch_one<7, kBits>(a, grid, smem, s, pdl, order);
+        case 6: return launch_one<6, kBits>(a, grid, smem, s, pdl, order);
+        case 1: return launch_one<1, kBits>(a, grid, smem, s, pdl, order);
+        case 0: return launch_one<0, kBits>(a, grid, smem, s, pdl, order);
         default: break;
     }
     if constexpr (kBits == 4) {
         switch (x_mode) {
-            case 11: return launch_one<11, 4>(a, grid, smem, s, pdl);
-            case 9: return launch_one<9, 4>(a, grid, smem, s, pdl);
+            case 11: return launch_one<11, 4>(a, grid, smem, s, pdl, order);
+            case 9: return launch_one<9, 4>(a, grid, smem, s, pdl, order);
             default: break;
         }
     }
@@ -849,19 +1094,20 @@ cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm) 
     }
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
+                        int order) {
     switch (bits) {
-        case 4: return launch_bits<4>(a, grid, x_mode, smem, s, pdl);
-        case 2: return launch_bits<2>(a, grid, x_mode, smem, s, pdl);
-        case 8: return launch_bits<8>(a, grid, x_mode, smem, s, pdl);
-        case 1: return launch_bits<1>(a, grid, x_mode, smem, s, pdl);
+        case 4: return launch_bits<4>(a, grid, x_mode, smem, s, pdl, order);
+        case 2: return launch_bits<2>(a, grid, x_mode, smem, s, pdl, order);
+        case 8: return launch_bits<8>(a, grid, x_mode, smem, s, pdl, order);
+        case 1: return launch_bits<1>(a, grid, x_mode, smem, s, pdl, order);
         default: return cudaErrorInvalidValue;
     }
 }
 
-template <int kXMode>
+template <int kXMode, int kOrder>
 static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode, kOrder>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -873,20 +1119,26 @@ static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode>, ops, n, bar);
+    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode, kOrder>, ops, n, bar);
 }
 
 cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s) {
+                         cudaStream_t s, int order) {
+#define MK_CHAIN(M)                                                                                       \
+    case M:                                                                                               \
+        return order == 1 ? chain_one<M, 1>(d_ops, n_ops, d_bar, grid, smem, s)                           \
+                          : chain_one<M, 0>(d_ops, n_ops, d_bar, grid, smem, s);
     switch (x_mode) {
-        case 9: return chain_one<9>(d_ops, n_ops, d_bar, grid, smem, s);
-        case 8: return chain_one<8>(d_ops, n_ops, d_bar, grid, smem, s);
-        case 7: return chain_one<7>(d_ops, n_ops, d_bar, grid, smem, s);
-        case 6: return chain_one<6>(d_ops, n_ops, d_bar, grid, smem, s);
-        case 1: return chain_one<1>(d_ops, n_ops, d_bar, grid, smem, s);
-        case 0: return chain_one<0>(d_ops, n_ops, d_bar, grid, smem, s);
+        MK_CHAIN(10)
+        MK_CHAIN(9)
+        MK_CHAIN(8)
+        MK_CHAIN(7)
+        MK_CHAIN(6)
+        MK_CHAIN(1)
+        MK_CHAIN(0)
         default: return cudaErrorInvalidValue;
     }
+#undef MK_CHAIN
 }
 
 #ifdef MACKO_TRACE
@@ -896,11 +1148,11 @@ cudaError_t trace_read(unsigned long long* host, size_t n) {
 }
 #endif
 
-cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks,
-                                cudaStream_t s) {
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
+                                uint32_t n_chunks, cudaStream_t s) {
     const int threads = 256;
     const int blocks = (int)((n_chunks * (uint64_t)kWarp + threads - 1) / threads);
-    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, bits, warps, n_chunks);
+    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, bits, order, warps, n_chunks);
     return cudaGetLastError();
 }
 

@@ -37,6 +37,7 @@ struct SpmvArgs {
     uint16_t* y;
     cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode 0, 6..9)
     uint64_t value_elems, delta_bytes;  // allocated sizes (payload + one zeroed chunk of slack)
+    uint32_t value_count;               // pad_nnz (the flat walk's last warp owns trailing empty rows)
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
@@ -70,14 +71,16 @@ bool spmv_valid_x_mode(int x_mode);
 cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
 #endif
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
-cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
+// order: 0 = ROMA row-relative walk (macko_spmv), 1 = flat global windows (macko_spmv_flat)
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
+                        int order);
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
 bool spmv_valid_config(int x_mode, int bits);
 // Persistent chain of dependent SpMVs (d_ops: device array of n_ops SpmvArgs; d_bar: 2 zeroed u32
 // for the grid barrier).  Cooperative launch of `grid` CTAs; all ops share x_mode, ring and smem.
 cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s);
-cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks,
-                                cudaStream_t s);
+                         cudaStream_t s, int order);
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
+                                uint32_t n_chunks, cudaStream_t s);
 
 }  // namespace mk

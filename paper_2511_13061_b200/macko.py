@@ -143,6 +143,14 @@ class DeviceMatrix:
         CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""
         check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
 
+    def set_order(self, order: int, stream=None) -> None:
+        """SpMV walk: 1 flat global windows (default), 0 ROMA row-relative."""
+        check(_lib.load().macko_dev_set_order(self._h, order, _stream_ptr(stream)))
+
+    @property
+    def order(self) -> int:
+        return self.launch_info().order
+
     # -- operations -------------------------------------------------------------------------
     def download(self, stream=None) -> MackoMatrix:
         i = self.info

@@ -11,7 +11,7 @@ import torch
 from oracle import oracle as O
 from paper_2511_13061_b200 import decoder_chain as D
 from paper_2511_13061_b200 import macko as M
-from tests.helpers import UNIT_STEPS, to_host_u16
+from tests.helpers import b200_y, to_host_u16
 
 pytestmark = pytest.mark.gpu
 
@@ -30,15 +30,16 @@ def test_chain_matches_oracle(cuda):
     ch.forward_token(pdl=False)
     torch.cuda.synchronize()
     H, I = shape.hidden, shape.inter
+    order = ch.mats[0]["qkv"].order
     for layer in range(shape.layers):
         ws = {}
         for name in D.LINEARS:
             R, C = shape.shape(name)
             ws[name] = O.encode_dense(O.gen_dense(R, C, 0.5, D.weight_seed(seed, layer, name)))
-        qkv = O.b200_order_spmv(ws["qkv"], h, UNIT_STEPS)
-        o = O.b200_order_spmv(ws["o"], qkv[:H], UNIT_STEPS)  # v = first H rows of [W_v; W_q; W_k]
-        gu = O.b200_order_spmv(ws["gate_up"], o, UNIT_STEPS)
-        h = O.b200_order_spmv(ws["down"], gu[:I], UNIT_STEPS)  # up = first I rows of [W_up; W_gate]
+        qkv = b200_y(order, ws["qkv"], h)
+        o = b200_y(order, ws["o"], qkv[:H])  # v = first H rows of [W_v; W_q; W_k]
+        gu = b200_y(order, ws["gate_up"], o)
+        h = b200_y(order, ws["down"], gu[:I])  # up = first I rows of [W_up; W_gate]
     assert np.isfinite(h.view(np.float16).astype(np.float32)).all()
     assert np.array_equal(to_host_u16(ch.acts["h"]), h)
     ch.close()

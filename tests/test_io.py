@@ -10,7 +10,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_2511_13061_b200 import macko as M
-from tests.helpers import UNIT_STEPS, to_dev, to_host_u16
+from tests.helpers import b200_y, to_dev, to_host_u16
 
 
 def _host(c) -> M.MackoMatrix:
@@ -143,6 +143,6 @@ def test_device_write_read_spmv(cuda, tmp_path):
         x = O.gen_vector(C, 42)
         y = M.spmv(dm2, to_dev(x))
         torch.cuda.synchronize()
-        assert np.array_equal(to_host_u16(y), O.b200_order_spmv(m, x, UNIT_STEPS))
+        assert np.array_equal(to_host_u16(y), b200_y(dm2, m, x))
         dm.close()
         dm2.close()

@@ -5,7 +5,7 @@ import torch
 
 from oracle import oracle as O
 from paper_2511_13061_b200.linear import MackoLinear
-from tests.helpers import UNIT_STEPS, to_dev, to_host_u16
+from tests.helpers import b200_y, to_dev, to_host_u16
 
 pytestmark = pytest.mark.gpu
 
@@ -22,7 +22,7 @@ def test_macko_linear_matches_oracle(cuda):
     xd = to_dev(x)
     y = ml(xd)
     torch.cuda.synchronize()
-    y_ref = O.b200_order_spmv(O.encode_dense(A), x, UNIT_STEPS)
+    y_ref = b200_y(ml.matrix, O.encode_dense(A), x)
     expect = (torch.from_numpy(y_ref.view(np.float16)).to(cuda) + lin.bias).view(torch.int16)
     assert np.array_equal(to_host_u16(y), expect.cpu().numpy().view(np.uint16))
     # [1, 1, in] and a batch of 3 (one SpMV per vector)
