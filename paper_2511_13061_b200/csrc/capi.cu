@@ -135,7 +135,7 @@ struct macko_dev_matrix {
 
 struct macko_chain {
     int device = 0;
-    int grid = 0, x_mode = 0, order = 0;
+    int grid = 0, x_mode = 0;
     size_t smem = 0;
     uint32_t n_ops = 0;
     DevBuf<uint8_t> ops;     // n_ops mk::SpmvArgs
@@ -1083,7 +1083,6 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
         c->device = dev;
         c->n_ops = n_ops;
         c->grid = mats[0]->grid;
-        c->order = mats[0]->order;
         // one x_mode for all ops (a template parameter): the op with the most bytes decides
         uint64_t best = 0;
         size_t xtab = 0;
@@ -1092,8 +1091,9 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
             if (!m || !xs[k] || !ys[k]) fail(MACKO_EINVAL, "null matrix or vector in the chain");
             if (m->device != dev) fail(MACKO_EINVAL, "chain ops must live on one device");
             if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
-            if (m->grid != c->grid || m->ring != mats[0]->ring || m->order != mats[0]->order)
-                fail(MACKO_EINVAL, "chain ops must share the launch plan geometry and order");
+            if (m->grid != c->grid || m->ring != mats[0]->ring)
+                fail(MACKO_EINVAL, "chain ops must share the launch plan geometry");
+            if (m->order != 0) fail(MACKO_EINVAL, "the persistent chain runs the ROMA walk (order 0) only");
             const uint64_t tb = values_bytes(m->pad_nnz) + delta_bytes(m->pad_nnz, 4);
             if (tb >= best) {
                 best = tb;
@@ -1162,7 +1162,7 @@ macko_status macko_chain_run(macko_chain* c, void* stream) {
         if (!c) fail(MACKO_EINVAL, "null chain");
         DeviceGuard g(c->device);
         ck(mk::launch_chain(reinterpret_cast<const mk::SpmvArgs*>(c->ops.p), c->n_ops, c->bar.p, c->grid, c->x_mode,
-                            c->smem, (cudaStream_t)stream, c->order),
+                            c->smem, (cudaStream_t)stream),
            "macko_chain launch");
         g_launches.fetch_add(1);
     });

@@ -316,26 +316,25 @@ struct Ring {
     uint32_t wslot, wphase;
 };
 
-// Copy the chunk starting at element g.iss into its slot (lane 0; full-size, never clamped).
+// Copy the chunk starting at element g.iss into its slot (one elected lane; full-size, never
+// clamped).  Called by the whole warp with warp-uniform operands: elect.sync inside the asm keeps
+// the copies to one lane without a divergent branch around them.
 template <int kBits>
 __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int lane) {
-    if (lane == 0) {
-        const uint32_t e0 = g.iss;
-        const uint32_t rel = (e0 - g.ebase) & g.emask;
-        const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
-        // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
-        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "n"(kChunkVBytes + dbytes<kBits>())
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         g.vbase + 2u * rel),
-                     "l"(a.values + e0), "n"(kChunkVBytes), "r"(bar)
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         g.dbase + rel * kBits / 8u),
-                     "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "n"(dbytes<kBits>()), "r"(bar)
-                     : "memory");
-    }
+    const uint32_t e0 = g.iss;
+    const uint32_t rel = (e0 - g.ebase) & g.emask;
+    const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
+    // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it.
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %5;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %6, [%4];\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %7, [%4];\n\t}" ::"r"(
+            g.vbase + 2u * rel),
+        "l"(a.values + e0), "r"(g.dbase + (rel / 8u) * kBits), "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(bar),
+        "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
+        : "memory");
 }
 
 // The walk is at S: every chunk wholly below S was consumed by all lanes (their LDS results fed
@@ -374,7 +373,7 @@ __device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
                  : "r"(g.vbase + 2u * rel));
-    const uint32_t da = g.dbase + rel * kBits / 8u;
+    const uint32_t da = g.dbase + (rel / 8u) * kBits;
     sl.d2 = 0;
     if constexpr (kBits == 8) {
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(sl.d), "=r"(sl.d2) : "r"(da));
@@ -881,8 +880,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     if (a.pdl) stage_x<kXMode, false>(a, xs);
     __syncthreads();
     MK_TRACE(4);
-    if (!has_work) return;
-    run_rows<kXMode, kBits>(a, w, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g, rs);
+    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+    if (has_work) run_rows<kXMode, kBits>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
 }
 
@@ -917,7 +916,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar) {
 // Persistent chain of dependent SpMVs (decoder stacks): op k+1 reads op k's y.  Each warp sets up
 // op k+1 (plan record, first ring fills) as soon as its part of op k is done — BEFORE the grid
 // barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
-template <int kXMode, int kOrder>
+template <int kXMode>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     macko_chain_b4(const SpmvArgs* __restrict__ ops, uint32_t n_ops, uint32_t* bar) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -947,17 +946,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     Ring g;
     g.wslot = 0;
     g.wphase = 0;
-    PlanRecord pr = load_record(args[0], w);
-    auto begin = [&](const SpmvArgs& an) -> bool {
-        if constexpr (kOrder == 1) {
-            if (pr.q0.x == 0) return false;
-            ring_begin<4, false>(an, pr.q0.w, pr.q1.x, warp, lane, smem_base, bar0, g);
-            return true;
-        } else {
-            return op_begin<4, false>(an, pr, warp, lane, smem_base, bar0, g, rs);
-        }
-    };
-    bool has_work = begin(args[0]);
+    bool has_work = op_begin<4, false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
     for (uint32_t k = 0; k < n_ops; ++k) {
         const SpmvArgs& a = args[k & 1];
         MK_CTRACE(k, 0);
@@ -1105,9 +1094,9 @@ cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_
     }
 }
 
-template <int kXMode, int kOrder>
+template <int kXMode>
 static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode, kOrder>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -1119,15 +1108,14 @@ static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode, kOrder>, ops, n, bar);
+    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode>, ops, n, bar);
 }
 
 cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s, int order) {
-#define MK_CHAIN(M)                                                                                       \
-    case M:                                                                                               \
-        return order == 1 ? chain_one<M, 1>(d_ops, n_ops, d_bar, grid, smem, s)                           \
-                          : chain_one<M, 0>(d_ops, n_ops, d_bar, grid, smem, s);
+                         cudaStream_t s) {
+#define MK_CHAIN(M) \
+    case M:         \
+        return chain_one<M>(d_ops, n_ops, d_bar, grid, smem, s);
     switch (x_mode) {
         MK_CHAIN(10)
         MK_CHAIN(9)

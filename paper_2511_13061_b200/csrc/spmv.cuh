@@ -79,7 +79,7 @@ bool spmv_valid_config(int x_mode, int bits);
 // Persistent chain of dependent SpMVs (d_ops: device array of n_ops SpmvArgs; d_bar: 2 zeroed u32
 // for the grid barrier).  Cooperative launch of `grid` CTAs; all ops share x_mode, ring and smem.
 cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s, int order);
+                         cudaStream_t s);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
                                 uint32_t n_chunks, cudaStream_t s);
 

@@ -101,3 +101,12 @@ def test_persistent_chain_bit_identical(cuda):
             torch.cuda.synchronize()
             assert np.array_equal(to_host_u16(ch.acts["h"]), refs[tok]["h"]), ("graph", shape, tok)
         ch.close()
+
+
+def test_persistent_chain_rejects_flat_walk(cuda):
+    # the cooperative chain kernel runs the ROMA walk only; a flat-walk matrix is refused
+    ch = D.SparseDecoderChain(D.ChainShape(layers=1, hidden=256, inter=688), density=0.5, seed=3)
+    ch.mats[0]["o"].set_order(1)
+    with pytest.raises(ValueError):
+        ch.persistent()
+    ch.close()

@@ -1,23 +1,25 @@
 // Microbenchmark: can x gathers be split between the LSU data pipe (LDS from a shared-memory
 // table) and the TEX pipe (tex1Dfetch from an L1-resident texture) so that the two run in
 // parallel?  1 CTA/SM x 16 warps.  Each warp-gather mimics the SpMV's lane-consecutive pattern:
-// lane l reads column base + 16 l + r (r random in [0,16)), i.e. a 1 KiB window of fp16.
+// lane l reads column base + S l + r (r random in [0,S)), S = argv[1] (16: a 1 KiB window of fp16,
+// the lane-consecutive SpMV at d = 0.5; 4: the pair-interleaved mapping).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int kIters = 4096;
 constexpr int kTable = 8192;  // fp16 entries (16 KiB)
 
-__device__ __forceinline__ uint32_t col_of(uint32_t& h, int lane) {
+__device__ __forceinline__ uint32_t col_of(uint32_t& h, int lane, uint32_t stride) {
     h = h * 1664525u + 1013904223u;
     const uint32_t base = (h >> 8) & (kTable - 1);  // varies per step (warp-uniform-ish: same seed)
-    return (base + 16u * lane + ((h >> 24) & 15u)) & (kTable - 1);
+    return (base + stride * lane + ((h >> 24) & (stride - 1u))) & (kTable - 1);
 }
 
 // mode: 0 all LDS, 1 all TEX, 2 half LDS + half TEX, 3 half LDS only, 4 half TEX only, 5 all LDG(L1)
 __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, const uint16_t* __restrict__ g, float* out,
-                                             int mode) {
+                                             int mode, uint32_t stride) {
     __shared__ uint16_t xs[kTable];
     for (int i = threadIdx.x; i < kTable; i += blockDim.x) xs[i] = (uint16_t)(i * 7);
     __syncthreads();
@@ -34,18 +36,19 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, const uint1
     if (mode == 5) ldg = true;
     if (lds) {
 #pragma unroll 8
-        for (int i = 0; i < kIters; ++i) acc += xs[col_of(hl, lane)];
+        for (int i = 0; i < kIters; ++i) acc += xs[col_of(hl, lane, stride)];
     } else if (tx) {
 #pragma unroll 8
-        for (int i = 0; i < kIters; ++i) acc += tex1Dfetch<unsigned short>(tex, (int)col_of(hl, lane));
+        for (int i = 0; i < kIters; ++i) acc += tex1Dfetch<unsigned short>(tex, (int)col_of(hl, lane, stride));
     } else if (ldg) {
 #pragma unroll 8
-        for (int i = 0; i < kIters; ++i) acc += __ldg(g + col_of(hl, lane));
+        for (int i = 0; i < kIters; ++i) acc += __ldg(g + col_of(hl, lane, stride));
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const uint32_t stride = argc > 1 ? (uint32_t)atoi(argv[1]) : 16u;  // lane column stride (power of 2)
     int sms = 0, clk_khz = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
@@ -69,9 +72,9 @@ int main() {
     const char* names[] = {"16w LDS", "16w TEX", "8 LDS + 8 TEX", "8w LDS only", "8w TEX only", "16w LDG"};
     const double gw[] = {16, 16, 16, 8, 8, 16};
     for (int mode = 0; mode < 6; ++mode) {
-        k<<<sms, 512>>>(tex, g, out, mode);
+        k<<<sms, 512>>>(tex, g, out, mode, stride);
         cudaEventRecord(a);
-        for (int r = 0; r < 5; ++r) k<<<sms, 512>>>(tex, g, out, mode);
+        for (int r = 0; r < 5; ++r) k<<<sms, 512>>>(tex, g, out, mode, stride);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
