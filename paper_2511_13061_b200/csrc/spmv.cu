@@ -162,8 +162,9 @@ __device__ __forceinline__ Dec8 decode8(uint32_t w0, uint32_t w1) {
 }
 
 // 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.  Masked
-// steps (row edges): element m gathers only if bit m of vm is set, else it multiplies x = +0
-// (its value is already +0), so nothing outside the row reaches the sum, not even 0 * inf.
+// steps (row edges): element m gathers and accumulates only if bit m of vm is set (predicated
+// gather and FHFMA), so nothing outside the row reaches the sum, not even 0 * inf.  Skipping
+// equals adding +0 here: a lane sum that starts at +0 never becomes -0.
 template <int kXMode, bool kMasked, uint32_t kTex = tex_slots<kXMode>(), class D>
 __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& dc, int cb, uint32_t xs_addr,
                                            cudaTextureObject_t xt, uint32_t vm) {
@@ -183,13 +184,10 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
             b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
             b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
         }
-        uint16_t x0 = 0, x1 = 0;
         if (!kMasked || ((vm >> (2 * m)) & 1u))
-            x0 = ((kTex >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0);
+            acc = fma_f16f16f32(v0, ((kTex >> (2 * m)) & 1u) ? xtex(xt, cb + (int)b0) : lds_u16(base + 2u * b0), acc);
         if (!kMasked || ((vm >> (2 * m + 1)) & 1u))
-            x1 = ((kTex >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1);
-        acc = fma_f16f16f32(v0, x0, acc);
-        acc = fma_f16f16f32(v1, x1, acc);
+            acc = fma_f16f16f32(v1, ((kTex >> (2 * m + 1)) & 1u) ? xtex(xt, cb + (int)b1) : lds_u16(base + 2u * b1), acc);
     }
     return acc;
 }
@@ -387,41 +385,21 @@ __device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
     return sl;
 }
 
-// Keep only the lane's elements inside [s, e) (eb = the lane's first element): the others get
-// codeword 0 (delta 1) and value +0, and their columns fall on zero guards / out-of-range texels,
-// so they add exactly +0 (also when the masked values or x hold inf / NaN).
+// Valid-element mask of a lane's elements [eb, eb + 8) for the row [s, e).  The ROMA head (the
+// previous row's elements before s: lane 0 of the row's first step, klo <= 7) also gets codeword
+// 0 (delta 1) so the scan stays exact — the row's column base is shifted by the ROMA offset.
+// Elements past e need no codeword change (prefixes run forward); values are never touched:
+// masked elements skip their gather and FHFMA (lane_step).
 template <int kBits>
 __device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s, uint32_t e) {
-    const int klo = min(max((int)(s - eb), 0), 8);
+    const int klo = min(max((int)(s - eb), 0), 7);
     const int khi = min(max((int)(e - eb), klo), 8);
     const uint32_t vm = (0xFFu >> (8 - khi)) & (0xFFu << klo) & 0xFFu;  // valid-element mask
-    if constexpr (kBits == 4) {
-        const uint32_t nm = (uint32_t)(((1ull << (4 * khi)) - 1ull) & ~((1ull << (4 * klo)) - 1ull));
-        sl.d &= nm;
-        // value masks: 16-bit halves replicate the msb of their element's nibble (PRMT sign mode)
-        const uint32_t lo = nm << 4;
-        sl.v.x &= prmt(lo, nm, 0xCC88u);
-        sl.v.y &= prmt(lo, nm, 0xDD99u);
-        sl.v.z &= prmt(lo, nm, 0xEEAAu);
-        sl.v.w &= prmt(lo, nm, 0xFFBBu);
+    if constexpr (kBits == 8) {
+        sl.d &= klo >= 4 ? 0u : ~0u << (8 * klo);
+        sl.d2 &= ~0u << (8 * max(klo - 4, 0));
     } else {
-        if constexpr (kBits == 8) {
-            sl.d &= ((vm & 0x0Fu) * 0x204081u & 0x01010101u) * 0xFFu;
-            sl.d2 &= ((vm >> 4) * 0x204081u & 0x01010101u) * 0xFFu;
-        } else if constexpr (kBits == 2) {
-            uint32_t c = vm;  // bit k -> crumb k
-            c = (c | (c << 4)) & 0x0F0Fu;
-            c = (c | (c << 2)) & 0x3333u;
-            c = (c | (c << 1)) & 0x5555u;
-            sl.d &= c * 3u;
-        } else {
-            sl.d &= vm;
-        }
-        auto hm = [&](int k) { return ((vm >> k) & 1u) ? 0xFFFFu : 0u; };
-        sl.v.x &= hm(0) | (hm(1) << 16);
-        sl.v.y &= hm(2) | (hm(3) << 16);
-        sl.v.z &= hm(4) | (hm(5) << 16);
-        sl.v.w &= hm(6) | (hm(7) << 16);
+        sl.d &= ~0u << (kBits * klo);
     }
     return vm;
 }
@@ -543,7 +521,6 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
 template <int kXMode, int kBits>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr, Ring& g,
                                          RowState& rs) {
-    const uint32_t C = a.cols;
     if (rs.T == 0) {
         if (lane == 0) a.y[rs.r] = 0;
         if (!next_piece(rs, a, w, lane)) return;
@@ -589,20 +566,10 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - (dA.local - bias) + lane_bias);
         const int cbB = rs.col_base + (int)((tot & 0xFFFFu) + tot_bias) + (int)((incl >> 16) - (dB.local - bias) + lane_bias);
         if constexpr (kMasked) {
-            // Only the step holding the row end (step T-1) predicates its gathers: its masked
-            // elements decode to columns right after the row's last one.  Leading ROMA elements
-            // decode to -7..-1 and a phantom step is pointed at column C: both read zero guards
-            // (or out-of-range texels) with value +0.
-            if (t + 1u == rs.T) {
-                rs.acc = lane_step<kXMode, true>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, (int)C, xs_addr, a.xtex, vmB);
-            } else if (t + 2u == rs.T) {
-                rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
-            } else {
-                rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-                rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
-            }
+            // Edge pair (the row's first and last): both steps predicated by their valid-element
+            // masks; a phantom second step (the row ends in step A) has vmB = 0.
+            rs.acc = lane_step<kXMode, true>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+            rs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
         } else {
             rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
             rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
@@ -658,15 +625,6 @@ __device__ __forceinline__ uint32_t incl_at(const D& d, uint32_t m) {
     } else {
         return __byte_perm((m & 1u) ? d.odd : d.even, 0u, 0x4440u + (m >> 1));
     }
-}
-
-__device__ __forceinline__ uint4 mask_values(uint4 v, uint32_t vm) {
-    auto hm = [&](int k) { return ((vm >> k) & 1u) ? 0xFFFFu : 0u; };
-    v.x &= hm(0) | (hm(1) << 16);
-    v.y &= hm(2) | (hm(3) << 16);
-    v.z &= hm(4) | (hm(5) << 16);
-    v.w &= hm(6) | (hm(7) << 16);
-    return v;
 }
 
 // Finish a row cut between warps (flat plan): the first piece stores its sum at the slot of its
@@ -792,9 +750,9 @@ __device__ __forceinline__ void run_flat(const SpmvArgs& a, const PlanRecord& pr
             const uint32_t ebB = eb + kStepElts;
             const uint32_t vmB = (0xFFu >> (8 - min(max((int)(hi - ebB), 0), 8))) & (0xFFu << min(max((int)(lo - ebB), 0), 8)) & 0xFFu;
             if (lo < W + kStepElts)
-                fs.acc = lane_step<kXMode, true>(fs.acc, mask_values(A.v, vmA), dA, base + relA, xs_addr, a.xtex, vmA);
+                fs.acc = lane_step<kXMode, true>(fs.acc, A.v, dA, base + relA, xs_addr, a.xtex, vmA);
             if (hi > W + kStepElts)
-                fs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(fs.acc, mask_values(B.v, vmB), dB, base + relB,
+                fs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(fs.acc, B.v, dB, base + relB,
                                                                         xs_addr, a.xtex, vmB);
             if (fs.e <= W + 2u * kStepElts) {  // the row ends in this window
                 unit_end((fs.e - 1u) / kUnitElts);
