@@ -322,13 +322,15 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int
     const uint32_t e0 = g.iss;
     const uint32_t rel = (e0 - g.ebase) & g.emask;
     const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
-    // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it.
+    // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it.  The matrix is
+    // streamed once per SpMV: L2 evict_first keeps x, the plan records and the code resident.
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p;\n\t.reg .b64 pol;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
         "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %5;\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %6, [%4];\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %7, [%4];\n\t}" ::"r"(
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %6, [%4], pol;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %7, [%4], pol;\n\t}" ::"r"(
             g.vbase + 2u * rel),
         "l"(a.values + e0), "r"(g.dbase + (rel / 8u) * kBits), "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(bar),
         "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
@@ -455,12 +457,14 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
                              "r"(n * (kChunkVBytes + dbytes<kBits>()))
                              : "memory");
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}" ::"r"(
                         g.vbase),
                     "l"(a.values + e0), "r"(n * kChunkVBytes), "r"(g.bar0)
                     : "memory");
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}" ::"r"(
                         g.dbase),
                     "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(n * dbytes<kBits>()), "r"(g.bar0)
                     : "memory");
