@@ -83,7 +83,9 @@ macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uin
                                 uint32_t* row_ptrs, void* stream);
 
 /* y = A*x on the device: fp16 in, fp32 accumulate, one RNE per row, fp16 out.
- * Replaces reference_spmv / warp_spmv.  d_x: cols fp16, d_y: rows fp16. */
+ * Replaces reference_spmv / warp_spmv.  d_x: cols fp16, d_y: rows fp16.
+ * SpMVs of one matrix must be stream-ordered: the handle holds the arrival counters of rows
+ * split between warps (reset by each launch).  Different matrices may run concurrently. */
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y,
                             void* stream);
 
