@@ -192,12 +192,6 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
     return acc;
 }
 
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
-
 // ------------------------------------------------------------------------------------------
 // Compute-side row state
 // ------------------------------------------------------------------------------------------

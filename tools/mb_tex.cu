@@ -11,10 +11,13 @@
 constexpr int kIters = 4096;
 constexpr int kTable = 8192;  // fp16 entries (16 KiB)
 
+__device__ uint32_t g_lanerand = 0;  // 1: the in-lane offset r is random per lane (the SpMV's
+                                     // pattern); 0: warp-uniform r (a pathological bank pattern)
 __device__ __forceinline__ uint32_t col_of(uint32_t& h, int lane, uint32_t stride) {
     h = h * 1664525u + 1013904223u;
-    const uint32_t base = (h >> 8) & (kTable - 1);  // varies per step (warp-uniform-ish: same seed)
-    return (base + stride * lane + ((h >> 24) & (stride - 1u))) & (kTable - 1);
+    const uint32_t base = (h >> 8) & (kTable - 1);  // varies per step (warp-uniform)
+    const uint32_t hl = g_lanerand ? h ^ (uint32_t)(lane * 0x9E3779B9u) : h;
+    return (base + stride * lane + ((hl >> 24) & (stride - 1u))) & (kTable - 1);
 }
 
 // mode: 0 all LDS, 1 all TEX, 2 half LDS + half TEX, 3 half LDS only, 4 half TEX only, 5 all LDG(L1)
@@ -49,6 +52,8 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, const uint1
 
 int main(int argc, char** argv) {
     const uint32_t stride = argc > 1 ? (uint32_t)atoi(argv[1]) : 16u;  // lane column stride (power of 2)
+    const uint32_t lanerand = argc > 2 ? (uint32_t)atoi(argv[2]) : 1u;
+    cudaMemcpyToSymbol(g_lanerand, &lanerand, 4);
     int sms = 0, clk_khz = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
