@@ -26,20 +26,28 @@ namespace {
 constexpr int kCompressWarpsPerCta = 8;
 constexpr int kStageWords = 72;  // 256 entries x 8 bits = 64 words, + carry + spill
 
-// Loads the 8 columns [c, c+8) of a dense row (zeros past `cols`) and returns their nonzero
-// mask; `h` receives the raw fp16 bits.
-__device__ __forceinline__ uint32_t load8(const uint16_t* row, uint32_t c, uint32_t cols, bool vec_ok, uint16_t h[8]) {
-    if (vec_ok && c + 8 <= cols) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + c));
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+// The 8 columns [c, c+8) of a dense row (zeros past `cols`) as four fp16 pairs.  Loops issue
+// the next chunk's fetch before working on the current one (one 16-byte load per lane in flight
+// under the classification).
+__device__ __forceinline__ uint4 fetch8(const uint16_t* row, uint32_t c, uint32_t cols, bool vec_ok) {
+    if (vec_ok && c + 8 <= cols) return __ldg(reinterpret_cast<const uint4*>(row + c));
+    uint32_t w[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            h[2 * m] = (uint16_t)(w[m] & 0xFFFFu);
-            h[2 * m + 1] = (uint16_t)(w[m] >> 16);
-        }
-    } else {
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t lo = (c + 2 * m < cols) ? row[c + 2 * m] : 0u;
+        const uint32_t hi = (c + 2 * m + 1 < cols) ? row[c + 2 * m + 1] : 0u;
+        w[m] = lo | (hi << 16);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Nonzero mask of 8 fetched columns (+-0 are zero); `h` receives the raw fp16 bits.
+__device__ __forceinline__ uint32_t unpack8(const uint4 q, uint16_t h[8]) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) h[k] = (c + k < cols) ? row[c + k] : (uint16_t)0;
+    for (int m = 0; m < 4; ++m) {
+        h[2 * m] = (uint16_t)(w[m] & 0xFFFFu);
+        h[2 * m + 1] = (uint16_t)(w[m] >> 16);
     }
     uint32_t nz = 0;
 #pragma unroll
@@ -47,21 +55,30 @@ __device__ __forceinline__ uint32_t load8(const uint16_t* row, uint32_t c, uint3
     return nz;
 }
 
-// Exclusive max-scan of "last nonzero column" over lanes, seeded with `carry`; returns the
-// previous nonzero column before this lane's first column and updates carry to the warp max.
+// Previous nonzero column before this lane's first column (-1: none in the row so far), seeded
+// with `carry` (the last nonzero column of the earlier chunks); carry becomes the chunk's last.
+// One ballot finds the nearest lower lane holding a nonzero, one shuffle fetches its column.
 __device__ __forceinline__ int prev_nonzero(int lane_last, int lane, int& carry) {
-    int incl = lane_last;
-#pragma unroll
-    for (int off = 1; off < kWarp; off <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, off);
-        if (lane >= off) incl = max(incl, t);
-    }
-    int excl = __shfl_up_sync(kFull, incl, 1);
-    excl = lane == 0 ? carry : max(excl, carry);
-    carry = max(carry, __shfl_sync(kFull, incl, kWarp - 1));
-    return excl;
+    const uint32_t bal = __ballot_sync(kFull, lane_last >= 0);
+    const uint32_t below = bal & ((1u << lane) - 1u);
+    const int from = __shfl_sync(kFull, lane_last, below ? 31 - __clz(below) : lane);
+    const int p = below ? from : carry;
+    const int last = __shfl_sync(kFull, lane_last, bal ? 31 - __clz(bal) : 0);
+    if (bal) carry = last;
+    return p;
 }
 
+// b_delta >= 4 (max delta >= 16 > 8 columns of a lane): a lane holds at most one padding entry,
+// at the first column cc0 >= c with cc0 = p (mod 2^b), cc0 > p, before the lane's first nonzero
+// (and before the row's last nonzero L); the nonzeros after the lane's first are never padded.
+__device__ __forceinline__ uint32_t pad_bit(uint32_t nz, int c, int p, int L, uint32_t bits) {
+    const int maxd = 1 << bits;
+    const int cc0 = p + maxd * ((c - p + maxd - 1) >> bits);  // smallest p + k*maxd >= c (c > p)
+    const int lim = min(nz ? c + __ffs(nz) - 1 : c + 8, L);
+    return cc0 < lim ? 1u << (cc0 - c) : 0u;
+}
+
+template <bool kFast>
 __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
     count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
                uint32_t* counts, int32_t* lastcol) {
@@ -72,19 +89,27 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
         const uint16_t* row = dense + (uint64_t)r * ld;
         int carry = -1;
         uint32_t cnt = 0;
+        uint4 next = fetch8(row, 8u * lane, cols, vec_base);
         for (uint32_t c0 = 0; c0 < cols; c0 += kWarp * 8) {
             const uint32_t c = c0 + 8u * lane;
+            const uint4 cur = next;
+            if (c0 + kWarp * 8 < cols) next = fetch8(row, c + kWarp * 8, cols, vec_base);
             uint16_t h[8];
-            uint32_t nz = load8(row, c, cols, vec_base, h);
+            uint32_t nz = unpack8(cur, h);
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
             int p = prev_nonzero(lane_last, lane, carry);
             cnt += __popc(nz);
-            while (nz) {
-                const int k = __ffs(nz) - 1;
-                nz &= nz - 1;
-                const int cc = (int)c + k;
-                cnt += (uint32_t)(cc - p - 1) >> bits;
-                p = cc;
+            if constexpr (kFast) {
+                // pads of the gap before the lane's first nonzero (the others are < 2^b apart)
+                if (nz) cnt += (uint32_t)((int)c + __ffs(nz) - 2 - p) >> bits;
+            } else {
+                while (nz) {
+                    const int k = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const int cc = (int)c + k;
+                    cnt += (uint32_t)(cc - p - 1) >> bits;
+                    p = cc;
+                }
             }
         }
 #pragma unroll
@@ -132,11 +157,30 @@ __global__ void __launch_bounds__(1024) scan_counts(const uint32_t* counts, uint
     if (t == nt - 1) *total = run;
 }
 
+template <bool kFast>
 __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
     emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
               const uint32_t* row_ptrs, const int32_t* lastcol, uint16_t* values, uint32_t* delta_words) {
     __shared__ uint32_t stage_all[kCompressWarpsPerCta][kStageWords];
+    // kFast: codes of the nonzeros after a lane's first one, per 8-column nonzero pattern (their
+    // deltas are the gaps between set bits, < 8), packed at b_delta bits each
+    __shared__ uint64_t gap_codes[kFast ? 256 : 1];
     const int lane = threadIdx.x & (kWarp - 1);
+    if constexpr (kFast) {
+        for (uint32_t pat = threadIdx.x; pat < 256; pat += blockDim.x) {
+            uint64_t v = 0;
+            uint32_t i = 0, rest = pat;
+            int prev = -1;
+            while (rest) {
+                const int k = __ffs(rest) - 1;
+                rest &= rest - 1;
+                if (prev >= 0) v |= (uint64_t)(uint32_t)(k - prev - 1) << (bits * i++);
+                prev = k;
+            }
+            gap_codes[pat] = v;
+        }
+        __syncthreads();
+    }
     uint32_t* stage = stage_all[threadIdx.x >> 5];
     const uint32_t nwarps = gridDim.x * kCompressWarpsPerCta;
     const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
@@ -153,33 +197,48 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
         int carry = -1;
         uint32_t emitted = 0;                // entries of this row written so far
         uint64_t wb = row_first_word;        // global word held in stage[0]
+        uint4 next = fetch8(row, 8u * lane, cols, vec_base);
         for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kWarp * 8) {
             const uint32_t c = c0 + 8u * lane;
+            const uint4 cur = next;
+            if (c0 + kWarp * 8 < cols && (int)(c0 + kWarp * 8) <= L) next = fetch8(row, c + kWarp * 8, cols, vec_base);
             uint16_t h[8];
-            const uint32_t nz = load8(row, c, cols, vec_base, h);
+            const uint32_t nz = unpack8(cur, h);
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
             int p = prev_nonzero(lane_last, lane, carry);
-            // classify the lane's 8 columns: nonzero entry, padding entry or nothing
-            uint32_t em = 0;       // entry mask
-            uint32_t code[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int cc = (int)c + k;
-                code[k] = 0;
-                if ((nz >> k) & 1u) {
-                    code[k] = (uint32_t)(cc - p - 1) & (maxd - 1);  // delta - 1
-                    em |= 1u << k;
-                    p = cc;
-                } else if (cc < L && cc > p && (((uint32_t)(cc - p)) & (maxd - 1)) == 0) {
-                    code[k] = maxd - 1;
-                    em |= 1u << k;
+            // classify the lane's 8 columns: nonzero entry, padding entry or nothing; codes of the
+            // lane's entries packed in column order (entry i at bits [i*b, (i+1)*b))
+            uint32_t em = 0;  // entry mask
+            uint64_t codes = 0;
+            if constexpr (kFast) {
+                const uint32_t pb = pad_bit(nz, (int)c, p, L, bits);
+                em = nz | pb;
+                const uint32_t sh = pb ? bits : 0u;  // the pad entry comes first
+                codes = pb ? (uint64_t)(maxd - 1) : 0ull;
+                if (nz) {
+                    const uint32_t first = (uint32_t)((int)c + __ffs(nz) - 2 - p) & (maxd - 1);
+                    codes |= ((uint64_t)first << sh) | (gap_codes[nz] << (sh + bits));
                 }
+            } else {
+                uint32_t code[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int cc = (int)c + k;
+                    code[k] = 0;
+                    if ((nz >> k) & 1u) {
+                        code[k] = (uint32_t)(cc - p - 1) & (maxd - 1);  // delta - 1
+                        em |= 1u << k;
+                        p = cc;
+                    } else if (cc < L && cc > p && (((uint32_t)(cc - p)) & (maxd - 1)) == 0) {
+                        code[k] = maxd - 1;
+                        em |= 1u << k;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if ((em >> k) & 1u) codes |= (uint64_t)code[k] << (__popc(em & ((1u << k) - 1u)) * bits);
             }
             const uint32_t n = __popc(em);
-            uint64_t codes = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((em >> k) & 1u) codes |= (uint64_t)code[k] << (__popc(em & ((1u << k) - 1u)) * bits);
             // lane offsets of the entries
             uint32_t incl = n;
 #pragma unroll
@@ -236,7 +295,12 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
 cudaError_t launch_count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
                               uint32_t* counts, int32_t* lastcol, int sms, cudaStream_t s) {
     const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
-    if (grid > 0) count_rows<<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+    if (grid > 0) {
+        if (bits >= 4)
+            count_rows<true><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+        else
+            count_rows<false><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+    }
     return cudaGetLastError();
 }
 
@@ -250,9 +314,14 @@ cudaError_t launch_emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, 
                              const uint32_t* row_ptrs, const int32_t* lastcol, uint16_t* values, uint32_t* delta_words,
                              int sms, cudaStream_t s) {
     const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
-    if (grid > 0)
-        emit_rows<<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values,
-                                                                delta_words);
+    if (grid > 0) {
+        if (bits >= 4)
+            emit_rows<true><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol,
+                                                                          values, delta_words);
+        else
+            emit_rows<false><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol,
+                                                                           values, delta_words);
+    }
     return cudaGetLastError();
 }
 
