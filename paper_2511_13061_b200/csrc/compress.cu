@@ -248,9 +248,18 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
             }
             const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
             const uint64_t o = (uint64_t)start + emitted + (incl - n);
+            {
+                // predicated stores (no branch per column): entry k goes to the lane's base + rank
+                uint16_t* vp = values + o;
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((em >> k) & 1u) values[o + __popc(em & ((1u << k) - 1u))] = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;
+                for (int k = 0; k < 8; ++k) {
+                    const uint16_t val = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;  // pads are +0
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u16 [%0], %1;\n\t}" ::"l"(
+                                     vp + __popc(em & ((1u << k) - 1u))),
+                                 "h"(val), "r"(em & (1u << k))
+                                 : "memory");
+                }
+            }
             if (n) {
                 const uint64_t bit0 = o * bits;
                 const uint32_t sh = (uint32_t)(bit0 & 31u);
@@ -278,7 +287,7 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
             // move the partial word (and anything after it, all zero) to the front
             const uint32_t partial = (end_bit & 31u) ? stage[ncomplete] : 0u;
             __syncwarp();
-            for (int i = lane; i < kStageWords; i += kWarp) stage[i] = 0;
+            for (int i = lane; i <= ncomplete; i += kWarp) stage[i] = 0;  // beyond: still zero
             __syncwarp();
             if (lane == 0) stage[0] = partial;
             __syncwarp();
