@@ -53,10 +53,16 @@ struct SpmvArgs {
 // 8 % slower on 36864x12288 and no faster on the decode chain; one 32-warp CTA is the default.
 constexpr int kSpmvWarpsPerCta = MACKO_WARPS_PER_CTA;
 constexpr int kSpmvCtasPerSm = 32 / kSpmvWarpsPerCta;
-constexpr uint32_t kChunk = 1024;             // elements per TMA chunk (two step pairs)
+#ifndef MACKO_CHUNK
+#define MACKO_CHUNK 1024
+#endif
+constexpr uint32_t kChunk = MACKO_CHUNK;      // elements per TMA chunk (two step pairs)
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
 constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas (b_delta = 4; kChunk * b / 8 in general)
-constexpr uint32_t kMaxRing = 4;
+#ifndef MACKO_MAX_RING
+#define MACKO_MAX_RING 4
+#endif
+constexpr uint32_t kMaxRing = MACKO_MAX_RING;
 // fp16 x table in shared memory with zero guards: kXGuardLo entries before x[0] (the ROMA-masked
 // elements of a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (a phantom
 // step past the row end is pointed at column C, its elements land on C+1..C+8).
