@@ -14,7 +14,27 @@ from typing import Optional
 import torch
 from torch import nn
 
+from . import _lib
 from . import macko as M
+
+
+@torch.library.custom_op("macko::spmv", mutates_args=())
+def spmv_op(handle: int, x: torch.Tensor, rows: int) -> torch.Tensor:
+    """y = A x as a registered torch operator (torch.ops.macko.spmv): `handle` is a live
+    DeviceMatrix's C-ABI handle, x a contiguous fp16 CUDA vector.  Launches on the current stream
+    (CUDA-graph capturable); no CPU implementation exists."""
+    if not x.is_cuda or x.dtype != torch.float16 or x.dim() != 1:
+        raise ValueError("macko::spmv takes a 1-D fp16 CUDA tensor")
+    x = x.contiguous()
+    y = torch.empty(rows, dtype=torch.float16, device=x.device)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    _lib.check(_lib.load().macko_dev_spmv(handle, x.data_ptr(), y.data_ptr(), stream))
+    return y
+
+
+@spmv_op.register_fake
+def _spmv_fake(handle: int, x: torch.Tensor, rows: int) -> torch.Tensor:
+    return x.new_empty(rows)
 
 
 class MackoLinear(nn.Module):
@@ -43,12 +63,10 @@ class MackoLinear(nn.Module):
             raise ValueError(f"expected last dimension {self.in_features}, got {x.shape[-1]}")
         lead = x.shape[:-1]
         xs = x.reshape(-1, self.in_features).to(torch.float16).contiguous()
-        out = torch.empty((xs.shape[0], self.out_features), dtype=torch.float16, device=x.device)
-        stream = torch.cuda.current_stream(x.device)
-        for i in range(xs.shape[0]):
-            self.matrix.spmv_into(xs[i], out[i], stream)
+        h = self.matrix.handle
+        out = torch.stack([torch.ops.macko.spmv(h, xs[i], self.out_features) for i in range(xs.shape[0])])
         if self.bias is not None:
-            out += self.bias
+            out = out + self.bias
         return out.reshape(*lead, self.out_features)
 
     def extra_repr(self) -> str:

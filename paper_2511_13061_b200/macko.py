@@ -84,6 +84,13 @@ class DeviceMatrix:
         check(_lib.load().macko_dev_get_info(self._h, C.byref(info)))
         self.info = info
 
+    @property
+    def handle(self) -> int:
+        """The C-ABI handle (torch.ops.macko.spmv, foreign bindings); valid until close()."""
+        if not getattr(self, "_h", None) or not self._h.value:
+            raise ValueError("matrix is closed")
+        return self._h.value
+
     # -- construction -----------------------------------------------------------------------
     @classmethod
     def upload(cls, m: MackoMatrix, device: int = 0, stream=None) -> "DeviceMatrix":
