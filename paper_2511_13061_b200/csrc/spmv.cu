@@ -1,34 +1,37 @@
-// spmv.cu — MACKO SpMV for sm_100a (b_delta = 4, fp16 values, fp32 accumulation).
+// spmv.cu — MACKO SpMV for sm_100a (b_delta 1/2/4/8, fp16 values, fp32 accumulation).
 //
 // Realises the paper's warp kernel (SPEC.md:255-264 warp_spmv) natively:
 //   * one warp walks a row in steps of 256 elements, lane l owning elements 8l..8l+7 of the
 //     step;
 //   * ROMA: the row start is aligned down to 8 elements; elements outside
 //     the row (before its start in the first step, past its end in the last) are masked;
-//   * column reconstruction: the 8 nibbles are widened to bytes, paired and prefix-summed with
+//   * column reconstruction: the codewords are widened to bytes, paired and prefix-summed with
 //     one integer multiply (byte-SIMD), then Algorithm 1's shfl_up scan gives the lane offset
 //     and the warp total advances the running column.  Two steps share one
 //     scan (their lane sums packed into 16-bit halves); the total comes from REDUX;
 //   * every element's x value is gathered and multiply-added with FHFMA (fp16 x fp16 -> fp32
 //     accumulate, exact product).
-// B200 specifics (profiles/r01_pipes.md): the kernel is bound by on-chip data pipes, not HBM.
+// B200 specifics (profiles/r01_pipes.md, r01_experiments.md): the kernel is bound by the L1TEX
+// data pipes and the latency of each warp's pair chain, not by HBM.
 //   * The matrix stream arrives by TMA: every warp owns a contiguous element range (static
 //     equal-weight plan of 2048-element units, built once per matrix) and keeps a ring of
-//     1024-element chunks in flight with cp.async.bulk + mbarrier (no LSU wavefronts); values
-//     and deltas are read back with one LDS.128 + one LDS.32 per lane step.
+//     1024-element chunks in flight with cp.async.bulk + mbarrier (no LSU wavefronts; issued by
+//     one elect.sync lane, L2 evict_first); values and codewords are read back with one LDS.128
+//     + one LDS per lane step.
 //   * x gathers are split between two pipes that run in parallel: an fp16 copy of x in shared
 //     memory (LDS, LSU pipe) and x as a 1-D texture (TEX pipe, L1-resident); which of a lane's
 //     8 element slots use the texture is a compile-time mask (x_mode).
-//   * Row edges run the interior code with cheap masks: elements outside the row get codeword 0
-//     (delta 1, so the scan stays exact) and value +0, and they gather x = +0 (zero guards /
-//     out-of-range texels, or a predicated-off gather in the step holding the row end), so
-//     nothing outside the row reaches the sum, not even 0 * inf.
+//   * Row edges (a row's first and last step pair) run the interior code with predication: the
+//     ROMA head gets codeword 0 (delta 1, so the scan stays exact), and every element outside
+//     the row skips its gather and FHFMA, so nothing outside the row reaches the sum, not even
+//     0 * inf.
 //   * One persistent CTA of 32 warps per SM.  Rows cut between warps are finished by the
 //     last-arriving warp, which adds the per-unit partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
 // lanes once per unit (8 steps; the row's last unit absorbs a shorter remainder), sequential
 // over units — mirrored bit-exactly by oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  It
 // depends on a row's elements and on its start offset mod 8 (ROMA), never on the plan.
+// The flat walk (order 1, macko_spmv_flat) is the alternative order of oracle mo_b200_flat_spmv.
 #include "common.cuh"
 #include "spmv.cuh"
 
