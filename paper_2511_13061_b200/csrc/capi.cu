@@ -138,7 +138,7 @@ struct macko_chain {
     int grid = 0, x_mode = 0;
     size_t smem = 0;
     uint32_t n_ops = 0;
-    DevBuf<uint8_t> ops;     // n_ops mk::SpmvArgs
+    std::vector<mk::SpmvArgs> ops;  // n_ops arguments (passed as kernel parameters)
     DevBuf<uint32_t> bar;    // grid barrier {count, generation}
     std::vector<cudaTextureObject_t> tex;
     ~macko_chain() {
@@ -270,9 +270,9 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
     // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
-    // the mbarriers and the chain kernel's argument buffers)
+    // the mbarriers)
     const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
-    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 2 * sizeof(mk::SpmvArgs) - 64;
+    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 64;
     const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunk * m->b_delta / 8);
     auto x_bytes = [&](int mode) -> size_t {
         return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
@@ -1109,7 +1109,7 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
         int per_sm = 0;
         ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem attribute");
         if (c->smem > std::min<size_t>((size_t)optin, (size_t)per_sm / mk::kSpmvCtasPerSm - 1024) -
-                          mk::kSpmvWarpsPerCta * mk::kMaxRing * 8 - 2 * sizeof(mk::SpmvArgs) - 64)
+                          mk::kSpmvWarpsPerCta * mk::kMaxRing * 8 - 64)
             fail(MACKO_EINVAL, "chain x table + rings exceed shared memory");
         int align = 0;
         ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev), "texture alignment");
@@ -1149,9 +1149,8 @@ macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint1
                 a.xtex = t;
             }
         }
-        c->ops.alloc(n_ops * sizeof(mk::SpmvArgs));
+        c->ops = ops;
         c->bar.alloc(2);
-        ck(cudaMemcpy(c->ops.p, ops.data(), n_ops * sizeof(mk::SpmvArgs), cudaMemcpyHostToDevice), "chain upload");
         ck(cudaMemset(c->bar.p, 0, 8), "chain barrier");
         *out = hold.release();
     });
@@ -1161,7 +1160,7 @@ macko_status macko_chain_run(macko_chain* c, void* stream) {
     return guarded([&] {
         if (!c) fail(MACKO_EINVAL, "null chain");
         DeviceGuard g(c->device);
-        ck(mk::launch_chain(reinterpret_cast<const mk::SpmvArgs*>(c->ops.p), c->n_ops, c->bar.p, c->grid, c->x_mode,
+        ck(mk::launch_chain(c->ops.data(), c->n_ops, c->bar.p, c->grid, c->x_mode,
                             c->smem, (cudaStream_t)stream),
            "macko_chain launch");
         g_launches.fetch_add(1);

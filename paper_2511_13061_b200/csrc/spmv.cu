@@ -877,12 +877,11 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar) {
 // barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
 template <int kXMode>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
-    macko_chain_b4(const SpmvArgs* __restrict__ ops, uint32_t n_ops, uint32_t* bar) {
+    macko_chain_b4(const __grid_constant__ ChainOps P, uint32_t n_ops, uint32_t* bar) {
+    // The ops' arguments live in the kernel's parameter space (constant bank): uniform loads
+    // through the constant cache, no shared-memory reads in the walk.
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
-    __shared__ __align__(16) SpmvArgs args[2];  // op k and op k+1 (double buffer)
-    constexpr uint32_t kArgWords = sizeof(SpmvArgs) / 4;
-    static_assert(sizeof(SpmvArgs) % 4 == 0 && kArgWords <= 64, "SpmvArgs is copied word by word");
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
@@ -890,12 +889,6 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    auto load_args = [&](uint32_t k) {  // whole CTA; caller synchronises
-        if (threadIdx.x < kArgWords)
-            reinterpret_cast<uint32_t*>(&args[k & 1])[threadIdx.x] = __ldg(reinterpret_cast<const uint32_t*>(ops + k) + threadIdx.x);
-    };
-    load_args(0);
-    if (n_ops > 1) load_args(1);
     if (lane == 0) {
         for (uint32_t i = 0; i < kMaxRing; ++i) mbar_init(bar0 + 8u * i);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -905,9 +898,9 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
     Ring g;
     g.wslot = 0;
     g.wphase = 0;
-    bool has_work = op_begin<4, false>(args[0], load_record(args[0], w), warp, lane, smem_base, bar0, g, rs);
+    bool has_work = op_begin<4, false>(P.op[0], load_record(P.op[0], w), warp, lane, smem_base, bar0, g, rs);
     for (uint32_t k = 0; k < n_ops; ++k) {
-        const SpmvArgs& a = args[k & 1];
+        const SpmvArgs& a = P.op[k];
         MK_CTRACE(k, 0);
         if (k) grid_barrier(bar);  // op k-1's y (this op's x) is complete everywhere
         MK_CTRACE(k, 1);
@@ -917,12 +910,11 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
         if (has_work) run_rows<kXMode, 4>(a, w, lane, xs_addr, g, rs);
         MK_CTRACE(k, 3);
         if (k + 1 < n_ops) {
-            const SpmvArgs& an = args[(k + 1) & 1];
+            const SpmvArgs& an = P.op[k + 1];
             has_work = op_begin<4, false>(an, load_record(an, w), warp, lane, smem_base, bar0, g, rs);
         }
         MK_CTRACE(k, 4);
-        __syncthreads();  // every warp is done with op k's x table and arguments
-        if (k + 2 < n_ops) load_args(k + 2);  // into op k's slot (visible after the next barrier)
+        __syncthreads();  // every warp is done with op k's x table
     }
 }
 
@@ -1054,7 +1046,7 @@ cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_
 }
 
 template <int kXMode>
-static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
+static cudaError_t chain_one(const ChainOps& ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
@@ -1070,22 +1062,32 @@ static cudaError_t chain_one(const SpmvArgs* ops, uint32_t n, uint32_t* bar, int
     return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode>, ops, n, bar);
 }
 
-cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
+cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
                          cudaStream_t s) {
-#define MK_CHAIN(M) \
-    case M:         \
-        return chain_one<M>(d_ops, n_ops, d_bar, grid, smem, s);
-    switch (x_mode) {
-        MK_CHAIN(10)
-        MK_CHAIN(9)
-        MK_CHAIN(8)
-        MK_CHAIN(7)
-        MK_CHAIN(6)
-        MK_CHAIN(1)
-        MK_CHAIN(0)
-        default: return cudaErrorInvalidValue;
-    }
+    // one cooperative launch per kChainOpsPerLaunch ops (the arguments travel as kernel parameters)
+    static thread_local ChainOps ops;
+    for (uint32_t k0 = 0; k0 < n_ops; k0 += kChainOpsPerLaunch) {
+        const uint32_t n = n_ops - k0 < kChainOpsPerLaunch ? n_ops - k0 : kChainOpsPerLaunch;
+        for (uint32_t k = 0; k < n; ++k) ops.op[k] = h_ops[k0 + k];
+        cudaError_t e = cudaErrorInvalidValue;
+#define MK_CHAIN(M)                                           \
+    case M:                                                   \
+        e = chain_one<M>(ops, n, d_bar, grid, smem, s);       \
+        break;
+        switch (x_mode) {
+            MK_CHAIN(10)
+            MK_CHAIN(9)
+            MK_CHAIN(8)
+            MK_CHAIN(7)
+            MK_CHAIN(6)
+            MK_CHAIN(1)
+            MK_CHAIN(0)
+            default: break;
+        }
 #undef MK_CHAIN
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 #ifdef MACKO_TRACE

@@ -82,9 +82,14 @@ cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_
                         int order);
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
 bool spmv_valid_config(int x_mode, int bits);
-// Persistent chain of dependent SpMVs (d_ops: device array of n_ops SpmvArgs; d_bar: 2 zeroed u32
-// for the grid barrier).  Cooperative launch of `grid` CTAs; all ops share x_mode, ring and smem.
-cudaError_t launch_chain(const SpmvArgs* d_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
+// Persistent chain of dependent SpMVs (h_ops: host array of n_ops SpmvArgs, passed to the kernel
+// as parameters, kChainOpsPerLaunch per cooperative launch; d_bar: 2 zeroed u32 for the grid
+// barrier).  `grid` CTAs; all ops share x_mode, ring and smem.
+constexpr uint32_t kChainOpsPerLaunch = 32000 / sizeof(SpmvArgs);  // kernel parameters <= 32764 B
+struct ChainOps {
+    SpmvArgs op[kChainOpsPerLaunch];
+};
+cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
                          cudaStream_t s);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
                                 uint32_t n_chunks, cudaStream_t s);
