@@ -884,11 +884,34 @@ macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t*
             m->hx_aligned = reinterpret_cast<uint16_t*>((p + a - 1) / a * a);
         }
         if (!m->hy.p) m->hy.alloc(m->rows);
-        // Plain stream order (a cached CUDA graph of the three steps measured 11 us slower).
-        ck(cudaMemcpyAsync(m->hx_aligned, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
-        const macko_status sp = macko_dev_spmv(m, m->hx_aligned, m->hy.p, st);
+        // Pinned host buffers are device-mapped (UVA): x is pulled and y pushed by small kernels
+        // chained to the SpMV with programmatic dependent launch, so the SpMV prologue overlaps
+        // the x transfer.  Pageable buffers take cudaMemcpyAsync.  (A cached CUDA graph of the
+        // memcpy variant measured 11 us slower.)
+        auto mapped = [](const void* p) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+                cudaGetLastError();
+                return (const void*)nullptr;
+            }
+            return at.type == cudaMemoryTypeHost ? (const void*)at.devicePointer : (const void*)nullptr;
+        };
+        const uint16_t* dx = static_cast<const uint16_t*>(mapped(h_x));
+        uint16_t* dy = const_cast<uint16_t*>(static_cast<const uint16_t*>(mapped(h_y)));
+        if (dx) {
+            ck(mk::launch_copy_u16(dx, m->hx_aligned, (uint32_t)m->cols, 1, false, st), "x pull");
+            g_launches.fetch_add(1);
+        } else {
+            ck(cudaMemcpyAsync(m->hx_aligned, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
+        }
+        const macko_status sp = macko_dev_spmv_ex(m, m->hx_aligned, m->hy.p, st, dx ? MACKO_SPMV_PDL : 0u);
         if (sp != MACKO_OK) fail(sp, g_err);
-        ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
+        if (dy) {
+            ck(mk::launch_copy_u16(m->hy.p, dy, (uint32_t)m->rows, 8, true, st), "y push");
+            g_launches.fetch_add(1);
+        } else {
+            ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
+        }
         ck(cudaStreamSynchronize(st), "sync");
     });
 }

@@ -974,6 +974,34 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 
+// Host-buffer SpMV (macko_spmv_host) with pinned, device-mapped host x / y: a one-CTA kernel pulls
+// x over the host link into the device buffer, the SpMV follows as its programmatic dependent (its
+// plan load and first matrix fills overlap the pull), and a second small kernel pushes y to the
+// host buffer as the SpMV's dependent.  n16: 16-byte vectors; the remainder moves as 2-byte words.
+__global__ void __launch_bounds__(1024) copy_u16_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                                         uint32_t n, uint32_t wait_producer) {
+    if (wait_producer) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t n16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) ? 0u : n / 8u;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = tid; i < n16; i += nt)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (uint32_t i = n16 * 8u + tid; i < n; i += nt) dst[i] = src[i];
+}
+
+cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int blocks, bool dependent, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = dependent ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, copy_u16_kernel, src, dst, n, dependent ? 1u : 0u);
+}
+
 // b_delta = 4 (the paper's format) gets every x_mode; the other widths the automatic ones.
 bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 11); }
 bool spmv_valid_config(int x_mode, int bits) {

@@ -91,6 +91,9 @@ struct ChainOps {
 };
 cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
                          cudaStream_t s);
+// n fp16 words src -> dst (device or device-mapped host pointers); dependent: launched as the
+// programmatic dependent of the previous kernel on the stream (waits for it before copying).
+cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int blocks, bool dependent, cudaStream_t s);
 cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
                                 uint32_t n_chunks, cudaStream_t s);
 

@@ -249,9 +249,20 @@ def test_spmv_host_buffers_e2e(cuda):
     A = O.gen_dense(777, 3333, 0.5, 10)
     x = O.gen_vector(3333, 11)
     dm = gpu_encode(A)
-    y_host = dm.spmv_host(x)
+    y_host = dm.spmv_host(x)  # pageable numpy buffers: cudaMemcpyAsync both ways
     assert np.array_equal(y_host, gpu_spmv(dm, x))
     assert np.array_equal(y_host, b200_y(dm, O.encode_dense(A), x))
+    # pinned (device-mapped) buffers: x pulled / y pushed by kernels chained with PDL; odd offsets
+    # exercise the 2-byte path of the copies
+    for off in (0, 1):
+        hx = torch.empty(3333 + off, dtype=torch.int16, pin_memory=True)
+        hy = torch.zeros(777 + off, dtype=torch.int16, pin_memory=True)
+        hxn, hyn = hx.numpy().view(np.uint16)[off:], hy.numpy().view(np.uint16)[off:]
+        hxn[:] = x
+        for _ in range(3):
+            hyn[:] = 0
+            dm.spmv_host(hxn, hyn)
+            assert np.array_equal(hyn, y_host), off
 
 
 def test_row_slabs_and_grid_independence(cuda):
