@@ -433,3 +433,43 @@ def test_large_offsets_beyond_2_30(cuda):
         assert np.array_equal(_codes(h.packed_deltas, e0, e1 - e0), _codes(m.deltas, 0, e1 - e0))
         dms.close()
     dm.close()
+
+
+def _random_values(rng, n):
+    # nonzero fp16 in (-1, 1), like the generator (long rows must not overflow fp16 sums)
+    u = rng.integers(1, 1 << 16, n)
+    u[u == 1 << 15] += 1
+    return ((u - 32768) / 32768.0).astype(np.float16).view(np.uint16)
+
+
+def test_rows_split_across_many_warps(cuda):
+    # three ~1M-element rows: every row is cut into hundreds of warp pieces, finished by the last
+    # arriving warp from per-unit partials; both walks, float and integer values
+    R, C = 3, 2_000_000
+    for int_mode in (False, True):
+        A = O.gen_dense(R, C, 0.5, 515, int_mode)
+        A[1, : C // 3] = 0  # a row starting far from column 0
+        x = O.gen_vector(C, 516, int_mode)
+        m = O.encode_dense(A)
+        dm = gpu_encode(A)
+        assert dm.launch_info().n_split_rows >= 3
+        for order in (0, 1):
+            dm.set_order(order)
+            check_y(A, m, x, gpu_spmv(dm, x), int_mode, ("split", int_mode, order), order)
+
+
+def test_power_law_row_lengths(cuda):
+    # Zipf-like row lengths (a few dense rows, a long tail of short and empty rows) in random order
+    rng = np.random.default_rng(77)
+    R, C = 6000, 8192
+    p = np.minimum(1.0, 3.0 / (np.arange(R) + 1.0) ** 0.8)
+    rng.shuffle(p)
+    mask = rng.random((R, C)) < p[:, None]
+    A = np.zeros((R, C), np.uint16)
+    A[mask] = _random_values(rng, int(mask.sum()))
+    x = O.gen_vector(C, 78)
+    m = O.encode_dense(A)
+    dm = gpu_encode(A)
+    for order in (0, 1):
+        dm.set_order(order)
+        check_y(A, m, x, gpu_spmv(dm, x), False, ("zipf", order), order)
