@@ -89,11 +89,14 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
         const uint16_t* row = dense + (uint64_t)r * ld;
         int carry = -1;
         uint32_t cnt = 0;
+        // two chunks in flight per warp (64 KiB per SM at full occupancy covers the HBM latency)
         uint4 next = fetch8(row, 8u * lane, cols, vec_base);
+        uint4 next2 = kWarp * 8 < cols ? fetch8(row, 8u * lane + kWarp * 8, cols, vec_base) : make_uint4(0, 0, 0, 0);
         for (uint32_t c0 = 0; c0 < cols; c0 += kWarp * 8) {
             const uint32_t c = c0 + 8u * lane;
             const uint4 cur = next;
-            if (c0 + kWarp * 8 < cols) next = fetch8(row, c + kWarp * 8, cols, vec_base);
+            next = next2;
+            if (c0 + 2 * kWarp * 8 < cols) next2 = fetch8(row, c + 2 * kWarp * 8, cols, vec_base);
             uint16_t h[8];
             uint32_t nz = unpack8(cur, h);
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
