@@ -151,7 +151,7 @@ class DeviceMatrix:
         check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
 
     def set_order(self, order: int, stream=None) -> None:
-        """SpMV walk: 1 flat global windows (default), 0 ROMA row-relative."""
+        """SpMV walk: 0 ROMA row-relative (default), 1 flat global windows."""
         check(_lib.load().macko_dev_set_order(self._h, order, _stream_ptr(stream)))
 
     @property
