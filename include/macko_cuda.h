@@ -34,7 +34,7 @@ typedef enum macko_status {
     MACKO_EIO = 3,         /* macko::IoError (errors.hpp:14-16) */
     MACKO_EINFEASIBLE = 4, /* macko::InfeasibleError (errors.hpp:19-21) */
     MACKO_ECUDA = 5,       /* CUDA runtime failure (no reference counterpart) */
-    MACKO_ENCCL = 6,       /* reserved for collective failures */
+    MACKO_ENCCL = 6,       /* NCCL failure (macko_sharded_spmv; no reference counterpart) */
     MACKO_ENOMEM = 7       /* device allocation failure */
 } macko_status;
 
@@ -157,6 +157,14 @@ macko_status macko_gen_vector(int device, uint16_t* d_out, uint64_t n, uint64_t 
 /* ---- row sharding (contiguous equal-row slabs) ---- */
 macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, uint64_t* r0,
                               uint64_t* r1);
+
+/* One row-sharded SpMV step over NCCL: rank g of `nccl_comm` (an ncclComm_t)
+ * holds slab g = rows [g*R/N, (g+1)*R/N) of an R x C matrix (R = rows_total, equal slabs).
+ * d_x (C fp16) is broadcast in place from `root`, the slab's SpMV writes its part of d_y (R fp16)
+ * and an in-place all-gather completes d_y on every rank.  Stream-ordered.  NCCL is loaded at run
+ * time (libnccl.so.2); MACKO_ENCCL reports its errors. */
+macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, int root, uint16_t* d_x,
+                                uint16_t* d_y, uint64_t rows_total, void* stream);
 
 /* ---- introspection ---- */
 typedef struct macko_launch_info {

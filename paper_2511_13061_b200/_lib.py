@@ -21,7 +21,7 @@ EXPORTS = (
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_configure", "macko_dev_set_order", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
-    "macko_mm_read_dense", "macko_chain_create", "macko_chain_run", "macko_chain_free",
+    "macko_mm_read_dense", "macko_chain_create", "macko_chain_run", "macko_chain_free", "macko_sharded_spmv",
 )
 
 
@@ -129,6 +129,8 @@ def load() -> C.CDLL:
     L.macko_chain_run.argtypes = [vp, vp]
     L.macko_chain_free.restype = st
     L.macko_chain_free.argtypes = [vp]
+    L.macko_sharded_spmv.restype = st
+    L.macko_sharded_spmv.argtypes = [vp, vp, C.c_int, vp, vp, C.c_uint64, vp]
     L.macko_mm_read_dense.restype = st
     L.macko_mm_read_dense.argtypes = [cp, C.POINTER(u64), C.POINTER(u64), vp]
     L.macko_dev_launch_info.restype = st

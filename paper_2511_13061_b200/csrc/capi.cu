@@ -4,6 +4,8 @@
 // matrix.hpp:57-81), builds the static SpMV work plan once per matrix, drives the compressor
 // and maps every failure onto a status code + thread-local message (no exception crosses the
 // C boundary; the C++ wrapper include/macko/macko_cuda.hpp rethrows the reference types).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -1203,6 +1205,63 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
         if (!r0 || !r1 || n_shards == 0 || shard >= n_shards) fail(MACKO_EINVAL, "bad shard request");
         *r0 = rows * shard / n_shards;
         *r1 = rows * (shard + 1) / n_shards;
+    });
+}
+
+namespace {
+// NCCL resolved at run time (no link-time dependency; in a torch process the NCCL it already
+// loaded is reused).  nccl.h: ncclResult_t / ncclDataType_t are int enums, ncclComm_t a pointer.
+struct NcclApi {
+    int (*bcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*allgather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*user_rank)(void*, int*) = nullptr;
+    int (*count)(void*, int*) = nullptr;
+    const char* (*errstr)(int) = nullptr;
+};
+constexpr int kNcclFloat16 = 6;  // nccl.h ncclFloat16
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.bcast = reinterpret_cast<decltype(a.bcast)>(dlsym(h, "ncclBroadcast"));
+        a.allgather = reinterpret_cast<decltype(a.allgather)>(dlsym(h, "ncclAllGather"));
+        a.user_rank = reinterpret_cast<decltype(a.user_rank)>(dlsym(h, "ncclCommUserRank"));
+        a.count = reinterpret_cast<decltype(a.count)>(dlsym(h, "ncclCommCount"));
+        a.errstr = reinterpret_cast<decltype(a.errstr)>(dlsym(h, "ncclGetErrorString"));
+        return a;
+    }();
+    return api;
+}
+
+void nck(int r, const char* what) {
+    if (r != 0) fail(MACKO_ENCCL, std::string(what) + ": " + (nccl().errstr ? nccl().errstr(r) : "NCCL error"));
+}
+}  // namespace
+
+macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, int root, uint16_t* d_x,
+                                uint16_t* d_y, uint64_t rows_total, void* stream) {
+    return guarded([&] {
+        if (!slab || !nccl_comm || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
+        const NcclApi& api = nccl();
+        if (!api.bcast || !api.allgather || !api.user_rank || !api.count)
+            fail(MACKO_ENCCL, "libnccl.so.2 not found (macko_sharded_spmv needs NCCL)");
+        int n = 0, r = 0;
+        nck(api.count(nccl_comm, &n), "ncclCommCount");
+        nck(api.user_rank(nccl_comm, &r), "ncclCommUserRank");
+        if (n < 1 || rows_total % (uint64_t)n != 0)
+            fail(MACKO_EINVAL, "rows_total must split into equal slabs (all-gather of equal counts)");
+        const uint64_t slab_rows = rows_total / (uint64_t)n, r0 = slab_rows * (uint64_t)r;
+        if (slab->rows != slab_rows) fail(MACKO_EINVAL, "slab rows do not match rows_total / ranks");
+        if (root < 0 || root >= n) fail(MACKO_EINVAL, "root out of range");
+        DeviceGuard g(slab->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        nck(api.bcast(d_x, d_x, slab->cols, kNcclFloat16, root, nccl_comm, st), "ncclBroadcast x");
+        const macko_status sp = macko_dev_spmv(slab, d_x, d_y + r0, stream);
+        if (sp != MACKO_OK) fail(sp, g_err);
+        nck(api.allgather(d_y + r0, d_y, slab_rows, kNcclFloat16, nccl_comm, st), "ncclAllGather y");
     });
 }
 

@@ -84,3 +84,15 @@ def device_local_spmv(dm: "M.DeviceMatrix", stream=None) -> Callable[[torch.Tens
         dm.spmv_into(x, y, stream)
 
     return run
+
+
+def nccl_sharded_spmv(dm: "M.DeviceMatrix", nccl_comm: int, x: torch.Tensor, y: torch.Tensor, root: int = 0,
+                      stream=None) -> torch.Tensor:
+    """One sharded step inside libmacko_cuda (macko_sharded_spmv): NCCL broadcast of x from
+    `root`, this rank's slab SpMV into its part of y, in-place NCCL all-gather of y.  `nccl_comm`
+    is an ncclComm_t (as an int); dm is this rank's slab of a y.numel() x x.numel() matrix."""
+    from . import _lib
+
+    _lib.check(_lib.load().macko_sharded_spmv(dm.handle, nccl_comm, root, x.data_ptr(), y.data_ptr(), y.numel(),
+                                              M._stream_ptr(stream)))
+    return y

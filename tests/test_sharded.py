@@ -70,3 +70,36 @@ def test_slab_bounds_cover_rows():
         assert b[0][0] == 0 and b[-1][1] == R
         assert all(b[i][1] == b[i + 1][0] for i in range(N - 1))
         assert max(y - x for x, y in b) - min(y - x for x, y in b) <= 1
+
+
+@pytest.mark.gpu
+def test_nccl_sharded_spmv_single_rank(cuda):
+    # macko_sharded_spmv over a real (one-rank) NCCL communicator: broadcast + slab SpMV +
+    # in-place all-gather; y equals the plain SpMV.  Multi-rank runs need one GPU per rank.
+    import ctypes as C
+
+    from oracle import oracle as O
+    from paper_2511_13061_b200 import macko as M
+    from paper_2511_13061_b200.sharded import nccl_sharded_spmv
+    from tests.helpers import to_dev, to_host_u16
+
+    class UniqueId(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+
+    nccl = C.CDLL("libnccl.so.2")
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        A = O.gen_dense(2048, 3000, 0.5, 61)
+        x = to_dev(O.gen_vector(3000, 62))
+        dm = M.DeviceMatrix.from_dense(to_dev(A))
+        y = torch.zeros(2048, dtype=torch.float16, device=cuda)
+        nccl_sharded_spmv(dm, comm.value, x, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host_u16(y), to_host_u16(M.spmv(dm, x)))
+        with pytest.raises(ValueError):  # slab rows must equal rows_total / ranks
+            nccl_sharded_spmv(dm, comm.value, x, torch.zeros(4096, dtype=torch.float16, device=cuda))
+    finally:
+        nccl.ncclCommDestroy(comm)
