@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
     p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture only, 1 smem table only, 6..9 smem + texture split")
     p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs per SM (0 = occupancy maximum)")
+    p.add_argument("--fused", action="store_true",
+                   help="N > 1: all-gather of y fused into the SpMV kernel (peer stores over NVLink + flags; "
+                        "x replicated, no broadcast) instead of NCCL broadcast + all_gather")
     return p.parse_args()
 
 
@@ -231,7 +234,15 @@ def main():
             flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back
 
     # N > 1: rows [rank*R, (rank+1)*R) of an (N*R) x C matrix; NCCL broadcast(x) + SpMV + all_gather(y)
-    sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev) if world > 1 else None
+    sharded = None
+    if world > 1:
+        if args.fused:
+            from paper_2511_13061_b200.sharded import FusedRowShardedSpmv
+
+            fused = FusedRowShardedSpmv(dm, R * world, dev)
+            sharded = lambda xx: fused(xx, stream)  # noqa: E731
+        else:
+            sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev)
 
     def step():
         if sharded is not None:
@@ -362,7 +373,9 @@ def main():
             "us_per_spmv": round(kern_ms * 1e3, 2), "us_per_step_median": round(ms_med * 1e3, 2),
             "config": {
                 "workload": f"{R}x{C} fp16 @{sparsity_pct}% sparsity (random unstructured), single SpMV"
-                + (f" per rank, {R * world}x{C} row-sharded, NCCL broadcast x + all_gather y" if world > 1 else ""),
+                + ((f" per rank, {R * world}x{C} row-sharded, all-gather of y fused into the SpMV (peer stores + flags)"
+                    if args.fused else f" per rank, {R * world}x{C} row-sharded, NCCL broadcast x + all_gather y")
+                   if world > 1 else ""),
                 "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4, "pad_nnz": pad_nnz,
                 "bytes_per_spmv_per_rank": bytes_rank, "parallelism": f"row-shard x{world}",
                 "l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush else

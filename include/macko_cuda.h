@@ -93,6 +93,10 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
  * may begin (plan load, first matrix fills) while the previous kernel on the stream drains, and
  * waits for it before reading x.  For chains of SpMVs (decoder stacks); CUDA-graph capturable. */
 #define MACKO_SPMV_PDL 1u
+/* MACKO_SPMV_PEERS: fused all-gather — every y row is also stored into the peers' y buffers set
+ * with macko_dev_set_peers (P2P over NVLink), and each CTA then adds 1 (system scope) to this
+ * rank's counter in every peer's flag array; consumers wait with macko_wait_flags. */
+#define MACKO_SPMV_PEERS 2u
 macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
                                uint32_t flags);
 
@@ -165,6 +169,22 @@ macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, 
  * time (libnccl.so.2); MACKO_ENCCL reports its errors. */
 macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, int root, uint16_t* d_x,
                                 uint16_t* d_y, uint64_t rows_total, void* stream);
+
+/* Fused all-gather destinations of a row slab (n <= 8, n = 0 disables): peer_y[p] = peer p's
+ * full-y buffer already offset to this slab's first row, peer_flags[p] = this rank's u32 counter
+ * in peer p's flag array (device or IPC-mapped pointers; one of them may be this rank's own).
+ * After a MACKO_SPMV_PEERS launch every counter has grown by the launch's grid size.  Synchronous. */
+macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, uint32_t* const* peer_flags, uint32_t n,
+                                 void* stream);
+/* Stream-ordered wait until d_flags[i] >= target (wrap-around compare) for i < n (n <= 32): the
+ * consumer side of MACKO_SPMV_PEERS.  Traps after ~4 s instead of hanging. */
+macko_status macko_wait_flags(const uint32_t* d_flags, uint32_t n, uint32_t target, void* stream);
+/* CUDA IPC of device buffers between the ranks' processes: the 64-byte handle names the
+ * allocation holding d_ptr, *offset is d_ptr's offset in it; macko_ipc_open returns the mapped
+ * base (add the offset), macko_ipc_close unmaps that base. */
+macko_status macko_ipc_get_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset);
+macko_status macko_ipc_open(const uint8_t* handle64, int device, void** d_base);
+macko_status macko_ipc_close(void* d_base);
 
 /* ---- introspection ---- */
 typedef struct macko_launch_info {

@@ -22,6 +22,7 @@ EXPORTS = (
     "macko_dev_launch_info", "macko_dev_configure", "macko_dev_set_order", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
     "macko_mm_read_dense", "macko_chain_create", "macko_chain_run", "macko_chain_free", "macko_sharded_spmv",
+    "macko_dev_set_peers", "macko_wait_flags", "macko_ipc_get_handle", "macko_ipc_open", "macko_ipc_close",
 )
 
 
@@ -131,6 +132,16 @@ def load() -> C.CDLL:
     L.macko_chain_free.argtypes = [vp]
     L.macko_sharded_spmv.restype = st
     L.macko_sharded_spmv.argtypes = [vp, vp, C.c_int, vp, vp, C.c_uint64, vp]
+    L.macko_dev_set_peers.restype = st
+    L.macko_dev_set_peers.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_uint32, vp]
+    L.macko_wait_flags.restype = st
+    L.macko_wait_flags.argtypes = [vp, C.c_uint32, C.c_uint32, vp]
+    L.macko_ipc_get_handle.restype = st
+    L.macko_ipc_get_handle.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint64)]
+    L.macko_ipc_open.restype = st
+    L.macko_ipc_open.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.macko_ipc_close.restype = st
+    L.macko_ipc_close.argtypes = [vp]
     L.macko_mm_read_dense.restype = st
     L.macko_mm_read_dense.argtypes = [cp, C.POINTER(u64), C.POINTER(u64), vp]
     L.macko_dev_launch_info.restype = st

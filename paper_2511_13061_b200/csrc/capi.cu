@@ -123,6 +123,8 @@ struct macko_dev_matrix {
     mk::SpmvPlanDev plan{};
     // scratch for macko_spmv_host (x texture-aligned inside hx, so the SpMV needs no staging copy)
     DevBuf<uint16_t> hx, hy;
+    DevBuf<mk::PeerTable> peer_table;  // fused all-gather destinations (macko_dev_set_peers)
+    uint32_t n_peer = 0;
     uint16_t* hx_aligned = nullptr;
     // x as a 1-D fp16 texture for x_mode >= 3 (created per x buffer, reused while it stays the same)
     mutable std::mutex tex_mu;
@@ -837,7 +839,8 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
                                uint32_t flags) {
     return guarded([&] {
         if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
-        if (flags & ~(uint32_t)MACKO_SPMV_PDL) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
+        if (flags & ~(uint32_t)(MACKO_SPMV_PDL | MACKO_SPMV_PEERS)) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
+        if ((flags & MACKO_SPMV_PEERS) && m->n_peer == 0) fail(MACKO_EINVAL, "MACKO_SPMV_PEERS without macko_dev_set_peers");
         if (!mk::spmv_valid_config(m->x_mode, (int)m->b_delta))
             fail(MACKO_EINVAL, "no SpMV kernel for b_delta " + std::to_string(m->b_delta) + " with this x_mode");
         DeviceGuard g(m->device);
@@ -856,8 +859,13 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
+        if (flags & MACKO_SPMV_PEERS) {
+            a.n_peer = m->n_peer;
+            a.peers = m->peer_table.p;
+        }
         a.value_count = (uint32_t)m->pad_nnz;
         if (m->pad_nnz == 0) {  // no stored entries: every row is empty, y = +0
+            if (flags & MACKO_SPMV_PEERS) fail(MACKO_EINVAL, "fused all-gather needs stored entries");
             ck(cudaMemsetAsync(d_y, 0, m->rows * 2, (cudaStream_t)stream), "y = 0");
             return;
         }
@@ -1240,6 +1248,78 @@ void nck(int r, const char* what) {
     if (r != 0) fail(MACKO_ENCCL, std::string(what) + ": " + (nccl().errstr ? nccl().errstr(r) : "NCCL error"));
 }
 }  // namespace
+
+macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, uint32_t* const* peer_flags, uint32_t n,
+                                 void* stream) {
+    return guarded([&] {
+        if (!m || (n && (!peer_y || !peer_flags))) fail(MACKO_EINVAL, "null argument");
+        if (n > mk::kMaxPeers) fail(MACKO_EINVAL, "at most 8 peers");
+        DeviceGuard g(m->device);
+        mk::PeerTable t{};
+        for (uint32_t p = 0; p < n; ++p) {
+            if (!peer_y[p] || !peer_flags[p]) fail(MACKO_EINVAL, "null peer pointer");
+            t.y[p] = peer_y[p];
+            t.flag[p] = peer_flags[p];
+        }
+        if (!m->peer_table.p) m->peer_table.alloc(1);
+        ck(cudaMemcpyAsync(m->peer_table.p, &t, sizeof t, cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table");
+        ck(cudaStreamSynchronize((cudaStream_t)stream), "peer table");
+        m->n_peer = n;
+    });
+}
+
+macko_status macko_wait_flags(const uint32_t* d_flags, uint32_t n, uint32_t target, void* stream) {
+    return guarded([&] {
+        if (!d_flags || n == 0 || n > 32) fail(MACKO_EINVAL, "flags: 1..32 counters");
+        ck(mk::launch_wait_flags(d_flags, n, target, (cudaStream_t)stream), "wait_flags");
+        g_launches.fetch_add(1);
+    });
+}
+
+macko_status macko_ipc_get_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset) {
+    return guarded([&] {
+        if (!d_ptr || !handle64 || !offset) fail(MACKO_EINVAL, "null argument");
+        // the handle names the whole allocation (a caching allocator hands out sub-blocks): the
+        // peer opens the base and adds the offset (driver cuMemGetAddressRange, via the runtime's
+        // entry-point query, so the library keeps no link-time libcuda dependency)
+        using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+        static RangeFn range = [] {
+            void* f = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                f = nullptr;
+            return reinterpret_cast<RangeFn>(f);
+        }();
+        if (!range) fail(MACKO_ECUDA, "cuMemGetAddressRange unavailable");
+        unsigned long long base = 0;
+        size_t size = 0;
+        if (range(&base, &size, (unsigned long long)reinterpret_cast<uintptr_t>(d_ptr)) != 0)
+            fail(MACKO_EINVAL, "not a device allocation");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(handle64, &h, 64);
+        *offset = (uint64_t)(reinterpret_cast<uintptr_t>(d_ptr) - base);
+    });
+}
+
+macko_status macko_ipc_open(const uint8_t* handle64, int device, void** d_ptr) {
+    return guarded([&] {
+        if (!handle64 || !d_ptr) fail(MACKO_EINVAL, "null argument");
+        DeviceGuard g(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, 64);
+        ck(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+macko_status macko_ipc_close(void* d_ptr) {
+    return guarded([&] {
+        if (!d_ptr) fail(MACKO_EINVAL, "null argument");
+        ck(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+    });
+}
 
 macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, int root, uint16_t* d_x,
                                 uint16_t* d_y, uint64_t rows_total, void* stream) {

@@ -195,6 +195,24 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
     return acc;
 }
 
+// y[r] = v, and the same 2 bytes into every peer's y for the fused all-gather (one row per call,
+// lane 0).
+__device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
+    a.y[r] = v;
+    for (uint32_t p = 0; p < a.n_peer; ++p) reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[p])))[r] = v;
+}
+
+// Fused all-gather: once all warps of the CTA wrote their rows, make them visible system-wide and
+// count the CTA in every peer's flag slot for this rank (consumers: wait_flags_kernel).
+__device__ __forceinline__ void signal_peers(const SpmvArgs& a) {
+    if (a.n_peer == 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (uint32_t p = 0; p < a.n_peer; ++p) atomicAdd_system(a.peers->flag[p], 1u);
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Compute-side row state
 // ------------------------------------------------------------------------------------------
@@ -233,8 +251,9 @@ __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colba
 // Finish the current piece (write y or hand the split row to its last arrival).  Lane 0 wrote
 // the piece's unit partials; the release atomic orders them before its arrival (no full fence,
 // no L1 invalidation), and the last arrival reads every partial from L2 (ld.cg).
-__device__ __noinline__ void finish_split(uint32_t r, uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot,
-                                          int32_t sid, float row_acc, const SpmvPlanDev P, uint16_t* y, int lane) {
+// Returns y[r]'s fp16 bits in lane 0 of the last arrival, -1 elsewhere (the caller stores it).
+__device__ __noinline__ int finish_split(uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot, int32_t sid,
+                                         float row_acc, const SpmvPlanDev P, int lane) {
     uint32_t last = 0, first = 0;
     if (lane == 0) {
         if (j0 == 0) P.partials[slot + tend / kUnitSteps - 1u] = row_acc;  // a first piece ends on a unit boundary
@@ -248,9 +267,10 @@ __device__ __noinline__ void finish_split(uint32_t r, uint32_t j0, uint32_t tend
     if (last && lane == 0) {
         float tot = __ldcg(P.partials + slot + first - 1);
         for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
-        y[r] = f32_to_f16_rn(tot);
         P.counters[sid] = 0;  // ready for the next launch (stream order)
+        return (int)f32_to_f16_rn(tot);
     }
+    return -1;
 }
 
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
@@ -269,7 +289,7 @@ __device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint
             rs.slot = q.w;
         }
         if (rs.T) return true;
-        if (lane == 0) a.y[rs.r] = 0;  // empty row: fp16(+0.0)
+        if (lane == 0) put_y(a, rs.r, 0);  // empty row: fp16(+0.0)
     }
 }
 
@@ -523,7 +543,7 @@ template <int kXMode, int kBits>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr, Ring& g,
                                          RowState& rs) {
     if (rs.T == 0) {
-        if (lane == 0) a.y[rs.r] = 0;
+        if (lane == 0) put_y(a, rs.r, 0);
         if (!next_piece(rs, a, w, lane)) return;
     }
     // ring event: refill once the walk passes rel_mark, wait once a pair reaches ready_end
@@ -596,9 +616,10 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         }
         // -- piece end
         if (!rs.split) {
-            if (lane == 0) a.y[rs.r] = f32_to_f16_rn(rs.row_acc);
+            if (lane == 0) put_y(a, rs.r, f32_to_f16_rn(rs.row_acc));
         } else {
-            finish_split(rs.r, rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, a.y, lane);
+            const int v = finish_split(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, lane);
+            if (v >= 0) put_y(a, rs.r, (uint16_t)v);
         }
         if (!next_piece(rs, a, w, lane)) break;
     }
@@ -631,8 +652,10 @@ __device__ __forceinline__ uint32_t incl_at(const D& d, uint32_t m) {
 // Finish a row cut between warps (flat plan): the first piece stores its sum at the slot of its
 // last unit, other pieces stored per-unit partials at their unit ends; the last arrival adds them
 // in unit order.
-__device__ __noinline__ void finish_split_flat(uint32_t r, bool first_piece, uint32_t n_r, const uint4* rec,
-                                               float row_acc, const SpmvPlanDev P, uint16_t* y, int lane) {
+// Returns y[r]'s fp16 bits in lane 0 of the last arrival, -1 elsewhere (the caller stores it).
+__device__ __noinline__ int finish_split_flat(bool first_piece, uint32_t n_r, const uint4* rec, float row_acc,
+                                              const SpmvPlanDev P, int lane) {
+    int out = -1;
     uint32_t last = 0, first = 0, slot = 0;
     if (lane == 0) {
         const uint4 q2 = __ldg(rec + 2);  // sid0, sid1, slot0, slot1 (spmv.cuh WarpPlan)
@@ -647,11 +670,12 @@ __device__ __noinline__ void finish_split_flat(uint32_t r, bool first_piece, uin
         if (last) {
             float tot = __ldcg(P.partials + slot + first - 1);
             for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
-            y[r] = f32_to_f16_rn(tot);
+            out = (int)f32_to_f16_rn(tot);
             P.counters[sid] = 0;
         }
     }
     __syncwarp();
+    return out;
 }
 
 template <int kXMode, int kBits>
@@ -678,10 +702,11 @@ __device__ __forceinline__ void run_flat(const SpmvArgs& a, const PlanRecord& pr
     };
     auto finish_row = [&]() {
         if (fs.s >= E0 && fs.e <= E1) {
-            if (lane == 0) a.y[fs.r] = f32_to_f16_rn(fs.row_acc);
+            if (lane == 0) put_y(a, fs.r, f32_to_f16_rn(fs.row_acc));
         } else {
             const uint32_t n_r = (fs.e - 1u) / kUnitElts - fs.s / kUnitElts + 1u;
-            finish_split_flat(fs.r, fs.s >= E0, n_r, rec, fs.row_acc, a.plan, a.y, lane);
+            const int v = finish_split_flat(fs.s >= E0, n_r, rec, fs.row_acc, a.plan, lane);
+            if (v >= 0) put_y(a, fs.r, (uint16_t)v);
         }
     };
     // Move to the next row this warp owns (empty rows get +0).  Returns false when the walk is over.
@@ -697,12 +722,12 @@ __device__ __forceinline__ void run_flat(const SpmvArgs& a, const PlanRecord& pr
             fs.row_acc = 0.0f;
             fs.col_base = -1;  // a row starting at a window start
             if (fs.e > fs.s) return true;
-            if (lane == 0) a.y[fs.r] = 0;  // empty row
+            if (lane == 0) put_y(a, fs.r, 0);  // empty row
         }
     };
     // leading empty rows of this warp
     if (fs.e == fs.s) {
-        if (lane == 0) a.y[fs.r] = 0;
+        if (lane == 0) put_y(a, fs.r, 0);
         if (!next_row()) return;
     }
 
@@ -806,8 +831,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.pdl) stage_x<kXMode, false>(a, xs);
     __syncthreads();
-    if (!has_work) return;
-    run_flat<kXMode, kBits>(a, pr, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g);
+    if (has_work) run_flat<kXMode, kBits>(a, pr, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g);
+    signal_peers(a);
 }
 
 template <int kXMode, int kBits>
@@ -842,6 +867,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
     if (has_work) run_rows<kXMode, kBits>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
+    signal_peers(a);
 }
 
 // Grid-wide barrier for the persistent chain kernel (all CTAs co-resident: cooperative launch).
@@ -987,6 +1013,28 @@ __global__ void __launch_bounds__(1024) copy_u16_kernel(const uint16_t* __restri
     for (uint32_t i = tid; i < n16; i += nt)
         reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
     for (uint32_t i = n16 * 8u + tid; i < n; i += nt) dst[i] = src[i];
+}
+
+// Consumer side of the fused all-gather: one thread per rank slot spins (system-scope acquire)
+// until every peer's CTAs have signalled; traps after ~4 s instead of hanging the GPU.
+__global__ void wait_flags_kernel(const uint32_t* flags, uint32_t n, uint32_t target) {
+    if (threadIdx.x < n) {
+        const long long t0 = clock64();
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
+            if ((int32_t)(v - target) >= 0) break;
+            __nanosleep(64);
+            if (clock64() - t0 > 8000000000LL) __trap();
+        }
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+cudaError_t launch_wait_flags(const uint32_t* flags, uint32_t n, uint32_t target, cudaStream_t s) {
+    wait_flags_kernel<<<1, 32, 0, s>>>(flags, n, target);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int blocks, bool dependent, cudaStream_t s) {

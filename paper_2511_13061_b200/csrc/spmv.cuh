@@ -29,6 +29,13 @@ struct SpmvPlanDev {
     uint32_t* counters;      // S: arrival counters (zero between launches)
 };
 
+// Fused all-gather of y (row-sharded SpMV over NVLink peers): up to kMaxPeers destinations.
+constexpr uint32_t kMaxPeers = 8;
+struct PeerTable {  // device memory, one per matrix (macko_dev_set_peers)
+    uint16_t* y[kMaxPeers];    // peer p's full y, already offset to this slab's first row
+    uint32_t* flag[kMaxPeers]; // this rank's completion counter in peer p's flag array
+};
+
 struct SpmvArgs {
     const uint16_t* values;
     const uint8_t* deltas;
@@ -42,6 +49,9 @@ struct SpmvArgs {
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
     uint32_t pdl;          // launched as a PDL dependent: x may still be written by the producer
+    uint32_t n_peer;       // fused all-gather: y rows also go to peers->y[0..n_peer) and each CTA adds 1
+                           // to *peers->flag[p] (system scope) once its rows are written
+    const PeerTable* peers;
     SpmvPlanDev plan;
 };
 
@@ -91,6 +101,8 @@ struct ChainOps {
 };
 cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
                          cudaStream_t s);
+// Wait until flags[i] >= target for i < n (system-scope acquire; peers' fused all-gathers).
+cudaError_t launch_wait_flags(const uint32_t* flags, uint32_t n, uint32_t target, cudaStream_t s);
 // n fp16 words src -> dst (device or device-mapped host pointers); dependent: launched as the
 // programmatic dependent of the previous kernel on the stream (waits for it before copying).
 cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int blocks, bool dependent, cudaStream_t s);

@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Optional
+from typing import Optional, Sequence
 
 import numpy as np
 
@@ -171,13 +171,22 @@ class DeviceMatrix:
     def validate(self, stream=None) -> None:
         check(_lib.load().macko_dev_validate(self._h, _stream_ptr(stream)))
 
-    def spmv_into(self, x, y, stream=None, pdl: bool = False) -> None:
+    def spmv_into(self, x, y, stream=None, pdl: bool = False, peers: bool = False) -> None:
         """y = A*x with device tensors / pointers (stream-ordered, asynchronous).  pdl: launch as
-        a programmatic dependent of the previous kernel on the stream (SpMV chains)."""
-        if pdl:
-            check(_lib.load().macko_dev_spmv_ex(self._h, _ptr(x), _ptr(y), _stream_ptr(stream), 1))
+        a programmatic dependent of the previous kernel on the stream (SpMV chains).  peers: also
+        store y into the peer buffers of set_peers and signal their flags (fused all-gather)."""
+        flags = (1 if pdl else 0) | (2 if peers else 0)
+        if flags:
+            check(_lib.load().macko_dev_spmv_ex(self._h, _ptr(x), _ptr(y), _stream_ptr(stream), flags))
         else:
             check(_lib.load().macko_dev_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+
+    def set_peers(self, peer_y: Sequence[int], peer_flags: Sequence[int], stream=None) -> None:
+        """Fused all-gather destinations (device / IPC-mapped addresses; see macko_dev_set_peers)."""
+        n = len(peer_y)
+        ys = (C.c_void_p * max(n, 1))(*peer_y)
+        fs = (C.c_void_p * max(n, 1))(*peer_flags)
+        check(_lib.load().macko_dev_set_peers(self._h, ys, fs, n, _stream_ptr(stream)))
 
     def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
         """End-to-end call with host buffers (H2D x, kernel, D2H y, synchronise)."""
@@ -334,3 +343,27 @@ def kernel_launches() -> int:
 
 def version() -> str:
     return _lib.load().macko_version().decode()
+
+
+def wait_flags(flags, n: int, target: int, stream=None) -> None:
+    """Stream-ordered wait until flags[i] >= target for i < n (macko_wait_flags)."""
+    check(_lib.load().macko_wait_flags(_ptr(flags), n, target & 0xFFFFFFFF, _stream_ptr(stream)))
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, t's byte offset in it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    check(_lib.load().macko_ipc_get_handle(_ptr(t), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map a peer allocation; returns its base address (close with ipc_close)."""
+    p = C.c_void_p()
+    check(_lib.load().macko_ipc_open(handle, device, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(_lib.load().macko_ipc_close(ptr))

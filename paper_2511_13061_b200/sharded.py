@@ -96,3 +96,64 @@ def nccl_sharded_spmv(dm: "M.DeviceMatrix", nccl_comm: int, x: torch.Tensor, y: 
     _lib.check(_lib.load().macko_sharded_spmv(dm.handle, nccl_comm, root, x.data_ptr(), y.data_ptr(), y.numel(),
                                               M._stream_ptr(stream)))
     return y
+
+
+class FusedRowShardedSpmv:
+    """Row-sharded y = A x whose all-gather is fused into the SpMV kernel: every rank's kernel
+    stores its slab's rows straight into every rank's full-y buffer (CUDA IPC / P2P over NVLink)
+    and counts its CTAs into every rank's flag array; a step ends with a stream-ordered wait until
+    all ranks' CTAs have signalled (MACKO_SPMV_PEERS, macko_wait_flags).  x must already be
+    identical on every rank (in a decode chain it is the previous step's full y).
+
+    Setup exchanges IPC handles over `group` (any backend; gloo works).  Every rank's slab must
+    use the same launch grid (same GPU model), which the flag target assumes.
+    """
+
+    def __init__(self, dm: "M.DeviceMatrix", rows_total: int, device: torch.device, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.dm = dm
+        self.r0, self.r1 = slab_bounds(rows_total, self.world, self.rank)
+        if dm.rows != self.r1 - self.r0:
+            raise ValueError("slab rows do not match this rank's share of rows_total")
+        self.y = torch.zeros(rows_total, dtype=torch.float16, device=device)
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device=device)
+        self.grid = dm.launch_info().grid
+        self.epoch = 0
+        dev = device.index if device.index is not None else torch.cuda.current_device()
+        mine = (M.ipc_handle(self.y), M.ipc_handle(self.flags), self.r0)
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self._opened, self._bases = [], {}
+        peer_y, peer_f = [], []
+        for p, ((hy, oy), (hf, of), _) in enumerate(allh):
+            if p == self.rank:
+                yb, fb = self.y.data_ptr(), self.flags.data_ptr()
+            else:
+                yb, fb = self._open(hy, dev) + oy, self._open(hf, dev) + of
+            peer_y.append(yb + 2 * self.r0)
+            peer_f.append(fb + 4 * self.rank)
+        dm.set_peers(peer_y, peer_f)
+
+    def _open(self, handle: bytes, dev: int) -> int:
+        # one mapping per allocation (y and flags may come from the same caching-allocator segment)
+        if handle not in self._bases:
+            self._bases[handle] = M.ipc_open(handle, dev)
+            self._opened.append(self._bases[handle])
+        return self._bases[handle]
+
+    def __call__(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        self.epoch += 1
+        self.dm.spmv_into(x, self.y[self.r0:self.r1], stream, peers=True)
+        M.wait_flags(self.flags, self.world, self.epoch * self.grid, stream)
+        return self.y
+
+    def close(self) -> None:
+        self.dm.set_peers([], [])
+        for ptr in self._opened:
+            M.ipc_close(ptr)
+        self._opened = []

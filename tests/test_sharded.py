@@ -103,3 +103,74 @@ def test_nccl_sharded_spmv_single_rank(cuda):
             nccl_sharded_spmv(dm, comm.value, x, torch.zeros(4096, dtype=torch.float16, device=cuda))
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+def _fused_worker(rank, world, port, R, C, out_path):
+    # one GPU shared by `world` processes: CUDA IPC between processes on the same device exercises
+    # the whole fused all-gather protocol (peer stores, system-scope flags, waits)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2511_13061_b200 import macko as M
+        from paper_2511_13061_b200.sharded import FusedRowShardedSpmv, slab_bounds
+
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        r0, r1 = slab_bounds(R, world, rank)
+        A = O.gen_dense(R, C, 0.5, 17)[r0:r1]
+        dm = M.DeviceMatrix.from_dense(torch.from_numpy(A.view(np.int16)).to(dev).view(torch.float16))
+        fused = FusedRowShardedSpmv(dm, R, dev)
+        x = torch.from_numpy(O.gen_vector(C, 18).view(np.int16)).to(dev).view(torch.float16)
+        for step in range(3):
+            y = fused(x)
+            torch.cuda.synchronize()
+            dist.barrier()  # nobody starts step k+1 (overwriting peers' y) before all read step k
+            got = y.view(torch.int16).cpu().numpy().view(np.uint16).copy()
+            if rank == 0:
+                np.save(out_path + f".{step}.npy", got)
+            dist.barrier()
+        assert int(fused.flags.cpu().numpy().min()) == 3 * fused.grid
+        fused.close()
+        dm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_allgather_single_rank(cuda):
+    from oracle import oracle as O
+    from paper_2511_13061_b200 import macko as M
+    from paper_2511_13061_b200.sharded import FusedRowShardedSpmv
+    from tests.helpers import b200_y, to_dev, to_host_u16
+
+    A = O.gen_dense(3000, 5000, 0.5, 71)
+    x = O.gen_vector(5000, 72)
+    dm = M.DeviceMatrix.from_dense(to_dev(A))
+    fused = FusedRowShardedSpmv(dm, 3000, cuda)
+    ref = b200_y(dm, O.encode_dense(A), x)
+    for step in range(1, 4):
+        y = fused(to_dev(x))
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host_u16(y), ref), step
+        assert int(fused.flags.item()) == step * fused.grid
+    fused.close()
+    dm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_fused_allgather_two_processes_one_gpu(cuda, tmp_path):
+    from oracle import oracle as O
+
+    R, C = 4000, 3000
+    out = str(tmp_path / "fy")
+    mp.spawn(_fused_worker, args=(2, _free_port(), R, C, out), nprocs=2, join=True)
+    A = O.gen_dense(R, C, 0.5, 17)
+    ref = O.reference_spmv(O.encode_dense(A), O.gen_vector(C, 18), 8)
+    for step in range(3):
+        y = np.load(out + f".{step}.npy")
+        from tests.helpers import within_bound
+
+        assert within_bound(A, O.gen_vector(C, 18), y, ref), step
