@@ -429,10 +429,10 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
     from paper_2511_13061_b200 import macko as M
 
     t0 = time.time()
-    ch = D.SparseDecoderChain(D.LLAMA2_7B, density=0.5, keep_dense=(world == 1))
+    ch = D.SparseDecoderChain(D.LLAMA2_7B, density=0.5, keep_dense=(world == 1), fused=(args.fused and world > 1))
     build_s = time.time() - t0
     M.gen_vector(ch.acts["h"], D.LLAMA2_7B.hidden, seed=SEED_X)
-    g = ch.capture(pdl=True)
+    g = None if ch.fused else ch.capture(pdl=True)
 
     def time_graph(graph, n):
         for _ in range(3):
@@ -453,9 +453,24 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
             ms = t.item()
         return ms
 
+    def time_tokens(n):  # fused all-gather: plain stream launches (flag targets grow per SpMV)
+        for _ in range(3):
+            ch.forward_token(pdl=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for a, b in evs:
+            a.record()
+            ch.forward_token(pdl=True)
+            b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / n], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
     n = max(3, args.chain_tokens)
     launches0 = M.kernel_launches()
-    ms_graph = time_graph(g, n)
+    ms_graph = time_tokens(n) if ch.fused else time_graph(g, n)
     launches_graph = M.kernel_launches() - launches0
     bytes_rank = ch.traffic_bytes
     total_bytes = bytes_rank * world
@@ -473,10 +488,14 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
     out = {
         "workload": "Llama2-7B decoder stack, 32 layers x {qkv 12288x4096, o 4096x4096, gate_up 22016x4096, "
                     "down 4096x11008} @50% sparsity, batch-1 decode (q/k/v and gate/up row-stacked), random-init",
-        "n_gpus": world, "parallelism": f"row-shard x{world}" + (" + NCCL all_gather per SpMV" if world > 1 else ""),
+        "n_gpus": world, "parallelism": f"row-shard x{world}" + (
+            (" + all-gather fused into each SpMV (peer stores + flags)" if ch.fused else " + NCCL all_gather per SpMV")
+            if world > 1 else ""),
         "spmvs_per_token": ch.kernels_per_token,
         "launch": ("one persistent cooperative kernel per token (grid barrier between dependent SpMVs, "
-                   "weights prefetched across it)" if ms == ms_pers else "PDL-chained SpMV kernels, one CUDA graph per token"),
+                   "weights prefetched across it)" if ms == ms_pers else
+                   "PDL-chained SpMV + flag-wait kernels, stream launches" if ch.fused else
+                   "PDL-chained SpMV kernels, one CUDA graph per token"),
         "us_per_token": round(ms * 1e3, 2), "tokens_per_s": round(1e3 / ms, 2),
         "us_per_token_pdl_graph": round(ms_graph * 1e3, 2),
         "us_per_token_persistent": None if ms_pers is None else round(ms_pers * 1e3, 2),

@@ -69,7 +69,7 @@ class SparseDecoderChain:
     """The decode chain over MACKO matrices built on the GPU (generator -> GPU compressor)."""
 
     def __init__(self, shape: ChainShape = LLAMA2_7B, density: float = 0.5, seed: int = 0x5EEDA000,
-                 device: Optional[torch.device] = None, keep_dense: bool = False, group=None):
+                 device: Optional[torch.device] = None, keep_dense: bool = False, group=None, fused: bool = False):
         self.shape = shape
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.group = group
@@ -106,6 +106,45 @@ class SparseDecoderChain:
             self.dense.append(dense)
         torch.cuda.synchronize(self.device)
         self.graph: Optional[torch.cuda.CUDAGraph] = None
+        self.fused = fused
+        if fused:
+            self._setup_fused()
+
+    def _setup_fused(self) -> None:
+        """Fused all-gather (MACKO_SPMV_PEERS): every slab SpMV stores its rows into every rank's
+        activation buffer and counts its CTAs into every rank's flag array; the next SpMV waits
+        for all ranks' counters (macko_wait_flags).  IPC handles are exchanged over the group."""
+        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        self._ops_done = 0
+        self._grid = self.mats[0][LINEARS[0]].launch_info().grid
+        mine = {k: M.ipc_handle(v) for k, v in self.acts.items()}
+        mine["flags"] = M.ipc_handle(self.flags)
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=self.group)
+        else:
+            allh = [mine]
+        self._bases, self._opened = {}, []
+        own = {k: v.data_ptr() for k, v in self.acts.items()}
+        own["flags"] = self.flags.data_ptr()
+        ptrs = []
+        for p, h in enumerate(allh):
+            if p == self.rank:
+                ptrs.append(own)
+                continue
+            d = {}
+            for k, (handle, off) in h.items():
+                if handle not in self._bases:
+                    self._bases[handle] = M.ipc_open(handle, dev)
+                    self._opened.append(self._bases[handle])
+                d[k] = self._bases[handle] + off
+            ptrs.append(d)
+        for mats in self.mats:
+            for name, m in mats.items():
+                r0 = self.bounds[name][0]
+                m.set_peers([ptrs[p][_out_name(name)] + 2 * r0 for p in range(self.world)],
+                            [ptrs[p]["flags"] + 4 * self.rank for p in range(self.world)])
 
     # -- accounting -------------------------------------------------------------------------
     @property
@@ -121,7 +160,12 @@ class SparseDecoderChain:
     def _spmv(self, layer: int, name: str, stream, pdl: bool) -> None:
         x = _x_slice(self.shape, name, self.acts)
         out = self.acts[_out_name(name)]
-        if self.world == 1:
+        if self.fused:
+            r0, r1 = self.bounds[name]
+            self.mats[layer][name].spmv_into(x, out[r0:r1], stream, pdl=pdl, peers=True)
+            self._ops_done += 1
+            M.wait_flags(self.flags, self.world, self._ops_done * self._grid, stream)
+        elif self.world == 1:
             self.mats[layer][name].spmv_into(x, out, stream, pdl=pdl)
         else:
             self.mats[layer][name].spmv_into(x, self.local[name], stream, pdl=pdl)
@@ -153,6 +197,8 @@ class SparseDecoderChain:
 
     def capture(self, pdl: bool = True) -> torch.cuda.CUDAGraph:
         """Capture forward_token into a CUDA graph (kernel nodes keep their PDL edges)."""
+        if self.fused:
+            raise ValueError("fused all-gather waits on growing flag targets: not graph-capturable")
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -169,6 +215,9 @@ class SparseDecoderChain:
         if getattr(self, "_chain", None) is not None:
             self._chain.close()
             self._chain = None
+        for ptr in getattr(self, "_opened", []):
+            M.ipc_close(ptr)
+        self._opened = []
         for mats in self.mats:
             for m in mats.values():
                 m.close()

@@ -174,3 +174,50 @@ def test_fused_allgather_two_processes_one_gpu(cuda, tmp_path):
         from tests.helpers import within_bound
 
         assert within_bound(A, O.gen_vector(C, 18), y, ref), step
+
+
+def _fused_chain_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_13061_b200 import decoder_chain as D
+        from paper_2511_13061_b200 import macko as M
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        # density 1: every row starts at a multiple of 8 in the slabs and in the whole matrices,
+        # so the sharded chain is bit-identical to the unsharded one
+        shape = D.ChainShape(layers=2, hidden=256, inter=688)
+        ch = D.SparseDecoderChain(shape, density=1.0, seed=5, device=dev, fused=True)
+        M.gen_vector(ch.acts["h"], 256, seed=6)
+        ch.acts["h"].mul_(2.0**-8)
+        for tok in range(2):
+            ch.forward_token(pdl=bool(tok))
+            torch.cuda.synchronize()
+            dist.barrier()
+        np.save(out_path + f".{rank}.npy", ch.acts["h"].view(torch.int16).cpu().numpy().view(np.uint16))
+        ch.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_fused_decode_chain_two_processes_one_gpu(cuda, tmp_path):
+    from paper_2511_13061_b200 import decoder_chain as D
+    from paper_2511_13061_b200 import macko as M
+
+    out = str(tmp_path / "chain")
+    mp.spawn(_fused_chain_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    shape = D.ChainShape(layers=2, hidden=256, inter=688)
+    ref = D.SparseDecoderChain(shape, density=1.0, seed=5)
+    M.gen_vector(ref.acts["h"], 256, seed=6)
+    ref.acts["h"].mul_(2.0**-8)
+    for _ in range(2):
+        ref.forward_token(pdl=False)
+    torch.cuda.synchronize()
+    want = ref.acts["h"].view(torch.int16).cpu().numpy().view(np.uint16)
+    for r in range(2):
+        assert np.array_equal(np.load(out + f".{r}.npy"), want), r
+    ref.close()
