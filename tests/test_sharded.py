@@ -161,12 +161,13 @@ def test_fused_allgather_single_rank(cuda):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(300)
-def test_fused_allgather_two_processes_one_gpu(cuda, tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_allgather_processes_one_gpu(cuda, tmp_path, world):
     from oracle import oracle as O
 
     R, C = 4000, 3000
     out = str(tmp_path / "fy")
-    mp.spawn(_fused_worker, args=(2, _free_port(), R, C, out), nprocs=2, join=True)
+    mp.spawn(_fused_worker, args=(world, _free_port(), R, C, out), nprocs=world, join=True)
     A = O.gen_dense(R, C, 0.5, 17)
     ref = O.reference_spmv(O.encode_dense(A), O.gen_vector(C, 18), 8)
     for step in range(3):
