@@ -24,7 +24,7 @@ namespace mk {
 namespace {
 
 constexpr int kCompressWarpsPerCta = 8;
-constexpr int kStageWords = 72;  // 256 entries x 8 bits = 64 words, + carry + spill
+constexpr int kStageWords = 72;  // per chunk <= 256 entries x 8 bits or 512 x 4 bits = 64 words, + carry + spill
 
 // The 8 columns [c, c+8) of a dense row (zeros past `cols`) as four fp16 pairs.  Loops issue
 // the next chunk's fetch before working on the current one (one 16-byte load per lane in flight
@@ -68,18 +68,19 @@ __device__ __forceinline__ int prev_nonzero(int lane_last, int lane, int& carry)
     return p;
 }
 
-// b_delta >= 4 (max delta >= 16 > 8 columns of a lane): a lane holds at most one padding entry,
+// b_delta >= 4 (max delta >= 16 >= the kCols columns of a lane): a lane holds at most one padding entry,
 // at the first column cc0 >= c with cc0 = p (mod 2^b), cc0 > p, before the lane's first nonzero
 // (and before the row's last nonzero L); the nonzeros after the lane's first are never padded.
+template <int kCols>
 __device__ __forceinline__ uint32_t pad_bit(uint32_t nz, int c, int p, int L, uint32_t bits) {
     const int maxd = 1 << bits;
     const int cc0 = p + maxd * ((c - p + maxd - 1) >> bits);  // smallest p + k*maxd >= c (c > p)
-    const int lim = min(nz ? c + __ffs(nz) - 1 : c + 8, L);
+    const int lim = min(nz ? c + __ffs(nz) - 1 : c + kCols, L);
     return cc0 < lim ? 1u << (cc0 - c) : 0u;
 }
 
 template <bool kFast>
-__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
+__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp, 4)
     count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
                uint32_t* counts, int32_t* lastcol) {
     const int lane = threadIdx.x & (kWarp - 1);
@@ -160,11 +161,15 @@ __global__ void __launch_bounds__(1024) scan_counts(const uint32_t* counts, uint
     if (t == nt - 1) *total = run;
 }
 
-template <bool kFast>
-__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
+// kCols columns per lane per chunk: 16 for b_delta = 4 (a lane's <= 16 entries fit one 64-bit code
+// word), else 8.
+template <bool kFast, int kCols>
+__global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp, 4)
     emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
               const uint32_t* row_ptrs, const int32_t* lastcol, uint16_t* values, uint32_t* delta_words) {
     __shared__ uint32_t stage_all[kCompressWarpsPerCta][kStageWords];
+    // a chunk's values (<= kWarp * kCols entries: a pad takes a zero column), written out coalesced
+    __shared__ uint16_t vstage_all[kCompressWarpsPerCta][kWarp * kCols];
     // kFast: codes of the nonzeros after a lane's first one, per 8-column nonzero pattern (their
     // deltas are the gaps between set bits, < 8), packed at b_delta bits each
     __shared__ uint64_t gap_codes[kFast ? 256 : 1];
@@ -185,6 +190,7 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
         __syncthreads();
     }
     uint32_t* stage = stage_all[threadIdx.x >> 5];
+    uint16_t* vstage = vstage_all[threadIdx.x >> 5];
     const uint32_t nwarps = gridDim.x * kCompressWarpsPerCta;
     const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
     const uint32_t maxd = 1u << bits;
@@ -200,13 +206,20 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
         int carry = -1;
         uint32_t emitted = 0;                // entries of this row written so far
         uint64_t wb = row_first_word;        // global word held in stage[0]
-        uint4 next = fetch8(row, 8u * lane, cols, vec_base);
-        for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kWarp * 8) {
-            const uint32_t c = c0 + 8u * lane;
-            const uint4 cur = next;
-            if (c0 + kWarp * 8 < cols && (int)(c0 + kWarp * 8) <= L) next = fetch8(row, c + kWarp * 8, cols, vec_base);
-            uint16_t h[8];
-            const uint32_t nz = unpack8(cur, h);
+        constexpr uint32_t kStep = kWarp * kCols;
+        uint4 next[kCols / 8];
+#pragma unroll
+        for (int q = 0; q < kCols / 8; ++q) next[q] = fetch8(row, kCols * lane + 8 * q, cols, vec_base);
+        for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kStep) {
+            const uint32_t c = c0 + kCols * lane;
+            uint16_t h[kCols];
+            uint32_t nz = 0;
+#pragma unroll
+            for (int q = 0; q < kCols / 8; ++q) nz |= unpack8(next[q], h + 8 * q) << (8 * q);
+            if (c0 + kStep < cols && (int)(c0 + kStep) <= L) {
+#pragma unroll
+                for (int q = 0; q < kCols / 8; ++q) next[q] = fetch8(row, c + kStep + 8 * q, cols, vec_base);
+            }
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
             int p = prev_nonzero(lane_last, lane, carry);
             // classify the lane's 8 columns: nonzero entry, padding entry or nothing; codes of the
@@ -214,13 +227,26 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
             uint32_t em = 0;  // entry mask
             uint64_t codes = 0;
             if constexpr (kFast) {
-                const uint32_t pb = pad_bit(nz, (int)c, p, L, bits);
+                const uint32_t pb = pad_bit<kCols>(nz, (int)c, p, L, bits);
                 em = nz | pb;
                 const uint32_t sh = pb ? bits : 0u;  // the pad entry comes first
                 codes = pb ? (uint64_t)(maxd - 1) : 0ull;
                 if (nz) {
                     const uint32_t first = (uint32_t)((int)c + __ffs(nz) - 2 - p) & (maxd - 1);
-                    codes |= ((uint64_t)first << sh) | (gap_codes[nz] << (sh + bits));
+                    uint64_t gaps;  // codes of the nonzeros after the lane's first, in order
+                    if constexpr (kCols == 8) {
+                        gaps = gap_codes[nz];
+                    } else {  // two 8-column halves joined by the gap across them
+                        const uint32_t lo = nz & 0xFFu, hi = nz >> 8;
+                        gaps = lo ? gap_codes[lo] : 0ull;
+                        uint32_t pos = lo ? bits * (__popc(lo) - 1) : 0u;
+                        if (lo && hi) {
+                            gaps |= (uint64_t)(uint32_t)(8 + __ffs(hi) - 1 - (31 - __clz(lo)) - 1) << pos;
+                            pos += bits;
+                        }
+                        if (hi) gaps |= gap_codes[hi] << pos;
+                    }
+                    codes |= ((uint64_t)first << sh) | (gaps << (sh + bits));
                 }
             } else {
                 uint32_t code[8];
@@ -252,16 +278,21 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp)
             const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
             const uint64_t o = (uint64_t)start + emitted + (incl - n);
             {
-                // predicated stores (no branch per column): entry k goes to the lane's base + rank
-                uint16_t* vp = values + o;
+                // the lane's entries into the warp's value stage (predicated, no branch per column),
+                // then the chunk's values to global memory with lane-consecutive 2-byte stores: scattered
+                // 2-byte global stores would cost a partial L2 sector write each
+                const uint32_t vs = static_cast<uint32_t>(__cvta_generic_to_shared(vstage)) + 2u * (incl - n);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < kCols; ++k) {
                     const uint16_t val = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;  // pads are +0
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.u16 [%0], %1;\n\t}" ::"l"(
-                                     vp + __popc(em & ((1u << k) - 1u))),
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u16 [%0], %1;\n\t}" ::"r"(
+                                     vs + 2u * __popc(em & ((1u << k) - 1u))),
                                  "h"(val), "r"(em & (1u << k))
                                  : "memory");
                 }
+                __syncwarp();
+                uint16_t* vdst = values + (uint64_t)start + emitted;
+                for (uint32_t i = lane; i < tot; i += kWarp) vdst[i] = vstage[i];
             }
             if (n) {
                 const uint64_t bit0 = o * bits;
@@ -327,12 +358,13 @@ cudaError_t launch_emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, 
                              int sms, cudaStream_t s) {
     const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
     if (grid > 0) {
-        if (bits >= 4)
-            emit_rows<true><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol,
-                                                                          values, delta_words);
+        const dim3 b(kCompressWarpsPerCta * kWarp);
+        if (bits == 4)
+            emit_rows<true, 16><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values, delta_words);
+        else if (bits == 8)
+            emit_rows<true, 8><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values, delta_words);
         else
-            emit_rows<false><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol,
-                                                                           values, delta_words);
+            emit_rows<false, 8><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values, delta_words);
     }
     return cudaGetLastError();
 }
