@@ -79,27 +79,32 @@ __device__ __forceinline__ uint32_t pad_bit(uint32_t nz, int c, int p, int L, ui
     return cc0 < lim ? 1u << (cc0 - c) : 0u;
 }
 
-template <bool kFast>
+// kCols columns per lane per chunk (16 for b_delta = 4: gaps inside a lane stay < 2^b).
+template <bool kFast, int kCols>
 __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp, 4)
     count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
                uint32_t* counts, int32_t* lastcol) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t nwarps = gridDim.x * kCompressWarpsPerCta;
     const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
+    constexpr uint32_t kStep = kWarp * kCols;
     for (uint32_t r = blockIdx.x * kCompressWarpsPerCta + (threadIdx.x >> 5); r < rows; r += nwarps) {
         const uint16_t* row = dense + (uint64_t)r * ld;
         int carry = -1;
         uint32_t cnt = 0;
-        // two chunks in flight per warp (64 KiB per SM at full occupancy covers the HBM latency)
-        uint4 next = fetch8(row, 8u * lane, cols, vec_base);
-        uint4 next2 = kWarp * 8 < cols ? fetch8(row, 8u * lane + kWarp * 8, cols, vec_base) : make_uint4(0, 0, 0, 0);
-        for (uint32_t c0 = 0; c0 < cols; c0 += kWarp * 8) {
-            const uint32_t c = c0 + 8u * lane;
-            const uint4 cur = next;
-            next = next2;
-            if (c0 + 2 * kWarp * 8 < cols) next2 = fetch8(row, c + 2 * kWarp * 8, cols, vec_base);
-            uint16_t h[8];
-            uint32_t nz = unpack8(cur, h);
+        uint4 next[kCols / 8];  // the next chunk's load is in flight while this one is classified
+#pragma unroll
+        for (int q = 0; q < kCols / 8; ++q) next[q] = fetch8(row, kCols * lane + 8 * q, cols, vec_base);
+        for (uint32_t c0 = 0; c0 < cols; c0 += kStep) {
+            const uint32_t c = c0 + kCols * lane;
+            uint16_t h[kCols];
+            uint32_t nz = 0;
+#pragma unroll
+            for (int q = 0; q < kCols / 8; ++q) nz |= unpack8(next[q], h + 8 * q) << (8 * q);
+            if (c0 + kStep < cols) {
+#pragma unroll
+                for (int q = 0; q < kCols / 8; ++q) next[q] = fetch8(row, c + kStep + 8 * q, cols, vec_base);
+            }
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
             int p = prev_nonzero(lane_last, lane, carry);
             cnt += __popc(nz);
@@ -339,10 +344,13 @@ cudaError_t launch_count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows,
                               uint32_t* counts, int32_t* lastcol, int sms, cudaStream_t s) {
     const int grid = (int)std::min<uint64_t>((rows + kCompressWarpsPerCta - 1) / kCompressWarpsPerCta, (uint64_t)sms * 8);
     if (grid > 0) {
-        if (bits >= 4)
-            count_rows<true><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+        const dim3 b(kCompressWarpsPerCta * kWarp);
+        if (bits == 4)
+            count_rows<true, 16><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+        else if (bits == 8)
+            count_rows<true, 8><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
         else
-            count_rows<false><<<grid, kCompressWarpsPerCta * kWarp, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
+            count_rows<false, 8><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, counts, lastcol);
     }
     return cudaGetLastError();
 }
