@@ -25,5 +25,6 @@ from .macko import (  # noqa: F401
     spmv,
     values_bytes,
     version,
+    wait_flags,
     write_mcko,
 )
