@@ -835,8 +835,10 @@ macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uin
     });
 }
 
-macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
-                               uint32_t flags) {
+namespace {
+// One SpMV launch (macko_dev_spmv_ex; macko_spmv_host adds a mapped host mirror of y).
+macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream, uint32_t flags,
+                         uint16_t* y_mirror) {
     return guarded([&] {
         if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
         if (flags & ~(uint32_t)(MACKO_SPMV_PDL | MACKO_SPMV_PEERS)) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
@@ -859,6 +861,7 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
+        a.y_mirror = y_mirror;
         if (flags & MACKO_SPMV_PEERS) {
             a.n_peer = m->n_peer;
             a.peers = m->peer_table.p;
@@ -874,6 +877,12 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
            "macko_spmv launch");
         g_launches.fetch_add(1);
     });
+}
+}  // namespace
+
+macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
+                               uint32_t flags) {
+    return spmv_launch(m, d_x, d_y, stream, flags, nullptr);
 }
 
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
@@ -914,14 +923,11 @@ macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t*
         } else {
             ck(cudaMemcpyAsync(m->hx_aligned, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
         }
-        const macko_status sp = macko_dev_spmv_ex(m, m->hx_aligned, m->hy.p, st, dx ? MACKO_SPMV_PDL : 0u);
+        // a mapped host y is written by the SpMV itself, row by row as rows finish (no push step)
+        const macko_status sp =
+            spmv_launch(m, m->hx_aligned, m->hy.p, st, dx ? MACKO_SPMV_PDL : 0u, m->pad_nnz ? dy : nullptr);
         if (sp != MACKO_OK) fail(sp, g_err);
-        if (dy) {
-            ck(mk::launch_copy_u16(m->hy.p, dy, (uint32_t)m->rows, 8, true, st), "y push");
-            g_launches.fetch_add(1);
-        } else {
-            ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
-        }
+        if (!dy || !m->pad_nnz) ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
         ck(cudaStreamSynchronize(st), "sync");
     });
 }

@@ -199,6 +199,7 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
 // lane 0).
 __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
     a.y[r] = v;
+    if (a.y_mirror) a.y_mirror[r] = v;
     for (uint32_t p = 0; p < a.n_peer; ++p) reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[p])))[r] = v;
 }
 

@@ -52,6 +52,7 @@ struct SpmvArgs {
     uint32_t n_peer;       // fused all-gather: y rows also go to peers->y[0..n_peer) and each CTA adds 1
                            // to *peers->flag[p] (system scope) once its rows are written
     const PeerTable* peers;
+    uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
     SpmvPlanDev plan;
 };
 
