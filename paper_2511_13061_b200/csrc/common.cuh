@@ -15,7 +15,10 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // unit and unit sums are added sequentially into the row sum.
 constexpr int kEltsPerLane = 8;
 constexpr int kStepElts = kWarp * kEltsPerLane;  // 256
-constexpr int kUnitSteps = 8;
+#ifndef MACKO_UNIT_STEPS
+#define MACKO_UNIT_STEPS 8
+#endif
+constexpr int kUnitSteps = MACKO_UNIT_STEPS;  // build knob for experiments (the oracle takes it as a parameter)
 constexpr int kUnitElts = kStepElts * kUnitSteps;  // 2048
 
 // ---- streaming loads (read-once data: no L1 allocation) ----
