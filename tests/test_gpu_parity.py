@@ -473,3 +473,18 @@ def test_power_law_row_lengths(cuda):
     for order in (0, 1):
         dm.set_order(order)
         check_y(A, m, x, gpu_spmv(dm, x), False, ("zipf", order), order)
+
+
+def test_other_widths_every_x_mode(cuda):
+    # b_delta 1 / 2 / 8: every x_mode built for them gives the same bits (the oracle order)
+    for bits, d in ((1, 0.9), (2, 0.6), (8, 0.05)):
+        A = O.gen_dense(1500, 6000, d, 90 + bits)
+        x = O.gen_vector(6000, 91)
+        m = O.encode_dense(A, bits)
+        dm = gpu_encode(A, bits)
+        ref = b200_y(dm, m, x)
+        for xm in (0, 1, 6, 7, 8, 10):
+            dm.configure(xm)
+            assert np.array_equal(gpu_spmv(dm, x), ref), (bits, xm)
+        with pytest.raises(ValueError):
+            dm.configure(9)  # b_delta = 4 only
