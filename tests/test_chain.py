@@ -110,3 +110,25 @@ def test_persistent_chain_rejects_flat_walk(cuda):
     with pytest.raises(ValueError):
         ch.persistent()
     ch.close()
+
+
+def test_chain_create_rejects_bad_ops(cuda):
+    # b_delta != 4 and a misaligned x are refused; a valid one-op chain equals macko_dev_spmv
+    w = torch.empty((512, 1024), dtype=torch.float16, device=cuda)
+    M.gen_dense(w, 512, 1024, 0.5, seed=1)
+    dm8 = M.DeviceMatrix.from_dense(w, b_delta=8)
+    dm4 = M.DeviceMatrix.from_dense(w)
+    buf = torch.zeros(4096, dtype=torch.float16, device=cuda)
+    y = torch.zeros(512, dtype=torch.float16, device=cuda)
+    with pytest.raises(ValueError):
+        M.Chain([(dm8, buf[:1024], y)])
+    with pytest.raises(ValueError):
+        M.Chain([(dm4, buf[1:1025], y)])  # 2-byte aligned only: the chain stages x without a copy
+    ch = M.Chain([(dm4, buf[:1024], y)])
+    ch.run()
+    torch.cuda.synchronize()
+    ref = M.spmv(dm4, buf[:1024])
+    assert torch.equal(ref, y)
+    ch.close()
+    dm8.close()
+    dm4.close()
