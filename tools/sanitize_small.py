@@ -1,0 +1,48 @@
+"""compute-sanitizer driver: small SpMVs of both walks and every width, the compressor, MCKO, the
+persistent chain and the host-buffer path — checked against the oracle (tools only)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import oracle as O  # noqa: E402
+from paper_2511_13061_b200 import decoder_chain as D  # noqa: E402
+from paper_2511_13061_b200 import macko as M  # noqa: E402
+from tests.helpers import b200_y, to_dev, to_host_u16  # noqa: E402
+
+bad = 0
+for bits in (1, 2, 4, 8):
+    for R, C, d in ((37, 1000, 0.3), (300, 2500, 0.9), (5, 9000, 0.05)):
+        A = O.gen_dense(R, C, d, R + C + bits)
+        x = O.gen_vector(C, 3)
+        m = O.encode_dense(A, bits)
+        dm = M.DeviceMatrix.from_dense(to_dev(A), b_delta=bits)
+        h = dm.download()
+        bad += int(not np.array_equal(h.values, m.values))
+        for order in (0, 1):
+            dm.set_order(order)
+            y = to_host_u16(M.spmv(dm, to_dev(x)))
+            bad += int(not np.array_equal(y, b200_y(dm, m, x)))
+        dm.close()
+A = O.gen_dense(200, 700, 0.5, 1)
+dm = M.DeviceMatrix.from_dense(to_dev(A))
+x = O.gen_vector(700, 2)
+hx = torch.empty(700, dtype=torch.int16, pin_memory=True)
+hx.numpy().view(np.uint16)[:] = x
+hy = torch.zeros(200, dtype=torch.int16, pin_memory=True)
+dm.spmv_host(hx.numpy().view(np.uint16), hy.numpy().view(np.uint16))
+bad += int(not np.array_equal(hy.numpy().view(np.uint16), b200_y(dm, O.encode_dense(A), x)))
+ch = D.SparseDecoderChain(D.ChainShape(2, 256, 688), density=0.5, seed=3)
+M.gen_vector(ch.acts["h"], 256, seed=4)
+ch.acts["h"].mul_(2.0**-8)
+h0 = ch.acts["h"].clone()
+ch.forward_token(pdl=True)
+torch.cuda.synchronize()
+ref = to_host_u16(ch.acts["h"])
+ch.acts["h"].copy_(h0)
+ch.forward_token_persistent()
+torch.cuda.synchronize()
+bad += int(not np.array_equal(to_host_u16(ch.acts["h"]), ref))
+print("mismatches", bad)
