@@ -155,6 +155,13 @@ def test_fused_allgather_single_rank(cuda):
         torch.cuda.synchronize()
         assert np.array_equal(to_host_u16(y), ref), step
         assert int(fused.flags.item()) == step * fused.grid
+    # the flat walk stores and signals the same way (set_order re-plans; the peer table stays)
+    dm.set_order(1)
+    ref1 = b200_y(dm, O.encode_dense(A), x)
+    y = fused(to_dev(x))
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host_u16(y), ref1)
+    assert int(fused.flags.item()) == 4 * fused.grid
     fused.close()
     dm.close()
 
