@@ -39,7 +39,15 @@ typedef enum macko_status {
 } macko_status;
 
 /* Opaque device-resident MACKO matrix (owns its values / deltas / row_pointers buffers and
- * the SpMV work plan).  Immutable after construction; usable from any stream on its device. */
+ * the SpMV work plan).  Immutable after construction: one handle may be used
+ * from any number of host threads and streams of its device at once.  Everything a launch
+ * mutates besides y (split-row counters and partial sums, the aligned copy of a misaligned x,
+ * macko_spmv_host's device buffers) lives in a per-stream workspace, so launches on different
+ * streams never share state; x texture objects are cached per x buffer and destroyed only with
+ * the handle.  Workspaces are created on a stream's first SpMV, which must not be inside a
+ * stream capture (run one SpMV on the capture stream first); a captured CUDA graph uses the
+ * workspace of its capture stream.  macko_dev_configure / macko_dev_free must not run
+ * concurrently with SpMVs of the same handle. */
 typedef struct macko_dev_matrix macko_dev_matrix;
 
 typedef struct macko_dev_info {
@@ -84,8 +92,8 @@ macko_status macko_dev_download(const macko_dev_matrix* m, uint16_t* values, uin
 
 /* y = A*x on the device: fp16 in, fp32 accumulate, one RNE per row, fp16 out.
  * Replaces reference_spmv / warp_spmv.  d_x: cols fp16, d_y: rows fp16.
- * SpMVs of one matrix must be stream-ordered: the handle holds the arrival counters of rows
- * split between warps (reset by each launch).  Different matrices may run concurrently. */
+ * Asynchronous and stream-ordered; concurrent calls on different streams are safe (per-stream
+ * workspaces, see macko_dev_matrix).  x must not overlap y. */
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y,
                             void* stream);
 
@@ -97,31 +105,24 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
  * with macko_dev_set_peers (P2P over NVLink), and each CTA then adds 1 (system scope) to this
  * rank's counter in every peer's flag array; consumers wait with macko_wait_flags. */
 #define MACKO_SPMV_PEERS 2u
+/* With MACKO_SPMV_PEERS: store into the peer table's y bank 1 (macko_dev_set_peer_bank) instead of
+ * bank 0 — double-buffered outputs, so a step may read the previous step's y as its x. */
+#define MACKO_SPMV_PEER_BANK1 4u
 macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
                                uint32_t flags);
 
-/* End-to-end call with HOST buffers (what a CPU caller of reference_spmv would bind): copies
- * x host->device, runs macko_dev_spmv, copies y device->host, synchronises the stream.
- * Pinned host buffers make the copies asynchronous DMA. */
-macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream);
+/* End-to-end call with HOST buffers (what a CPU caller of reference_spmv would bind): x
+ * host->device, the SpMV, y device->host, then the stream is synchronised.  Pinned
+ * (device-mapped) host buffers are read and written by the kernels directly: a one-CTA kernel
+ * pulls x, the SpMV follows as its programmatic dependent and stores every y row into the host
+ * buffer as well; pageable buffers take cudaMemcpyAsync both ways.  h_x: cols fp16, h_y: rows
+ * fp16.  Device scratch is per stream (thread-safe like macko_dev_spmv). */
+macko_status macko_spmv_host(const macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream);
 
 /* Device-side validate_macko (convert.hpp:25-27): every decoded column < cols.  Synchronous. */
 macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
 
 macko_status macko_dev_free(macko_dev_matrix* m);
-
-/* ---- persistent SpMV chains (decoder stacks) ------------------------------------------------
- * A fixed sequence of dependent SpMVs y_k = A_k x_k, where x_k may be (a slice of) an earlier
- * y_j, run by ONE persistent cooperative kernel: each warp sets up op k+1 (plan record, first
- * matrix ring fills) as soon as its part of op k is done and a grid barrier orders x_k after
- * the op that wrote it, so the weight stream keeps HBM busy across the dependencies.  The
- * matrices and vectors must outlive the chain; x buffers must be texture-aligned (512 B).
- * Results are bit-identical to running the ops one by one with macko_dev_spmv. */
-typedef struct macko_chain macko_chain;
-macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint16_t* const* xs, uint16_t* const* ys,
-                                uint32_t n_ops, macko_chain** out);
-macko_status macko_chain_run(macko_chain* c, void* stream); /* one launch; CUDA-graph capturable */
-macko_status macko_chain_free(macko_chain* c);
 
 /* ---- MCKO container (io.cpp write_macko / read_macko are absent) ----------
  * File: 32-byte little-endian header "MCKO" | u16 version=1 | u8 b_val=16 | u8 b_delta | u64 R |
@@ -176,6 +177,10 @@ macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, i
  * After a MACKO_SPMV_PEERS launch every counter has grown by the launch's grid size.  Synchronous. */
 macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, uint32_t* const* peer_flags, uint32_t n,
                                  void* stream);
+/* Second y destination set (bank 1, used with MACKO_SPMV_PEER_BANK1): same peer count and flags as
+ * macko_dev_set_peers, which resets both banks to its peer_y.  Synchronous. */
+macko_status macko_dev_set_peer_bank(macko_dev_matrix* m, uint32_t bank, uint16_t* const* peer_y, uint32_t n,
+                                     void* stream);
 /* Stream-ordered wait until d_flags[i] >= target (wrap-around compare) for i < n (n <= 32): the
  * consumer side of MACKO_SPMV_PEERS.  Traps after ~4 s instead of hanging. */
 macko_status macko_wait_flags(const uint32_t* d_flags, uint32_t n, uint32_t target, void* stream);
@@ -190,20 +195,17 @@ macko_status macko_ipc_close(void* d_base);
 typedef struct macko_launch_info {
     uint32_t grid, block, warps, ctas_per_sm, n_split_rows;
     uint32_t x_in_smem; /* x_mode: how x is gathered — 0 texture only, 1 fp16 shared-memory table
-                         * only, 6..11 table + texture split over the element slots */
+                         * only, 6 / 7 / 8 / 10 table + texture split over the element slots
+                         * */
     uint64_t n_units, smem_bytes;
-    uint32_t order; /* 0: ROMA row-relative walk (oracle mo_b200_order_spmv, the default), 1: flat
-                     * global windows (oracle mo_b200_flat_spmv) — DESIGN.md §2.1 */
-    uint32_t reserved;
+    uint32_t reserved0, reserved;
 } macko_launch_info;
 macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info* out);
-/* Re-plan the SpMV launch: x_mode (-1 automatic, else as above; 9 and 11 exist for b_delta = 4
- * only) and a cap on CTAs (k > 0: use k/4 of the persistent CTAs; 0 automatic).  Results are identical for every setting (the summation order does not
- * depend on the plan); exposed for tuning and for the grid-independence tests.  Synchronous. */
+/* Re-plan the SpMV launch: x_mode (-1 automatic, else as above) and a cap on CTAs (k > 0: use
+ * k/4 of the persistent CTAs; 0 automatic).  Results are identical for every setting (the
+ * summation order does not depend on the plan); exposed for tuning and for the grid-independence
+ * tests.  Synchronous; not concurrent with SpMVs of the handle. */
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream);
-/* Choose the SpMV walk (launch_info.order) and re-plan.  Both are deterministic and independent of
- * the plan; they differ in where lane / unit boundaries sit, hence in the float summation order. */
-macko_status macko_dev_set_order(macko_dev_matrix* m, int order, void* stream);
 /* Number of kernels this library has launched in the process (for bench gpu_launches). */
 uint64_t macko_kernel_launches(void);
 

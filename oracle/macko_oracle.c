@@ -164,7 +164,10 @@ typedef struct {
 static inline void enc_emit(row_encoder* en, uint16_t v, uint32_t delta) {
     if (en->values) {
         en->values[en->at] = v;
-        put_code(en->deltas, en->at, en->bits, delta - 1);
+        /* atomic OR: in the threaded encoder two row ranges may share a codeword byte */
+        const unsigned per = 8u / en->bits;
+        __atomic_fetch_or(&en->deltas[en->at / per], (uint8_t)((delta - 1) << ((unsigned)(en->at % per) * en->bits)),
+                          __ATOMIC_RELAXED);
     }
     ++en->at;
 }
@@ -478,30 +481,6 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
     return MO_OK;
 }
 
-/* The flat-window kernel's order: lane = (e mod 256) / 8 by global position, units = global
- * 2048-element blocks (see macko_oracle.h).  Independent of the launch plan by construction. */
-int mo_b200_flat_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values,
-                      const uint8_t* deltas, const uint32_t* rp, const uint16_t* x, uint16_t* y) {
-    if (!mo_is_valid_delta_bits(bits)) return fail(MO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits");
-    for (uint64_t r = 0; r < rows; ++r) {
-        const uint64_t s = rp[r], e = rp[r + 1];
-        float row_acc = 0.0f;
-        int64_t col = -1;
-        for (uint64_t u0 = s & ~(uint64_t)2047; u0 < e; u0 += 2048) {
-            float acc[32] = {0};
-            const uint64_t lo = u0 > s ? u0 : s, hi = u0 + 2048 < e ? u0 + 2048 : e;
-            for (uint64_t i = lo; i < hi; ++i) {
-                col += code_at(deltas, i, bits) + 1;
-                if ((uint64_t)col >= cols) return fail(MO_EFORMAT, "decoded column index past the column bound");
-                acc[(i % 256) / 8] += mo_half_to_float(values[i]) * mo_half_to_float(x[col]);
-            }
-            row_acc += lane_tree(acc);
-        }
-        y[r] = mo_float_to_half(row_acc);
-    }
-    return MO_OK;
-}
-
 /* ------------------------------------------------------------------------------------------
  * Synthetic inputs.  gen_random leaves the magnitude distribution and RNG
  * undocumented (generate.cpp is absent), so this generator is ours and identical on CPU and
@@ -573,4 +552,173 @@ void mo_float_to_half_array(const float* x, uint64_t n, uint16_t* out) {
 
 void mo_half_to_float_array(const uint16_t* h, uint64_t n, float* out) {
     for (uint64_t i = 0; i < n; ++i) out[i] = mo_half_to_float(h[i]);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Threaded variants for full-size parity tests (36864x12288 ... 131072x32768): rows are
+ * independent (convert.hpp:12-16: every row restarts at the virtual column -1), so a row
+ * partition over pthreads gives byte-identical output.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t r0, r1, cols, row0;
+    uint32_t thr24;
+    uint64_t seed;
+    int int_mode, status;
+    unsigned bits, unit_steps;
+    const uint16_t* dense;
+    uint16_t* out;
+    uint32_t* counts;
+    const uint32_t* rp;
+    uint16_t* values;
+    uint8_t* deltas;
+    const uint16_t* x;
+} mt_job;
+
+static void run_jobs(mt_job* jobs, int n, void* (*fn)(void*)) {
+    pthread_t* th = (pthread_t*)calloc((size_t)n, sizeof(pthread_t));
+    for (int t = 0; t < n; ++t) pthread_create(&th[t], NULL, fn, &jobs[t]);
+    for (int t = 0; t < n; ++t) pthread_join(th[t], NULL);
+    free(th);
+}
+
+static int clamp_threads(int nthreads, uint64_t rows) {
+    if (nthreads < 1) nthreads = 1;
+    if ((uint64_t)nthreads > rows) nthreads = rows ? (int)rows : 1;
+    return nthreads;
+}
+
+static void* gen_rows_job(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    for (uint64_t r = j->r0; r < j->r1; ++r)
+        for (uint64_t c = 0; c < j->cols; ++c)
+            j->out[r * j->cols + c] = mo_gen_value(j->seed, (j->row0 + r) * j->cols + c, j->thr24, j->int_mode);
+    return NULL;
+}
+
+void mo_gen_dense_rows_mt(uint64_t row0, uint64_t rows, uint64_t cols, uint32_t thr24, uint64_t seed, int int_mode,
+                          uint16_t* out, int nthreads) {
+    nthreads = clamp_threads(nthreads, rows);
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].r0 = rows * t / nthreads;
+        jobs[t].r1 = rows * (t + 1) / nthreads;
+        jobs[t].cols = cols;
+        jobs[t].row0 = row0;
+        jobs[t].thr24 = thr24;
+        jobs[t].seed = seed;
+        jobs[t].int_mode = int_mode;
+        jobs[t].out = out;
+    }
+    run_jobs(jobs, nthreads, gen_rows_job);
+    free(jobs);
+}
+
+static void* count_rows_job(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    row_encoder en = {NULL, NULL, 0, j->bits, -1, 1u << j->bits};
+    for (uint64_t r = j->r0; r < j->r1; ++r) {
+        const uint16_t* row = j->dense + r * j->cols;
+        en.prev = -1;
+        en.at = 0;
+        for (uint64_t c = 0; c < j->cols; ++c)
+            if (!mo_half_is_zero(row[c])) enc_push(&en, (int64_t)c, row[c]);
+        j->counts[r] = (uint32_t)en.at;
+    }
+    return NULL;
+}
+
+static void* fill_rows_job(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    row_encoder en = {j->values, j->deltas, 0, j->bits, -1, 1u << j->bits};
+    for (uint64_t r = j->r0; r < j->r1; ++r) {
+        const uint16_t* row = j->dense + r * j->cols;
+        en.prev = -1;
+        en.at = j->rp[r];
+        for (uint64_t c = 0; c < j->cols; ++c)
+            if (!mo_half_is_zero(row[c])) enc_push(&en, (int64_t)c, row[c]);
+    }
+    return NULL;
+}
+
+/* encode_dense over a row partition: count pass (per-row entries), scan, fill pass. */
+int mo_encode_dense_count_mt(const uint16_t* dense, uint64_t rows, uint64_t cols, unsigned bits, uint32_t* rp,
+                             uint64_t* pad_nnz, int nthreads) {
+    if (!mo_is_valid_delta_bits(bits)) return fail(MO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits");
+    nthreads = clamp_threads(nthreads, rows);
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].r0 = rows * t / nthreads;
+        jobs[t].r1 = rows * (t + 1) / nthreads;
+        jobs[t].cols = cols;
+        jobs[t].bits = bits;
+        jobs[t].dense = dense;
+        jobs[t].counts = rp + 1;
+    }
+    run_jobs(jobs, nthreads, count_rows_job);
+    free(jobs);
+    uint64_t acc = 0;
+    rp[0] = 0;
+    for (uint64_t r = 0; r < rows; ++r) {
+        acc += rp[r + 1];
+        if (acc > 0xFFFFFFFFull) return fail(MO_EINVAL, "pad_nnz does not fit u32 row pointers");
+        rp[r + 1] = (uint32_t)acc;
+    }
+    *pad_nnz = acc;
+    return MO_OK;
+}
+
+int mo_encode_dense_fill_mt(const uint16_t* dense, uint64_t rows, uint64_t cols, unsigned bits, const uint32_t* rp,
+                            uint16_t* values, uint8_t* deltas, int nthreads) {
+    if (!mo_is_valid_delta_bits(bits)) return fail(MO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits");
+    const uint64_t pad_nnz = rows ? rp[rows] : 0;
+    memset(values, 0, (size_t)mo_values_bytes(pad_nnz));
+    memset(deltas, 0, (size_t)mo_delta_bytes(pad_nnz, bits));
+    nthreads = clamp_threads(nthreads, rows);
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].r0 = rows * t / nthreads;
+        jobs[t].r1 = rows * (t + 1) / nthreads;
+        jobs[t].cols = cols;
+        jobs[t].bits = bits;
+        jobs[t].dense = dense;
+        jobs[t].rp = rp;
+        jobs[t].values = values;
+        jobs[t].deltas = deltas;
+    }
+    run_jobs(jobs, nthreads, fill_rows_job);
+    free(jobs);
+    return MO_OK;
+}
+
+static void* order_rows_job(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    /* the row range's own slice of row pointers (absolute offsets stay valid) */
+    j->status = mo_b200_order_spmv(j->r1 - j->r0, j->cols, j->bits, j->values, j->deltas, j->rp + j->r0, j->x,
+                                   j->out + j->r0, j->unit_steps);
+    return NULL;
+}
+
+int mo_b200_order_spmv_mt(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values, const uint8_t* deltas,
+                          const uint32_t* rp, const uint16_t* x, uint16_t* y, unsigned unit_steps, int nthreads) {
+    if (!mo_is_valid_delta_bits(bits)) return fail(MO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits");
+    nthreads = clamp_threads(nthreads, rows);
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].r0 = rows * t / nthreads;
+        jobs[t].r1 = rows * (t + 1) / nthreads;
+        jobs[t].cols = cols;
+        jobs[t].bits = bits;
+        jobs[t].unit_steps = unit_steps;
+        jobs[t].values = (uint16_t*)values;
+        jobs[t].deltas = (uint8_t*)deltas;
+        jobs[t].rp = rp;
+        jobs[t].x = x;
+        jobs[t].out = y;
+    }
+    run_jobs(jobs, nthreads, order_rows_job);
+    int st = MO_OK;
+    for (int t = 0; t < nthreads; ++t)
+        if (jobs[t].status != MO_OK) st = jobs[t].status;
+    free(jobs);
+    return st == MO_OK ? MO_OK : fail(st, "decoded column index past the column bound");
 }

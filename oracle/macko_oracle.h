@@ -95,13 +95,16 @@ int mo_b200_order_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16
                        const uint8_t* deltas, const uint32_t* row_ptrs, const uint16_t* x,
                        uint16_t* y, unsigned unit_steps);
 
-/* The flat-window kernel's order: lanes, steps and units are aligned to GLOBAL
- * element positions — element e of a row goes to lane (e mod 256)/8; the row's elements are
- * split at global 2048-element unit boundaries; within a unit each lane sums its elements
- * sequentially, the 32 lanes are xor-tree reduced, and the unit sums are added sequentially into
- * the row accumulator (+0 start); one RNE at the end. */
-int mo_b200_flat_spmv(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values,
-                      const uint8_t* deltas, const uint32_t* row_ptrs, const uint16_t* x, uint16_t* y);
+/* Threaded variants (row partitions; byte-identical to the single-threaded functions), for the
+ * full-size parity tests. */
+void mo_gen_dense_rows_mt(uint64_t row0, uint64_t rows, uint64_t cols, uint32_t thr24, uint64_t seed, int int_mode,
+                          uint16_t* out, int nthreads);
+int mo_encode_dense_count_mt(const uint16_t* dense, uint64_t rows, uint64_t cols, unsigned bits, uint32_t* rp,
+                             uint64_t* pad_nnz, int nthreads);
+int mo_encode_dense_fill_mt(const uint16_t* dense, uint64_t rows, uint64_t cols, unsigned bits, const uint32_t* rp,
+                            uint16_t* values, uint8_t* deltas, int nthreads);
+int mo_b200_order_spmv_mt(uint64_t rows, uint64_t cols, unsigned bits, const uint16_t* values, const uint8_t* deltas,
+                          const uint32_t* rp, const uint16_t* x, uint16_t* y, unsigned unit_steps, int nthreads);
 
 /* ---- synthetic inputs (our counter-hash generator) ---- */
 uint32_t mo_density_threshold(double density);

@@ -76,7 +76,10 @@ def lib() -> C.CDLL:
         L.mo_warp_prefix_sum.argtypes = [_u32p, _u32p]
         L.mo_warp_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p]
         L.mo_b200_order_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p, C.c_uint]
-        L.mo_b200_flat_spmv.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p]
+        L.mo_b200_order_spmv_mt.argtypes = [_u64, _u64, C.c_uint, _u16p, _u8p, _u32p, _u16p, _u16p, C.c_uint, C.c_int]
+        L.mo_gen_dense_rows_mt.argtypes = [_u64, _u64, _u64, C.c_uint32, _u64, C.c_int, _u16p, C.c_int]
+        L.mo_encode_dense_count_mt.argtypes = [_u16p, _u64, _u64, C.c_uint, _u32p, C.POINTER(_u64), C.c_int]
+        L.mo_encode_dense_fill_mt.argtypes = [_u16p, _u64, _u64, C.c_uint, _u32p, _u16p, _u8p, C.c_int]
         L.mo_density_threshold.restype = C.c_uint32
         L.mo_density_threshold.argtypes = [C.c_double]
         L.mo_gen_dense.argtypes = [_u64, _u64, C.c_uint32, _u64, C.c_int, _u16p]
@@ -221,16 +224,22 @@ def _nz(a: np.ndarray) -> np.ndarray:
     return a if a.size else np.zeros(1, a.dtype)
 
 
-def encode_dense(dense: np.ndarray, bits: int = 4) -> Macko:
+def encode_dense(dense: np.ndarray, bits: int = 4, nthreads: int = 1) -> Macko:
     d = np.ascontiguousarray(dense, np.uint16)
     R, Cc = d.shape
     rp = np.zeros(R + 1, np.uint32)
     pn = _u64(0)
-    _check(lib().mo_encode_dense_count(_nz(d.reshape(-1)), R, Cc, bits, rp, C.byref(pn)))
+    if nthreads > 1:
+        _check(lib().mo_encode_dense_count_mt(_nz(d.reshape(-1)), R, Cc, bits, rp, C.byref(pn), nthreads))
+    else:
+        _check(lib().mo_encode_dense_count(_nz(d.reshape(-1)), R, Cc, bits, rp, C.byref(pn)))
     values = np.zeros(values_bytes(pn.value) // 2, np.uint16)
     deltas = np.zeros(delta_bytes(pn.value, bits), np.uint8)
     if pn.value:
-        _check(lib().mo_encode_dense_fill(_nz(d.reshape(-1)), R, Cc, bits, rp, values, deltas))
+        if nthreads > 1:
+            _check(lib().mo_encode_dense_fill_mt(_nz(d.reshape(-1)), R, Cc, bits, rp, values, deltas, nthreads))
+        else:
+            _check(lib().mo_encode_dense_fill(_nz(d.reshape(-1)), R, Cc, bits, rp, values, deltas))
     return Macko(R, Cc, bits, values, deltas, rp)
 
 
@@ -276,23 +285,29 @@ def warp_spmv(m: Macko, x: np.ndarray) -> np.ndarray:
     return y[: m.rows]
 
 
-def b200_order_spmv(m: Macko, x: np.ndarray, unit_steps: int) -> np.ndarray:
+def b200_order_spmv(m: Macko, x: np.ndarray, unit_steps: int, nthreads: int = 1) -> np.ndarray:
     y = np.zeros(max(m.rows, 1), np.uint16)
-    _check(lib().mo_b200_order_spmv(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), m.row_ptrs,
-                                    _nz(np.ascontiguousarray(x, np.uint16)), y, unit_steps))
-    return y[: m.rows]
-
-
-def b200_flat_spmv(m: Macko, x: np.ndarray) -> np.ndarray:
-    """The flat-window kernel's order (global lane / unit alignment)."""
-    y = np.zeros(max(m.rows, 1), np.uint16)
-    _check(lib().mo_b200_flat_spmv(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), m.row_ptrs,
-                                   _nz(np.ascontiguousarray(x, np.uint16)), y))
+    xx = _nz(np.ascontiguousarray(x, np.uint16))
+    rp = np.ascontiguousarray(m.row_ptrs, np.uint32)
+    if nthreads > 1:
+        _check(lib().mo_b200_order_spmv_mt(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), rp, xx, y,
+                                           unit_steps, nthreads))
+    else:
+        _check(lib().mo_b200_order_spmv(m.rows, m.cols, m.b_delta, _nz(m.values), _nz(m.deltas), rp, xx, y,
+                                        unit_steps))
     return y[: m.rows]
 
 
 def density_threshold(d: float) -> int:
     return lib().mo_density_threshold(d)
+
+
+def gen_dense_rows(row0: int, rows: int, cols: int, density: float, seed: int, int_mode: bool = False,
+                   nthreads: int = 1) -> np.ndarray:
+    """Rows [row0, row0 + rows) of the generator's conceptual matrix (threaded)."""
+    out = np.zeros(max(rows * cols, 1), np.uint16)
+    lib().mo_gen_dense_rows_mt(row0, rows, cols, density_threshold(density), seed, int(int_mode), out, nthreads)
+    return out[: rows * cols].reshape(rows, cols)
 
 
 def gen_dense(rows: int, cols: int, density: float, seed: int, int_mode: bool = False) -> np.ndarray:

@@ -4,7 +4,6 @@ The product is libmacko_cuda.so (include/macko_cuda.h).  This package is the thi
 mirror of the reference interface used by tests and bench.py; it never falls back to CPU.
 """
 from .macko import (  # noqa: F401
-    Chain,
     CudaError,
     DeviceMatrix,
     FormatError,

@@ -19,10 +19,10 @@ EXPORTS = (
     "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_get_info",
     "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
-    "macko_dev_launch_info", "macko_dev_configure", "macko_dev_set_order", "macko_kernel_launches",
+    "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
-    "macko_mm_read_dense", "macko_chain_create", "macko_chain_run", "macko_chain_free", "macko_sharded_spmv",
-    "macko_dev_set_peers", "macko_wait_flags", "macko_ipc_get_handle", "macko_ipc_open", "macko_ipc_close",
+    "macko_mm_read_dense", "macko_sharded_spmv",
+    "macko_dev_set_peers", "macko_dev_set_peer_bank", "macko_wait_flags", "macko_ipc_get_handle", "macko_ipc_open", "macko_ipc_close",
 )
 
 
@@ -66,7 +66,7 @@ class LaunchInfo(C.Structure):
     _fields_ = [
         ("grid", C.c_uint32), ("block", C.c_uint32), ("warps", C.c_uint32), ("ctas_per_sm", C.c_uint32),
         ("n_split_rows", C.c_uint32), ("x_in_smem", C.c_uint32), ("n_units", C.c_uint64), ("smem_bytes", C.c_uint64),
-        ("order", C.c_uint32), ("reserved", C.c_uint32),
+        ("reserved0", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 
@@ -122,18 +122,12 @@ def load() -> C.CDLL:
     L.macko_mcko_write_dev.argtypes = [vp, cp, vp]
     L.macko_mcko_read_dev.restype = st
     L.macko_mcko_read_dev.argtypes = [C.c_int, cp, vp, C.POINTER(vp)]
-    L.macko_dev_set_order.restype = st
-    L.macko_dev_set_order.argtypes = [vp, C.c_int, vp]
-    L.macko_chain_create.restype = st
-    L.macko_chain_create.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), u32, C.POINTER(vp)]
-    L.macko_chain_run.restype = st
-    L.macko_chain_run.argtypes = [vp, vp]
-    L.macko_chain_free.restype = st
-    L.macko_chain_free.argtypes = [vp]
     L.macko_sharded_spmv.restype = st
     L.macko_sharded_spmv.argtypes = [vp, vp, C.c_int, vp, vp, C.c_uint64, vp]
     L.macko_dev_set_peers.restype = st
     L.macko_dev_set_peers.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_uint32, vp]
+    L.macko_dev_set_peer_bank.restype = st
+    L.macko_dev_set_peer_bank.argtypes = [vp, C.c_uint32, C.POINTER(C.c_void_p), C.c_uint32, vp]
     L.macko_wait_flags.restype = st
     L.macko_wait_flags.argtypes = [vp, C.c_uint32, C.c_uint32, vp]
     L.macko_ipc_get_handle.restype = st

@@ -11,8 +11,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <set>
 #include <cstring>
+#include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -97,6 +98,23 @@ constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (el
 
 }  // namespace
 
+// Per-stream mutable state of one matrix (a handle is read-only after build and
+// may be shared across streams and threads).  SpMVs on one stream are ordered, so everything a
+// launch writes besides y lives here: the split-row arrival counters (zero between launches:
+// each launch's last arrival resets them) and partial sums, the aligned copy of a misaligned x,
+// and macko_spmv_host's device x / y.  A captured CUDA graph keeps the workspace of its capture
+// stream.
+struct Workspace {
+    DevBuf<uint32_t> counters;  // n_split arrival counters
+    DevBuf<float> partials;     // n_slots per-unit partial sums of split rows
+    DevBuf<uint16_t> xcopy;     // texture-aligned copy of a misaligned x
+    DevBuf<uint16_t> hx, hy;    // macko_spmv_host device buffers (hx texture-aligned inside)
+    uint16_t* hx_aligned = nullptr;
+};
+
+constexpr size_t kMaxWorkspaces = 16;  // streams per matrix before the pool is recycled
+constexpr size_t kMaxTextures = 64;    // cached x texture objects per matrix
+
 struct macko_dev_matrix {
     int device = 0;
     int sms = 0;
@@ -106,49 +124,33 @@ struct macko_dev_matrix {
     DevBuf<uint8_t> deltas;
     DevBuf<uint32_t> row_ptrs;
     std::vector<uint32_t> h_row_ptrs;
-    // SpMV plan
-    int x_mode = 1;             // 0 global x, 1 fp16 smem table, 2 pair smem table
-    int force_x_mode = -1;      // macko_dev_configure overrides (-1 / 0 = automatic)
+    // SpMV plan (immutable between macko_dev_configure calls)
+    int x_mode = 1;             // 0 texture only, 1 fp16 smem table, 6 / 7 / 8 / 10 table + texture split
+    int force_x_mode = -1;      // macko_dev_configure override (-1 = automatic rule)
     int force_ctas = 0;
-    int order = 0;              // 0: ROMA row-relative walk, 1: flat global windows
     uint32_t ring = 0;          // TMA ring slots per warp
     size_t ring_offset = 0;     // x table bytes (rings follow it in dynamic smem)
     size_t smem = 0;
     int grid = 0, ctas_per_sm = 0;
     uint32_t n_chunks = 0, n_split = 0;
-    uint64_t n_units = 0;
+    uint64_t n_units = 0, n_slots = 0;
     DevBuf<uint32_t> plan_recs;  // W mk::WarpPlan records
-    DevBuf<uint32_t> plan_u32;   // S split records {slot, first, pieces, 0} | S counters
-    DevBuf<float> partials;
-    mk::SpmvPlanDev plan{};
-    // scratch for macko_spmv_host (x texture-aligned inside hx, so the SpMV needs no staging copy)
-    DevBuf<uint16_t> hx, hy;
+    DevBuf<uint32_t> plan_u32;   // S split records {slot, first, pieces, 0}
+    mk::SpmvPlanDev plan{};      // counters / partials filled per launch from the stream's workspace
     DevBuf<mk::PeerTable> peer_table;  // fused all-gather destinations (macko_dev_set_peers)
+    mk::PeerTable h_peers{};           // host copy of the table
     uint32_t n_peer = 0;
-    uint16_t* hx_aligned = nullptr;
-    // x as a 1-D fp16 texture for x_mode >= 3 (created per x buffer, reused while it stays the same)
-    mutable std::mutex tex_mu;
-    mutable const void* tex_ptr = nullptr;
-    mutable cudaTextureObject_t tex = 0;
-    mutable int tex_align = 0;
-    mutable DevBuf<uint16_t> xcopy;  // aligned copy of a misaligned x
-    ~macko_dev_matrix() {
-        if (tex) cudaDestroyTextureObject(tex);
+    int tex_align = 0;
+    // per-stream workspaces and the x texture cache (guarded by mu)
+    mutable std::mutex mu;
+    mutable std::vector<std::unique_ptr<Workspace>> ws_pool;
+    mutable std::map<cudaStream_t, Workspace*> ws_of;
+    mutable std::map<const void*, cudaTextureObject_t> tex_of;
+    void drop_textures() const {
+        for (auto& kv : tex_of) cudaDestroyTextureObject(kv.second);
+        tex_of.clear();
     }
-};
-
-struct macko_chain {
-    int device = 0;
-    int grid = 0, x_mode = 0;
-    size_t smem = 0;
-    uint32_t n_ops = 0;
-    std::vector<mk::SpmvArgs> ops;  // n_ops arguments (passed as kernel parameters)
-    DevBuf<uint32_t> bar;    // grid barrier {count, generation}
-    std::vector<cudaTextureObject_t> tex;
-    ~macko_chain() {
-        for (auto t : tex)
-            if (t) cudaDestroyTextureObject(t);
-    }
+    ~macko_dev_matrix() { drop_textures(); }
 };
 
 namespace {
@@ -164,113 +166,12 @@ void check_bits(uint32_t bits) {
         fail(MACKO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits; got " + std::to_string(bits));
 }
 
-constexpr uint64_t kRowOverheadFlat = 384;  // flat-plan weight of a row start (element equivalents)
-
-// Flat plan (order 1): units are the global 2048-element blocks of the payload; warp k owns the
-// whole units [cu[k], cu[k+1]) of roughly equal weight and the rows that start there (plus the
-// row it continues into).  Rows cut at unit boundaries between warps get per-unit partial slots.
-void build_plan_flat(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
-    using namespace mk;
-    const std::vector<uint32_t>& rp = m->h_row_ptrs;
-    const uint64_t R = m->rows, N = m->pad_nnz;
-    const uint64_t U = (N + kUnitElts - 1) / kUnitElts;
-    std::vector<uint64_t> wpre(U + 1, 0);
-    {
-        std::vector<uint32_t> starts(U, 0);
-        for (uint64_t r = 0; r < R; ++r)
-            if (rp[r + 1] > rp[r]) ++starts[rp[r] / kUnitElts];
-        for (uint64_t u = 0; u < U; ++u)
-            wpre[u + 1] = wpre[u] + std::min<uint64_t>(kUnitElts, N - u * kUnitElts) + kRowOverheadFlat * starts[u];
-    }
-    const uint64_t total = wpre[U];
-    std::vector<uint64_t> cu(W + 1, U);
-    cu[0] = 0;
-    for (uint32_t k = 1; k < W; ++k) {
-        const uint64_t target = (uint64_t)((unsigned __int128)total * k / W);
-        cu[k] = (uint64_t)(std::lower_bound(wpre.begin(), wpre.end(), target) - wpre.begin());
-        cu[k] = std::min<uint64_t>(std::max<uint64_t>(cu[k], cu[k - 1]), U);
-    }
-    m->n_units = U;
-    std::vector<mk::WarpPlan> recs(W);
-    for (uint32_t k = 0; k < W; ++k) {
-        mk::WarpPlan& c = recs[k];
-        std::memset(&c, 0, sizeof c);
-        c.sid0 = c.sid1 = -1;
-        c.colbase = -1;
-        if (cu[k] >= cu[k + 1]) continue;
-        const uint64_t E0 = cu[k] * kUnitElts, E1 = std::min<uint64_t>(cu[k + 1] * kUnitElts, N);
-        c.units_left = (uint32_t)(cu[k + 1] - cu[k]);
-        c.e0 = (uint32_t)E0;
-        c.e1 = (uint32_t)E1;
-        // first row starting at or after E0; the row before it continues into this warp iff it ends past E0
-        uint64_t q = (uint64_t)(std::lower_bound(rp.begin(), rp.begin() + R, (uint32_t)E0) - rp.begin());
-        if (q > 0 && rp[q] > E0) --q;
-        c.row = (uint32_t)q;
-        c.s = rp[q];
-        c.e = rp[q + 1];
-    }
-    // split rows
-    std::vector<uint32_t> split_slot, split_first, split_pieces;
-    uint64_t slots = 0;
-    auto warp_of = [&](uint64_t elem) -> uint32_t {  // the non-idle warp whose units contain elem
-        const uint64_t u = elem / kUnitElts;
-        return (uint32_t)(std::upper_bound(cu.begin(), cu.end(), u) - cu.begin()) - 1u;
-    };
-    for (uint64_t r = 0; r < R; ++r) {
-        const uint64_t s = rp[r], e = rp[r + 1];
-        if (e <= s) continue;
-        const uint32_t kf = warp_of(s), kl = warp_of(e - 1);
-        if (kf == kl) continue;
-        const int32_t sid = (int32_t)split_slot.size();
-        const uint64_t n_r = (e - 1) / kUnitElts - s / kUnitElts + 1;
-        uint32_t pieces = 0;
-        for (uint32_t k = kf; k <= kl; ++k) pieces += cu[k] < cu[k + 1];
-        split_slot.push_back((uint32_t)slots);
-        split_first.push_back((uint32_t)(cu[kf + 1] - s / kUnitElts));
-        split_pieces.push_back(pieces);
-        for (uint32_t k = kf; k <= kl; ++k) {
-            if (cu[k] >= cu[k + 1]) continue;
-            if (k != kf) {
-                recs[k].sid0 = sid;
-                recs[k].slot0 = (uint32_t)slots;
-            }
-            if (k != kl) {
-                recs[k].sid1 = sid;
-                recs[k].slot1 = (uint32_t)slots;
-            }
-        }
-        slots += n_r;
-    }
-    const uint32_t S = (uint32_t)split_slot.size();
-    m->n_split = S;
-    std::vector<uint32_t> sp(4 * (size_t)S + 4 * (size_t)((S + 3) / 4 + 1), 0);
-    for (uint32_t q = 0; q < S; ++q) {
-        sp[4 * (size_t)q] = split_slot[q];
-        sp[4 * (size_t)q + 1] = split_first[q];
-        sp[4 * (size_t)q + 2] = split_pieces[q];
-    }
-    m->plan_recs.alloc(recs.size() * sizeof(mk::WarpPlan) / 4);
-    m->plan_u32.alloc(sp.size());
-    m->partials.alloc(std::max<uint64_t>(slots, 1));
-    ck(cudaMemcpyAsync(m->plan_recs.p, recs.data(), recs.size() * sizeof(mk::WarpPlan), cudaMemcpyHostToDevice, st),
-       "plan upload");
-    ck(cudaMemcpyAsync(m->plan_u32.p, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
-    mk::SpmvPlanDev& P = m->plan;
-    P.warps = reinterpret_cast<const mk::WarpPlan*>(m->plan_recs.p);
-    P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
-    P.counters = m->plan_u32.p + 4 * (size_t)S;
-    P.partials = m->partials.p;
-    ck(launch_plan_colbase(m->deltas.p, m->b_delta, 1, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
-       "plan colbase");
-    g_launches.fetch_add(1);
-    ck(cudaStreamSynchronize(st), "plan sync");
-}
-
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
     // Shared memory: fp16 x table with zero guards (every x_mode but 0) + per-warp TMA rings.
     int optin = 0, per_sm = 0;
+    ck(cudaDeviceGetAttribute(&m->tex_align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
     // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
@@ -319,10 +220,6 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     m->n_chunks = W;
     // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
     if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
-    if (m->order == 1) {
-        build_plan_flat(m, st, W);
-        return;
-    }
     const uint64_t R = m->rows;
     const std::vector<uint32_t>& rp = m->h_row_ptrs;
 
@@ -416,24 +313,30 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         c.slot0 = c.sid0 >= 0 ? split_slot[c.sid0] : 0;
         c.slot1 = c.sid1 >= 0 ? split_slot[c.sid1] : 0;
     }
-    std::vector<uint32_t> sp(4 * (size_t)S + 4 * (size_t)((S + 3) / 4 + 1), 0);  // splits, then counters
+    std::vector<uint32_t> sp(4 * (size_t)std::max<uint32_t>(S, 1), 0);  // split records
     for (uint32_t q = 0; q < S; ++q) {
         sp[4 * (size_t)q] = split_slot[q];
         sp[4 * (size_t)q + 1] = split_first[q];
         sp[4 * (size_t)q + 2] = split_pieces[q];
     }
+    m->n_slots = slots;
+    // a re-plan changes the workspace sizes: no launch of the old plan may still be running
+    if (!m->ws_pool.empty()) {
+        ck(cudaDeviceSynchronize(), "re-plan sync");
+        m->ws_of.clear();
+        m->ws_pool.clear();
+    }
     m->plan_recs.alloc(recs.size() * sizeof(mk::WarpPlan) / 4);
     m->plan_u32.alloc(sp.size());
-    m->partials.alloc(std::max<uint64_t>(slots, 1));
     ck(cudaMemcpyAsync(m->plan_recs.p, recs.data(), recs.size() * sizeof(mk::WarpPlan), cudaMemcpyHostToDevice, st),
        "plan upload");
     ck(cudaMemcpyAsync(m->plan_u32.p, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice, st), "plan upload");
     mk::SpmvPlanDev& P = m->plan;
     P.warps = reinterpret_cast<const mk::WarpPlan*>(m->plan_recs.p);
     P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
-    P.counters = m->plan_u32.p + 4 * (size_t)S;
-    P.partials = m->partials.p;
-    ck(launch_plan_colbase(m->deltas.p, m->b_delta, 0, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
+    P.counters = nullptr;
+    P.partials = nullptr;
+    ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<mk::WarpPlan*>(m->plan_recs.p), W, st),
        "plan colbase");
     g_launches.fetch_add(1);
     ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
@@ -455,29 +358,64 @@ void device_validate(macko_dev_matrix* m, cudaStream_t st) {
     if (h & 2u) fail(MACKO_EFORMAT, "padding value must be +0");
 }
 
+bool stream_capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return cs != cudaStreamCaptureStatusNone;
+}
+
+// The stream's workspace (caller holds m->mu).  Workspaces are allocated and zeroed outside any
+// stream capture (the first SpMV on a stream, or warm-up before capturing); when the pool is full
+// and no stream captures, the device is synchronised and the pool is reassigned.
+Workspace* workspace(const macko_dev_matrix* m, cudaStream_t st) {
+    auto it = m->ws_of.find(st);
+    if (it != m->ws_of.end()) return it->second;
+    if (stream_capturing(st))
+        fail(MACKO_EINVAL, "first SpMV of this matrix on a capturing stream: run it once on that stream before capture");
+    if (m->ws_pool.size() >= kMaxWorkspaces) {
+        ck(cudaDeviceSynchronize(), "workspace recycle");
+        m->ws_of.clear();
+        m->ws_pool.clear();
+    }
+    auto w = std::make_unique<Workspace>();
+    w->counters.alloc(std::max<uint32_t>(m->n_split, 1));
+    w->partials.alloc(std::max<uint64_t>(m->n_slots, 1));
+    ck(cudaMemsetAsync(w->counters.p, 0, w->counters.n * 4, st), "workspace zero");
+    Workspace* raw = w.get();
+    m->ws_pool.push_back(std::move(w));
+    m->ws_of[st] = raw;
+    return raw;
+}
+
 // x as the kernel reads it: 16-byte aligned for the shared-memory staging and texture-aligned
-// for the TEX gathers; a misaligned x is first copied into the matrix's aligned scratch buffer.
-// The texture object is cached per x buffer.
-const uint16_t* x_view(const macko_dev_matrix* m, const uint16_t* d_x, bool need_tex, cudaTextureObject_t* tex,
-                       cudaStream_t st) {
-    std::lock_guard<std::mutex> lk(m->tex_mu);
-    if (!m->tex_align) ck(cudaDeviceGetAttribute(&m->tex_align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
+// for the TEX gathers; a misaligned x is first copied into the stream's aligned scratch buffer.
+// Texture objects are cached per x buffer and destroyed only with the matrix (or when the cache
+// is recycled after a device synchronisation), never while a launch may still read them.
+const uint16_t* x_view(const macko_dev_matrix* m, Workspace* w, const uint16_t* d_x, bool need_tex,
+                       cudaTextureObject_t* tex, cudaStream_t st) {
     const uintptr_t align = std::max<uintptr_t>(16, (uintptr_t)m->tex_align);
     if (reinterpret_cast<uintptr_t>(d_x) % align != 0) {
-        if (!m->xcopy.p) m->xcopy.alloc(m->cols);
-        ck(cudaMemcpyAsync(m->xcopy.p, d_x, m->cols * 2, cudaMemcpyDeviceToDevice, st), "x copy");
-        d_x = m->xcopy.p;
+        if (!w->xcopy.p) {
+            if (stream_capturing(st)) fail(MACKO_EINVAL, "misaligned x first seen during stream capture");
+            w->xcopy.alloc(m->cols);
+        }
+        ck(cudaMemcpyAsync(w->xcopy.p, d_x, m->cols * 2, cudaMemcpyDeviceToDevice, st), "x copy");
+        d_x = w->xcopy.p;
     }
     *tex = 0;
     if (!need_tex) return d_x;
-    if (m->tex && m->tex_ptr == d_x) {
-        *tex = m->tex;
+    auto it = m->tex_of.find(d_x);
+    if (it != m->tex_of.end()) {
+        *tex = it->second;
         return d_x;
     }
-    if (m->tex) {
-        cudaDestroyTextureObject(m->tex);
-        m->tex = 0;
-        m->tex_ptr = nullptr;
+    if (m->tex_of.size() >= kMaxTextures) {
+        if (stream_capturing(st)) fail(MACKO_EINVAL, "x texture cache full during stream capture");
+        ck(cudaDeviceSynchronize(), "texture cache recycle");
+        m->drop_textures();
     }
     cudaResourceDesc rd{};
     rd.resType = cudaResourceTypeLinear;
@@ -486,9 +424,10 @@ const uint16_t* x_view(const macko_dev_matrix* m, const uint16_t* d_x, bool need
     rd.res.linear.sizeInBytes = m->cols * 2;
     cudaTextureDesc td{};
     td.readMode = cudaReadModeElementType;
-    ck(cudaCreateTextureObject(&m->tex, &rd, &td, nullptr), "x texture");
-    m->tex_ptr = d_x;
-    *tex = m->tex;
+    cudaTextureObject_t t = 0;
+    ck(cudaCreateTextureObject(&t, &rd, &td, nullptr), "x texture");
+    m->tex_of[d_x] = t;
+    *tex = t;
     return d_x;
 }
 
@@ -841,17 +780,23 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
                          uint16_t* y_mirror) {
     return guarded([&] {
         if (!m || !d_x || !d_y) fail(MACKO_EINVAL, "null argument");
-        if (flags & ~(uint32_t)(MACKO_SPMV_PDL | MACKO_SPMV_PEERS)) fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
+        if (flags & ~(uint32_t)(MACKO_SPMV_PDL | MACKO_SPMV_PEERS | MACKO_SPMV_PEER_BANK1))
+            fail(MACKO_EINVAL, "unknown macko_dev_spmv_ex flag");
+        if ((flags & MACKO_SPMV_PEER_BANK1) && !(flags & MACKO_SPMV_PEERS))
+            fail(MACKO_EINVAL, "MACKO_SPMV_PEER_BANK1 without MACKO_SPMV_PEERS");
         if ((flags & MACKO_SPMV_PEERS) && m->n_peer == 0) fail(MACKO_EINVAL, "MACKO_SPMV_PEERS without macko_dev_set_peers");
         if (!mk::spmv_valid_config(m->x_mode, (int)m->b_delta))
             fail(MACKO_EINVAL, "no SpMV kernel for b_delta " + std::to_string(m->b_delta) + " with this x_mode");
         DeviceGuard g(m->device);
+        const cudaStream_t st = (cudaStream_t)stream;
+        std::lock_guard<std::mutex> lk(m->mu);
+        Workspace* w = workspace(m, st);
         mk::SpmvArgs a{};
         a.values = m->values.p;
         a.deltas = m->deltas.p;
         a.row_ptrs = m->row_ptrs.p;
         const int mode = m->x_mode;
-        a.x = x_view(m, d_x, mode != 1, &a.xtex, (cudaStream_t)stream);
+        a.x = x_view(m, w, d_x, mode != 1, &a.xtex, st);
         a.y = d_y;
         a.rows = (uint32_t)m->rows;
         a.cols = (uint32_t)m->cols;
@@ -860,20 +805,23 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.plan = m->plan;
+        a.plan.counters = w->counters.p;
+        a.plan.partials = w->partials.p;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
         a.y_mirror = y_mirror;
         if (flags & MACKO_SPMV_PEERS) {
             a.n_peer = m->n_peer;
             a.peers = m->peer_table.p;
+            a.peer_bank = (flags & MACKO_SPMV_PEER_BANK1) ? 1u : 0u;
         }
         a.value_count = (uint32_t)m->pad_nnz;
         if (m->pad_nnz == 0) {  // no stored entries: every row is empty, y = +0
             if (flags & MACKO_SPMV_PEERS) fail(MACKO_EINVAL, "fused all-gather needs stored entries");
-            ck(cudaMemsetAsync(d_y, 0, m->rows * 2, (cudaStream_t)stream), "y = 0");
+            ck(cudaMemsetAsync(d_y, 0, m->rows * 2, st), "y = 0");
+            if (y_mirror) ck(cudaMemsetAsync(y_mirror, 0, m->rows * 2, st), "y = 0");
             return;
         }
-        ck(mk::launch_spmv(a, (int)m->b_delta, m->grid, mode, m->smem, (cudaStream_t)stream, (flags & MACKO_SPMV_PDL) != 0,
-                           m->order),
+        ck(mk::launch_spmv(a, (int)m->b_delta, m->grid, mode, m->smem, st, (flags & MACKO_SPMV_PDL) != 0),
            "macko_spmv launch");
         g_launches.fetch_add(1);
     });
@@ -889,20 +837,26 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
     return macko_dev_spmv_ex(m, d_x, d_y, stream, 0);
 }
 
-macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream) {
+macko_status macko_spmv_host(const macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream) {
     return guarded([&] {
         if (!m || !h_x || !h_y) fail(MACKO_EINVAL, "null argument");
         DeviceGuard g(m->device);
         cudaStream_t st = (cudaStream_t)stream;
-        if (!m->hx.p) {
-            // texture-aligned device x (no staging copy inside the SpMV): over-allocate and align
-            int align = 0;
-            ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
-            m->hx.alloc(m->cols + (uint64_t)std::max(align, 16) / 2);
-            const uintptr_t p = reinterpret_cast<uintptr_t>(m->hx.p), a = (uintptr_t)std::max(align, 16);
-            m->hx_aligned = reinterpret_cast<uint16_t*>((p + a - 1) / a * a);
+        uint16_t *hx_dev = nullptr, *hy_dev = nullptr;
+        {
+            // the stream's device x / y (texture-aligned x: no staging copy inside the SpMV)
+            std::lock_guard<std::mutex> lk(m->mu);
+            Workspace* w = workspace(m, st);
+            if (!w->hx.p) {
+                const uintptr_t a = std::max<uintptr_t>(16, (uintptr_t)m->tex_align);
+                w->hx.alloc(m->cols + a / 2);
+                const uintptr_t p = reinterpret_cast<uintptr_t>(w->hx.p);
+                w->hx_aligned = reinterpret_cast<uint16_t*>((p + a - 1) / a * a);
+                w->hy.alloc(m->rows);
+            }
+            hx_dev = w->hx_aligned;
+            hy_dev = w->hy.p;
         }
-        if (!m->hy.p) m->hy.alloc(m->rows);
         // Pinned host buffers are device-mapped (UVA): x is pulled and y pushed by small kernels
         // chained to the SpMV with programmatic dependent launch, so the SpMV prologue overlaps
         // the x transfer.  Pageable buffers take cudaMemcpyAsync.  (A cached CUDA graph of the
@@ -918,16 +872,15 @@ macko_status macko_spmv_host(macko_dev_matrix* m, const uint16_t* h_x, uint16_t*
         const uint16_t* dx = static_cast<const uint16_t*>(mapped(h_x));
         uint16_t* dy = const_cast<uint16_t*>(static_cast<const uint16_t*>(mapped(h_y)));
         if (dx) {
-            ck(mk::launch_copy_u16(dx, m->hx_aligned, (uint32_t)m->cols, 1, false, st), "x pull");
+            ck(mk::launch_copy_u16(dx, hx_dev, (uint32_t)m->cols, 1, false, st), "x pull");
             g_launches.fetch_add(1);
         } else {
-            ck(cudaMemcpyAsync(m->hx_aligned, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
+            ck(cudaMemcpyAsync(hx_dev, h_x, m->cols * 2, cudaMemcpyHostToDevice, st), "H2D x");
         }
         // a mapped host y is written by the SpMV itself, row by row as rows finish (no push step)
-        const macko_status sp =
-            spmv_launch(m, m->hx_aligned, m->hy.p, st, dx ? MACKO_SPMV_PDL : 0u, m->pad_nnz ? dy : nullptr);
+        const macko_status sp = spmv_launch(m, hx_dev, hy_dev, st, dx ? MACKO_SPMV_PDL : 0u, dy);
         if (sp != MACKO_OK) fail(sp, g_err);
-        if (!dy || !m->pad_nnz) ck(cudaMemcpyAsync(h_y, m->hy.p, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
+        if (!dy) ck(cudaMemcpyAsync(h_y, hy_dev, m->rows * 2, cudaMemcpyDeviceToHost, st), "D2H y");
         ck(cudaStreamSynchronize(st), "sync");
     });
 }
@@ -1109,111 +1062,6 @@ macko_status macko_mm_read_dense(const char* path, uint64_t* rows, uint64_t* col
 }
 
 
-// ---- persistent SpMV chains -----------------------------------------------------------------
-macko_status macko_chain_create(const macko_dev_matrix* const* mats, const uint16_t* const* xs, uint16_t* const* ys,
-                                uint32_t n_ops, macko_chain** out) {
-    return guarded([&] {
-        if (!out || !mats || !xs || !ys || n_ops == 0) fail(MACKO_EINVAL, "bad chain arguments");
-        *out = nullptr;
-        const int dev = mats[0]->device;
-        DeviceGuard g(dev);
-        auto* c = new macko_chain;
-        std::unique_ptr<macko_chain> hold(c);
-        c->device = dev;
-        c->n_ops = n_ops;
-        c->grid = mats[0]->grid;
-        // one x_mode for all ops (a template parameter): the op with the most bytes decides
-        uint64_t best = 0;
-        size_t xtab = 0;
-        for (uint32_t k = 0; k < n_ops; ++k) {
-            const macko_dev_matrix* m = mats[k];
-            if (!m || !xs[k] || !ys[k]) fail(MACKO_EINVAL, "null matrix or vector in the chain");
-            if (m->device != dev) fail(MACKO_EINVAL, "chain ops must live on one device");
-            if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMV kernel is built for b_delta = 4 only");
-            if (m->grid != c->grid || m->ring != mats[0]->ring)
-                fail(MACKO_EINVAL, "chain ops must share the launch plan geometry");
-            if (m->order != 0) fail(MACKO_EINVAL, "the persistent chain runs the ROMA walk (order 0) only");
-            const uint64_t tb = values_bytes(m->pad_nnz) + delta_bytes(m->pad_nnz, 4);
-            if (tb >= best) {
-                best = tb;
-                c->x_mode = m->x_mode;
-            }
-            xtab = std::max<size_t>(xtab, align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128));
-        }
-        if (c->x_mode == 0) xtab = 0;
-        const uint32_t ring = mats[0]->ring;
-        c->smem = xtab + (size_t)ring * mk::kSpmvWarpsPerCta * (mk::kChunkVBytes + mk::kChunkDBytes);
-        int optin = 0;
-        ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attribute");
-        int per_sm = 0;
-        ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem attribute");
-        if (c->smem > std::min<size_t>((size_t)optin, (size_t)per_sm / mk::kSpmvCtasPerSm - 1024) -
-                          mk::kSpmvWarpsPerCta * mk::kMaxRing * 8 - 64)
-            fail(MACKO_EINVAL, "chain x table + rings exceed shared memory");
-        int align = 0;
-        ck(cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev), "texture alignment");
-        std::vector<mk::SpmvArgs> ops(n_ops);
-        for (uint32_t k = 0; k < n_ops; ++k) {
-            const macko_dev_matrix* m = mats[k];
-            if (reinterpret_cast<uintptr_t>(xs[k]) % std::max<uintptr_t>(16, (uintptr_t)align) != 0)
-                fail(MACKO_EINVAL, "chain x buffers must be texture-aligned (no staging copy inside a chain)");
-            mk::SpmvArgs& a = ops[k];
-            std::memset(&a, 0, sizeof a);
-            a.values = m->values.p;
-            a.deltas = m->deltas.p;
-            a.row_ptrs = m->row_ptrs.p;
-            a.x = xs[k];
-            a.y = ys[k];
-            a.rows = (uint32_t)m->rows;
-            a.cols = (uint32_t)m->cols;
-            a.value_elems = m->values.n;
-            a.delta_bytes = m->deltas.n;
-            a.ring = ring;
-            a.ring_offset = (uint32_t)xtab;
-            a.plan = m->plan;
-            a.value_count = (uint32_t)m->pad_nnz;
-            if (m->pad_nnz == 0) fail(MACKO_EINVAL, "chain ops need stored entries");
-            a.xtex = 0;
-            if (c->x_mode != 1) {
-                cudaResourceDesc rd{};
-                rd.resType = cudaResourceTypeLinear;
-                rd.res.linear.devPtr = const_cast<uint16_t*>(xs[k]);
-                rd.res.linear.desc = cudaCreateChannelDesc<unsigned short>();
-                rd.res.linear.sizeInBytes = m->cols * 2;
-                cudaTextureDesc td{};
-                td.readMode = cudaReadModeElementType;
-                cudaTextureObject_t t = 0;
-                ck(cudaCreateTextureObject(&t, &rd, &td, nullptr), "x texture");
-                c->tex.push_back(t);
-                a.xtex = t;
-            }
-        }
-        c->ops = ops;
-        c->bar.alloc(2);
-        ck(cudaMemset(c->bar.p, 0, 8), "chain barrier");
-        *out = hold.release();
-    });
-}
-
-macko_status macko_chain_run(macko_chain* c, void* stream) {
-    return guarded([&] {
-        if (!c) fail(MACKO_EINVAL, "null chain");
-        DeviceGuard g(c->device);
-        ck(mk::launch_chain(c->ops.data(), c->n_ops, c->bar.p, c->grid, c->x_mode,
-                            c->smem, (cudaStream_t)stream),
-           "macko_chain launch");
-        g_launches.fetch_add(1);
-    });
-}
-
-macko_status macko_chain_free(macko_chain* c) {
-    return guarded([&] {
-        if (!c) return;
-        DeviceGuard g(c->device);
-        delete c;
-    });
-}
-
 macko_status macko_shard_rows(uint64_t rows, uint32_t n_shards, uint32_t shard, uint64_t* r0, uint64_t* r1) {
     return guarded([&] {
         if (!r0 || !r1 || n_shards == 0 || shard >= n_shards) fail(MACKO_EINVAL, "bad shard request");
@@ -1264,13 +1112,32 @@ macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, u
         mk::PeerTable t{};
         for (uint32_t p = 0; p < n; ++p) {
             if (!peer_y[p] || !peer_flags[p]) fail(MACKO_EINVAL, "null peer pointer");
-            t.y[p] = peer_y[p];
+            t.y[0][p] = t.y[1][p] = peer_y[p];
             t.flag[p] = peer_flags[p];
         }
         if (!m->peer_table.p) m->peer_table.alloc(1);
         ck(cudaMemcpyAsync(m->peer_table.p, &t, sizeof t, cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table");
         ck(cudaStreamSynchronize((cudaStream_t)stream), "peer table");
+        m->h_peers = t;
         m->n_peer = n;
+    });
+}
+
+macko_status macko_dev_set_peer_bank(macko_dev_matrix* m, uint32_t bank, uint16_t* const* peer_y, uint32_t n,
+                                     void* stream) {
+    return guarded([&] {
+        if (!m || !peer_y) fail(MACKO_EINVAL, "null argument");
+        if (bank > 1) fail(MACKO_EINVAL, "peer bank must be 0 or 1");
+        if (n != m->n_peer || n == 0) fail(MACKO_EINVAL, "set the peers (macko_dev_set_peers) first, same count");
+        DeviceGuard g(m->device);
+        mk::PeerTable t = m->h_peers;
+        for (uint32_t p = 0; p < n; ++p) {
+            if (!peer_y[p]) fail(MACKO_EINVAL, "null peer pointer");
+            t.y[bank][p] = peer_y[p];
+        }
+        ck(cudaMemcpyAsync(m->peer_table.p, &t, sizeof t, cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table");
+        ck(cudaStreamSynchronize((cudaStream_t)stream), "peer table");
+        m->h_peers = t;
     });
 }
 
@@ -1355,21 +1222,12 @@ macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_s
     return guarded([&] {
         if (!m) fail(MACKO_EINVAL, "null handle");
         if (x_mode != -1 && !mk::spmv_valid_config(x_mode, (int)m->b_delta))
-            fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1 or 6..11 (6..8, 10 for b_delta != 4)");
+            fail(MACKO_EINVAL, "x_mode must be -1 (auto), 0, 1, 6, 7, 8 or 10");
         if (x_mode > 0 && m->cols * 2 > 220 * 1024) fail(MACKO_EINVAL, "x table does not fit shared memory");
         DeviceGuard g(m->device);
+        std::lock_guard<std::mutex> lk(m->mu);
         m->force_x_mode = x_mode;
         m->force_ctas = ctas_per_sm;
-        build_plan(m, (cudaStream_t)stream);
-    });
-}
-
-macko_status macko_dev_set_order(macko_dev_matrix* m, int order, void* stream) {
-    return guarded([&] {
-        if (!m) fail(MACKO_EINVAL, "null handle");
-        if (order != 0 && order != 1) fail(MACKO_EINVAL, "order must be 0 (ROMA) or 1 (flat)");
-        DeviceGuard g(m->device);
-        m->order = order;
         build_plan(m, (cudaStream_t)stream);
     });
 }
@@ -1385,7 +1243,7 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
         out->x_in_smem = (uint32_t)m->x_mode;
         out->n_units = m->n_units;
         out->smem_bytes = m->smem;
-        out->order = (uint32_t)m->order;
+        out->reserved0 = 0;
         out->reserved = 0;
     });
 }

@@ -31,7 +31,6 @@
 // lanes once per unit (8 steps; the row's last unit absorbs a shorter remainder), sequential
 // over units — mirrored bit-exactly by oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  It
 // depends on a row's elements and on its start offset mod 8 (ROMA), never on the plan.
-// The flat walk (order 1, macko_spmv_flat) is the alternative order of oracle mo_b200_flat_spmv.
 #include "common.cuh"
 #include "spmv.cuh"
 
@@ -41,14 +40,6 @@
 // Opt-in trace build (`make trace` -> libmacko_cuda_trace.so): per warp, %globaltimer at each
 // prologue phase and at the end, for latency studies of small SpMVs (tools/trace_spmv.py).
 __device__ unsigned long long g_macko_trace[148 * 32 * 8];
-#define MK_CTRACE(k, i)                                                                                \
-    do {                                                                                                \
-        if (threadIdx.x == 0 && (k) < 32) {                                                             \
-            unsigned long long t_;                                                                      \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
-            g_macko_trace[(blockIdx.x * 32 + (k)) * 8 + (i)] = t_;                                      \
-        }                                                                                               \
-    } while (0)
 #define MK_TRACE(i)                                                                                    \
     do {                                                                                                \
         if ((threadIdx.x & 31) == 0 && blockIdx.x < 148) {                                              \
@@ -58,9 +49,6 @@ __device__ unsigned long long g_macko_trace[148 * 32 * 8];
         }                                                                                               \
     } while (0)
 #else
-#define MK_CTRACE(k, i) \
-    do {                \
-    } while (0)
 #define MK_TRACE(i) \
     do {            \
     } while (0)
@@ -89,18 +77,17 @@ __device__ __forceinline__ uint16_t xtex(cudaTextureObject_t t, int col) {
 
 // Lane element slots k (0..7) gathered through the texture (bit k set) rather than the shared
 // table.  x_mode 0: texture only (x too large for shared memory); 1: shared table only;
-// 6..9: split between the LSU and TEX data pipes (profiles/r01_pipes.md).
+// 6, 7, 8, 10: split between the LSU and TEX data pipes (profiles/r01_pipes.md).
 template <int kXMode>
 constexpr uint32_t tex_slots() {
-    return kXMode == 0 ? 0xFFu : kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 9 ? 0x92u
-         : kXMode == 10 ? 0xAAu : kXMode == 11 ? 0xABu : 0u;
+    return kXMode == 0 ? 0xFFu : kXMode == 6 ? 0x2Au : kXMode == 7 ? 0xAAu : kXMode == 8 ? 0x22u : kXMode == 10 ? 0xAAu : 0u;
 }
 
 // Second step of a pair: x_mode 10 alternates 4 and 3 texture slots between the two steps
-// (3.5 of 8 on average), x_mode 11 alternates 5 and 4.
+// (3.5 of 8 on average).
 template <int kXMode>
 constexpr uint32_t tex_slots_b() {
-    return kXMode == 10 ? 0x2Au : kXMode == 11 ? 0xAAu : tex_slots<kXMode>();
+    return kXMode == 10 ? 0x2Au : tex_slots<kXMode>();
 }
 
 template <int kXMode>
@@ -200,7 +187,8 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
 __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
     a.y[r] = v;
     if (a.y_mirror) a.y_mirror[r] = v;
-    for (uint32_t p = 0; p < a.n_peer; ++p) reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[p])))[r] = v;
+    for (uint32_t p = 0; p < a.n_peer; ++p)
+        reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[a.peer_bank][p])))[r] = v;
 }
 
 // Fused all-gather: once all warps of the CTA wrote their rows, make them visible system-wide and
@@ -250,8 +238,8 @@ __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colba
 }
 
 // Finish the current piece (write y or hand the split row to its last arrival).  Lane 0 wrote
-// the piece's unit partials; the release atomic orders them before its arrival (no full fence,
-// no L1 invalidation), and the last arrival reads every partial from L2 (ld.cg).
+// the piece's unit partials; the acq_rel arrival releases them and, for the last arrival,
+// acquires every other piece's partials, which it then reads from L2 (ld.cg).
 // Returns y[r]'s fp16 bits in lane 0 of the last arrival, -1 elsewhere (the caller stores it).
 __device__ __noinline__ int finish_split(uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot, int32_t sid,
                                          float row_acc, const SpmvPlanDev P, int lane) {
@@ -261,7 +249,7 @@ __device__ __noinline__ int finish_split(uint32_t j0, uint32_t tend, uint32_t n_
         const uint4 sp = P.splits[sid];
         first = sp.y;
         uint32_t prev;
-        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
         last = prev + 1 == sp.z;
     }
     last = __shfl_sync(kFull, last, 0);
@@ -425,12 +413,8 @@ __device__ __forceinline__ uint32_t mask_slot(Slot& sl, uint32_t eb, uint32_t s,
 }
 
 // ------------------------------------------------------------------------------------------
-// Per-op building blocks (shared by the single-SpMV kernel and the persistent chain kernel)
+// Per-SpMV building blocks
 // ------------------------------------------------------------------------------------------
-// Set up the warp's ring and walk for one SpMV and issue the first ring fills.  `fresh`: the
-// barriers are initialised here and the first fill is one copy per array (single-SpMV kernel);
-// otherwise (chain) the ring continues where the previous op left it — the first chunk goes to
-// the slot after the last one consumed, each chunk on its own barrier phase.
 struct PlanRecord {
     uint4 q0, q1, q2;  // the warp's WarpPlan (48 bytes)
 };
@@ -440,11 +424,9 @@ __device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w)
     return PlanRecord{__ldg(rec), __ldg(rec + 1), __ldg(rec + 2)};
 }
 
-// Ring set-up for the warp's element stream [E0, E1) and its first fills.  `fresh`: the
-// barriers are initialised here and the first fill is one copy per array (single-SpMV kernels);
-// otherwise (chain) the ring continues where the previous op left it — the first chunk goes to
-// the slot after the last one consumed, each chunk on its own barrier phase.
-template <int kBits, bool kFresh>
+// Ring set-up for the warp's element stream [E0, E1): the barriers are initialised and the first
+// fill is one copy per array.
+template <int kBits>
 __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint32_t E1, uint32_t warp, int lane,
                                            uint32_t smem_base, uint32_t bar0, Ring& g) {
     g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
@@ -456,7 +438,7 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
     g.ready_end = e0;
     g.rel_mark = e0 + kChunk;
     const uint32_t limit = min(e0 + a.ring * kChunk, g.stream_end);
-    if constexpr (kFresh) {
+    {
         g.ebase = e0;
         g.wslot = 0;
         g.wphase = 0;
@@ -492,22 +474,18 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
             MK_TRACE(7);
         }
         g.iss = limit;
-    } else {
-        // element e0 maps to the slot the consumer waits on next (all earlier chunks consumed)
-        g.ebase = e0 - g.wslot * kChunk;
-        for (g.iss = e0; g.iss < limit; g.iss += kChunk) ring_issue<kBits>(g, a, lane);
     }
     __syncwarp();
 }
 
 // Set up the warp's ring and ROMA walk for one SpMV (plan record pr) and issue the first fills.
-template <int kBits, bool kFresh>
+template <int kBits>
 __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
                                          uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
     const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
     MK_TRACE(1);
     if (q0.x == 0) return false;
-    ring_begin<kBits, kFresh>(a, q0.w, q1.x, warp, lane, smem_base, bar0, g);
+    ring_begin<kBits>(a, q0.w, q1.x, warp, lane, smem_base, bar0, g);
     rs.r = q0.y;
     rs.units_left = q0.x;
     rs.s = q1.y;
@@ -518,9 +496,8 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
 }
 
 // Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries); all
-// threads of the CTA, the caller synchronises.  kCoherent: read x from L2 (ld.cg) — x was
-// written earlier in the same launch (chain kernel).
-template <int kXMode, bool kCoherent>
+// threads of the CTA, the caller synchronises.
+template <int kXMode>
 __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
     if constexpr (x_table<kXMode>()) {
         const uint32_t C = a.cols;
@@ -531,10 +508,10 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
         const uint32_t rot = nv ? (blockIdx.x * 97u) % nv : 0u;
         for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
             const uint32_t k = i + rot < nv ? i + rot : i + rot - nv;
-            reinterpret_cast<uint4*>(xs)[k] = kCoherent ? __ldcg(x4 + k) : __ldg(x4 + k);
+            reinterpret_cast<uint4*>(xs)[k] = __ldg(x4 + k);
         }
         for (uint32_t i = nv * 8 + threadIdx.x; i < C + kXGuardHi; i += blockDim.x)
-            xs[i] = i < C ? (kCoherent ? __ldcg(a.x + i) : a.x[i]) : (uint16_t)0;
+            xs[i] = i < C ? a.x[i] : (uint16_t)0;
         if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
     }
 }
@@ -626,216 +603,6 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// Flat-window walk (order 1): lanes, steps and units aligned to GLOBAL element positions
-// (oracle mo_b200_flat_spmv).  A warp owns whole 2048-element units [E0, E1) and walks them in
-// 512-element windows, two per 1024-element TMA chunk, so the ring is serviced once per chunk
-// at a fixed point.  A window inside one row is the interior pair; a window holding row
-// boundaries decodes and scans its 512 codewords once and gathers each row segment with masks.
-// ------------------------------------------------------------------------------------------
-struct FlatState {
-    uint32_t r, s, e, e_next;  // current row and its bounds; row_ptrs[r + 2] prefetched
-    int col_base;              // column of the element just before the current window (-1: none)
-    float acc, row_acc;
-};
-
-// Inclusive in-lane prefix of element m (0..7) of the lane's step.
-template <class D>
-__device__ __forceinline__ uint32_t incl_at(const D& d, uint32_t m) {
-    if constexpr (std::is_same<D, Dec8>::value) {
-        const uint32_t w = d.p[0] * (m < 2) + d.p[1] * (m >= 2 && m < 4) + d.p[2] * (m >= 4 && m < 6) + d.p[3] * (m >= 6);
-        return (m & 1u) ? (w >> 16) : (w & 0xFFFFu);
-    } else {
-        return __byte_perm((m & 1u) ? d.odd : d.even, 0u, 0x4440u + (m >> 1));
-    }
-}
-
-// Finish a row cut between warps (flat plan): the first piece stores its sum at the slot of its
-// last unit, other pieces stored per-unit partials at their unit ends; the last arrival adds them
-// in unit order.
-// Returns y[r]'s fp16 bits in lane 0 of the last arrival, -1 elsewhere (the caller stores it).
-__device__ __noinline__ int finish_split_flat(bool first_piece, uint32_t n_r, const uint4* rec, float row_acc,
-                                              const SpmvPlanDev P, int lane) {
-    int out = -1;
-    uint32_t last = 0, first = 0, slot = 0;
-    if (lane == 0) {
-        const uint4 q2 = __ldg(rec + 2);  // sid0, sid1, slot0, slot1 (spmv.cuh WarpPlan)
-        const int32_t sid = (int32_t)(first_piece ? q2.y : q2.x);
-        slot = first_piece ? q2.w : q2.z;
-        const uint4 sp = P.splits[sid];
-        first = sp.y;
-        if (first_piece) P.partials[slot + first - 1u] = row_acc;
-        uint32_t prev;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
-        last = prev + 1 == sp.z;
-        if (last) {
-            float tot = __ldcg(P.partials + slot + first - 1);
-            for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + slot + q);
-            out = (int)f32_to_f16_rn(tot);
-            P.counters[sid] = 0;
-        }
-    }
-    __syncwarp();
-    return out;
-}
-
-template <int kXMode, int kBits>
-__device__ __forceinline__ void run_flat(const SpmvArgs& a, const PlanRecord& pr, int lane, uint32_t xs_addr, Ring& g) {
-    using D = typename std::conditional<kBits == 8, Dec8, Dec>::type;
-    constexpr uint32_t kBias = kBits == 8 ? 8u : 0u;  // b = 8: the packed scan runs on (total - 8)
-    const uint32_t E0 = pr.q0.w, E1 = pr.q1.x;
-    // the warp's plan record: split ids / partial slots are re-read when a split row finishes
-    const uint4* rec = reinterpret_cast<const uint4*>(a.plan.warps + blockIdx.x * kSpmvWarpsPerCta + (threadIdx.x >> 5));
-    FlatState fs;
-    fs.r = pr.q0.y;
-    fs.s = pr.q1.y;
-    fs.e = pr.q1.z;
-    fs.e_next = fs.r + 2u <= a.rows ? __ldg(a.row_ptrs + fs.r + 2u) : 0u;
-    fs.col_base = (int)pr.q1.w;
-    fs.acc = 0.0f;
-    fs.row_acc = 0.0f;
-    // a row that began before E0 (a continuation piece of a split row) stores per-unit partials
-    auto unit_end = [&](uint32_t unit) {  // tree over lanes
-        const float red = warp_tree_sum(fs.acc);
-        fs.acc = 0.0f;
-        if (fs.s < E0 && lane == 0) a.plan.partials[__ldg(&rec[2].z) + unit - fs.s / kUnitElts] = red;
-        fs.row_acc += red;
-    };
-    auto finish_row = [&]() {
-        if (fs.s >= E0 && fs.e <= E1) {
-            if (lane == 0) put_y(a, fs.r, f32_to_f16_rn(fs.row_acc));
-        } else {
-            const uint32_t n_r = (fs.e - 1u) / kUnitElts - fs.s / kUnitElts + 1u;
-            const int v = finish_split_flat(fs.s >= E0, n_r, rec, fs.row_acc, a.plan, lane);
-            if (v >= 0) put_y(a, fs.r, (uint16_t)v);
-        }
-    };
-    // Move to the next row this warp owns (empty rows get +0).  Returns false when the walk is over.
-    auto next_row = [&]() -> bool {
-        for (;;) {
-            if (fs.r + 1u >= a.rows) return false;
-            ++fs.r;
-            fs.s = fs.e;
-            fs.e = fs.e_next;
-            if (fs.r + 2u <= a.rows) fs.e_next = __ldg(a.row_ptrs + fs.r + 2u);
-            if (fs.s >= E1 && E1 != a.value_count) return false;  // the next warp's row
-            fs.acc = 0.0f;
-            fs.row_acc = 0.0f;
-            fs.col_base = -1;  // a row starting at a window start
-            if (fs.e > fs.s) return true;
-            if (lane == 0) put_y(a, fs.r, 0);  // empty row
-        }
-    };
-    // leading empty rows of this warp
-    if (fs.e == fs.s) {
-        if (lane == 0) put_y(a, fs.r, 0);
-        if (!next_row()) return;
-    }
-
-    auto window = [&](uint32_t W) -> bool {  // false: the walk is over
-        const uint32_t relA0 = (W + 8u * lane - g.ebase) & g.emask;
-        const Slot A = lds_slot<kBits>(g, relA0);
-        const Slot B = lds_slot<kBits>(g, (relA0 + kStepElts) & g.emask);
-        D dA, dB;
-        if constexpr (kBits == 8) {
-            dA = decode8(A.d, A.d2);
-            dB = decode8(B.d, B.d2);
-        } else {
-            dA = decode<kBits>(A.d);
-            dB = decode<kBits>(B.d);
-        }
-        const uint32_t pk = (dA.local - kBias) | ((dB.local - kBias) << 16);
-        const uint32_t incl = warp_incl_scan_p(pk);
-        const uint32_t tot = __reduce_add_sync(kFull, pk);
-        const uint32_t lane_bias = kBias * (uint32_t)lane, tot_bias = kBias * kWarp;
-        const uint32_t totA = (tot & 0xFFFFu) + tot_bias, totAB = totA + (tot >> 16) + tot_bias;
-        const int relA = (int)((incl & 0xFFFFu) - (dA.local - kBias) + lane_bias);
-        const int relB = (int)totA + (int)((incl >> 16) - (dB.local - kBias) + lane_bias);
-        if (fs.e > W + 2u * kStepElts) {  // the whole window lies inside the current row
-            fs.acc = lane_step<kXMode, false>(fs.acc, A.v, dA, fs.col_base + relA, xs_addr, a.xtex, 0xFFu);
-            fs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(fs.acc, B.v, dB, fs.col_base + relB, xs_addr,
-                                                                     a.xtex, 0xFFu);
-            fs.col_base += (int)totAB;
-            if (((W + 2u * kStepElts) & (kUnitElts - 1u)) == 0) unit_end(W / kUnitElts);
-            return true;
-        }
-        // boundary window: row segments one after the other
-        for (;;) {
-            int base;
-            if (fs.s < W) {
-                base = fs.col_base;
-            } else if (fs.s == W) {
-                base = -1;
-            } else {  // the row starts inside the window: base = -1 - P(s - 1)
-                const uint32_t x = fs.s - 1u - W, m = x & 7u, L = (x >> 3) & 31u;
-                const uint32_t mine = (x < kStepElts) ? (uint32_t)relA + incl_at(dA, m) : (uint32_t)relB + incl_at(dB, m);
-                base = -1 - (int)__shfl_sync(kFull, mine, (int)L);
-            }
-            const uint32_t lo = max(fs.s, W), hi = min(fs.e, W + 2u * kStepElts);
-            const uint32_t eb = W + 8u * lane;
-            const uint32_t vmA = (0xFFu >> (8 - min(max((int)(hi - eb), 0), 8))) & (0xFFu << min(max((int)(lo - eb), 0), 8)) & 0xFFu;
-            const uint32_t ebB = eb + kStepElts;
-            const uint32_t vmB = (0xFFu >> (8 - min(max((int)(hi - ebB), 0), 8))) & (0xFFu << min(max((int)(lo - ebB), 0), 8)) & 0xFFu;
-            if (lo < W + kStepElts)
-                fs.acc = lane_step<kXMode, true>(fs.acc, A.v, dA, base + relA, xs_addr, a.xtex, vmA);
-            if (hi > W + kStepElts)
-                fs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(fs.acc, B.v, dB, base + relB,
-                                                                        xs_addr, a.xtex, vmB);
-            if (fs.e <= W + 2u * kStepElts) {  // the row ends in this window
-                unit_end((fs.e - 1u) / kUnitElts);
-                finish_row();
-                if (!next_row()) return false;
-                if (fs.s >= W + 2u * kStepElts) return true;  // next row starts at the next window
-                continue;
-            }
-            fs.col_base = base + (int)totAB;  // the row continues past the window
-            if (((W + 2u * kStepElts) & (kUnitElts - 1u)) == 0) unit_end(W / kUnitElts);
-            return true;
-        }
-    };
-
-    // Fixed ring schedule: chunk k of the warp's range lives in slot k mod ring (phase k / ring);
-    // consuming chunk k first refills the slot of chunk k - 1 with chunk k - 1 + ring.
-    const uint32_t rshift = a.ring == 4u ? 2u : 1u;
-    for (uint32_t cs = E0; cs < E1; cs += kChunk) {
-        const uint32_t k = (cs - E0) / kChunk;
-        if (k) {
-            __syncwarp();
-            g.iss = cs + (a.ring - 1u) * kChunk;
-            if (g.iss < E1) ring_issue<kBits>(g, a, lane);
-        }
-        mbar_wait(g.bar0 + 8u * (k & (a.ring - 1u)), (k >> rshift) & 1u);
-        if (!window(cs)) return;
-        if (cs + 2u * kStepElts < E1 && !window(cs + 2u * kStepElts)) return;
-    }
-    // the warp's range ends inside the current row (a split row)
-    if (fs.e > E1) finish_row();
-}
-
-template <int kXMode, int kBits>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv_flat(const SpmvArgs a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
-    const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const PlanRecord pr = load_record(a, w);
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
-    if (!a.pdl) stage_x<kXMode, false>(a, xs);
-    Ring g;
-    const bool has_work = pr.q0.x != 0;
-    if (has_work)
-        ring_begin<kBits, true>(a, pr.q0.w, pr.q1.x, warp, lane, smem_base,
-                                static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (a.pdl) stage_x<kXMode, false>(a, xs);
-    __syncthreads();
-    if (has_work) run_flat<kXMode, kBits>(a, pr, lane, static_cast<uint32_t>(__cvta_generic_to_shared(xs)), g);
-    signal_peers(a);
-}
-
 template <int kXMode, int kBits>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -852,17 +619,17 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     const PlanRecord pr = load_record(a, w);
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
     // Without a PDL producer x is final at entry: its loads overlap the plan record's latency.
-    if (!a.pdl) stage_x<kXMode, false>(a, xs);
+    if (!a.pdl) stage_x<kXMode>(a, xs);
     // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
     RowState rs;
     Ring g;
-    const bool has_work = op_begin<kBits, true>(a, pr, warp, lane, smem_base,
+    const bool has_work = op_begin<kBits>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
     MK_TRACE(2);
     // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     MK_TRACE(3);
-    if (a.pdl) stage_x<kXMode, false>(a, xs);
+    if (a.pdl) stage_x<kXMode>(a, xs);
     __syncthreads();
     MK_TRACE(4);
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
@@ -871,92 +638,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     signal_peers(a);
 }
 
-// Grid-wide barrier for the persistent chain kernel (all CTAs co-resident: cooperative launch).
-// Sense-reversing and self-resetting, so it works across launches and CUDA-graph replays.  The
-// fences around it are the cooperative-groups pattern: the first releases this CTA's y writes
-// (ordered before it by bar.sync), the second acquires the other CTAs' writes and invalidates
-// this SM's L1 / texture lines, so the next op's x (staged with ld.cg, gathered through TEX)
-// is never stale.
-__device__ __forceinline__ void grid_barrier(uint32_t* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile uint32_t* gen = bar + 1;
-        const uint32_t g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1u) {
-            bar[0] = 0;
-            __threadfence();
-            *gen = g0 + 1u;
-        } else {
-            const long long t0 = clock64();
-            while (*gen == g0) {
-                __nanosleep(20);
-                if (clock64() - t0 > 8000000000LL) __trap();  // ~4 s: never hang the GPU
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// Persistent chain of dependent SpMVs (decoder stacks): op k+1 reads op k's y.  Each warp sets up
-// op k+1 (plan record, first ring fills) as soon as its part of op k is done — BEFORE the grid
-// barrier — so the matrix stream keeps HBM busy across the dependency, and only x staging waits.
-template <int kXMode>
-__global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm)
-    macko_chain_b4(const __grid_constant__ ChainOps P, uint32_t n_ops, uint32_t* bar) {
-    // The ops' arguments live in the kernel's parameter space (constant bank): uniform loads
-    // through the constant cache, no shared-memory reads in the walk.
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
-    const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0]));
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
-    const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    if (lane == 0) {
-        for (uint32_t i = 0; i < kMaxRing; ++i) mbar_init(bar0 + 8u * i);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    RowState rs;
-    Ring g;
-    g.wslot = 0;
-    g.wphase = 0;
-    bool has_work = op_begin<4, false>(P.op[0], load_record(P.op[0], w), warp, lane, smem_base, bar0, g, rs);
-    for (uint32_t k = 0; k < n_ops; ++k) {
-        const SpmvArgs& a = P.op[k];
-        MK_CTRACE(k, 0);
-        if (k) grid_barrier(bar);  // op k-1's y (this op's x) is complete everywhere
-        MK_CTRACE(k, 1);
-        stage_x<kXMode, true>(a, xs);
-        __syncthreads();
-        MK_CTRACE(k, 2);
-        if (has_work) run_rows<kXMode, 4>(a, w, lane, xs_addr, g, rs);
-        MK_CTRACE(k, 3);
-        if (k + 1 < n_ops) {
-            const SpmvArgs& an = P.op[k + 1];
-            has_work = op_begin<4, false>(an, load_record(an, w), warp, lane, smem_base, bar0, g, rs);
-        }
-        MK_CTRACE(k, 4);
-        __syncthreads();  // every warp is done with op k's x table
-    }
-}
-
-// Column just before the first unit of every chunk that starts inside a row:
-// sum of the row's deltas over [row start, unit start) minus one.  Setup only.
-// order 0 (ROMA): lim = the row's 8-aligned start + j units; order 1 (flat): lim = E0, the warp's
-// first element (-1 for rows starting at or after it).
-__global__ void plan_colbase_kernel(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
-                                    uint32_t n_chunks) {
+// Column just before the first unit of every chunk that starts inside a row: sum of the row's
+// deltas over [row start, the row's 8-aligned start + j units) minus one.  Setup only.
+__global__ void plan_colbase_kernel(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
     if (w >= n_chunks) return;
     const uint32_t s = warps[w].s;
-    const uint32_t lim = order ? warps[w].e0 : (s & ~7u) + warps[w].j * kUnitElts;
-    if (warps[w].units_left == 0 || (order ? s >= lim : warps[w].j == 0)) {
+    const uint32_t lim = (s & ~7u) + warps[w].j * kUnitElts;
+    if (warps[w].units_left == 0 || warps[w].j == 0) {
         if (lane == 0) warps[w].colbase = -1;
         return;
     }
@@ -975,18 +665,12 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     const int threads = kSpmvWarpsPerCta * kWarp;
     cudaError_t e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(macko_spmv_flat<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
-    int flat = 0;
-    if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&flat, macko_spmv_flat<kXMode, kBits>, threads, smem);
-    if (e == cudaSuccess) *ctas_per_sm = std::min(*ctas_per_sm, flat);
     return e;
 }
 
 template <int kXMode, int kBits>
-static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl, int order) {
+static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kSpmvWarpsPerCta * kWarp);
@@ -997,7 +681,6 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (order == 1) return cudaLaunchKernelEx(&cfg, macko_spmv_flat<kXMode, kBits>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 
@@ -1051,11 +734,10 @@ cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int 
     return cudaLaunchKernelEx(&cfg, copy_u16_kernel, src, dst, n, dependent ? 1u : 0u);
 }
 
-// b_delta = 4 (the paper's format) gets every x_mode; the other widths the automatic ones.
-bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 11); }
+// Every width gets the x_modes of the automatic rule (build_plan).
+bool spmv_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 8) || x_mode == 10; }
 bool spmv_valid_config(int x_mode, int bits) {
-    if (bits == 4) return spmv_valid_x_mode(x_mode);
-    return (bits == 1 || bits == 2 || bits == 8) && (x_mode == 0 || x_mode == 1 || (x_mode >= 6 && x_mode <= 8) || x_mode == 10);
+    return (bits == 1 || bits == 2 || bits == 4 || bits == 8) && spmv_valid_x_mode(x_mode);
 }
 
 template <int kBits>
@@ -1069,34 +751,19 @@ static cudaError_t occ_bits(int x_mode, size_t smem, int* c) {
         case 0: return occ_one<0, kBits>(smem, c);
         default: break;
     }
-    if constexpr (kBits == 4) {
-        switch (x_mode) {
-            case 11: return occ_one<11, 4>(smem, c);
-            case 9: return occ_one<9, 4>(smem, c);
-            default: break;
-        }
-    }
     return cudaErrorInvalidValue;
 }
 
 template <int kBits>
-static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
-                               int order) {
+static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
     switch (x_mode) {
-        case 10: return launch_one<10, kBits>(a, grid, smem, s, pdl, order);
-        case 8: return launch_one<8, kBits>(a, grid, smem, s, pdl, order);
-        case 7: return launch_one<7, kBits>(a, grid, smem, s, pdl, order);
-        case 6: return launch_one<6, kBits>(a, grid, smem, s, pdl, order);
-        case 1: return launch_one<1, kBits>(a, grid, smem, s, pdl, order);
-        case 0: return launch_one<0, kBits>(a, grid, smem, s, pdl, order);
+        case 10: return launch_one<10, kBits>(a, grid, smem, s, pdl);
+        case 8: return launch_one<8, kBits>(a, grid, smem, s, pdl);
+        case 7: return launch_one<7, kBits>(a, grid, smem, s, pdl);
+        case 6: return launch_one<6, kBits>(a, grid, smem, s, pdl);
+        case 1: return launch_one<1, kBits>(a, grid, smem, s, pdl);
+        case 0: return launch_one<0, kBits>(a, grid, smem, s, pdl);
         default: break;
-    }
-    if constexpr (kBits == 4) {
-        switch (x_mode) {
-            case 11: return launch_one<11, 4>(a, grid, smem, s, pdl, order);
-            case 9: return launch_one<9, 4>(a, grid, smem, s, pdl, order);
-            default: break;
-        }
     }
     return cudaErrorInvalidValue;
 }
@@ -1111,60 +778,14 @@ cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm) 
     }
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
-                        int order) {
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl) {
     switch (bits) {
-        case 4: return launch_bits<4>(a, grid, x_mode, smem, s, pdl, order);
-        case 2: return launch_bits<2>(a, grid, x_mode, smem, s, pdl, order);
-        case 8: return launch_bits<8>(a, grid, x_mode, smem, s, pdl, order);
-        case 1: return launch_bits<1>(a, grid, x_mode, smem, s, pdl, order);
+        case 4: return launch_bits<4>(a, grid, x_mode, smem, s, pdl);
+        case 2: return launch_bits<2>(a, grid, x_mode, smem, s, pdl);
+        case 8: return launch_bits<8>(a, grid, x_mode, smem, s, pdl);
+        case 1: return launch_bits<1>(a, grid, x_mode, smem, s, pdl);
         default: return cudaErrorInvalidValue;
     }
-}
-
-template <int kXMode>
-static cudaError_t chain_one(const ChainOps& ops, uint32_t n, uint32_t* bar, int grid, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(macko_chain_b4<kXMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kSpmvWarpsPerCta * kWarp);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, macko_chain_b4<kXMode>, ops, n, bar);
-}
-
-cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s) {
-    // one cooperative launch per kChainOpsPerLaunch ops (the arguments travel as kernel parameters)
-    static thread_local ChainOps ops;
-    for (uint32_t k0 = 0; k0 < n_ops; k0 += kChainOpsPerLaunch) {
-        const uint32_t n = n_ops - k0 < kChainOpsPerLaunch ? n_ops - k0 : kChainOpsPerLaunch;
-        for (uint32_t k = 0; k < n; ++k) ops.op[k] = h_ops[k0 + k];
-        cudaError_t e = cudaErrorInvalidValue;
-#define MK_CHAIN(M)                                           \
-    case M:                                                   \
-        e = chain_one<M>(ops, n, d_bar, grid, smem, s);       \
-        break;
-        switch (x_mode) {
-            MK_CHAIN(10)
-            MK_CHAIN(9)
-            MK_CHAIN(8)
-            MK_CHAIN(7)
-            MK_CHAIN(6)
-            MK_CHAIN(1)
-            MK_CHAIN(0)
-            default: break;
-        }
-#undef MK_CHAIN
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
 }
 
 #ifdef MACKO_TRACE
@@ -1174,11 +795,10 @@ cudaError_t trace_read(unsigned long long* host, size_t n) {
 }
 #endif
 
-cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
-                                uint32_t n_chunks, cudaStream_t s) {
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s) {
     const int threads = 256;
     const int blocks = (int)((n_chunks * (uint64_t)kWarp + threads - 1) / threads);
-    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, bits, order, warps, n_chunks);
+    if (blocks) plan_colbase_kernel<<<blocks, threads, 0, s>>>(deltas, bits, warps, n_chunks);
     return cudaGetLastError();
 }
 

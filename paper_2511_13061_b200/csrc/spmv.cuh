@@ -25,14 +25,16 @@ static_assert(sizeof(WarpPlan) == 48, "WarpPlan is loaded as three 16-byte vecto
 struct SpmvPlanDev {
     const WarpPlan* warps;   // W records
     const uint4* splits;     // S: {first partial slot, units of the first piece, pieces, 0}
+    // Per-launch workspace (one per stream, capi.cu Workspace): launches of one matrix on different
+    // streams never share these.
     float* partials;         // per split row, one slot per unit
     uint32_t* counters;      // S: arrival counters (zero between launches)
 };
 
 // Fused all-gather of y (row-sharded SpMV over NVLink peers): up to kMaxPeers destinations.
 constexpr uint32_t kMaxPeers = 8;
-struct PeerTable {  // device memory, one per matrix (macko_dev_set_peers)
-    uint16_t* y[kMaxPeers];    // peer p's full y, already offset to this slab's first row
+struct PeerTable {  // device memory, one per matrix (macko_dev_set_peers / macko_dev_set_peer_bank)
+    uint16_t* y[2][kMaxPeers]; // bank b: peer p's full y, already offset to this slab's first row
     uint32_t* flag[kMaxPeers]; // this rank's completion counter in peer p's flag array
 };
 
@@ -42,9 +44,9 @@ struct SpmvArgs {
     const uint32_t* row_ptrs;
     const uint16_t* x;
     uint16_t* y;
-    cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode 0, 6..9)
+    cudaTextureObject_t xtex;           // x as a 1-D fp16 texture (x_mode 0, 6, 7, 8, 10)
     uint64_t value_elems, delta_bytes;  // allocated sizes (payload + one zeroed chunk of slack)
-    uint32_t value_count;               // pad_nnz (the flat walk's last warp owns trailing empty rows)
+    uint32_t value_count;               // pad_nnz
     uint32_t rows, cols;
     uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
@@ -52,6 +54,7 @@ struct SpmvArgs {
     uint32_t n_peer;       // fused all-gather: y rows also go to peers->y[0..n_peer) and each CTA adds 1
                            // to *peers->flag[p] (system scope) once its rows are written
     const PeerTable* peers;
+    uint32_t peer_bank;    // which y bank of the peer table this launch stores into (0 / 1)
     uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
     SpmvPlanDev plan;
 };
@@ -81,33 +84,21 @@ constexpr int kXGuardLo = 8;
 constexpr int kXGuardHi = 16;
 
 // Launchers (return cudaGetLastError()).
-// x_mode: 0 = texture gathers only, 1 = fp16 shared-memory table only, 6..9 = table + texture
-// gathers for a fixed subset of element slots (TEX pipe in parallel with the LSU pipe)
+// x_mode: 0 = texture gathers only, 1 = fp16 shared-memory table only, 6 / 7 / 8 / 10 = table +
+// texture gathers for a fixed subset of element slots (TEX pipe in parallel with the LSU pipe)
 bool spmv_valid_x_mode(int x_mode);
 #ifdef MACKO_TRACE
 cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
 #endif
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
-// order: 0 = ROMA row-relative walk (macko_spmv), 1 = flat global windows (macko_spmv_flat)
-cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl,
-                        int order);
+cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
 bool spmv_valid_config(int x_mode, int bits);
-// Persistent chain of dependent SpMVs (h_ops: host array of n_ops SpmvArgs, passed to the kernel
-// as parameters, kChainOpsPerLaunch per cooperative launch; d_bar: 2 zeroed u32 for the grid
-// barrier).  `grid` CTAs; all ops share x_mode, ring and smem.
-constexpr uint32_t kChainOpsPerLaunch = 32000 / sizeof(SpmvArgs);  // kernel parameters <= 32764 B
-struct ChainOps {
-    SpmvArgs op[kChainOpsPerLaunch];
-};
-cudaError_t launch_chain(const SpmvArgs* h_ops, uint32_t n_ops, uint32_t* d_bar, int grid, int x_mode, size_t smem,
-                         cudaStream_t s);
 // Wait until flags[i] >= target for i < n (system-scope acquire; peers' fused all-gathers).
 cudaError_t launch_wait_flags(const uint32_t* flags, uint32_t n, uint32_t target, cudaStream_t s);
 // n fp16 words src -> dst (device or device-mapped host pointers); dependent: launched as the
 // programmatic dependent of the previous kernel on the stream (waits for it before copying).
 cudaError_t launch_copy_u16(const uint16_t* src, uint16_t* dst, uint32_t n, int blocks, bool dependent, cudaStream_t s);
-cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, uint32_t order, WarpPlan* warps,
-                                uint32_t n_chunks, cudaStream_t s);
+cudaError_t launch_plan_colbase(const uint8_t* deltas, uint32_t bits, WarpPlan* warps, uint32_t n_chunks, cudaStream_t s);
 
 }  // namespace mk

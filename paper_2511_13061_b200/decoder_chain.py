@@ -179,22 +179,6 @@ class SparseDecoderChain:
                 self._spmv(layer, name, stream, pdl)
         return self.acts["h"]
 
-    def persistent(self) -> "M.Chain":
-        """The token as ONE persistent cooperative kernel (macko_chain_*): op k+1's plan load and
-        first weight fills are issued before the grid barrier that waits for op k's output, so
-        the weight stream keeps HBM busy across the dependencies (N = 1 only)."""
-        if self.world != 1:
-            raise ValueError("the persistent chain runs on one GPU (sharded chains all-gather between SpMVs)")
-        if getattr(self, "_chain", None) is None:
-            ops = [(self.mats[layer][name], _x_slice(self.shape, name, self.acts), self.acts[_out_name(name)])
-                   for layer in range(self.shape.layers) for name in LINEARS]
-            self._chain = M.Chain(ops)
-        return self._chain
-
-    def forward_token_persistent(self, stream=None) -> torch.Tensor:
-        self.persistent().run(stream)
-        return self.acts["h"]
-
     def capture(self, pdl: bool = True) -> torch.cuda.CUDAGraph:
         """Capture forward_token into a CUDA graph (kernel nodes keep their PDL edges)."""
         if self.fused:
@@ -212,9 +196,6 @@ class SparseDecoderChain:
         return g
 
     def close(self) -> None:
-        if getattr(self, "_chain", None) is not None:
-            self._chain.close()
-            self._chain = None
         for ptr in getattr(self, "_opened", []):
             M.ipc_close(ptr)
         self._opened = []

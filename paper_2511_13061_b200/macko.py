@@ -146,17 +146,9 @@ class DeviceMatrix:
         return li
 
     def configure(self, x_mode: int = -1, ctas_per_sm: int = 0, stream=None) -> None:
-        """Re-plan the launch (x_mode: -1 auto, 0 texture only, 1 shared table only, 6..11 split;
-        CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""
+        """Re-plan the launch (x_mode: -1 auto, 0 texture only, 1 shared table only, 6 / 7 / 8 / 10
+        split; CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""
         check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
-
-    def set_order(self, order: int, stream=None) -> None:
-        """SpMV walk: 0 ROMA row-relative (default), 1 flat global windows."""
-        check(_lib.load().macko_dev_set_order(self._h, order, _stream_ptr(stream)))
-
-    @property
-    def order(self) -> int:
-        return self.launch_info().order
 
     # -- operations -------------------------------------------------------------------------
     def download(self, stream=None) -> MackoMatrix:
@@ -171,11 +163,12 @@ class DeviceMatrix:
     def validate(self, stream=None) -> None:
         check(_lib.load().macko_dev_validate(self._h, _stream_ptr(stream)))
 
-    def spmv_into(self, x, y, stream=None, pdl: bool = False, peers: bool = False) -> None:
+    def spmv_into(self, x, y, stream=None, pdl: bool = False, peers: bool = False, bank: int = 0) -> None:
         """y = A*x with device tensors / pointers (stream-ordered, asynchronous).  pdl: launch as
         a programmatic dependent of the previous kernel on the stream (SpMV chains).  peers: also
-        store y into the peer buffers of set_peers and signal their flags (fused all-gather)."""
-        flags = (1 if pdl else 0) | (2 if peers else 0)
+        store y into the peer buffers of set_peers (bank 0) or set_peer_bank(1, ...) (bank 1) and
+        signal their flags (fused all-gather)."""
+        flags = (1 if pdl else 0) | (2 if peers else 0) | (4 if (peers and bank) else 0)
         if flags:
             check(_lib.load().macko_dev_spmv_ex(self._h, _ptr(x), _ptr(y), _stream_ptr(stream), flags))
         else:
@@ -188,6 +181,12 @@ class DeviceMatrix:
         fs = (C.c_void_p * max(n, 1))(*peer_flags)
         check(_lib.load().macko_dev_set_peers(self._h, ys, fs, n, _stream_ptr(stream)))
 
+    def set_peer_bank(self, bank: int, peer_y: Sequence[int], stream=None) -> None:
+        """Second set of y destinations (double-buffered fused all-gather)."""
+        n = len(peer_y)
+        ys = (C.c_void_p * max(n, 1))(*peer_y)
+        check(_lib.load().macko_dev_set_peer_bank(self._h, bank, ys, n, _stream_ptr(stream)))
+
     def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
         """End-to-end call with host buffers (H2D x, kernel, D2H y, synchronise)."""
         x = np.ascontiguousarray(x, np.uint16)
@@ -195,42 +194,15 @@ class DeviceMatrix:
             raise ValueError("dimension mismatch: x must have cols entries")
         if y is None:
             y = np.zeros(self.rows, np.uint16)
+        elif not (isinstance(y, np.ndarray) and y.dtype == np.uint16 and y.shape == (self.rows,)
+                  and y.flags.c_contiguous and y.flags.writeable):
+            raise ValueError("y must be a writeable C-contiguous uint16 array of rows entries")
         check(_lib.load().macko_spmv_host(self._h, x.ctypes.data, y.ctypes.data, _stream_ptr(stream)))
         return y
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.load().macko_dev_free(self._h)
-            self._h = C.c_void_p()
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
-
-
-class Chain:
-    """A persistent chain of dependent SpMVs (macko_chain_*): ops = [(DeviceMatrix, x, y), ...]
-    with device tensors; x_k may alias (a slice of) an earlier y_j.  run() is one cooperative
-    launch, bit-identical to the ops run one by one."""
-
-    def __init__(self, ops):
-        n = len(ops)
-        self._keep = ops  # matrices and vectors must outlive the chain
-        mats = (C.c_void_p * n)(*[m._h.value for m, _, _ in ops])
-        xs = (C.c_void_p * n)(*[_ptr(x) for _, x, _ in ops])
-        ys = (C.c_void_p * n)(*[_ptr(y) for _, _, y in ops])
-        h = C.c_void_p()
-        check(_lib.load().macko_chain_create(mats, xs, ys, n, C.byref(h)))
-        self._h = h
-
-    def run(self, stream=None) -> None:
-        check(_lib.load().macko_chain_run(self._h, _stream_ptr(stream)))
-
-    def close(self) -> None:
-        if getattr(self, "_h", None) is not None and self._h.value:
-            _lib.load().macko_chain_free(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -103,7 +103,12 @@ class FusedRowShardedSpmv:
     stores its slab's rows straight into every rank's full-y buffer (CUDA IPC / P2P over NVLink)
     and counts its CTAs into every rank's flag array; a step ends with a stream-ordered wait until
     all ranks' CTAs have signalled (MACKO_SPMV_PEERS, macko_wait_flags).  x must already be
-    identical on every rank (in a decode chain it is the previous step's full y).
+    identical on every rank.
+
+    The output is double-buffered by step parity (peer banks 0 / 1), so `y = fused(y)` is safe:
+    step k writes the buffer that was step k-1's x, and a rank only starts step k after every
+    rank's CTAs of step k-1 signalled — which they do after their last read of x.  The returned
+    buffer is valid until the call after next.
 
     Setup exchanges IPC handles over `group` (any backend; gloo works).  Every rank's slab must
     use the same launch grid (same GPU model), which the flag target assumes.
@@ -117,27 +122,27 @@ class FusedRowShardedSpmv:
         self.r0, self.r1 = slab_bounds(rows_total, self.world, self.rank)
         if dm.rows != self.r1 - self.r0:
             raise ValueError("slab rows do not match this rank's share of rows_total")
-        self.y = torch.zeros(rows_total, dtype=torch.float16, device=device)
+        self.ys = [torch.zeros(rows_total, dtype=torch.float16, device=device) for _ in range(2)]
         self.flags = torch.zeros(self.world, dtype=torch.int32, device=device)
         self.grid = dm.launch_info().grid
         self.epoch = 0
         dev = device.index if device.index is not None else torch.cuda.current_device()
-        mine = (M.ipc_handle(self.y), M.ipc_handle(self.flags), self.r0)
+        mine = ([M.ipc_handle(y) for y in self.ys], M.ipc_handle(self.flags), self.r0)
         if self.world > 1:
             allh = [None] * self.world
             dist.all_gather_object(allh, mine, group=group)
         else:
             allh = [mine]
         self._opened, self._bases = [], {}
-        peer_y, peer_f = [], []
-        for p, ((hy, oy), (hf, of), _) in enumerate(allh):
-            if p == self.rank:
-                yb, fb = self.y.data_ptr(), self.flags.data_ptr()
-            else:
-                yb, fb = self._open(hy, dev) + oy, self._open(hf, dev) + of
-            peer_y.append(yb + 2 * self.r0)
+        peer_y, peer_f = [[], []], []
+        for p, (hys, (hf, of), _) in enumerate(allh):
+            for b, (hy, oy) in enumerate(hys):
+                yb = self.ys[b].data_ptr() if p == self.rank else self._open(hy, dev) + oy
+                peer_y[b].append(yb + 2 * self.r0)
+            fb = self.flags.data_ptr() if p == self.rank else self._open(hf, dev) + of
             peer_f.append(fb + 4 * self.rank)
-        dm.set_peers(peer_y, peer_f)
+        dm.set_peers(peer_y[0], peer_f)
+        dm.set_peer_bank(1, peer_y[1])
 
     def _open(self, handle: bytes, dev: int) -> int:
         # one mapping per allocation (y and flags may come from the same caching-allocator segment)
@@ -146,11 +151,21 @@ class FusedRowShardedSpmv:
             self._opened.append(self._bases[handle])
         return self._bases[handle]
 
+    @property
+    def y(self) -> torch.Tensor:
+        """The buffer the last call filled."""
+        return self.ys[(self.epoch + 1) % 2]
+
     def __call__(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        bank = self.epoch % 2
+        out = self.ys[bank]
+        xs, xe = x.data_ptr(), x.data_ptr() + 2 * x.numel()
+        if xs < out.data_ptr() + 2 * out.numel() and out.data_ptr() < xe:
+            raise ValueError("x overlaps this step's output buffer (pass the previous step's y or another buffer)")
         self.epoch += 1
-        self.dm.spmv_into(x, self.y[self.r0:self.r1], stream, peers=True)
+        self.dm.spmv_into(x, out[self.r0:self.r1], stream, peers=True, bank=bank)
         M.wait_flags(self.flags, self.world, self.epoch * self.grid, stream)
-        return self.y
+        return out
 
     def close(self) -> None:
         self.dm.set_peers([], [])

@@ -4,13 +4,12 @@ import numpy as np
 UNIT_STEPS = 8  # csrc/common.cuh kUnitSteps: the kernel's canonical reduction granularity
 
 
-def b200_y(order_or_dm, m, x):
-    """The oracle emulation of the GPU's summation order for a device matrix (or an order):
-    0 = ROMA row-relative walk (mo_b200_order_spmv), 1 = flat global windows (mo_b200_flat_spmv)."""
+def b200_y(m, x):
+    """The oracle emulation of the GPU's summation order (mo_b200_order_spmv: the ROMA walk,
+    per-lane sequential, xor-tree per unit of UNIT_STEPS steps, units in order)."""
     from oracle import oracle as O
 
-    order = order_or_dm if isinstance(order_or_dm, int) else order_or_dm.order
-    return O.b200_flat_spmv(m, x) if order == 1 else O.b200_order_spmv(m, x, UNIT_STEPS)
+    return O.b200_order_spmv(m, x, UNIT_STEPS)
 
 
 def tol_bound(dense: np.ndarray, x: np.ndarray, y_ref: np.ndarray):

@@ -4,7 +4,7 @@ caller binds.
 
 Bars: format (values / packed deltas / row pointers, tails included) bit-exact; y bit-exact in
 integer mode; in float mode bit-exact against the oracle's emulation of the kernel's summation
-order (oracle mo_b200_flat_spmv / mo_b200_order_spmv for the flat / ROMA walk, tests.helpers.b200_y)
+order (oracle mo_b200_order_spmv, tests.helpers.b200_y)
 AND within the stated bound of the sequential reference.
 """
 import numpy as np
@@ -45,11 +45,11 @@ def gpu_spmv(dm: M.DeviceMatrix, x: np.ndarray) -> np.ndarray:
     return to_host_u16(y)
 
 
-def check_y(dense, m, x, y, int_mode, ctx="", order=1):
+def check_y(dense, m, x, y, int_mode, ctx=""):
     if int_mode:
         assert np.array_equal(y, O.reference_spmv(m, x, 8)), ctx
     else:
-        assert np.array_equal(y, b200_y(order, m, x)), ctx
+        assert np.array_equal(y, b200_y(m, x)), ctx
         assert within_bound(dense, x, y, O.reference_spmv(m, x, 8)), ctx
 
 
@@ -121,7 +121,7 @@ def test_spmv_on_reference_golden_vectors(cuda, golden):
         if name.endswith("_int") or name in ("fig3_b2", "diag", "zeros3", "dense16", "single31", "worst1x32"):
             assert np.array_equal(y, c["y_ref"]), name
         else:
-            assert np.array_equal(y, b200_y(dm, m, c["x"])), name
+            assert np.array_equal(y, b200_y(m, c["x"])), name
             assert within_bound(c["dense"], c["x"], y, c["y_ref"]), name
         n += 1
     assert n >= 10
@@ -144,9 +144,7 @@ def test_spmv_random_shapes(cuda, int_mode):
         x = O.gen_vector(C, 99 + i, int_mode)
         m = O.encode_dense(A)
         dm = gpu_encode(A)
-        for order in (1, 0):  # flat global windows (default) and the ROMA row-relative walk
-            dm.set_order(order)
-            check_y(A, m, x, gpu_spmv(dm, x), int_mode, (R, C, d, order), order)
+        check_y(A, m, x, gpu_spmv(dm, x), int_mode, (R, C, d))
 
 
 @pytest.mark.parametrize("R,C", [(4096, 4096), (11008, 4096), (4096, 11008)])
@@ -159,25 +157,7 @@ def test_spmv_llama_shapes(cuda, R, C):
         m = O.encode_dense(A)
         assert_same_format(dm, m, (R, C))
         x = O.gen_vector(C, 6, int_mode)
-        check_y(A, m, x, gpu_spmv(dm, x), int_mode, (R, C), dm.order)
-
-
-@pytest.mark.parametrize("density", [0.5, 0.7, 0.3, 0.1])
-def test_spmv_headline_shape(cuda, density):
-    """36864 x 12288 (BASELINE.json configs[1]); full size at 50 %, 4608-row slabs elsewhere."""
-    R, C = (36864, 12288) if density == 0.5 else (4608, 12288)
-    t = torch.empty((R, C), dtype=torch.float16, device=cuda)
-    M.gen_dense(t, R, C, density, seed=1234)
-    dm = M.DeviceMatrix.from_dense(t)
-    A = O.gen_dense(R, C, density, 1234)
-    m = O.encode_dense(A)
-    assert_same_format(dm, m, (R, C, density))
-    x = O.gen_vector(C, 4321)
-    for order in (1, 0):
-        dm.set_order(order)
-        y = gpu_spmv(dm, x)
-        assert np.array_equal(y, b200_y(order, m, x)), order
-        assert within_bound(A, x, y, O.reference_spmv(m, x, 16))
+        check_y(A, m, x, gpu_spmv(dm, x), int_mode, (R, C))
 
 
 def test_spmv_x_in_global_memory_path(cuda):
@@ -187,7 +167,7 @@ def test_spmv_x_in_global_memory_path(cuda):
     x = O.gen_vector(C, 4)
     dm = gpu_encode(A)
     assert dm.launch_info().x_in_smem == 0
-    check_y(A, O.encode_dense(A), x, gpu_spmv(dm, x), False, "", dm.order)
+    check_y(A, O.encode_dense(A), x, gpu_spmv(dm, x), False, "")
 
 
 def test_spmv_deterministic_graph_and_unaligned_x(cuda):
@@ -230,19 +210,17 @@ def test_plan_and_x_staging_do_not_change_y(cuda):
         A = O.gen_dense(R, C, d, 31)
         x = O.gen_vector(C, 32)
         dm = gpu_encode(A)
-        for order in (1, 0):
-            dm.set_order(order)
-            y0 = gpu_spmv(dm, x)
-            assert np.array_equal(y0, b200_y(order, O.encode_dense(A), x)), order
-            for x_mode in (0, 1, 6, 7, 8, 9):
-                for ctas in (1, 2, 0):
-                    try:
-                        dm.configure(x_mode, ctas)
-                    except ValueError:  # the x table would not leave room for the TMA rings
-                        assert x_mode > 0 and C * 2 >= 64_000
-                        continue
-                    assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, order, x_mode, ctas)
-            dm.configure(-1, 0)
+        y0 = gpu_spmv(dm, x)
+        assert np.array_equal(y0, b200_y(O.encode_dense(A), x))
+        for x_mode in (0, 1, 6, 7, 8, 10):
+            for ctas in (1, 2, 0):
+                try:
+                    dm.configure(x_mode, ctas)
+                except ValueError:  # the x table would not leave room for the TMA rings
+                    assert x_mode > 0 and C * 2 >= 64_000
+                    continue
+                assert np.array_equal(gpu_spmv(dm, x), y0), (R, C, d, x_mode, ctas)
+        dm.configure(-1, 0)
 
 
 def test_spmv_host_buffers_e2e(cuda):
@@ -251,7 +229,7 @@ def test_spmv_host_buffers_e2e(cuda):
     dm = gpu_encode(A)
     y_host = dm.spmv_host(x)  # pageable numpy buffers: cudaMemcpyAsync both ways
     assert np.array_equal(y_host, gpu_spmv(dm, x))
-    assert np.array_equal(y_host, b200_y(dm, O.encode_dense(A), x))
+    assert np.array_equal(y_host, b200_y(O.encode_dense(A), x))
     # pinned (device-mapped) buffers: x pulled / y pushed by kernels chained with PDL; odd offsets
     # exercise the 2-byte path of the copies
     for off in (0, 1):
@@ -266,36 +244,33 @@ def test_spmv_host_buffers_e2e(cuda):
 
 
 def test_row_slabs_and_grid_independence(cuda):
-    # The kernel's summation order depends only on a row's elements and on their positions
-    # (mod 8 for the ROMA walk; mod 2048 for the flat walk) — never on the grid,
-    # the work plan or where warps cut rows.  So: a slab encoded alone matches the oracle on that
-    # slab bit-exactly; it is bit-identical to the full-matrix rows when its base offset keeps the
-    # alignment; otherwise it is within the stated bound.
+    # The kernel's summation order depends only on a row's elements and on their positions mod 8
+    # (ROMA) — never on the grid, the work plan or where warps cut rows.  So: a
+    # slab encoded alone matches the oracle on that slab bit-exactly; it is bit-identical to the
+    # full-matrix rows when its base offset keeps the alignment; otherwise it is within the
+    # stated bound.
     R, C = 4096, 8192
     A = O.gen_dense(R, C, 0.5, 21)
     x = O.gen_vector(C, 22)
     g = O.encode_dense(A)
     dm_full = gpu_encode(A)
     y_seq = O.reference_spmv(g, x, 8)
-    for order, align in ((1, 2048), (0, 8)):
-        dm_full.set_order(order)
-        y_full = gpu_spmv(dm_full, x)
-        for r0, r1 in ((0, 512), (512, 1536), (1536, 4096), (100, 101), (7, 3000)):
-            s = O.encode_dense(A[r0:r1])
-            dms = gpu_encode(A[r0:r1])
-            dms.set_order(order)
-            y = gpu_spmv(dms, x)
-            assert np.array_equal(y, b200_y(order, s, x)), (order, r0, r1)
-            if int(g.row_ptrs[r0]) % align == 0:
-                assert np.array_equal(y, y_full[r0:r1]), (order, r0, r1)
-            assert within_bound(A[r0:r1], x, y, y_seq[r0:r1])
+    y_full = gpu_spmv(dm_full, x)
+    for r0, r1 in ((0, 512), (512, 1536), (1536, 4096), (100, 101), (7, 3000)):
+        s = O.encode_dense(A[r0:r1])
+        dms = gpu_encode(A[r0:r1])
+        y = gpu_spmv(dms, x)
+        assert np.array_equal(y, b200_y(s, x)), (r0, r1)
+        if int(g.row_ptrs[r0]) % 8 == 0:
+            assert np.array_equal(y, y_full[r0:r1]), (r0, r1)
+        assert within_bound(A[r0:r1], x, y, y_seq[r0:r1])
     # device-generated slab with a row offset equals the slab of the global matrix
     t = torch.empty((1024, C), dtype=torch.float16, device=cuda)
     M.gen_dense(t, 1024, C, 0.5, seed=21, row0=2048)
     dm = M.DeviceMatrix.from_dense(t)
     s = O.encode_dense(A[2048:3072])
     assert_same_format(dm, s)
-    assert np.array_equal(gpu_spmv(dm, x), b200_y(dm, s, x))
+    assert np.array_equal(gpu_spmv(dm, x), b200_y(s, x))
 
 
 def test_error_behaviour(cuda):
@@ -312,7 +287,7 @@ def test_error_behaviour(cuda):
     if (v != m.values).any():
         with pytest.raises(M.FormatError):
             M.DeviceMatrix.upload(M.MackoMatrix(4, 64, 4, v, m.deltas, m.row_ptrs))
-    # b_delta = 2 has no x_mode 9 / 11 instantiation (b_delta = 4 only)
+    # x_mode 9 / 11 do not exist
     dm2 = gpu_encode(A, 2)
     with pytest.raises(ValueError, match="x_mode"):
         dm2.configure(9)
@@ -363,7 +338,7 @@ def test_masked_edges_do_not_leak_inf_nan(cuda, x_mode):
         dm.configure(x_mode)
     m = O.encode_dense(A)
     y = gpu_spmv(dm, x)
-    y_ref = b200_y(dm, m, x)
+    y_ref = b200_y(m, x)
     assert _same_or_both_nan(y, y_ref)
     assert np.isfinite(y_ref[0::2].view(np.float16)).all()
     assert np.array_equal(y[0::2], y_ref[0::2])
@@ -383,9 +358,7 @@ def test_spmv_other_delta_widths(cuda, bits):
             m = O.encode_dense(A, bits)
             dm = gpu_encode(A, bits)
             assert_same_format(dm, m, (bits, R, C, d))
-            for order in (1, 0):
-                dm.set_order(order)
-                check_y(A, m, x, gpu_spmv(dm, x), int_mode, (bits, R, C, d, int_mode, order), order)
+            check_y(A, m, x, gpu_spmv(dm, x), int_mode, (bits, R, C, d, int_mode))
     A = O.gen_dense(500, 9000, 0.3, 72)
     x = O.gen_vector(9000, 73)
     dm = gpu_encode(A, bits)
@@ -444,7 +417,7 @@ def _random_values(rng, n):
 
 def test_rows_split_across_many_warps(cuda):
     # three ~1M-element rows: every row is cut into hundreds of warp pieces, finished by the last
-    # arriving warp from per-unit partials; both walks, float and integer values
+    # arriving warp from per-unit partials; float and integer values
     R, C = 3, 2_000_000
     for int_mode in (False, True):
         A = O.gen_dense(R, C, 0.5, 515, int_mode)
@@ -453,9 +426,7 @@ def test_rows_split_across_many_warps(cuda):
         m = O.encode_dense(A)
         dm = gpu_encode(A)
         assert dm.launch_info().n_split_rows >= 3
-        for order in (0, 1):
-            dm.set_order(order)
-            check_y(A, m, x, gpu_spmv(dm, x), int_mode, ("split", int_mode, order), order)
+        check_y(A, m, x, gpu_spmv(dm, x), int_mode, ("split", int_mode))
 
 
 def test_power_law_row_lengths(cuda):
@@ -470,9 +441,7 @@ def test_power_law_row_lengths(cuda):
     x = O.gen_vector(C, 78)
     m = O.encode_dense(A)
     dm = gpu_encode(A)
-    for order in (0, 1):
-        dm.set_order(order)
-        check_y(A, m, x, gpu_spmv(dm, x), False, ("zipf", order), order)
+    check_y(A, m, x, gpu_spmv(dm, x), False, "zipf")
 
 
 def test_other_widths_every_x_mode(cuda):
@@ -482,9 +451,9 @@ def test_other_widths_every_x_mode(cuda):
         x = O.gen_vector(6000, 91)
         m = O.encode_dense(A, bits)
         dm = gpu_encode(A, bits)
-        ref = b200_y(dm, m, x)
+        ref = b200_y(m, x)
         for xm in (0, 1, 6, 7, 8, 10):
             dm.configure(xm)
             assert np.array_equal(gpu_spmv(dm, x), ref), (bits, xm)
         with pytest.raises(ValueError):
-            dm.configure(9)  # b_delta = 4 only
+            dm.configure(11)

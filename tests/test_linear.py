@@ -23,7 +23,7 @@ def test_macko_linear_matches_oracle(cuda):
     xd = to_dev(x)
     y = ml(xd)
     torch.cuda.synchronize()
-    y_ref = b200_y(ml.matrix, O.encode_dense(A), x)
+    y_ref = b200_y(O.encode_dense(A), x)
     expect = (torch.from_numpy(y_ref.view(np.float16)).to(cuda) + lin.bias).view(torch.int16)
     assert np.array_equal(to_host_u16(y), expect.cpu().numpy().view(np.uint16))
     # [1, 1, in] and a batch of 3 (one SpMV per vector)
@@ -44,7 +44,7 @@ def test_torch_op_and_graph_capture(cuda):
     x = to_dev(O.gen_vector(in_f, 92))
     y = torch.ops.macko.spmv(ml.matrix.handle, x, out_f)
     torch.cuda.synchronize()
-    assert np.array_equal(to_host_u16(y), b200_y(ml.matrix, O.encode_dense(A), O.gen_vector(in_f, 92)))
+    assert np.array_equal(to_host_u16(y), b200_y(O.encode_dense(A), O.gen_vector(in_f, 92)))
     from torch._subclasses.fake_tensor import FakeTensorMode
     with FakeTensorMode() as mode:
         fx = mode.from_tensor(x)

@@ -105,7 +105,6 @@ def test_golden_vectors_encoder_and_spmv(golden):
             assert np.array_equal(c["y_ref"], c["y_dense"]), name
             assert np.array_equal(O.warp_spmv(m, c["x"]), c["y_ref"]), name
             assert np.array_equal(O.b200_order_spmv(m, c["x"], 4), c["y_ref"]), name
-            assert np.array_equal(O.b200_flat_spmv(m, c["x"]), c["y_ref"]), name
 
 
 def test_fig3_worked_example(golden):
@@ -222,7 +221,6 @@ def test_integer_mode_executors_bit_exact():
         assert np.array_equal(O.reference_spmv(m, x), y)
         assert np.array_equal(O.warp_spmv(m, x), y)
         assert np.array_equal(O.b200_order_spmv(m, x, 4), y)
-        assert np.array_equal(O.b200_flat_spmv(m, x), y)
         assert np.array_equal(O.reference_spmv(m, x, 4), y)
 
 
@@ -256,44 +254,52 @@ def test_float_mode_error_budget_4096():
     y_seq = O.reference_spmv(m, x, 8)
     y_b200 = O.b200_order_spmv(m, x, 4)
     y_warp = O.warp_spmv(m, x)
-    y_flat = O.b200_flat_spmv(m, x)
     bound, yr = tol_bound(A, x, y_seq)
-    for y in (y_b200, y_warp, y_flat):
+    for y in (y_b200, y_warp):
         dy = np.abs(y.view(np.float16).astype(np.float64) - yr)
         assert (dy <= bound).all()
     assert np.array_equal(O.b200_order_spmv(m, x, 0), y_warp)
 
 
-def _flat_py(m, x):
-    """Pure-Python restatement of the flat-window order (small cases): element i of a row goes to
-    lane (i mod 256) / 8 of the 2048-element global window holding i; each window's 32 lane sums
-    are reduced by the xor butterfly and the window totals are added in window order."""
+def _b200_py(m, x, unit_steps=8):
+    """Pure-Python restatement of the kernel's summation order (small cases): the
+    row's walk starts at its 8-aligned element al (ROMA); element i goes to lane
+    ((i - al) mod 256) / 8 of step (i - al) / 256; steps form units of unit_steps (the row's last
+    unit absorbs a shorter remainder); per unit the 32 lane sums are reduced by the xor butterfly
+    and the unit totals are added in order (+0 start); one RNE at the end."""
     h = lambda a: np.float32(np.uint16(a).view(np.float16))
     codes = O.unpack_deltas(m.deltas, m.pad_nnz, m.b_delta)
     y = np.zeros(m.rows, np.uint16)
     for r in range(m.rows):
         s, e = int(m.row_ptrs[r]), int(m.row_ptrs[r + 1])
+        al = s & ~7
+        T = (e - al + 255) // 256 if e > s else 0
+        n_r = T // unit_steps if T >= unit_steps else 1
         col, tot = -1, np.float32(0)
-        for w0 in range((s // 2048) * 2048, e, 2048):
+        for j in range(n_r if T else 0):
+            lo_step, hi_step = j * unit_steps, (T if j == n_r - 1 else (j + 1) * unit_steps)
             acc = [np.float32(0)] * 32
-            for i in range(max(s, w0), min(e, w0 + 2048)):
+            for i in range(max(s, al + 256 * lo_step), min(e, al + 256 * hi_step)):
                 col += int(codes[i])
-                acc[(i % 256) // 8] = np.float32(acc[(i % 256) // 8] + h(m.values[i]) * h(x[col]))
+                ln = ((i - al) % 256) // 8
+                acc[ln] = np.float32(acc[ln] + h(m.values[i]) * h(x[col]))
             for k in (16, 8, 4, 2, 1):
-                acc = [np.float32(acc[j] + acc[j ^ k]) for j in range(32)]
+                acc = [np.float32(acc[q] + acc[q ^ k]) for q in range(32)]
             tot = np.float32(tot + acc[0])
         y[r] = np.float16(tot).view(np.uint16)
     return y
 
 
-def test_flat_order_restatement():
-    # the C restatement of the flat kernel's summation order == the Python one, on rows that
-    # straddle 2048-element windows and start at every lane alignment
-    for seed, (R, C, d) in enumerate(((3, 9000, 0.6), (40, 700, 0.5), (5, 5000, 1.0), (9, 64, 0.3))):
+def test_b200_order_restatement():
+    # the C restatement of the kernel's summation order (mo_b200_order_spmv) == the Python one, on
+    # rows that start at every alignment mod 8, span several units, and are empty
+    for seed, (R, C, d) in enumerate(((3, 9000, 0.6), (40, 700, 0.5), (5, 5000, 1.0), (9, 64, 0.3), (2, 20000, 0.2))):
         A = O.gen_dense(R, C, d, 300 + seed)
+        A[R // 2] = 0
         x = O.gen_vector(C, 400 + seed)
         m = O.encode_dense(A)
-        assert np.array_equal(O.b200_flat_spmv(m, x), _flat_py(m, x)), (R, C, d)
+        assert np.array_equal(O.b200_order_spmv(m, x, 8), _b200_py(m, x, 8)), (R, C, d)
+        assert np.array_equal(O.b200_order_spmv(m, x, 2), _b200_py(m, x, 2)), (R, C, d)
 
 
 def test_slab_encoding_equals_global_slice():

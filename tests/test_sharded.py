@@ -105,9 +105,18 @@ def test_nccl_sharded_spmv_single_rank(cuda):
         nccl.ncclCommDestroy(comm)
 
 
+def _fused_matrix(R, C):
+    """Float-mode test matrix scaled by 2^-4 (exact in fp16) so iterating y = A y stays in range."""
+    from oracle import oracle as O
+
+    A = O.gen_dense(R, C, 0.5, 17)
+    return (A.view(np.float16) * np.float16(2.0**-4)).astype(np.float16).view(np.uint16)
+
+
 def _fused_worker(rank, world, port, R, C, out_path):
     # one GPU shared by `world` processes: CUDA IPC between processes on the same device exercises
-    # the whole fused all-gather protocol (peer stores, system-scope flags, waits)
+    # the whole fused all-gather protocol (peer stores, system-scope flags, waits).  The natural
+    # loop y = fused(y) runs without any barrier: the double-buffered outputs make it safe.
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -119,19 +128,22 @@ def _fused_worker(rank, world, port, R, C, out_path):
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
         r0, r1 = slab_bounds(R, world, rank)
-        A = O.gen_dense(R, C, 0.5, 17)[r0:r1]
+        A = _fused_matrix(R, C)[r0:r1]
         dm = M.DeviceMatrix.from_dense(torch.from_numpy(A.view(np.int16)).to(dev).view(torch.float16))
         fused = FusedRowShardedSpmv(dm, R, dev)
-        x = torch.from_numpy(O.gen_vector(C, 18).view(np.int16)).to(dev).view(torch.float16)
-        for step in range(3):
-            y = fused(x)
-            torch.cuda.synchronize()
-            dist.barrier()  # nobody starts step k+1 (overwriting peers' y) before all read step k
-            got = y.view(torch.int16).cpu().numpy().view(np.uint16).copy()
-            if rank == 0:
-                np.save(out_path + f".{step}.npy", got)
-            dist.barrier()
-        assert int(fused.flags.cpu().numpy().min()) == 3 * fused.grid
+        y = torch.from_numpy(O.gen_vector(C, 18).view(np.int16)).to(dev).view(torch.float16)
+        outs = []
+        for step in range(4):
+            y = fused(y)
+            outs.append(y.clone())  # stream-ordered copy of this step's full y
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError):
+            fused(fused.ys[fused.epoch % 2])  # x overlapping the output buffer is refused
+        if rank == 0:
+            for step, t in enumerate(outs):
+                np.save(out_path + f".{step}.npy", t.view(torch.int16).cpu().numpy().view(np.uint16))
+        dist.barrier()
+        assert int(fused.flags.cpu().numpy().min()) == 4 * fused.grid
         fused.close()
         dm.close()
     finally:
@@ -149,19 +161,13 @@ def test_fused_allgather_single_rank(cuda):
     x = O.gen_vector(5000, 72)
     dm = M.DeviceMatrix.from_dense(to_dev(A))
     fused = FusedRowShardedSpmv(dm, 3000, cuda)
-    ref = b200_y(dm, O.encode_dense(A), x)
+    ref = b200_y(O.encode_dense(A), x)
     for step in range(1, 4):
         y = fused(to_dev(x))
         torch.cuda.synchronize()
         assert np.array_equal(to_host_u16(y), ref), step
+        assert y.data_ptr() == fused.ys[(step - 1) % 2].data_ptr()
         assert int(fused.flags.item()) == step * fused.grid
-    # the flat walk stores and signals the same way (set_order re-plans; the peer table stays)
-    dm.set_order(1)
-    ref1 = b200_y(dm, O.encode_dense(A), x)
-    y = fused(to_dev(x))
-    torch.cuda.synchronize()
-    assert np.array_equal(to_host_u16(y), ref1)
-    assert int(fused.flags.item()) == 4 * fused.grid
     fused.close()
     dm.close()
 
@@ -170,18 +176,21 @@ def test_fused_allgather_single_rank(cuda):
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("world", [2, 4])
 def test_fused_allgather_processes_one_gpu(cuda, tmp_path, world):
+    # bit-exact against the slab-order oracle: rank g's rows are the kernel order on its own slab
     from oracle import oracle as O
+    from paper_2511_13061_b200.sharded import slab_bounds
+    from tests.helpers import b200_y
 
-    R, C = 4000, 3000
+    R = C = 3000
     out = str(tmp_path / "fy")
     mp.spawn(_fused_worker, args=(world, _free_port(), R, C, out), nprocs=world, join=True)
-    A = O.gen_dense(R, C, 0.5, 17)
-    ref = O.reference_spmv(O.encode_dense(A), O.gen_vector(C, 18), 8)
-    for step in range(3):
-        y = np.load(out + f".{step}.npy")
-        from tests.helpers import within_bound
-
-        assert within_bound(A, O.gen_vector(C, 18), y, ref), step
+    A = _fused_matrix(R, C)
+    slabs = [O.encode_dense(A[a:b]) for a, b in (slab_bounds(R, world, g) for g in range(world))]
+    x = O.gen_vector(C, 18)
+    for step in range(4):
+        x = np.concatenate([b200_y(s, x) for s in slabs])
+        assert np.isfinite(x.view(np.float16)).all()
+        assert np.array_equal(np.load(out + f".{step}.npy"), x), step
 
 
 def _fused_chain_worker(rank, world, port, out_path):
