@@ -2,21 +2,30 @@
 """bench.py — MACKO SpMV on B200 (BASELINE.json metric: effective HBM GB/s & µs,
 36864x12288 fp16 @ 50 % sparsity vs cuBLAS GEMV).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--sweep] [--chain] [--decode] [--strong] [--fused]
 
 One step = one SpMV y = A·x over the resident MACKO matrix (GPU-compressed from a synthetic
-random-unstructured fp16 matrix).  N > 1 (torchrun, one rank per GPU): weak scaling — every
-rank owns a 36864-row slab of an (N·36864)x12288 matrix; a step is NCCL broadcast(x) + SpMV +
-NCCL all_gather(y), timed on the device and reduced as the max over ranks.
+random-unstructured fp16 matrix of the configured shape; inputs resident in HBM).
+
+N > 1 ranks (one per GPU; `--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset): weak scaling of the headline — rank g owns rows [g·R, (g+1)·R) of an
+(N·R) x C matrix; a step is NCCL broadcast(x) + the slab SpMV + NCCL all_gather(y), timed on the
+device and reduced as the max over ranks.  Beside it, `strong` reports BASELINE config 5
+(131072x32768 @50 / 90 %, rows/N per rank): per-rank SpMV µs, the collectives' µs alone, the full
+NCCL step and the step with the all-gather fused into the SpMV kernel (peer stores over NVLink).
 
 `value` = algorithmic bytes of all ranks (spmv_traffic) / device time of one
-step.  L2 is flushed (read of a 2xL2 buffer) before every step, outside the step's events.
+step.  Inputs larger than 3x L2 stream from HBM every step; smaller ones get an L2 flush (a read
+of a 2xL2 buffer) before every step, outside the step's events.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -29,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SpMV effective HBM GB/s & µs, 36864×12288 fp16 @50% sparsity vs cuBLAS GEMV"
 HEADLINE = dict(rows=36864, cols=12288, density=0.5)
+CONFIG5 = dict(rows=131072, cols=32768)
 SEED_A, SEED_X = 1234, 4321
 
 
@@ -41,18 +51,46 @@ def parse():
     p.add_argument("--rows", type=int, default=HEADLINE["rows"])
     p.add_argument("--cols", type=int, default=HEADLINE["cols"])
     p.add_argument("--density", type=float, default=HEADLINE["density"])
-    p.add_argument("--sweep", action="store_true", help="also report 30/50/70/90 %% sparsity and Llama shapes")
-    p.add_argument("--chain", action="store_true",
-                   help="also report the Llama2-7B 32-layer decode SpMV chain (config 4) vs a dense cuBLAS chain")
+    p.add_argument("--sweep", action="store_true", help="30/50/70/90 %% sparsity, Llama shapes, 131072x32768")
+    p.add_argument("--chain", action="store_true", help="Llama2-7B 32-layer decode SpMV chain (config 4) vs cuBLAS")
+    p.add_argument("--decode", action="store_true", help="Llama2-7B decode (attention, RMSNorm, SiLU) tokens/s")
+    p.add_argument("--strong", action="store_true", help="config 5 strong scaling also at N = 1")
     p.add_argument("--chain-tokens", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
-    p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture only, 1 smem table only, 6..9 smem + texture split")
-    p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs per SM (0 = occupancy maximum)")
-    p.add_argument("--fused", action="store_true",
-                   help="N > 1: all-gather of y fused into the SpMV kernel (peer stores over NVLink + flags; "
-                        "x replicated, no broadcast) instead of NCCL broadcast + all_gather")
+    p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture, 1 smem table, 6/7/8/10 split")
+    p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs (k/4 of the persistent grid, 0 = all)")
+    p.add_argument("--fused", action="store_true", help="N > 1: also the chain with the all-gather fused into the SpMV")
     return p.parse_args()
+
+
+def maybe_spawn(args) -> None:
+    """`--gpus N` without a launcher: re-exec under torch.distributed.run, one rank per GPU."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def sparsity_pct(d: float) -> int:
+    return int(round((1 - d) * 100))
+
+
+def workload_config(R: int, C: int, d: float, world: int) -> dict:
+    """The `config` object — identical in both arms (same_config)."""
+    sp = sparsity_pct(d)
+    if world > 1:
+        wl = (f"{R}x{C} fp16 @{sp}% sparsity per rank (random unstructured), weak scaling: {world * R}x{C} "
+              f"row-sharded over {world} GPUs, NCCL broadcast x + all_gather y per SpMV")
+    else:
+        wl = f"{R}x{C} fp16 @{sp}% sparsity (random unstructured), single SpMV"
+    return {"workload": wl, "rows": R * world, "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4,
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"}
 
 
 def load_peaks():
@@ -84,7 +122,7 @@ def cpu_model():
 # ---------------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu,power.draw")
 
     def __init__(self, index: int):
         self.index = index
@@ -110,10 +148,10 @@ class ClockSampler:
         rows = []
         for line in out.strip().splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6])))
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6]), float(parts[7])))
             except ValueError:
                 continue
         if not rows:
@@ -122,13 +160,16 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_median": statistics.median(r[4] for r in loaded)}
 
 
 # ---------------------------------------------------------------------------------- reference arm
-def run_reference(args, rank: int):
-    """The reference's own CPU path (oracle/_ref: reference fp16.cpp / bitpack.cpp / headers +
-    SPEC-restated bodies) on the box's host cores, same config / metric / unit."""
+def run_reference(args, rank: int, world: int):
+    """The reference's own CPU path (oracle/_ref: the reference fp16.cpp / bitpack.cpp / headers
+    + SPEC-restated bodies) on the box's host cores, same config / metric / unit.  Rows are
+    independent, so at N > 1 the sample is one rank's slab of the (N·R) x C matrix: GB/s is a
+    rate, and the whole job's time is N x the slab's."""
     if rank != 0:
         return
     from oracle import oracle as O
@@ -136,21 +177,20 @@ def run_reference(args, rank: int):
     kind = "reference" if O.ref_available() else "port"
     threads = host_cores()
     R, C, d = args.rows, args.cols, args.density
+    n = max(world, args.gpus)
     t0 = time.time()
-    # bounded sample: full-width row slab; full matrix unless the build would be too slow
-    rows_s = R
-    A = O.gen_dense(rows_s, C, d, SEED_A)
+    A = O.gen_dense_rows(0, R, C, d, SEED_A, False, threads)
     if kind == "reference":
         rm = O.RefMatrix.encode(A, 4)
-        m = rm.to_macko(rows_s, C, 4)
-        run = lambda x: rm.spmv(x, rows_s, threads)  # noqa: E731
+        m = rm.to_macko(R, C, 4)
+        run = lambda x: rm.spmv(x, R, threads)  # noqa: E731
     else:
-        m = O.encode_dense(A, 4)
+        m = O.encode_dense(A, 4, threads)
         run = lambda x: O.reference_spmv(m, x, threads)  # noqa: E731
     del A
     build_s = time.time() - t0
     x = O.gen_vector(C, SEED_X)
-    bytes_step = O.spmv_traffic_bytes(rows_s, C, m.pad_nnz, 4)
+    bytes_sample = O.spmv_traffic_bytes(R, C, m.pad_nnz, 4)
     t1 = time.perf_counter()
     run(x)
     one = time.perf_counter() - t1
@@ -158,7 +198,7 @@ def run_reference(args, rank: int):
     budget = 120.0
     if one * (steps + args.warmup) > budget:  # keep the whole arm within a few minutes
         steps = max(3, int(budget / max(one, 1e-6)) - args.warmup)
-    for _ in range(min(args.warmup, 3)):
+    for _ in range(min(max(args.warmup, 1), 3)):
         run(x)
     times = []
     for _ in range(steps):
@@ -166,30 +206,120 @@ def run_reference(args, rank: int):
         run(x)
         times.append(time.perf_counter() - t1)
     ms = statistics.median(times) * 1e3
-    gbs = bytes_step / (ms * 1e-3) / 1e9
-    sample = (f"{rows_s}x{C} @{int(round((1 - d) * 100))}% sparsity (full workload), reference_spmv, "
-              f"{steps} timed steps (median), {threads} threads std::thread row partition, build {build_s:.1f}s, "
-              f"CPU {cpu_model()}")
+    gbs = bytes_sample / (ms * 1e-3) / 1e9
+    sample = (f"{'rows [0, %d) of the %dx%d matrix (one rank slab; rows independent), ' % (R, n * R, C) if n > 1 else ''}"
+              f"{R}x{C} @{sparsity_pct(d)}% sparsity, reference_spmv (reference encoder build {build_s:.1f} s), "
+              f"{steps} timed steps (median), {threads} threads std::thread row partition, CPU {cpu_model()}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-        "config": {"workload": f"{R}x{C} fp16 @{int(round((1 - d) * 100))}% sparsity, single SpMV", "rows": rows_s,
-                   "cols": C, "density": d, "b_delta": 4, "pad_nnz": m.pad_nnz, "bytes_per_spmv": bytes_step},
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": n,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms * n, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic (counter-hash generator)",
+        "config": workload_config(R, C, d, n),
+        "pad_nnz_sample": m.pad_nnz, "bytes_per_spmv_sample": bytes_sample,
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------------- timing helpers
+class Timer:
+    """CUDA-event timing on the launching stream with an optional L2 flush before every rep."""
+
+    def __init__(self, torch, stream, flush_buf):
+        self.torch, self.stream, self.flush_buf = torch, stream, flush_buf
+
+    def flush(self):
+        self.flush_buf.sum()  # reads 2x L2 of clean lines: evicts without dirty write-back
+
+    def run(self, fn, reps: int, warmup: int = 3, flush: bool = False):
+        torch = self.torch
+        for _ in range(warmup):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda.synchronize()
+        for a, b in evs:
+            if flush:
+                self.flush()
+            a.record(self.stream)
+            fn()
+            b.record(self.stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]  # ms
+
+
+def allmax(torch, dist, dev, vals):
+    t = torch.tensor(vals, device=dev, dtype=torch.float64)
+    if dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def cublas_hsh_gemv():
+    """cublasHSHgemvStridedBatched (fp16 in/out, fp32 compute) through the cuBLAS torch loaded —
+    the GEMV the paper compares against."""
+    import torch
+
+    lib = None
+    for name in ("libcublas.so.12", os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cublas", "lib",
+                                                 "libcublas.so.12")):
+        try:
+            lib = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    if lib is None:
+        return None
+    fn = lib.cublasHSHgemvStridedBatched
+    c = ctypes
+    fn.argtypes = [c.c_void_p, c.c_int, c.c_int, c.c_int, c.POINTER(c.c_float), c.c_void_p, c.c_int, c.c_longlong,
+                   c.c_void_p, c.c_int, c.c_longlong, c.POINTER(c.c_float), c.c_void_p, c.c_int, c.c_longlong, c.c_int]
+    fn.restype = c.c_int
+    setstream = lib.cublasSetStream_v2
+    setstream.argtypes = [c.c_void_p, c.c_void_p]
+    alpha, beta = c.c_float(1.0), c.c_float(0.0)
+
+    def run(A, x, y):  # A row-major R x C = column-major C x R; y = op_T(A_cm) x
+        R, C = A.shape
+        h = torch.cuda.current_blas_handle()
+        setstream(h, torch.cuda.current_stream().cuda_stream)
+        st = fn(h, 1, C, R, c.byref(alpha), A.data_ptr(), C, R * C, x.data_ptr(), 1, C, c.byref(beta),
+                y.data_ptr(), 1, R, 1)
+        if st != 0:
+            raise RuntimeError(f"cublasHSHgemvStridedBatched status {st}")
+
+    return run
+
+
+def dense_baseline(torch, timer, dense, x, reps, flush):
+    """The faster of cublasGemmEx (torch.mv: fp16 in/out, fp32 compute) and
+    cublasHSHgemvStridedBatched on the same dense matrix."""
+    R, C = dense.shape
+    y1 = torch.empty(R, dtype=torch.float16, device=dense.device)
+    y2 = torch.empty(R, dtype=torch.float16, device=dense.device)
+    out = {}
+    t = timer.run(lambda: torch.mv(dense, x, out=y1), reps, flush=flush)
+    out["cublasGemmEx (torch.mv)"] = statistics.median(t) * 1e3
+    hsh = cublas_hsh_gemv()
+    if hsh is not None:
+        hsh(dense, x, y2)
+        torch.cuda.synchronize()
+        if torch.allclose(y1.float(), y2.float(), rtol=2e-2, atol=1e-2):
+            t = timer.run(lambda: hsh(dense, x, y2), reps, flush=flush)
+            out["cublasHSHgemvStridedBatched"] = statistics.median(t) * 1e3
+    best = min(out, key=out.get)
+    return best, out[best], {k: round(v, 2) for k, v in out.items()}
+
+
 # ---------------------------------------------------------------------------------- our arm
 def main():
     args = parse()
+    maybe_spawn(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
 
     import torch
@@ -206,7 +336,9 @@ def main():
     stream = torch.cuda.current_stream()
     peak, peak_src = load_peaks()
     R, C, d = args.rows, args.cols, args.density
-    sparsity_pct = int(round((1 - d) * 100))
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    timer = Timer(torch, stream, flush_buf)
 
     # ---- build the rank's slab on the device: generator -> GPU compressor (no host copies)
     dense = torch.empty((R, C), dtype=torch.float16, device=dev)
@@ -222,27 +354,11 @@ def main():
     M.gen_vector(x, C, seed=SEED_X)
     y = torch.empty(R, dtype=torch.float16, device=dev)
     bytes_rank = dm.traffic_bytes
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
-    # Inputs several times larger than L2 stream from HBM on every step (verified with ncu on
-    # back-to-back launches: L2 hit rate < 1 %, DRAM bytes = algorithmic bytes); smaller inputs
-    # get an L2 flush (a read of a 2xL2 buffer) before every step, outside the step events.
     need_flush = bytes_rank < 3 * l2
 
-    def l2_flush(force=False):
-        if need_flush or force:
-            flush.sum()  # reads 2xL2 of clean lines: evicts the matrix without dirty write-back
-
-    # N > 1: rows [rank*R, (rank+1)*R) of an (N*R) x C matrix; NCCL broadcast(x) + SpMV + all_gather(y)
     sharded = None
     if world > 1:
-        if args.fused:
-            from paper_2511_13061_b200.sharded import FusedRowShardedSpmv
-
-            fused = FusedRowShardedSpmv(dm, R * world, dev)
-            sharded = lambda xx: fused(xx, stream)  # noqa: E731
-        else:
-            sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev)
+        sharded = RowShardedSpmv(R * world, C, device_local_spmv(dm, stream), device=dev)
 
     def step():
         if sharded is not None:
@@ -251,21 +367,9 @@ def main():
             dm.spmv_into(x, y, stream)
 
     # ---- dense cuBLAS GEMV on the same matrix (before freeing the dense copy)
-    dense_us = None
+    dense_best = None
     if rank == 0:
-        yd = torch.empty(R, dtype=torch.float16, device=dev)
-        for _ in range(3):
-            torch.mv(dense, x, out=yd)
-        ts = []
-        for _ in range(max(10, min(args.steps, 50))):
-            l2_flush()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            torch.mv(dense, x, out=yd)
-            e1.record()
-            e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        dense_us = statistics.median(ts) * 1e3
+        dense_best = dense_baseline(torch, timer, dense, x, max(10, min(args.steps, 50)), need_flush)
     del dense
     torch.cuda.empty_cache()
 
@@ -289,7 +393,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
-        l2_flush()
+        if need_flush:
+            timer.flush()
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)
@@ -299,108 +404,110 @@ def main():
     launches = M.kernel_launches() - launches0
     clocks = sampler.stop() if rank == 0 else None
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms_mean = sum(step_ms) / len(step_ms)
-    ms_med = statistics.median(step_ms)
-    if world > 1:
-        t = torch.tensor([ms_mean, ms_med], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_mean, ms_med = t.tolist()
+    ms_mean, ms_med = allmax(torch, dist, dev, [sum(step_ms) / len(step_ms), statistics.median(step_ms)])
     total_bytes = bytes_rank * world
     value = total_bytes / (ms_mean * 1e-3) / 1e9
 
-    # ---- kernel-only roofline of the dominant kernel (macko_spmv_b4), rank 0 alone
+    # ---- kernel-only roofline of the dominant kernel (the rank's SpMV)
     kern_ms = ms_mean
+    coll_us = None
     if world > 1:
-        kts = []
-        for _ in range(min(args.steps, 50)):
-            l2_flush()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            dm.spmv_into(x, y, stream)
-            b.record(stream)
-            b.synchronize()
-            kts.append(a.elapsed_time(b))
-        kern_ms = sum(kts) / len(kts)
+        kern_ms = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: dm.spmv_into(x, y, stream),
+                                                                     min(args.steps, 50), flush=need_flush))])[0]
+        cm = timer.run(lambda: (sharded.broadcast_x(x), sharded.gather_y()), min(args.steps, 50))
+        coll_us = allmax(torch, dist, dev, [statistics.mean(cm)])[0] * 1e3
     achieved = bytes_rank / (kern_ms * 1e-3) / 1e9
 
-    # ---- e2e through the C-ABI with pinned host buffers (H2D x, kernel, D2H y, sync)
+    # ---- e2e through the public API with pinned host buffers (H2D x, SpMV, D2H y, synchronise)
     hx = torch.empty(C, dtype=torch.int16, pin_memory=True)
-    hy = torch.empty(R, dtype=torch.int16, pin_memory=True)
     hx.copy_(x.view(torch.int16).cpu())
-    hxn, hyn = hx.numpy().view(np.uint16), hy.numpy().view(np.uint16)
-    for _ in range(3):
-        dm.spmv_host(hxn, hyn, stream)
-    e2e_ms = []
-    for _ in range(min(args.steps, 100)):
-        l2_flush()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        dm.spmv_host(hxn, hyn, stream)  # synchronises the stream internally
-        b.record(stream)
-        b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-    e2e_mean = sum(e2e_ms) / len(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_mean], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_mean = t.item()
+    if world == 1:
+        hy = torch.empty(R, dtype=torch.int16, pin_memory=True)
+        hxn, hyn = hx.numpy().view(np.uint16), hy.numpy().view(np.uint16)
+        e2e_fn = lambda: dm.spmv_host(hxn, hyn, stream)  # noqa: E731  (C-ABI macko_spmv_host, synchronises)
+        d2h = 2 * R
+    else:
+        hy = torch.empty(R * world, dtype=torch.int16, pin_memory=True)
+
+        def e2e_fn():  # rank 0's host x -> every rank's host y
+            if rank == 0:
+                x.view(torch.int16).copy_(hx, non_blocking=True)
+            yy = sharded(x)
+            hy.copy_(yy.view(torch.int16), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        d2h = 2 * R * world
+    e2e_ms = timer.run(e2e_fn, min(args.steps, 100), flush=need_flush)
+    e2e_mean = allmax(torch, dist, dev, [sum(e2e_ms) / len(e2e_ms)])[0]
     e2e_val = total_bytes / (e2e_mean * 1e-3) / 1e9
+
+    # ---- small-batch SpMM (batch 1/2/4/8 stream the matrix once)
+    spmm = run_spmm(M, torch, dm, timer, stream, need_flush) if (rank == 0 and hasattr(dm, "spmm_into")) else None
 
     cpu_src = dm.download() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     li = dm.launch_info()
     pad_nnz = dm.pad_nnz
-    sweep = None
-    if args.sweep and rank == 0:
-        sweep = run_sweep(M, torch, dev, stream, l2_flush, peak)
-
+    sweep = run_sweep(M, torch, dev, stream, timer, peak) if (args.sweep and rank == 0) else None
+    strong = None
+    if world > 1 or args.strong:
+        del dm, sharded
+        torch.cuda.empty_cache()
+        dm = None
+        strong = run_strong(args, M, torch, dist, dev, stream, timer, world, rank, peak)
     chain = None
     if args.chain:
-        del dm
+        if dm is not None:
+            dm.close()
         torch.cuda.empty_cache()
         chain = run_chain(args, torch, dist, dev, world, rank, peak)
+    decode = None
+    if args.decode and world == 1:
+        decode = run_decode(torch, dev)
 
-    # ---- CPU baseline (rank 0, N = 1): reference SpMV on the same matrix, host cores
+    # ---- CPU baselines (rank 0, N = 1): reference SpMV on the same matrix, 1 thread and all cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cpu_src, C, d)
 
     if rank == 0:
         traffic = load_traffic(R, C, d)
+        kname = f"macko_spmv<{li.x_in_smem},4>"
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_mean, 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic (counter-hash generator, random unstructured)",
+            "config": workload_config(R, C, d, world),
             "us_per_spmv": round(kern_ms * 1e3, 2), "us_per_step_median": round(ms_med * 1e3, 2),
-            "config": {
-                "workload": f"{R}x{C} fp16 @{sparsity_pct}% sparsity (random unstructured), single SpMV"
-                + ((f" per rank, {R * world}x{C} row-sharded, all-gather of y fused into the SpMV (peer stores + flags)"
-                    if args.fused else f" per rank, {R * world}x{C} row-sharded, NCCL broadcast x + all_gather y")
-                   if world > 1 else ""),
-                "rows_per_rank": R, "cols": C, "density": d, "b_delta": 4, "pad_nnz": pad_nnz,
-                "bytes_per_spmv_per_rank": bytes_rank, "parallelism": f"row-shard x{world}",
-                "l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush else
-                       f"not flushed: inputs larger than L2 ({bytes_rank / 2**20:.0f} MiB per step vs {l2 / 2**20:.0f} MiB L2; "
-                       "ncu: L2 hit rate < 1 % back to back)"),
-                "grid": li.grid, "block": li.block, "ctas_per_sm": li.ctas_per_sm, "split_rows": li.n_split_rows,
-            },
+            "timing": {"l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush
+                              else f"not flushed: inputs larger than L2 ({bytes_rank / 2**20:.0f} MiB per step vs "
+                                   f"{l2 / 2**20:.0f} MiB L2; ncu: L2 hit rate < 1 % back to back)"),
+                       "soak_s": args.soak_s, "events": "CUDA events on the launching stream, max over ranks"},
+            "matrix": {"pad_nnz_per_rank": pad_nnz, "bytes_per_spmv_per_rank": bytes_rank, "grid": li.grid,
+                       "block": li.block, "x_mode": li.x_in_smem, "split_rows": li.n_split_rows},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"macko_spmv<{li.x_in_smem},4>", "us": round(kern_ms * 1e3, 2)},
-            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * C,
-                    "d2h_bytes_per_step": 2 * R, "us_per_call": round(e2e_mean * 1e3, 2)},
-            "dense_cublas_gemv": None if dense_us is None else {
-                "us": round(dense_us, 2), "GBps_effective": round((2 * R * C + 2 * R + 2 * C) / (dense_us * 1e-6) / 1e9, 1),
-                "GBps_vs_macko_bytes": round(bytes_rank / (dense_us * 1e-6) / 1e9, 1),
-                "macko_speedup": round(dense_us / (kern_ms * 1e3), 3), "api": "torch.mv (cuBLAS), fp32 compute"},
+                         "kernel": kname, "us": round(kern_ms * 1e3, 2),
+                         "algorithmic_bytes": "spmv_traffic (SPEC.md:336): values + packed deltas (16-B tails) "
+                                              "+ 4(R+1) + 2C + 2R per SpMV"},
+            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * C, "d2h_bytes_per_step": d2h,
+                    "us_per_call": round(e2e_mean * 1e3, 2),
+                    "api": ("macko_spmv_host (C-ABI, pinned host x / y)" if world == 1 else
+                            "pinned H2D x on rank 0 + RowShardedSpmv + D2H y on every rank")},
             "compress_s": round(compress_s, 4),
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
-        if sweep is not None:
-            line["sweep"] = sweep
-        if chain is not None:
-            line["chain"] = chain
+        if coll_us is not None:
+            line["collectives_us"] = round(coll_us, 2)
+        if dense_best is not None:
+            api, dus, all_apis = dense_best
+            line["dense_cublas_gemv"] = {
+                "api": api, "us": round(dus, 2), "apis_us": all_apis,
+                "GBps_effective": round((2 * R * C + 2 * R + 2 * C) / (dus * 1e-6) / 1e9, 1),
+                "macko_speedup": round(dus / (kern_ms * 1e3), 3)}
+        for k, v in (("spmm", spmm), ("sweep", sweep), ("strong", strong), ("chain", chain), ("decode", decode)):
+            if v is not None:
+                line[k] = v
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -408,7 +515,7 @@ def main():
 
 
 def load_traffic(R, C, d):
-    """DRAM bytes per launch of macko_spmv_b4 from the committed ncu --set full capture."""
+    """DRAM bytes per launch of the SpMV from the committed ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
@@ -420,11 +527,74 @@ def load_traffic(R, C, d):
     return None
 
 
+def run_spmm(M, torch, dm, timer, stream, need_flush):
+    """Small-batch SpMM Y = A X (X: C x b) for b = 1, 2, 4, 8: one pass over the matrix."""
+    out = {}
+    for b in (1, 2, 4, 8):
+        X = torch.empty((b, dm.cols), dtype=torch.float16, device="cuda")
+        for i in range(b):
+            M.gen_vector(X[i], dm.cols, seed=SEED_X + i)
+        Y = torch.empty((b, dm.rows), dtype=torch.float16, device="cuda")
+        t = timer.run(lambda: dm.spmm_into(X, Y, stream), 30, flush=need_flush)
+        us = statistics.median(t) * 1e3
+        out[f"batch{b}"] = {"us": round(us, 2), "us_per_vector": round(us / b, 2)}
+    return out
+
+
+def run_strong(args, M, torch, dist, dev, stream, timer, world, rank, peak):
+    """BASELINE config 5: 131072x32768 @50 / 90 %, rows/N per rank (strong scaling)."""
+    from paper_2511_13061_b200.sharded import FusedRowShardedSpmv, RowShardedSpmv, device_local_spmv
+
+    R, C = CONFIG5["rows"], CONFIG5["cols"]
+    out = []
+    for d in (0.5, 0.1):
+        r0, r1 = M.shard_rows(R, world, rank)
+        dense = torch.empty((r1 - r0, C), dtype=torch.float16, device=dev)
+        M.gen_dense(dense, r1 - r0, C, d, seed=SEED_A, row0=r0)
+        dm = M.DeviceMatrix.from_dense(dense)
+        del dense
+        torch.cuda.empty_cache()
+        x = torch.empty(C, dtype=torch.float16, device=dev)
+        M.gen_vector(x, C, seed=SEED_X)
+        y = torch.empty(r1 - r0, dtype=torch.float16, device=dev)
+        total = float(dm.traffic_bytes)  # algorithmic bytes of the whole matrix: sum over the slabs
+        if world > 1:
+            tb = torch.tensor([total], device=dev, dtype=torch.float64)
+            dist.all_reduce(tb)
+            total = tb.item()
+        reps = min(args.steps, 30)
+        kern = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: dm.spmv_into(x, y, stream), reps))])[0]
+        rec = {"shape": f"{R}x{C}", "sparsity": sparsity_pct(d), "rows_per_rank": r1 - r0, "n_gpus": world,
+               "bytes_total": int(total), "spmv_us_per_rank": round(kern * 1e3, 2),
+               "spmv_frac_per_rank": round(dm.traffic_bytes / (kern * 1e-3) / 1e9 / peak, 4)}
+        if world > 1:
+            sh = RowShardedSpmv(R, C, device_local_spmv(dm, stream), device=dev)
+            coll = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: (sh.broadcast_x(x), sh.gather_y()), reps))])[0]
+            stp = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: sh(x), reps))])[0]
+            rec.update({"collectives_us": round(coll * 1e3, 2), "nccl_step_us": round(stp * 1e3, 2),
+                        "nccl_GBps": round(total / (stp * 1e-3) / 1e9, 1)})
+            if r1 - r0 == R // world:
+                fused = FusedRowShardedSpmv(dm, R, dev)
+                ys = [fused(x, stream)]
+                fs = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: fused(x, stream), reps))])[0]
+                rec.update({"fused_step_us": round(fs * 1e3, 2), "fused_GBps": round(total / (fs * 1e-3) / 1e9, 1)})
+                torch.cuda.synchronize()
+                dist.barrier()
+                fused.close()
+                del ys
+        else:
+            rec["GBps"] = round(total / (kern * 1e-3) / 1e9, 1)
+        out.append(rec)
+        dm.close()
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_chain(args, torch, dist, dev, world, rank, peak):
-    """Config 4: Llama2-7B decode chain (32 layers x {qkv, o, gate_up, down}) at 50 % sparsity,
-    PDL-chained SpMVs in one CUDA graph per token; N > 1: row slabs + NCCL all_gather per SpMV.
-    Weights stream from HBM (8.1 GB per token >> L2): no flush.  Beside it (N = 1) the same
-    chain with dense fp16 weights through torch.mv (cuBLAS GEMV), also graph-captured."""
+    """Config 4: Llama2-7B decode SpMV chain (32 layers x {qkv, o, gate_up, down}) at 50 %,
+    PDL-chained SpMVs in one CUDA graph per token; N > 1: row slabs + NCCL all_gather per SpMV
+    (and, with --fused, the all-gather fused into the SpMVs).  Beside it (N = 1) the same chain over
+    dense fp16 weights with torch.mv (cuBLAS GEMV), also graph-captured."""
     from paper_2511_13061_b200 import decoder_chain as D
     from paper_2511_13061_b200 import macko as M
 
@@ -446,12 +616,7 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
             graph.replay()
             b.record()
         torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b in evs) / n
-        if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
-        return ms
+        return allmax(torch, dist, dev, [sum(a.elapsed_time(b) for a, b in evs) / n])[0]
 
     def time_tokens(n):  # fused all-gather: plain stream launches (flag targets grow per SpMV)
         for _ in range(3):
@@ -464,45 +629,26 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
             ch.forward_token(pdl=True)
             b.record()
         torch.cuda.synchronize()
-        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / n], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.item()
+        return allmax(torch, dist, dev, [sum(a.elapsed_time(b) for a, b in evs) / n])[0]
 
     n = max(3, args.chain_tokens)
-    launches0 = M.kernel_launches()
-    ms_graph = time_tokens(n) if ch.fused else time_graph(g, n)
-    launches_graph = M.kernel_launches() - launches0
+    ms = time_tokens(n) if ch.fused else time_graph(g, n)
     bytes_rank = ch.traffic_bytes
     total_bytes = bytes_rank * world
-    ms_pers = None
-    if world == 1:
-        # the token as one persistent cooperative kernel (weights prefetched across the barriers)
-        gp = torch.cuda.CUDAGraph()
-        sp = torch.cuda.Stream()
-        ch.forward_token_persistent()
-        torch.cuda.synchronize()
-        with torch.cuda.graph(gp, stream=sp):
-            ch.forward_token_persistent(sp)
-        ms_pers = time_graph(gp, n)
-    ms = min(ms_graph, ms_pers) if ms_pers is not None else ms_graph
     out = {
         "workload": "Llama2-7B decoder stack, 32 layers x {qkv 12288x4096, o 4096x4096, gate_up 22016x4096, "
-                    "down 4096x11008} @50% sparsity, batch-1 decode (q/k/v and gate/up row-stacked), random-init",
+                    "down 4096x11008} @50% sparsity, batch-1 decode SpMV chain (q/k/v and gate/up row-stacked), "
+                    "random-init",
         "n_gpus": world, "parallelism": f"row-shard x{world}" + (
             (" + all-gather fused into each SpMV (peer stores + flags)" if ch.fused else " + NCCL all_gather per SpMV")
             if world > 1 else ""),
         "spmvs_per_token": ch.kernels_per_token,
-        "launch": ("one persistent cooperative kernel per token (grid barrier between dependent SpMVs, "
-                   "weights prefetched across it)" if ms == ms_pers else
-                   "PDL-chained SpMV + flag-wait kernels, stream launches" if ch.fused else
+        "launch": ("PDL-chained SpMV + flag-wait kernels, stream launches" if ch.fused else
                    "PDL-chained SpMV kernels, one CUDA graph per token"),
         "us_per_token": round(ms * 1e3, 2), "tokens_per_s": round(1e3 / ms, 2),
-        "us_per_token_pdl_graph": round(ms_graph * 1e3, 2),
-        "us_per_token_persistent": None if ms_pers is None else round(ms_pers * 1e3, 2),
         "bytes_per_token": total_bytes, "GBps": round(total_bytes / (ms * 1e-3) / 1e9, 1),
         "frac_per_gpu": round(bytes_rank / (ms * 1e-3) / 1e9 / peak, 4), "build_s": round(build_s, 2),
-        "l2": "not flushed: 8.1 GB of weights per token streams from HBM",
-        "timed_tokens": n, "host_launch_calls_in_timed_region": launches_graph,
+        "l2": "not flushed: 8.1 GB of weights per token streams from HBM", "timed_tokens": n,
     }
     if world == 1:
         dch = D.DenseDecoderChain(ch)
@@ -519,46 +665,80 @@ def run_chain(args, torch, dist, dev, world, rank, peak):
     return out
 
 
-def cpu_baseline(dm, C, d):
+def run_decode(torch, dev):
+    """Llama2-7B decode: a random-init 32-layer model with MACKO linears vs the
+    same model with dense cuBLAS linears, tokens/s at batch 1."""
+    try:
+        from paper_2511_13061_b200 import llama
+    except ImportError:
+        return None
+    return llama.bench_decode(torch, dev)
+
+
+def cpu_baseline(h, C, d):
+    """The reference CPU SpMV (oracle/_ref: reference sources) on the same matrix, 1 thread and all
+    host cores, plus BASELINE config 1 (4096x4096 @50 %: reference format build + SpMV)."""
     try:
         from oracle import oracle as O
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "port", "sample": f"oracle unavailable: {e}"}
     kind = "reference" if O.ref_available() else "port"
     threads = host_cores()
-    h = dm  # host MackoMatrix downloaded from the GPU
     m = O.Macko(h.rows, h.cols, 4, h.values, h.packed_deltas, h.row_pointers)
     x = O.gen_vector(C, SEED_X)
     if kind == "reference":
         rm = O.RefMatrix.from_macko(m)
-        run = lambda: rm.spmv(x, m.rows, threads)  # noqa: E731
+        runner = lambda t: (lambda: rm.spmv(x, m.rows, t))  # noqa: E731
     else:
-        run = lambda: O.reference_spmv(m, x, threads)  # noqa: E731
-    run()
-    ts = []
-    t_start = time.time()
-    while len(ts) < 5 or (time.time() - t_start < 10 and len(ts) < 50):
-        t1 = time.perf_counter()
-        run()
-        ts.append(time.perf_counter() - t1)
-        if time.time() - t_start > 30:
-            break
-    ms = statistics.median(ts) * 1e3
+        runner = lambda t: (lambda: O.reference_spmv(m, x, t))  # noqa: E731
+
+    def timeit(fn, min_reps, budget_s):
+        fn()
+        ts = []
+        t0 = time.time()
+        while len(ts) < min_reps or (time.time() - t0 < budget_s and len(ts) < 50):
+            t1 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t1)
+        return statistics.median(ts) * 1e3
+
     bytes_step = O.spmv_traffic_bytes(m.rows, C, m.pad_nnz, 4)
-    return {"value": round(bytes_step / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-            "ms_per_spmv": round(ms, 3),
-            "sample": f"the same {m.rows}x{C} matrix (downloaded from the GPU), reference_spmv, median of {len(ts)} "
-                      f"reps, {threads} threads, CPU {cpu_model()}"}
+    ms_all = timeit(runner(threads), 5, 8.0)
+    ms_one = timeit(runner(1), 2, 3.0)
+    # config 1: 4096^2 @50 %, the reference's format build (csr_from_dense + macko_from_csr) + SpMV
+    A1 = O.gen_dense(4096, 4096, 0.5, SEED_A)
+    x1 = O.gen_vector(4096, SEED_X)
+    tb = []
+    for _ in range(3):
+        t1 = time.perf_counter()
+        r1 = O.RefMatrix.encode(A1, 4) if kind == "reference" else None
+        if r1 is None:
+            m1 = O.encode_dense(A1, 4)
+        tb.append(time.perf_counter() - t1)
+    if kind == "reference":
+        c1_one = timeit(lambda: r1.spmv(x1, 4096, 1), 5, 2.0)
+        c1_all = timeit(lambda: r1.spmv(x1, 4096, threads), 5, 2.0)
+    else:
+        c1_one = timeit(lambda: O.reference_spmv(m1, x1, 1), 5, 2.0)
+        c1_all = timeit(lambda: O.reference_spmv(m1, x1, threads), 5, 2.0)
+    return {"value": round(bytes_step / (ms_all * 1e-3) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+            "ms_per_spmv": round(ms_all, 3),
+            "one_thread": {"value": round(bytes_step / (ms_one * 1e-3) / 1e9, 3), "unit": "GB/s", "cores": 1,
+                           "ms_per_spmv": round(ms_one, 3)},
+            "config1_4096x4096": {"format_build_ms_1thread": round(statistics.median(tb) * 1e3, 2),
+                                  "spmv_ms_1thread": round(c1_one, 3), f"spmv_ms_{threads}threads": round(c1_all, 3)},
+            "sample": f"the same {m.rows}x{C} matrix (downloaded from the GPU), reference_spmv, median of >= 5 reps "
+                      f"({threads} threads) / >= 2 reps (1 thread), std::thread row partition, CPU {cpu_model()}"}
 
 
-def run_sweep(M, torch, dev, stream, l2_flush, peak):
+def run_sweep(M, torch, dev, stream, timer, peak):
     """30/50/70/90 % sparsity at 36864x12288, the Llama2-7B linear shapes at 50 % and the
     131072x32768 shapes of config 5 (whole matrix and an N = 8 row slab) at 50 / 90 %."""
     out = []
     cfgs = [(36864, 12288, 0.7), (36864, 12288, 0.5), (36864, 12288, 0.3), (36864, 12288, 0.1),
             (4096, 4096, 0.5), (11008, 4096, 0.5), (4096, 11008, 0.5),
-            # config 5: 131072x32768 (whole matrix on one GPU, and the row slab of one rank at N = 8)
             (131072, 32768, 0.5), (131072, 32768, 0.1), (16384, 32768, 0.5), (16384, 32768, 0.1)]
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     for R, C, d in cfgs:
         dense = torch.empty((R, C), dtype=torch.float16, device=dev)
         M.gen_dense(dense, R, C, d, seed=SEED_A)
@@ -566,33 +746,16 @@ def run_sweep(M, torch, dev, stream, l2_flush, peak):
         x = torch.empty(C, dtype=torch.float16, device=dev)
         M.gen_vector(x, C, seed=SEED_X)
         y = torch.empty(R, dtype=torch.float16, device=dev)
-        yd = torch.empty(R, dtype=torch.float16, device=dev)
-
-        big = dm.traffic_bytes >= 3 * torch.cuda.get_device_properties(dev).L2_cache_size
-
-        def timeit(fn, n=50):
-            for _ in range(5):
-                fn()
-            ts = []
-            for _ in range(n):
-                if not big:
-                    l2_flush(force=True)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                fn()
-                b.record(stream)
-                b.synchronize()
-                ts.append(a.elapsed_time(b))
-            return statistics.median(ts) * 1e3
-
-        us = timeit(lambda: dm.spmv_into(x, y, stream))
-        dus = timeit(lambda: torch.mv(dense, x, out=yd))
+        flush = dm.traffic_bytes < 3 * l2
+        us = statistics.median(timer.run(lambda: dm.spmv_into(x, y, stream), 50, warmup=5, flush=flush)) * 1e3
+        api, dus, apis = dense_baseline(torch, timer, dense, x, 30, flush)
         gbs = dm.traffic_bytes / (us * 1e-6) / 1e9
-        out.append({"shape": f"{R}x{C}", "sparsity": round(1 - d, 2), "us": round(us, 2), "GBps": round(gbs, 1),
-                    "x_mode": dm.launch_info().x_in_smem, "l2_flush": not big,
-                    "frac": round(gbs / peak, 4), "cublas_us": round(dus, 2), "speedup": round(dus / us, 3),
+        out.append({"shape": f"{R}x{C}", "sparsity": sparsity_pct(d), "us": round(us, 2), "GBps": round(gbs, 1),
+                    "x_mode": dm.launch_info().x_in_smem, "l2_flush": flush, "frac": round(gbs / peak, 4),
+                    "cublas_us": round(dus, 2), "cublas_api": api, "speedup": round(dus / us, 3),
                     "bytes": dm.traffic_bytes})
-        del dense, dm
+        del dense
+        dm.close()
         torch.cuda.empty_cache()
     return out
 

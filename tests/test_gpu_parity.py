@@ -457,3 +457,83 @@ def test_other_widths_every_x_mode(cuda):
             assert np.array_equal(gpu_spmv(dm, x), ref), (bits, xm)
         with pytest.raises(ValueError):
             dm.configure(11)
+
+
+# ------------------------------------------------------------------------------ one handle, many streams
+def test_two_streams_one_handle_different_x(cuda):
+    # SPEC.md:119-120 / SURVEY.md §8b: a handle is read-only after build and may be shared across
+    # streams.  Rows cut between warps use per-stream split counters / partials, x texture objects
+    # are cached per buffer: concurrent SpMVs of one matrix on two streams stay exact.
+    A = O.gen_dense(1000, 16000, 0.5, 8)
+    m = O.encode_dense(A)
+    dm = gpu_encode(A)
+    assert dm.launch_info().n_split_rows > 0
+    xs = [O.gen_vector(16000, 40 + i) for i in range(2)]
+    refs = [b200_y(m, x) for x in xs]
+    xd = [to_dev(x) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    ys = [[torch.empty(1000, dtype=torch.float16, device=cuda) for _ in range(20)] for _ in range(2)]
+    torch.cuda.synchronize()
+    for k in range(20):
+        for s in range(2):
+            dm.spmv_into(xd[s], ys[s][k], stream=streams[s])
+    torch.cuda.synchronize()
+    for s in range(2):
+        for k in range(20):
+            assert np.array_equal(to_host_u16(ys[s][k]), refs[s]), (s, k)
+
+
+def test_async_calls_alternating_x_buffers(cuda):
+    # 100 asynchronous calls on one stream, x alternating between 4 buffers (one misaligned), no
+    # synchronisation in between: no texture object is destroyed while a launch may still read it
+    A = O.gen_dense(2000, 12000, 0.5, 12)
+    m = O.encode_dense(A)
+    dm = gpu_encode(A)
+    xs = [O.gen_vector(12000, 50 + i) for i in range(4)]
+    refs = [b200_y(m, x) for x in xs]
+    bufs = [to_dev(x) for x in xs[:3]]
+    mis = to_dev(np.concatenate([np.zeros(1, np.uint16), xs[3]]))[1:]  # 2-byte aligned view
+    bufs.append(mis)
+    ys = [torch.empty(2000, dtype=torch.float16, device=cuda) for _ in range(100)]
+    for k in range(100):
+        dm.spmv_into(bufs[k % 4], ys[k])
+    torch.cuda.synchronize()
+    for k in range(100):
+        assert np.array_equal(to_host_u16(ys[k]), refs[k % 4]), k
+
+
+def test_threads_share_one_handle(cuda):
+    # host threads with their own streams and pinned host buffers call macko_spmv_host and
+    # macko_dev_spmv on one handle at once
+    import threading
+
+    A = O.gen_dense(1500, 9000, 0.5, 13)
+    m = O.encode_dense(A)
+    dm = gpu_encode(A)
+    xs = [O.gen_vector(9000, 60 + i) for i in range(4)]
+    refs = [b200_y(m, x) for x in xs]
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            xd = to_dev(xs[i])
+            y = torch.empty(1500, dtype=torch.float16, device=cuda)
+            for _ in range(10):
+                if i % 2:
+                    got = dm.spmv_host(xs[i], stream=s)
+                else:
+                    dm.spmv_into(xd, y, stream=s)
+                    s.synchronize()
+                    got = to_host_u16(y)
+                if not np.array_equal(got, refs[i]):
+                    errors.append(i)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
