@@ -310,62 +310,64 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (clock64() - t0 > 4000000000LL) __trap();
 }
 
+// Chunk c of the warp's stream (elements [e0 + c kChunk, e0 + (c+1) kChunk)) lives in slot
+// c & (ring - 1) and completes phase (c / ring) & 1 of that slot's mbarrier.  The walk position S
+// only grows, by at most one step pair per pair, so at most one chunk is released per pair.
+constexpr uint32_t kNever = 0xFFFFFFFFu;
+
 struct Ring {
     uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
-    uint32_t ebase, emask;        // element e lives at ring offset (e - ebase) & emask
-    uint32_t iss;                 // first element of the next chunk to issue
-    uint32_t stream_end;          // end (exclusive, chunk aligned) of the warp's chunk stream
-    uint32_t ready_end;           // elements below this have landed
-    uint32_t rel_mark;            // once S >= rel_mark, the oldest resident chunk's slot is refilled
-    uint32_t wslot, wphase;
+    uint32_t e0;                  // first element of the warp's chunk stream (chunk aligned)
+    uint32_t emask;               // ring elements - 1 (power of two)
+    uint32_t lane_rel;            // 8 lane - e0: the lane's element of a step at S sits at (S + lane_rel) & emask
+    uint32_t n_chunks;            // chunks in the stream
+    uint32_t released;            // chunks consumed and refilled (or nothing left to refill)
+    uint32_t landed;              // chunks waited for
+    uint32_t rel_at, wait_at;     // S thresholds of the next release / the next wait (kNever: none)
+    uint32_t rshift;              // log2(ring)
+    uint64_t policy;              // L2 evict_first (the matrix streams once per SpMV)
 };
 
-// Copy the chunk starting at element g.iss into its slot (one elected lane; full-size, never
-// clamped).  Called by the whole warp with warp-uniform operands: elect.sync inside the asm keeps
-// the copies to one lane without a divergent branch around them.
+__device__ __forceinline__ uint32_t ring_ev(const Ring& g) { return min(g.rel_at, g.wait_at); }
+
+// Refill slot (released & (ring-1)) with chunk released + ring (one elected lane; full-size copies,
+// never clamped: the payload buffers carry a zeroed chunk of slack).  Called by the whole warp with
+// warp-uniform operands: elect.sync inside the asm keeps the copies to one lane without a
+// divergent branch around them.
 template <int kBits>
-__device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, int lane) {
-    const uint32_t e0 = g.iss;
-    const uint32_t rel = (e0 - g.ebase) & g.emask;
-    const uint32_t bar = g.bar0 + 8u * (rel / kChunk);
-    // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it.  The matrix is
-    // streamed once per SpMV: L2 evict_first keeps x, the plan records and the code resident.
+__device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, uint32_t ring) {
+    const uint32_t slot = g.released & (ring - 1u);
+    const uint32_t e = g.e0 + (g.released + ring) * kChunk;
+    const uint32_t bar = g.bar0 + 8u * slot;
+    // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
     asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .b64 pol;\n\t"
+        "{\n\t.reg .pred p;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
-        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-        "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %5;\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %6, [%4], pol;\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %7, [%4], pol;\n\t}" ::"r"(
-            g.vbase + 2u * rel),
-        "l"(a.values + e0), "r"(g.dbase + (rel / 8u) * kBits), "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(bar),
-        "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
+        "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %6;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %7, [%4], %5;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %8, [%4], %5;\n\t}" ::"r"(
+            g.vbase + slot * kChunkVBytes),
+        "l"(a.values + e), "r"(g.dbase + slot * dbytes<kBits>()), "l"(a.deltas + (size_t)(e / 8u) * kBits), "r"(bar),
+        "l"(g.policy), "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
         : "memory");
 }
 
-// The walk is at S: every chunk wholly below S was consumed by all lanes (their LDS results fed
-// earlier FHFMAs; __syncwarp orders them before lane 0's copy), so its slot takes a new chunk.
+// The walk reached S (slow path, S >= ring_ev): release the chunk the walk has left (every lane's
+// LDS of it fed earlier FHFMAs; __syncwarp orders them before the refill) and wait until the
+// chunks holding [S, S + span) have landed.
 template <int kBits>
-__device__ __forceinline__ void ring_refill(Ring& g, const SpmvArgs& a, uint32_t S, int lane) {
-    __syncwarp();
-    do {
-        if (g.iss < g.stream_end) {
-            ring_issue<kBits>(g, a, lane);
-            g.iss += kChunk;
-        }
-        g.rel_mark += kChunk;
-    } while (S >= g.rel_mark);
-}
-
-// Make elements below Send resident (chunk granularity).
-__device__ __forceinline__ void ring_wait(Ring& g, uint32_t Send, uint32_t nslots) {
-    const uint32_t need = min(Send, g.stream_end);
-    while (g.ready_end < need) {
-        mbar_wait(g.bar0 + 8u * g.wslot, g.wphase);
-        g.wslot = (g.wslot + 1u) & (nslots - 1u);
-        g.wphase ^= g.wslot == 0 ? 1u : 0u;
-        g.ready_end += kChunk;
+__device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_t S, uint32_t span) {
+    const uint32_t ring = a.ring;
+    if (S >= g.rel_at) {
+        __syncwarp();
+        ring_issue<kBits>(g, a, ring);
+        ++g.released;
+        g.rel_at = g.released + ring < g.n_chunks ? g.e0 + (g.released + 1u) * kChunk : kNever;
     }
+    const uint32_t need = min(g.n_chunks, (S + span - 1u - g.e0) / kChunk + 1u);
+    for (; g.landed < need; ++g.landed)
+        mbar_wait(g.bar0 + 8u * (g.landed & (ring - 1u)), (g.landed >> g.rshift) & 1u);
+    g.wait_at = g.landed < g.n_chunks ? g.e0 + g.landed * kChunk - (2u * kStepElts - 1u) : kNever;
 }
 
 struct Slot {
@@ -374,12 +376,12 @@ struct Slot {
 };
 
 template <int kBits>
-__device__ __forceinline__ Slot lds_slot(const Ring& g, uint32_t rel) {
+__device__ __forceinline__ Slot lds_slot(uint32_t vbase, uint32_t dbase, uint32_t rel) {
     Slot sl;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
-                 : "r"(g.vbase + 2u * rel));
-    const uint32_t da = g.dbase + (rel / 8u) * kBits;
+                 : "r"(vbase + 2u * rel));
+    const uint32_t da = dbase + (rel / 8u) * kBits;
     sl.d2 = 0;
     if constexpr (kBits == 8) {
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(sl.d), "=r"(sl.d2) : "r"(da));
@@ -432,48 +434,44 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
     g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
     g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * dbytes<kBits>();
     g.bar0 = bar0;
-    const uint32_t e0 = E0 & ~(kChunk - 1u);
+    g.e0 = E0 & ~(kChunk - 1u);
     g.emask = a.ring * kChunk - 1u;
-    g.stream_end = E1 > E0 ? ((E1 - 1u) & ~(kChunk - 1u)) + kChunk : e0;
-    g.ready_end = e0;
-    g.rel_mark = e0 + kChunk;
-    const uint32_t limit = min(e0 + a.ring * kChunk, g.stream_end);
-    {
-        g.ebase = e0;
-        g.wslot = 0;
-        g.wphase = 0;
-        if (lane == 0) {
-            // The barriers are used by this warp and its own bulk copies only (no cluster): the
-            // async-proxy fence orders their initialisation before the copies' complete_tx.
-            for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            MK_TRACE(5);
-            // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so
-            // one copy per array fills them all and completes on barrier 0; the other barriers
-            // complete their first phase with a plain arrive (the consumer passes barrier 0 first).
-            const uint32_t n = (limit - e0) / kChunk;
-            if (n) {
-                asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
-                             "r"(n * (kChunkVBytes + dbytes<kBits>()))
-                             : "memory");
-                asm volatile(
-                    "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}" ::"r"(
-                        g.vbase),
-                    "l"(a.values + e0), "r"(n * kChunkVBytes), "r"(g.bar0)
-                    : "memory");
-                asm volatile(
-                    "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}" ::"r"(
-                        g.dbase),
-                    "l"(a.deltas + (size_t)(e0 / 8u) * kBits), "r"(n * dbytes<kBits>()), "r"(g.bar0)
-                    : "memory");
-                for (uint32_t i = 1; i < n; ++i)
-                    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
-            }
-            MK_TRACE(7);
+    g.lane_rel = 8u * (uint32_t)lane - g.e0;
+    g.n_chunks = E1 > E0 ? ((E1 - 1u) - g.e0) / kChunk + 1u : 0u;
+    g.rshift = 31u - __clz(a.ring);
+    g.released = 0;
+    g.landed = 0;
+    g.rel_at = a.ring < g.n_chunks ? g.e0 + kChunk : kNever;
+    g.wait_at = g.n_chunks ? 0u : kNever;  // the first pair waits for the first fill
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(g.policy));
+    const uint32_t n = min(a.ring, g.n_chunks);
+    if (lane == 0) {
+        // The barriers are used by this warp and its own bulk copies only (no cluster): the
+        // async-proxy fence orders their initialisation before the copies' complete_tx.
+        for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        MK_TRACE(5);
+        // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so one
+        // copy per array fills them all and completes on barrier 0; the other barriers complete
+        // their first phase with a plain arrive (the consumer passes barrier 0 first).
+        if (n) {
+            asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
+                         "r"(n * (kChunkVBytes + dbytes<kBits>()))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                    g.vbase),
+                "l"(a.values + g.e0), "r"(n * kChunkVBytes), "r"(g.bar0), "l"(g.policy)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                    g.dbase),
+                "l"(a.deltas + (size_t)(g.e0 / 8u) * kBits), "r"(n * dbytes<kBits>()), "r"(g.bar0), "l"(g.policy)
+                : "memory");
+            for (uint32_t i = 1; i < n; ++i)
+                asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
         }
-        g.iss = limit;
+        MK_TRACE(7);
     }
     __syncwarp();
 }
@@ -518,14 +516,20 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
 template <int kXMode, int kBits>
-__device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr, Ring& g,
+__device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
                                          RowState& rs) {
     if (rs.T == 0) {
         if (lane == 0) put_y(a, rs.r, 0);
         if (!next_piece(rs, a, w, lane)) return;
     }
-    // ring event: refill once the walk passes rel_mark, wait once a pair reaches ready_end
-    uint32_t ev = 0;
+    // loop invariants pinned in registers (not re-derived from the CTA's shared window per pair)
+    uint32_t xs_addr, vbase, dbase, lane_rel, emask;
+    asm volatile("mov.b32 %0, %1;" : "=r"(xs_addr) : "r"(xs_addr_in));
+    asm volatile("mov.b32 %0, %1;" : "=r"(vbase) : "r"(g.vbase));
+    asm volatile("mov.b32 %0, %1;" : "=r"(dbase) : "r"(g.dbase));
+    asm volatile("mov.b32 %0, %1;" : "=r"(lane_rel) : "r"(g.lane_rel));
+    asm volatile("mov.b32 %0, %1;" : "=r"(emask) : "r"(g.emask));
+    uint32_t ev = ring_ev(g);
 
     // One step pair (steps t, t+1 of the current row).  Masked pairs: the row's first pair
     // (ROMA) and its last (partial / phantom second step).
@@ -533,14 +537,13 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         constexpr bool kMasked = decltype(masked)::value;
         const uint32_t S = rs.al + t * kStepElts;
         if (S >= ev) {
-            const uint32_t Send = S + ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts;
-            if (S >= g.rel_mark) ring_refill<kBits>(g, a, S, lane);
-            if (Send > g.ready_end) ring_wait(g, Send, a.ring);
-            ev = min(g.rel_mark, g.ready_end > 2u * kStepElts - 1u ? g.ready_end - (2u * kStepElts - 1u) : 0u);
+            ring_advance<kBits>(g, a, S, ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts);
+            ev = ring_ev(g);
         }
-        const uint32_t relA = (S + 8u * lane - g.ebase) & g.emask;
-        Slot A = lds_slot<kBits>(g, relA);
-        Slot B = lds_slot<kBits>(g, (relA + kStepElts) & g.emask);
+        const uint32_t relA = (S + lane_rel) & emask;
+        const uint32_t relB = (relA + kStepElts) & emask;
+        Slot A = lds_slot<kBits>(vbase, dbase, relA);
+        Slot B = lds_slot<kBits>(vbase, dbase, relB);
         uint32_t vmA = 0xFFu, vmB = 0xFFu;
         if constexpr (kMasked) {
             const uint32_t eb = S + 8u * lane;
@@ -577,14 +580,19 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     };
 
     for (;;) {
-        // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T)
+        // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T).  Pair t is masked
+        // iff it is the row's first (t = 0) or last (t + 2 >= T); interior pairs run unmasked.
         for (uint32_t t = rs.t; t < rs.tend;) {
             const uint32_t ue = t < rs.last_b ? t + kUnitSteps : rs.tend;
-            for (; t < ue; t += 2u) {
-                if (t == 0u || t + 2u >= rs.T)
-                    pair(std::true_type{}, t);
-                else
-                    pair(std::false_type{}, t);
+            if (t == 0u) {
+                pair(std::true_type{}, 0u);
+                t = 2u;
+            }
+            const uint32_t lim = min(ue, rs.T - min(rs.T, 2u));
+            for (; t < lim; t += 2u) pair(std::false_type{}, t);
+            if (t < ue) {
+                pair(std::true_type{}, t);
+                t += 2u;
             }
             const float red = warp_tree_sum(rs.acc);
             rs.acc = 0.0f;

@@ -65,8 +65,11 @@ struct SpmvArgs {
 // kSpmvCtasPerSm persistent CTAs of kSpmvWarpsPerCta warps per SM (32 warps per SM either way).
 // Measured: two 16-warp CTAs per SM (so the next SpMV of a PDL chain can start on half an SM) are
 // 8 % slower on 36864x12288 and no faster on the decode chain; one 32-warp CTA is the default.
+#ifndef MACKO_WARPS_PER_SM
+#define MACKO_WARPS_PER_SM 32
+#endif
 constexpr int kSpmvWarpsPerCta = MACKO_WARPS_PER_CTA;
-constexpr int kSpmvCtasPerSm = 32 / kSpmvWarpsPerCta;
+constexpr int kSpmvCtasPerSm = MACKO_WARPS_PER_SM / kSpmvWarpsPerCta;
 #ifndef MACKO_CHUNK
 #define MACKO_CHUNK 1024
 #endif
