@@ -4,11 +4,11 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2511_13061_b200
 CSRC := $(PKG)/csrc
-SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu
+SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu $(CSRC)/convert.cu
 HDRS := $(wildcard $(CSRC)/*.cuh) include/macko_cuda.h
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 
-all: lib oracle
+all: lib dropin oracle
 
 lib: $(PKG)/libmacko_cuda.so
 
@@ -37,13 +37,26 @@ $(PKG)/libmacko_cuda_trace.so: $(patsubst $(CSRC)/%.cu,build/trace/%.o,$(SRCS))
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
 .PHONY: trace
 
-# C++ drop-in test (reference headers + our header); needs /root/reference at build time.
+# libmacko.so: the reference's C++ API (namespace macko: fp16 / bitpack / convert / the SPEC
+# executors) backed by libmacko_cuda.so.  Compiled against the reference's own headers, which exist
+# only in the build container (/root/reference); elsewhere the prebuilt .so is kept.
 REF_SRC ?= /root/reference/proj/src
-cpptest: lib oracle
+dropin: lib
+	@if [ -d "$(REF_SRC)" ]; then \
+	  g++ -std=c++20 -O2 -fPIC -shared -Wall -I include -I $(REF_SRC) -I /usr/local/cuda/include \
+	    $(CSRC)/dropin/macko_dropin.cpp -o $(PKG)/libmacko.so -L $(PKG) -lmacko_cuda -Wl,-rpath,'$$ORIGIN'; \
+	else echo "dropin: $(REF_SRC) absent, keeping prebuilt $(PKG)/libmacko.so"; fi
+
+# C++ drop-in tests (reference headers + our headers); need /root/reference at build time.
+#   dropin_test     — the reference's own types / encoder feeding libmacko_cuda.so via macko_cuda.hpp
+#   dropin_ref_test — a reference caller linked against libmacko.so only (no reference code)
+cpptest: lib dropin oracle
 	@if [ -d "$(REF_SRC)" ]; then \
 	  $(NVCC) $(ARCH) -std=c++20 -O2 -I include -I $(REF_SRC) tests/cpp/dropin_test.cpp -o tests/cpp/dropin_test \
 	    -L $(PKG) -L oracle/_ref -lmacko_cuda -lmacko_ref \
-	    -Xlinker -rpath,'$$ORIGIN/../../$(PKG)' -Xlinker -rpath,'$$ORIGIN/../../oracle/_ref'; \
-	else echo "cpptest: $(REF_SRC) absent, keeping prebuilt tests/cpp/dropin_test"; fi
+	    -Xlinker -rpath,'$$ORIGIN/../../$(PKG)' -Xlinker -rpath,'$$ORIGIN/../../oracle/_ref' && \
+	  g++ -std=c++20 -O2 -mf16c -Wall -I include -I $(REF_SRC) tests/cpp/dropin_ref_test.cpp -o tests/cpp/dropin_ref_test \
+	    -L $(PKG) -lmacko -Wl,-rpath,'$$ORIGIN/../../$(PKG)'; \
+	else echo "cpptest: $(REF_SRC) absent, keeping prebuilt tests/cpp/dropin_test*"; fi
 
-.PHONY: cpptest
+.PHONY: cpptest dropin

@@ -6,8 +6,9 @@
 // member names works (values / packed_deltas / row_pointers / rows / cols / params.b_delta,
 // payloads of 2-byte fp16 bit patterns).  C-ABI status codes become exceptions with the
 // reference's taxonomy: std::invalid_argument (bitpack.cpp:14-15) and FormatError / IoError /
-// InfeasibleError (errors.hpp:9-21) — pass the reference's types as template arguments of
-// check() (defaults: the equivalents below).
+// InfeasibleError (errors.hpp:9-21) — the reference's own types whenever its errors.hpp is on the
+// include path.  The reference's free functions themselves (convert.hpp, fp16.hpp, bitpack.hpp and
+// the SPEC executors in macko/spmv.hpp) are provided by libmacko.so (csrc/dropin/).
 #pragma once
 
 #include <cstdint>
@@ -19,9 +20,20 @@
 
 #include "../macko_cuda.h"
 
+#if __has_include("errors.hpp")
+#include "errors.hpp"  // the reference's exception taxonomy (proj/src/errors.hpp:9-21)
+#endif
+
 namespace macko {
 namespace cuda {
 
+// With the reference's errors.hpp on the include path (-I proj/src) the wrapper throws the
+// reference's own exception types; otherwise equivalents with the same bases.
+#if __has_include("errors.hpp")
+using FormatError = ::macko::FormatError;
+using IoError = ::macko::IoError;
+using InfeasibleError = ::macko::InfeasibleError;
+#else
 struct FormatError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -31,6 +43,7 @@ struct IoError : std::runtime_error {
 struct InfeasibleError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+#endif
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };

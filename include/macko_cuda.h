@@ -83,6 +83,32 @@ macko_status macko_dev_upload(int device, uint64_t rows, uint64_t cols, uint32_t
 macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t rows, uint64_t cols,
                                   uint64_t ld, uint32_t b_delta, void* stream, macko_dev_matrix** out);
 
+/* GPU compressor from a canonical CSR: replaces macko_from_csr (convert.hpp:12-16)
+ * with byte-identical output.  values: nnz fp16 bits, col_idx: nnz u32 (0-based, strictly
+ * increasing per row, < cols), row_ptrs: rows+1 u32.  on_device = 0: host arrays (the reference
+ * CsrMatrix, matrix.hpp:39-48; uploaded), 1: device pointers.  Non-canonical input -> MACKO_EINVAL
+ * (std::invalid_argument).  Synchronises `stream`. */
+macko_status macko_dev_from_csr(int device, uint64_t rows, uint64_t cols, uint32_t b_delta, const uint16_t* values,
+                                const uint32_t* col_idx, const uint32_t* row_ptrs, uint64_t nnz, int on_device,
+                                void* stream, macko_dev_matrix** out);
+
+/* csr_from_dense (convert.hpp:8-10) on the device: the nonzeros (+-0 dropped) of a
+ * rows x cols fp16 matrix (leading dimension ld; on_device = 0 host memory, 1 device memory) in
+ * row-major order, written to HOST arrays.  Call with values = col_idx = NULL to get row_ptrs
+ * (rows+1) and *nnz, then again with nnz-sized values / col_idx.  Synchronous. */
+macko_status macko_csr_from_dense(int device, const uint16_t* dense, uint64_t rows, uint64_t cols, uint64_t ld,
+                                  int on_device, uint32_t* row_ptrs, uint16_t* values, uint32_t* col_idx,
+                                  uint64_t* nnz, void* stream);
+
+/* dense_from_macko (convert.hpp:18-20) on the device: rows x cols fp16, leading dimension ld
+ * (elements); on_device = 0: `dense` is host memory (decoded on the device, then copied), 1: device
+ * memory.  A decoded column >= cols -> MACKO_EFORMAT (FormatError).  Synchronous. */
+macko_status macko_dev_to_dense(const macko_dev_matrix* m, uint16_t* dense, uint64_t ld, int on_device, void* stream);
+
+/* padding_count (convert.hpp:22-23): zero-valued entries among the pad_nnz stored
+ * ones (= pad_nnz - nnz of the source).  Synchronous. */
+macko_status macko_dev_padding_count(const macko_dev_matrix* m, uint64_t* out, void* stream);
+
 macko_status macko_dev_get_info(const macko_dev_matrix* m, macko_dev_info* out);
 
 /* Device -> host copy of the three arrays in reference layout (sizes from macko_dev_info;

@@ -15,6 +15,8 @@ from .macko import (  # noqa: F401
     gen_dense,
     gen_vector,
     kernel_launches,
+    csr_from_dense,
+    macko_from_csr,
     macko_from_dense,
     mcko_info,
     read_matrix_market,

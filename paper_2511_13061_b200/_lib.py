@@ -16,7 +16,8 @@ MACKO_OK, MACKO_EINVAL, MACKO_EFORMAT, MACKO_EIO, MACKO_EINFEASIBLE, MACKO_ECUDA
 
 # Every symbol include/macko_cuda.h declares (tests check the library exports all of them).
 EXPORTS = (
-    "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_get_info",
+    "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_from_csr", "macko_csr_from_dense",
+    "macko_dev_to_dense", "macko_dev_padding_count", "macko_dev_get_info",
     "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
@@ -89,6 +90,14 @@ def load() -> C.CDLL:
     L.macko_dev_upload.argtypes = [i32, u64, u64, u32, vp, u64, vp, u64, vp, vp, C.POINTER(vp)]
     L.macko_dev_from_dense.restype = st
     L.macko_dev_from_dense.argtypes = [i32, vp, u64, u64, u64, u32, vp, C.POINTER(vp)]
+    L.macko_dev_from_csr.restype = st
+    L.macko_dev_from_csr.argtypes = [i32, u64, u64, u32, vp, vp, vp, u64, i32, vp, C.POINTER(vp)]
+    L.macko_csr_from_dense.restype = st
+    L.macko_csr_from_dense.argtypes = [i32, vp, u64, u64, u64, i32, vp, vp, vp, C.POINTER(u64), vp]
+    L.macko_dev_to_dense.restype = st
+    L.macko_dev_to_dense.argtypes = [vp, vp, u64, i32, vp]
+    L.macko_dev_padding_count.restype = st
+    L.macko_dev_padding_count.argtypes = [vp, C.POINTER(u64), vp]
     L.macko_dev_get_info.restype = st
     L.macko_dev_get_info.argtypes = [vp, C.POINTER(DevInfo)]
     L.macko_dev_download.restype = st

@@ -740,6 +740,188 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
     });
 }
 
+macko_status macko_dev_from_csr(int device, uint64_t rows, uint64_t cols, uint32_t b_delta, const uint16_t* values,
+                                const uint32_t* col_idx, const uint32_t* row_ptrs, uint64_t nnz, int on_device,
+                                void* stream, macko_dev_matrix** out) {
+    return guarded([&] {
+        if (!out || !row_ptrs || (nnz && (!values || !col_idx))) fail(MACKO_EINVAL, "null argument");
+        *out = nullptr;
+        check_bits(b_delta);
+        check_shape(rows, cols);
+        if (nnz > 0xFFFFFFFFull) fail(MACKO_EINVAL, "nnz does not fit u32 row pointers");
+        DeviceGuard g(device);
+        cudaStream_t st = (cudaStream_t)stream;
+        DevBuf<uint32_t> drp, dci;
+        DevBuf<uint16_t> dcv;
+        const uint32_t* rp = row_ptrs;
+        const uint32_t* ci = col_idx;
+        const uint16_t* cv = values;
+        if (!on_device) {  // host CsrMatrix (matrix.hpp:39-48): row pointers checked here, arrays uploaded
+            if (row_ptrs[0] != 0) fail(MACKO_EINVAL, "row_pointers[0] must be 0");
+            for (uint64_t r = 0; r < rows; ++r)
+                if (row_ptrs[r + 1] < row_ptrs[r]) fail(MACKO_EINVAL, "row_pointers not monotone");
+            if (row_ptrs[rows] != nnz) fail(MACKO_EINVAL, "row_pointers[rows] != nnz");
+            drp.alloc(rows + 1);
+            ck(cudaMemcpyAsync(drp.p, row_ptrs, (rows + 1) * 4, cudaMemcpyHostToDevice, st), "upload row_ptrs");
+            if (nnz) {
+                dci.alloc(nnz);
+                dcv.alloc(nnz);
+                ck(cudaMemcpyAsync(dci.p, col_idx, nnz * 4, cudaMemcpyHostToDevice, st), "upload columns");
+                ck(cudaMemcpyAsync(dcv.p, values, nnz * 2, cudaMemcpyHostToDevice, st), "upload values");
+            }
+            rp = drp.p;
+            ci = dci.p;
+            cv = dcv.p;
+        }
+        auto* m = new macko_dev_matrix;
+        std::unique_ptr<macko_dev_matrix> hold(m);
+        m->device = device;
+        m->sms = sm_count(device);
+        m->rows = rows;
+        m->cols = cols;
+        m->b_delta = b_delta;
+        DevBuf<uint32_t> counts, err;
+        DevBuf<unsigned long long> total;
+        counts.alloc(rows);
+        err.alloc(1);
+        total.alloc(1);
+        m->row_ptrs.alloc(rows + 1);
+        ck(cudaMemsetAsync(err.p, 0, 4, st), "memset");
+        ck(mk::launch_csr_count(rp, ci, (uint32_t)rows, (uint32_t)cols, b_delta, counts.p, err.p, m->sms, st),
+           "csr_count");
+        ck(mk::launch_scan_counts(counts.p, (uint32_t)rows, m->row_ptrs.p, total.p, st), "scan_counts");
+        g_launches.fetch_add(2);
+        struct {
+            unsigned long long total;
+            uint32_t err;
+        } h{};
+        ck(cudaMemcpyAsync(&h.total, total.p, 8, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaMemcpyAsync(&h.err, err.p, 4, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        // macko_from_csr rejects a non-canonical CSR
+        if (h.err & 1u) fail(MACKO_EINVAL, "column index out of range");
+        if (h.err & 2u) fail(MACKO_EINVAL, "columns not strictly increasing within a row");
+        if (h.err & 4u) fail(MACKO_EINVAL, "row_pointers not monotone");
+        if (h.total > 0xFFFFFFFFull) fail(MACKO_EINVAL, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
+        const uint64_t pad_nnz = h.total;
+        m->pad_nnz = pad_nnz;
+        const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
+        m->values.alloc(vb / 2 + mk::kChunk);  // + one zeroed TMA chunk of slack (see upload)
+        m->deltas.alloc(db + mk::kChunk);
+        ck(cudaMemsetAsync(m->values.p, 0, m->values.n * 2, st), "memset");
+        ck(cudaMemsetAsync(m->deltas.p, 0, m->deltas.n, st), "memset");
+        if (pad_nnz) {
+            DevBuf<uint8_t> codes;
+            codes.alloc(pad_nnz);
+            ck(mk::launch_csr_emit(rp, ci, cv, (uint32_t)rows, b_delta, m->row_ptrs.p, m->values.p, codes.p, m->sms, st),
+               "csr_emit");
+            ck(mk::launch_pack_codes(codes.p, pad_nnz, b_delta, m->deltas.p, (pad_nnz * b_delta + 7) / 8, m->sms, st),
+               "pack_codes");
+            g_launches.fetch_add(2);
+            ck(cudaStreamSynchronize(st), "sync");  // codes goes out of scope
+        }
+        m->h_row_ptrs.resize(rows + 1);
+        ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        build_plan(m, st);
+        *out = hold.release();
+    });
+}
+
+macko_status macko_csr_from_dense(int device, const uint16_t* dense, uint64_t rows, uint64_t cols, uint64_t ld,
+                                  int on_device, uint32_t* row_ptrs, uint16_t* values, uint32_t* col_idx,
+                                  uint64_t* nnz, void* stream) {
+    return guarded([&] {
+        if (!dense || !row_ptrs || !nnz) fail(MACKO_EINVAL, "null argument");
+        if (rows >= 0x7FFFFFFFull || cols >= 0x7FFFFFFFull) fail(MACKO_EINVAL, "rows/cols must be < 2^31");
+        if (ld < cols) fail(MACKO_EINVAL, "leading dimension < cols");
+        DeviceGuard g(device);
+        cudaStream_t st = (cudaStream_t)stream;
+        int sms = sm_count(device);
+        DevBuf<uint16_t> dd;
+        const uint16_t* d = dense;
+        uint64_t dld = ld;
+        if (!on_device) {
+            dd.alloc(std::max<uint64_t>(rows * cols, 1));
+            ck(cudaMemcpy2DAsync(dd.p, cols * 2, dense, ld * 2, cols * 2, rows, cudaMemcpyHostToDevice, st), "upload");
+            d = dd.p;
+            dld = cols;
+        }
+        DevBuf<uint32_t> counts, rp;
+        DevBuf<unsigned long long> total;
+        counts.alloc(std::max<uint64_t>(rows, 1));
+        rp.alloc(rows + 1);
+        total.alloc(1);
+        ck(mk::launch_dense_nnz(d, dld, (uint32_t)rows, (uint32_t)cols, counts.p, sms, st), "dense_nnz");
+        ck(mk::launch_scan_counts(counts.p, (uint32_t)rows, rp.p, total.p, st), "scan_counts");
+        g_launches.fetch_add(2);
+        unsigned long long n = 0;
+        ck(cudaMemcpyAsync(&n, total.p, 8, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaMemcpyAsync(row_ptrs, rp.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (n > 0xFFFFFFFFull) fail(MACKO_EINVAL, "nnz does not fit u32 row pointers");
+        *nnz = n;
+        if (!values || !col_idx || n == 0) return;  // count-only call
+        DevBuf<uint16_t> v;
+        DevBuf<uint32_t> c;
+        v.alloc(n);
+        c.alloc(n);
+        ck(mk::launch_dense_csr_emit(d, dld, (uint32_t)rows, (uint32_t)cols, rp.p, v.p, c.p, sms, st), "csr_emit");
+        g_launches.fetch_add(1);
+        ck(cudaMemcpyAsync(values, v.p, n * 2, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaMemcpyAsync(col_idx, c.p, n * 4, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+macko_status macko_dev_to_dense(const macko_dev_matrix* m, uint16_t* dense, uint64_t ld, int on_device, void* stream) {
+    return guarded([&] {
+        if (!m || !dense) fail(MACKO_EINVAL, "null argument");
+        if (ld < m->cols) fail(MACKO_EINVAL, "leading dimension < cols");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        DevBuf<uint16_t> tmp;
+        uint16_t* d = dense;
+        uint64_t dld = ld;
+        if (!on_device) {
+            tmp.alloc(m->rows * m->cols);
+            d = tmp.p;
+            dld = m->cols;
+        }
+        ck(cudaMemset2DAsync(d, dld * 2, 0, m->cols * 2, m->rows, st), "memset");
+        DevBuf<uint32_t> err;
+        err.alloc(1);
+        ck(cudaMemsetAsync(err.p, 0, 4, st), "memset");
+        ck(mk::launch_to_dense(m->values.p, m->deltas.p, m->row_ptrs.p, (uint32_t)m->rows, (uint32_t)m->cols,
+                               m->b_delta, d, dld, err.p, m->sms, st),
+           "to_dense");
+        g_launches.fetch_add(1);
+        uint32_t h = 0;
+        ck(cudaMemcpyAsync(&h, err.p, 4, cudaMemcpyDeviceToHost, st), "readback");
+        if (!on_device)
+            ck(cudaMemcpy2DAsync(dense, ld * 2, d, dld * 2, m->cols * 2, m->rows, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (h) fail(MACKO_EFORMAT, "decoded column index past the column bound");
+    });
+}
+
+macko_status macko_dev_padding_count(const macko_dev_matrix* m, uint64_t* out, void* stream) {
+    return guarded([&] {
+        if (!m || !out) fail(MACKO_EINVAL, "null argument");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        DevBuf<unsigned long long> cnt;
+        cnt.alloc(1);
+        ck(cudaMemsetAsync(cnt.p, 0, 8, st), "memset");
+        ck(mk::launch_padding_count(m->values.p, m->pad_nnz, cnt.p, m->sms, st), "padding_count");
+        g_launches.fetch_add(1);
+        unsigned long long h = 0;
+        ck(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, st), "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+        *out = h;
+    });
+}
+
 macko_status macko_dev_get_info(const macko_dev_matrix* m, macko_dev_info* out) {
     return guarded([&] {
         if (!m || !out) fail(MACKO_EINVAL, "null argument");

