@@ -137,6 +137,15 @@ macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint
 macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream,
                                uint32_t flags);
 
+/* Small-batch SpMM Y = A X for 1 <= batch <= 8 vectors (the paper's future work):
+ * X row b at d_X + b*ldx (cols fp16), Y row b at d_Y + b*ldy (rows fp16).  The matrix streams
+ * from HBM once for the whole batch; X is interleaved per column so one gather fetches every
+ * vector's x value.  Column b of Y is bit-identical to macko_dev_spmv(X[b]) (same summation
+ * order).  batch = 1 is macko_dev_spmv; batches 3, 5-7 run the next wider kernel with zero
+ * vectors.  b_delta = 4 only (MACKO_EINVAL otherwise).  Asynchronous, stream-ordered. */
+macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint64_t ldx, uint16_t* d_Y, uint64_t ldy,
+                            uint32_t batch, void* stream);
+
 /* End-to-end call with HOST buffers (what a CPU caller of reference_spmv would bind): x
  * host->device, the SpMV, y device->host, then the stream is synchronised.  Pinned
  * (device-mapped) host buffers are read and written by the kernels directly: a one-CTA kernel

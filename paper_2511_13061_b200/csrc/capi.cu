@@ -106,10 +106,17 @@ constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (el
 // stream.
 struct Workspace {
     DevBuf<uint32_t> counters;  // n_split arrival counters
-    DevBuf<float> partials;     // n_slots per-unit partial sums of split rows
+    DevBuf<float> partials;     // n_slots x kMaxBatch per-unit partial sums of split rows
     DevBuf<uint16_t> xcopy;     // texture-aligned copy of a misaligned x
     DevBuf<uint16_t> hx, hy;    // macko_spmv_host device buffers (hx texture-aligned inside)
     uint16_t* hx_aligned = nullptr;
+    DevBuf<uint16_t> xt;        // SpMM: interleaved X (cols x 8 fp16, texture-aligned inside)
+    uint16_t* xt_aligned = nullptr;
+    cudaTextureObject_t xt_tex[3] = {0, 0, 0};  // over xt with 4 / 8 / 16-byte texels (kb 2 / 4 / 8)
+    ~Workspace() {
+        for (auto t : xt_tex)
+            if (t) cudaDestroyTextureObject(t);
+    }
 };
 
 constexpr size_t kMaxWorkspaces = 16;  // streams per matrix before the pool is recycled
@@ -131,6 +138,7 @@ struct macko_dev_matrix {
     uint32_t ring = 0;          // TMA ring slots per warp
     size_t ring_offset = 0;     // x table bytes (rings follow it in dynamic smem)
     size_t smem = 0;
+    size_t smem_budget = 0, per_slot = 0;  // dynamic smem left for x table + rings; bytes of one ring slot
     int grid = 0, ctas_per_sm = 0;
     uint32_t n_chunks = 0, n_split = 0;
     uint64_t n_units = 0, n_slots = 0;
@@ -205,6 +213,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         const int split = d >= 0.65 ? 10 : d >= 0.45 ? 7 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
         m->x_mode = ring_for(split) >= 2 ? split : 0;
     }
+    m->smem_budget = budget;
+    m->per_slot = per_slot;
     m->ring = ring_for(m->x_mode);
     if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
     m->ring_offset = x_bytes(m->x_mode);
@@ -382,7 +392,7 @@ Workspace* workspace(const macko_dev_matrix* m, cudaStream_t st) {
     }
     auto w = std::make_unique<Workspace>();
     w->counters.alloc(std::max<uint32_t>(m->n_split, 1));
-    w->partials.alloc(std::max<uint64_t>(m->n_slots, 1));
+    w->partials.alloc(std::max<uint64_t>(m->n_slots, 1) * mk::kMaxBatch);
     ck(cudaMemsetAsync(w->counters.p, 0, w->counters.n * 4, st), "workspace zero");
     Workspace* raw = w.get();
     m->ws_pool.push_back(std::move(w));
@@ -1017,6 +1027,76 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
 
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
     return macko_dev_spmv_ex(m, d_x, d_y, stream, 0);
+}
+
+macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint64_t ldx, uint16_t* d_Y, uint64_t ldy,
+                            uint32_t batch, void* stream) {
+    if (batch == 1) return macko_dev_spmv(m, d_X, d_Y, stream);
+    return guarded([&] {
+        if (!m || !d_X || !d_Y) fail(MACKO_EINVAL, "null argument");
+        if (batch < 1 || batch > mk::kMaxBatch) fail(MACKO_EINVAL, "batch must be 1..8");
+        if (m->b_delta != 4) fail(MACKO_EINVAL, "SpMM is built for b_delta = 4 (the paper's format)");
+        if (ldx < m->cols || ldy < m->rows) fail(MACKO_EINVAL, "leading dimension smaller than the vector length");
+        DeviceGuard g(m->device);
+        const cudaStream_t st = (cudaStream_t)stream;
+        if (m->pad_nnz == 0) {
+            ck(cudaMemset2DAsync(d_Y, ldy * 2, 0, m->rows * 2, batch, st), "Y = 0");
+            return;
+        }
+        const uint32_t kb = batch <= 2 ? 2u : batch <= 4 ? 4u : 8u;
+        const int ti = kb == 2 ? 0 : kb == 4 ? 1 : 2;
+        std::lock_guard<std::mutex> lk(m->mu);
+        Workspace* w = workspace(m, st);
+        const uint64_t xt_elems = m->cols * mk::kMaxBatch + 8;  // + 16 bytes: staging reads whole vectors
+        if (!w->xt.p) {
+            if (stream_capturing(st)) fail(MACKO_EINVAL, "first SpMM of this matrix on a capturing stream");
+            const uintptr_t al = std::max<uintptr_t>(16, (uintptr_t)m->tex_align);
+            w->xt.alloc(xt_elems + al / 2);
+            ck(cudaMemsetAsync(w->xt.p, 0, w->xt.n * 2, st), "memset");
+            const uintptr_t p = reinterpret_cast<uintptr_t>(w->xt.p);
+            w->xt_aligned = reinterpret_cast<uint16_t*>((p + al - 1) / al * al);
+        }
+        if (!w->xt_tex[ti]) {
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = w->xt_aligned;
+            rd.res.linear.desc = kb == 2 ? cudaCreateChannelDesc<unsigned int>()
+                                 : kb == 4 ? cudaCreateChannelDesc<uint2>() : cudaCreateChannelDesc<uint4>();
+            rd.res.linear.sizeInBytes = m->cols * kb * 2;
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            ck(cudaCreateTextureObject(&w->xt_tex[ti], &rd, &td, nullptr), "XT texture");
+        }
+        // interleaved X, then the SpMM: x_mode 7 when the interleaved table and two ring slots fit
+        // (whole 16-byte vectors: the table staging copies vectors, the tail past cols is zero)
+        ck(mk::launch_interleave(d_X, ldx, batch, kb, (uint32_t)m->cols, w->xt_aligned,
+                                 (uint32_t)((m->cols * kb + 7) / 8 * 8), st),
+           "interleave");
+        const size_t table = align_up(2 * kb * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
+        const int mode = table + 2 * m->per_slot <= m->smem_budget ? 7 : 0;
+        mk::SpmvArgs a{};
+        a.values = m->values.p;
+        a.deltas = m->deltas.p;
+        a.row_ptrs = m->row_ptrs.p;
+        a.x = w->xt_aligned;
+        a.xtex = w->xt_tex[ti];
+        a.y = d_Y;
+        a.ldy = ldy;
+        a.batch = batch;
+        a.rows = (uint32_t)m->rows;
+        a.cols = (uint32_t)m->cols;
+        a.value_elems = m->values.n;
+        a.delta_bytes = m->deltas.n;
+        a.ring = 2;
+        a.ring_offset = mode == 7 ? (uint32_t)table : 0u;
+        a.plan = m->plan;
+        a.plan.counters = w->counters.p;
+        a.plan.partials = w->partials.p;
+        a.value_count = (uint32_t)m->pad_nnz;
+        const size_t smem = (mode == 7 ? table : 0) + 2 * m->per_slot;
+        ck(mk::launch_spmm(a, (int)kb, m->grid, mode, smem, st), "macko_spmm launch");
+        g_launches.fetch_add(2);
+    });
 }
 
 macko_status macko_spmv_host(const macko_dev_matrix* m, const uint16_t* h_x, uint16_t* h_y, void* stream) {

@@ -182,6 +182,79 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
     return acc;
 }
 
+// Batched lane step (SpMM, kB vectors): x is interleaved per column (kB fp16 = 2 kB bytes per
+// column, XT[c][b]), so one gather fetches all kB values of a column — one TLD of a 32 / 64 / 128-bit
+// texel or one LDS.32 / .64 / .128 — and kB FHFMAs take its halves.  Column b's summation order is
+// exactly the SpMV's (the same element -> lane -> unit structure), so Y[b] == SpMV(X[b]) bit for bit.
+template <int kB>
+struct XVec {
+    uint32_t w[kB / 2];
+};
+
+template <int kB>
+__device__ __forceinline__ XVec<kB> xtex_b(cudaTextureObject_t t, int col) {
+    XVec<kB> r;
+    if constexpr (kB == 2) {
+        r.w[0] = tex1Dfetch<unsigned int>(t, col);
+    } else if constexpr (kB == 4) {
+        const uint2 q = tex1Dfetch<uint2>(t, col);
+        r.w[0] = q.x;
+        r.w[1] = q.y;
+    } else {
+        const uint4 q = tex1Dfetch<uint4>(t, col);
+        r.w[0] = q.x;
+        r.w[1] = q.y;
+        r.w[2] = q.z;
+        r.w[3] = q.w;
+    }
+    return r;
+}
+
+template <int kB>
+__device__ __forceinline__ XVec<kB> lds_b(uint32_t addr) {
+    XVec<kB> r;
+    if constexpr (kB == 2) {
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r.w[0]) : "r"(addr));
+    } else if constexpr (kB == 4) {
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.w[0]), "=r"(r.w[1]) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                     : "r"(addr));
+    }
+    return r;
+}
+
+template <int kB>
+__device__ __forceinline__ void fma_b(float (&acc)[kB], uint16_t v, const XVec<kB>& x) {
+#pragma unroll
+    for (int q = 0; q < kB / 2; ++q) {
+        uint16_t lo, hi;
+        split_halves(x.w[q], lo, hi);
+        acc[2 * q] = fma_f16f16f32(v, lo, acc[2 * q]);
+        acc[2 * q + 1] = fma_f16f16f32(v, hi, acc[2 * q + 1]);
+    }
+}
+
+template <int kXMode, bool kMasked, int kB, uint32_t kTex = tex_slots<kXMode>(), class D>
+__device__ __forceinline__ void lane_step_b(float (&acc)[kB], const uint4& v, const D& dc, int cb, uint32_t xs_addr,
+                                            cudaTextureObject_t xt, uint32_t vm) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t base = xs_addr + 2u * kB * (uint32_t)cb;
+    asm("mov.b32 %0, %0;" : "+r"(base));
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        uint16_t v0, v1;
+        split_halves(w[m], v0, v1);
+        const uint32_t b0 = __byte_perm(dc.even, 0u, 0x4440u + m);
+        const uint32_t b1 = __byte_perm(dc.odd, 0u, 0x4440u + m);
+        if (!kMasked || ((vm >> (2 * m)) & 1u))
+            fma_b<kB>(acc, v0, ((kTex >> (2 * m)) & 1u) ? xtex_b<kB>(xt, cb + (int)b0) : lds_b<kB>(base + 2u * kB * b0));
+        if (!kMasked || ((vm >> (2 * m + 1)) & 1u))
+            fma_b<kB>(acc, v1, ((kTex >> (2 * m + 1)) & 1u) ? xtex_b<kB>(xt, cb + (int)b1) : lds_b<kB>(base + 2u * kB * b1));
+    }
+}
+
 // y[r] = v, and the same 2 bytes into every peer's y for the fused all-gather (one row per call,
 // lane 0).
 __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
@@ -189,6 +262,18 @@ __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v)
     if (a.y_mirror) a.y_mirror[r] = v;
     for (uint32_t p = 0; p < a.n_peer; ++p)
         reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[a.peer_bank][p])))[r] = v;
+}
+
+// Batched outputs (SpMM): Y[b][r] for b < a.batch (Y rows ldy apart).
+template <int kB>
+__device__ __forceinline__ void put_y_b(const SpmvArgs& a, uint32_t r, const uint16_t (&v)[kB]) {
+    if constexpr (kB == 1) {
+        put_y(a, r, v[0]);
+    } else {
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+            if ((uint32_t)b < a.batch) a.y[(size_t)b * a.ldy + r] = v[b];
+    }
 }
 
 // Fused all-gather: once all warps of the CTA wrote their rows, make them visible system-wide and
@@ -205,17 +290,19 @@ __device__ __forceinline__ void signal_peers(const SpmvArgs& a) {
 // ------------------------------------------------------------------------------------------
 // Compute-side row state
 // ------------------------------------------------------------------------------------------
+template <int kB>
 struct RowState {
     uint32_t r, s, e, e_next, al, T, t, tend, j0, n_r, last_b, units_left, slot;
     int32_t sid;
     bool split;
     int col_base;
-    float acc, row_acc;
+    float acc[kB], row_acc[kB];  // per lane / per row, one per vector of the batch
 };
 
 // Set up the piece of row rs.r = [rs.s, rs.e) starting at unit j0.  sid / slot: the chunk's
 // split-row id for this piece (used only if the piece turns out to be split).
-__device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colbase, int32_t sid, uint32_t slot) {
+template <int kB>
+__device__ __forceinline__ void begin_piece(RowState<kB>& rs, uint32_t j0, int colbase, int32_t sid, uint32_t slot) {
     // A row's first step starts at the 8-aligned al (ROMA); its k = s - al leading elements
     // belong to the previous row and are decoded as codeword 0 (delta 1) after masking, so the
     // column before the row is -1 - k (the masked elements sit at columns -k..-1).
@@ -233,8 +320,11 @@ __device__ __forceinline__ void begin_piece(RowState& rs, uint32_t j0, int colba
     rs.sid = sid;
     rs.slot = slot;
     rs.col_base = j0 ? colbase : -1 - (int)(rs.s - rs.al);
-    rs.acc = 0.0f;
-    rs.row_acc = 0.0f;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+        rs.acc[b] = 0.0f;
+        rs.row_acc[b] = 0.0f;
+    }
 }
 
 // Finish the current piece (write y or hand the split row to its last arrival).  Lane 0 wrote
@@ -262,9 +352,42 @@ __device__ __noinline__ int finish_split(uint32_t j0, uint32_t tend, uint32_t n_
     return -1;
 }
 
+// finish_split for a batch: partial slot q of vector b at partials[(slot + q) kB + b].  Returns
+// true in lane 0 of the last arrival with the rows' fp16 bits in out.
+template <int kB>
+__device__ __forceinline__ bool finish_split_b(uint32_t j0, uint32_t tend, uint32_t n_r, uint32_t slot, int32_t sid,
+                                               const float (&row_acc)[kB], const SpmvPlanDev P, int lane,
+                                               uint16_t (&out)[kB]) {
+    uint32_t last = 0, first = 0;
+    if (lane == 0) {
+        if (j0 == 0) {  // a first piece ends on a unit boundary
+#pragma unroll
+            for (int b = 0; b < kB; ++b) P.partials[(size_t)(slot + tend / kUnitSteps - 1u) * kB + b] = row_acc[b];
+        }
+        const uint4 sp = P.splits[sid];
+        first = sp.y;
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.counters + sid) : "memory");
+        last = prev + 1 == sp.z;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last && lane == 0) {
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            float tot = __ldcg(P.partials + (size_t)(slot + first - 1) * kB + b);
+            for (uint32_t q = first; q < n_r; ++q) tot += __ldcg(P.partials + (size_t)(slot + q) * kB + b);
+            out[b] = f32_to_f16_rn(tot);
+        }
+        P.counters[sid] = 0;  // ready for the next launch (stream order)
+        return true;
+    }
+    return false;
+}
+
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
 // when the chunk is exhausted.  The row pointer after the next row is prefetched one row ahead.
-__device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint32_t w, int lane) {
+template <int kB>
+__device__ __forceinline__ bool next_piece(RowState<kB>& rs, const SpmvArgs& a, uint32_t w, int lane) {
     for (;;) {
         if (rs.units_left == 0) return false;
         ++rs.r;
@@ -278,7 +401,10 @@ __device__ __forceinline__ bool next_piece(RowState& rs, const SpmvArgs& a, uint
             rs.slot = q.w;
         }
         if (rs.T) return true;
-        if (lane == 0) put_y(a, rs.r, 0);  // empty row: fp16(+0.0)
+        if (lane == 0) {  // empty row: fp16(+0.0)
+            const uint16_t z[kB] = {};
+            put_y_b<kB>(a, rs.r, z);
+        }
     }
 }
 
@@ -477,9 +603,9 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
 }
 
 // Set up the warp's ring and ROMA walk for one SpMV (plan record pr) and issue the first fills.
-template <int kBits>
+template <int kBits, int kB>
 __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
-                                         uint32_t smem_base, uint32_t bar0, Ring& g, RowState& rs) {
+                                         uint32_t smem_base, uint32_t bar0, Ring& g, RowState<kB>& rs) {
     const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
     MK_TRACE(1);
     if (q0.x == 0) return false;
@@ -494,10 +620,19 @@ __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr
 }
 
 // Stage x in shared memory (fp16, with zero guards of kXGuardLo / kXGuardHi entries); all
-// threads of the CTA, the caller synchronises.
-template <int kXMode>
+// threads of the CTA, the caller synchronises.  Batches: the interleaved XT (kB halves per column,
+// guards kB halves per guard column) is staged the same way.
+template <int kXMode, int kB = 1>
 __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
-    if constexpr (x_table<kXMode>()) {
+    if constexpr (x_table<kXMode>() && kB > 1) {
+        const uint32_t nv = a.cols * kB / 8;  // 16-byte vectors of XT (cols * kB is a multiple of 8 for kB >= 8;
+        const uint4* x4 = reinterpret_cast<const uint4*>(a.x);  // capi pads XT to 16 bytes otherwise)
+        const uint32_t nvp = (a.cols * kB + 7) / 8;
+        for (uint32_t i = threadIdx.x; i < nvp; i += blockDim.x) reinterpret_cast<uint4*>(xs)[i] = __ldg(x4 + i);
+        (void)nv;
+        for (uint32_t i = nvp * 8 + threadIdx.x; i < (a.cols + kXGuardHi) * kB; i += blockDim.x) xs[i] = 0;
+        if (threadIdx.x < kXGuardLo * kB) xs[(int)threadIdx.x - kXGuardLo * kB] = 0;
+    } else if constexpr (x_table<kXMode>()) {
         const uint32_t C = a.cols;
         const uint4* x4 = reinterpret_cast<const uint4*>(a.x);  // 16-byte aligned (capi guarantees)
         const uint32_t nv = C / 8;
@@ -515,11 +650,14 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
-template <int kXMode, int kBits>
+template <int kXMode, int kBits, int kB>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
-                                         RowState& rs) {
+                                         RowState<kB>& rs) {
     if (rs.T == 0) {
-        if (lane == 0) put_y(a, rs.r, 0);
+        if (lane == 0) {
+            const uint16_t z[kB] = {};
+            put_y_b<kB>(a, rs.r, z);
+        }
         if (!next_piece(rs, a, w, lane)) return;
     }
     // loop invariants pinned in registers (not re-derived from the CTA's shared window per pair)
@@ -567,14 +705,14 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         const uint32_t lane_bias = bias * (uint32_t)lane, tot_bias = bias * kWarp;
         const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - (dA.local - bias) + lane_bias);
         const int cbB = rs.col_base + (int)((tot & 0xFFFFu) + tot_bias) + (int)((incl >> 16) - (dB.local - bias) + lane_bias);
-        if constexpr (kMasked) {
-            // Edge pair (the row's first and last): both steps predicated by their valid-element
-            // masks; a phantom second step (the row ends in step A) has vmB = 0.
-            rs.acc = lane_step<kXMode, true>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-            rs.acc = lane_step<kXMode, true, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+        // Edge pairs (the row's first and last): both steps predicated by their valid-element
+        // masks; a phantom second step (the row ends in step A) has vmB = 0.
+        if constexpr (kB == 1) {
+            rs.acc[0] = lane_step<kXMode, kMasked>(rs.acc[0], A.v, dA, cbA, xs_addr, a.xtex, vmA);
+            rs.acc[0] = lane_step<kXMode, kMasked, tex_slots_b<kXMode>()>(rs.acc[0], B.v, dB, cbB, xs_addr, a.xtex, vmB);
         } else {
-            rs.acc = lane_step<kXMode, false>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-            rs.acc = lane_step<kXMode, false, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            lane_step_b<kXMode, kMasked, kB>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
+            lane_step_b<kXMode, kMasked, kB, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
         }
         rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16) + 2 * (int)tot_bias;
     };
@@ -594,24 +732,39 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
                 pair(std::true_type{}, t);
                 t += 2u;
             }
-            const float red = warp_tree_sum(rs.acc);
-            rs.acc = 0.0f;
-            if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[rs.slot + min((ue - 1u) / kUnitSteps, rs.n_r - 1u)] = red;
-            rs.row_acc += red;
+            const uint32_t pslot = rs.slot + min((ue - 1u) / kUnitSteps, rs.n_r - 1u);
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                const float red = warp_tree_sum(rs.acc[b]);
+                rs.acc[b] = 0.0f;
+                if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[(size_t)pslot * kB + b] = red;
+                rs.row_acc[b] += red;
+            }
             t = ue;
         }
         // -- piece end
-        if (!rs.split) {
-            if (lane == 0) put_y(a, rs.r, f32_to_f16_rn(rs.row_acc));
+        if constexpr (kB == 1) {
+            if (!rs.split) {
+                if (lane == 0) put_y(a, rs.r, f32_to_f16_rn(rs.row_acc[0]));
+            } else {
+                const int v = finish_split(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc[0], a.plan, lane);
+                if (v >= 0) put_y(a, rs.r, (uint16_t)v);
+            }
         } else {
-            const int v = finish_split(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, lane);
-            if (v >= 0) put_y(a, rs.r, (uint16_t)v);
+            uint16_t out[kB];
+            if (!rs.split) {
+#pragma unroll
+                for (int b = 0; b < kB; ++b) out[b] = f32_to_f16_rn(rs.row_acc[b]);
+                if (lane == 0) put_y_b<kB>(a, rs.r, out);
+            } else if (finish_split_b<kB>(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, lane, out)) {
+                put_y_b<kB>(a, rs.r, out);
+            }
         }
         if (!next_piece(rs, a, w, lane)) break;
     }
 }
 
-template <int kXMode, int kBits>
+template <int kXMode, int kBits, int kB = 1>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
@@ -625,23 +778,23 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const PlanRecord pr = load_record(a, w);
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo;
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo * kB;
     // Without a PDL producer x is final at entry: its loads overlap the plan record's latency.
-    if (!a.pdl) stage_x<kXMode>(a, xs);
+    if (!a.pdl) stage_x<kXMode, kB>(a, xs);
     // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
-    RowState rs;
+    RowState<kB> rs;
     Ring g;
-    const bool has_work = op_begin<kBits>(a, pr, warp, lane, smem_base,
+    const bool has_work = op_begin<kBits, kB>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
     MK_TRACE(2);
     // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     MK_TRACE(3);
-    if (a.pdl) stage_x<kXMode>(a, xs);
+    if (a.pdl) stage_x<kXMode, kB>(a, xs);
     __syncthreads();
     MK_TRACE(4);
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    if (has_work) run_rows<kXMode, kBits>(a, w, lane, xs_addr, g, rs);
+    if (has_work) run_rows<kXMode, kBits, kB>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
     signal_peers(a);
 }
@@ -690,6 +843,52 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
+}
+
+// Small-batch SpMM (b_delta 4): x_mode 0 (TEX gathers of 2 kB-byte texels) or 7 (the SpMV's
+// LSU / TEX split over an interleaved shared-memory table).
+template <int kXMode, int kB>
+static cudaError_t launch_spmm_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(macko_spmv<kXMode, 4, kB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    macko_spmv<kXMode, 4, kB><<<grid, kSpmvWarpsPerCta * kWarp, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmm(const SpmvArgs& a, int kb, int grid, int x_mode, size_t smem, cudaStream_t s) {
+    if (x_mode == 0) {
+        switch (kb) {
+            case 2: return launch_spmm_one<0, 2>(a, grid, smem, s);
+            case 4: return launch_spmm_one<0, 4>(a, grid, smem, s);
+            case 8: return launch_spmm_one<0, 8>(a, grid, smem, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    if (x_mode == 7) {
+        switch (kb) {
+            case 2: return launch_spmm_one<7, 2>(a, grid, smem, s);
+            case 4: return launch_spmm_one<7, 4>(a, grid, smem, s);
+            case 8: return launch_spmm_one<7, 8>(a, grid, smem, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+// XT[c * kb + b] = X[b][c] (b < batch; 0 for the padding vectors), the SpMM's interleaved x.
+__global__ void interleave_kernel(const uint16_t* __restrict__ X, uint64_t ldx, uint32_t batch, uint32_t kb,
+                                  uint32_t cols, uint16_t* __restrict__ XT, uint32_t n_total) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_total; i += gridDim.x * blockDim.x) {
+        const uint32_t c = i / kb, b = i - c * kb;
+        XT[i] = (c < cols && b < batch) ? X[(size_t)b * ldx + c] : (uint16_t)0;
+    }
+}
+
+cudaError_t launch_interleave(const uint16_t* X, uint64_t ldx, uint32_t batch, uint32_t kb, uint32_t cols,
+                              uint16_t* XT, uint32_t n_total, cudaStream_t s) {
+    const int grid = (int)std::min<uint32_t>((n_total + 255) / 256, 1024u);
+    if (grid) interleave_kernel<<<grid, 256, 0, s>>>(X, ldx, batch, kb, cols, XT, n_total);
+    return cudaGetLastError();
 }
 
 // Host-buffer SpMV (macko_spmv_host) with pinned, device-mapped host x / y: a one-CTA kernel pulls

@@ -56,6 +56,8 @@ struct SpmvArgs {
     const PeerTable* peers;
     uint32_t peer_bank;    // which y bank of the peer table this launch stores into (0 / 1)
     uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
+    uint32_t batch;        // SpMM: vectors in the batch (<= the kernel's kB); x = XT interleaved
+    uint64_t ldy;          // SpMM: element stride between the batch's y vectors
     SpmvPlanDev plan;
 };
 
@@ -95,6 +97,12 @@ cudaError_t trace_read(unsigned long long* host, size_t n);  // trace build only
 #endif
 // pdl: launch with programmatic stream serialization (overlaps the previous kernel's tail)
 cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_t smem, cudaStream_t s, bool pdl);
+// Small-batch SpMM over a b_delta = 4 matrix: kb in {2, 4, 8}, x_mode 0 (texture) or 7 (split);
+// a.x is the interleaved XT (launch_interleave), a.xtex a texture of 2 kb-byte texels over it.
+cudaError_t launch_spmm(const SpmvArgs& a, int kb, int grid, int x_mode, size_t smem, cudaStream_t s);
+cudaError_t launch_interleave(const uint16_t* X, uint64_t ldx, uint32_t batch, uint32_t kb, uint32_t cols,
+                              uint16_t* XT, uint32_t n_total, cudaStream_t s);
+constexpr uint32_t kMaxBatch = 8;
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
 bool spmv_valid_config(int x_mode, int bits);
 // Wait until flags[i] >= target for i < n (system-scope acquire; peers' fused all-gathers).

@@ -3,9 +3,10 @@ end-to-end use, PAPER.md:86,496-510 — every linear of a pruned LLM becomes an 
 
 The fp16 weight is compressed once on the GPU (bit-exact MACKO format, b_delta = 4 by default);
 forward(x) for x of shape [in_features] or [1, ..., 1, in_features] is one sm_100a SpMV (fp32
-accumulate, one RNE) plus the optional bias.  Larger batches run one SpMV per input vector — the
-kernel is a matrix-vector product (SpMM is the paper's future work).  There is no CPU fallback:
-the module requires the CUDA library and a CUDA weight.
+accumulate, one RNE) plus the optional bias; batches of up to 8 vectors are one small-batch SpMM
+(macko_dev_spmm: the weight streams from HBM once per 8 vectors; row b bit-identical to the SpMV of
+vector b), larger batches run in groups of 8.  There is no CPU fallback: the module requires the
+CUDA library and a CUDA weight.
 """
 from __future__ import annotations
 
@@ -37,6 +38,24 @@ def _spmv_fake(handle: int, x: torch.Tensor, rows: int) -> torch.Tensor:
     return x.new_empty(rows)
 
 
+@torch.library.custom_op("macko::spmm", mutates_args=())
+def spmm_op(handle: int, X: torch.Tensor, rows: int) -> torch.Tensor:
+    """Y = (A X^T)^T for a batch X of 1..8 fp16 CUDA row vectors (batch x cols) as a registered
+    torch operator (torch.ops.macko.spmm); Y is batch x rows.  Launches on the current stream."""
+    if not X.is_cuda or X.dtype != torch.float16 or X.dim() != 2 or not 1 <= X.shape[0] <= 8:
+        raise ValueError("macko::spmm takes a (1..8) x cols fp16 CUDA tensor")
+    X = X.contiguous()
+    Y = torch.empty((X.shape[0], rows), dtype=torch.float16, device=X.device)
+    stream = torch.cuda.current_stream(X.device).cuda_stream
+    _lib.check(_lib.load().macko_dev_spmm(handle, X.data_ptr(), X.shape[1], Y.data_ptr(), rows, X.shape[0], stream))
+    return Y
+
+
+@spmm_op.register_fake
+def _spmm_fake(handle: int, X: torch.Tensor, rows: int) -> torch.Tensor:
+    return X.new_empty((X.shape[0], rows))
+
+
 class MackoLinear(nn.Module):
     def __init__(self, matrix: M.DeviceMatrix, bias: Optional[torch.Tensor] = None):
         super().__init__()
@@ -64,7 +83,10 @@ class MackoLinear(nn.Module):
         lead = x.shape[:-1]
         xs = x.reshape(-1, self.in_features).to(torch.float16).contiguous()
         h = self.matrix.handle
-        out = torch.stack([torch.ops.macko.spmv(h, xs[i], self.out_features) for i in range(xs.shape[0])])
+        if xs.shape[0] == 1:
+            out = torch.ops.macko.spmv(h, xs[0], self.out_features).unsqueeze(0)
+        else:  # groups of up to 8 vectors: one pass over the weight per group
+            out = torch.cat([torch.ops.macko.spmm(h, xs[i:i + 8], self.out_features) for i in range(0, xs.shape[0], 8)])
         if self.bias is not None:
             out = out + self.bias
         return out.reshape(*lead, self.out_features)

@@ -223,6 +223,19 @@ class DeviceMatrix:
         else:
             check(_lib.load().macko_dev_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
 
+    def spmm_into(self, X, Y, stream=None) -> None:
+        """Y = A X^T for a small batch: X (batch x cols) and Y (batch x rows) fp16 CUDA tensors with
+        unit column stride, 1 <= batch <= 8; the matrix streams once (macko_dev_spmm).  Row b of Y
+        is bit-identical to spmv_into(X[b])."""
+        if X.dim() != 2 or Y.dim() != 2 or X.shape[0] != Y.shape[0]:
+            raise ValueError("X and Y must be (batch x cols) and (batch x rows)")
+        if X.shape[1] != self.cols or Y.shape[1] != self.rows:
+            raise ValueError("dimension mismatch")
+        if X.stride(1) != 1 or Y.stride(1) != 1:
+            raise ValueError("X and Y rows must be contiguous")
+        check(_lib.load().macko_dev_spmm(self._h, _ptr(X), X.stride(0), _ptr(Y), Y.stride(0), X.shape[0],
+                                         _stream_ptr(stream)))
+
     def set_peers(self, peer_y: Sequence[int], peer_flags: Sequence[int], stream=None) -> None:
         """Fused all-gather destinations (device / IPC-mapped addresses; see macko_dev_set_peers)."""
         n = len(peer_y)

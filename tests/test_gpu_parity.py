@@ -579,3 +579,45 @@ def test_macko_from_csr_rejects_non_canonical(cuda):
     A = O.gen_dense(4, 64, 0.5, 1)
     dm = gpu_encode(A)
     assert dm.padding_count() == 0 or dm.padding_count() > 0
+
+
+# ------------------------------------------------------------------------------ small-batch SpMM
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 5, 8])
+def test_spmm_columns_equal_spmv(cuda, batch):
+    # PAPER.md:535 (future work): Y = A X for a batch of vectors, one pass over the matrix; column b
+    # is bit-exact against the order oracle on X[b] (and the integer-mode sequential reference)
+    cases = [(1000, 16000, 0.5), (300, 5000, 0.3), (4096, 4096, 0.5), (17, 20000, 0.02), (2000, 3000, 0.9),
+             (6, 120000, 0.3)]  # the last: x table too large -> texture-only kernel
+    for i, (R, C, d) in enumerate(cases):
+        for int_mode in (False, True):
+            A = O.gen_dense(R, C, d, 700 + i, int_mode)
+            if R > 8:
+                A[2::9] = 0
+            m = O.encode_dense(A)
+            dm = gpu_encode(A)
+            X = np.stack([O.gen_vector(C, 800 + 10 * i + b, int_mode) for b in range(batch)])
+            Xd = to_dev(X)
+            Y = torch.full((batch, R + 5), 7.0, dtype=torch.float16, device=cuda)[:, :R]  # ldy > rows
+            dm.spmm_into(Xd, Y)
+            torch.cuda.synchronize()
+            Yh = to_host_u16(Y.contiguous())
+            for b in range(batch):
+                if int_mode:
+                    assert np.array_equal(Yh[b], O.reference_spmv(m, X[b], 8)), (R, C, d, b)
+                else:
+                    assert np.array_equal(Yh[b], b200_y(m, X[b])), (R, C, d, b)
+            # padding outputs (R..R+5) untouched
+            assert (Y.as_strided((batch, 5), (R + 5, 1), R) == 7.0).all()
+
+
+def test_spmm_errors(cuda):
+    A = O.gen_dense(64, 512, 0.5, 1)
+    dm = gpu_encode(A)
+    X = torch.zeros((9, 512), dtype=torch.float16, device=cuda)
+    with pytest.raises(ValueError):
+        dm.spmm_into(X, torch.zeros((9, 64), dtype=torch.float16, device=cuda))  # batch > 8
+    with pytest.raises(ValueError):
+        dm.spmm_into(X[:2, :500], torch.zeros((2, 64), dtype=torch.float16, device=cuda))
+    dm2 = gpu_encode(A, 2)
+    with pytest.raises(ValueError, match="b_delta"):
+        dm2.spmm_into(X[:2], torch.zeros((2, 64), dtype=torch.float16, device=cuda))
