@@ -8,7 +8,7 @@ SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu 
 HDRS := $(wildcard $(CSRC)/*.cuh) include/macko_cuda.h
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 
-all: lib dropin oracle
+all: lib dropin llm oracle
 
 lib: $(PKG)/libmacko_cuda.so
 
@@ -22,11 +22,17 @@ $(PKG)/libmacko_cuda.so: $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# libmacko_llm.so: the per-token kernels of the Llama decode benchmark (the caller of the path)
+llm: $(PKG)/libmacko_llm.so
+$(PKG)/libmacko_llm.so: $(CSRC)/llm.cu include/macko_llm.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/llm.cu -cudart static 2> build/llm.ptxas.log || (cat build/llm.ptxas.log; exit 1)
+
 clean:
 	rm -rf build $(PKG)/libmacko_cuda.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean llm
 
 # opt-in trace build (per-warp %globaltimer stamps; tools/trace_spmv.py), never the product .so
 trace: $(PKG)/libmacko_cuda_trace.so

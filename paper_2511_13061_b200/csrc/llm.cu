@@ -1,0 +1,257 @@
+// llm.cu — libmacko_llm.so: the small per-token kernels of a Llama-style batch-1 decode step, the
+// caller of the MACKO path in the paper's end-to-end measurement (Llama2-7B,
+// 100 generated tokens, MACKO linears vs dense cuBLAS).  Not part of the SpMV boundary; the
+// linears themselves are libmacko_cuda.so SpMVs (or cuBLAS GEMVs for the dense baseline).
+//
+// Every kernel reads the decode position / token id from device memory, so one decode step is a
+// fixed sequence of launches that a CUDA graph replays token after token.  All of them are
+// programmatic dependent launches (PDL): each lets the next kernel launch at its start and waits for
+// its predecessor (griddepcontrol.wait) before touching data, so the SpMVs' prologues (plan record,
+// first matrix fills) and these kernels' launches overlap the previous kernel's tail.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#include "../../include/macko_llm.h"
+
+namespace {
+
+__device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
+
+template <int kThreads>
+__device__ float block_sum(float v, float* red) {
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < kThreads / 32 ? red[l] : 0.0f;
+        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// h += delta (fp16 residual stream, as the fp16 model keeps it); out = h / rms(h) * weight
+__global__ void __launch_bounds__(1024) add_rmsnorm_kernel(uint16_t* h, const uint16_t* delta, const uint16_t* weight,
+                                                           uint16_t* out, uint32_t n, float eps) {
+    __shared__ float red[32];
+    pdl_enter();
+    float ss = 0.0f;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        float v = h2f(h[i]);
+        if (delta) {
+            v = h2f(f2h(v + h2f(delta[i])));
+            h[i] = f2h(v);
+        }
+        ss += v * v;
+    }
+    const float inv = rsqrtf(block_sum<1024>(ss, red) / (float)n + eps);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = f2h(h2f(h[i]) * inv * h2f(weight[i]));
+}
+
+// Rotary embedding (rotate-half convention) of q and k at position *pos, k / v appended to the
+// layer's cache row *pos.  qkv = [q; k; v] (3 * heads * head_dim).
+__global__ void rope_kv_kernel(const uint16_t* qkv, const int32_t* pos, uint16_t* q_out, uint16_t* k_cache,
+                               uint16_t* v_cache, uint32_t heads, uint32_t head_dim, float theta) {
+    pdl_enter();
+    const uint32_t H = heads * head_dim, half = head_dim / 2;
+    const int32_t p = *pos;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
+        const uint32_t d = i % head_dim, j = d % half;
+        const float inv_freq = powf(theta, -2.0f * (float)j / (float)head_dim);
+        float s, c;
+        sincosf((float)p * inv_freq, &s, &c);
+        const uint32_t partner = d < half ? i + half : i - half;
+        const float sign = d < half ? -1.0f : 1.0f;  // rotate_half: [-x2, x1]
+        const float q = h2f(qkv[i]), qp = h2f(qkv[partner]);
+        const float k = h2f(qkv[H + i]), kp = h2f(qkv[H + partner]);
+        q_out[i] = f2h(q * c + sign * qp * s);
+        k_cache[(size_t)p * H + i] = f2h(k * c + sign * kp * s);
+        v_cache[(size_t)p * H + i] = qkv[2 * H + i];
+    }
+}
+
+// One query against positions [0, *pos]: a CTA of 4 warps per head, fp32 scores and softmax.
+// Warp w takes positions t = w (mod 4); lane l owns dims [l D, l D + D) (D = head_dim / 32 <= 8),
+// so every K / V row is read as one coalesced 2 D-byte load per lane.
+constexpr int kAttnWarps = 4;
+
+__global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(const uint16_t* q, const uint16_t* k_cache,
+                                                                    const uint16_t* v_cache, const int32_t* pos,
+                                                                    uint16_t* out, uint32_t heads, uint32_t head_dim,
+                                                                    uint32_t max_len) {
+    extern __shared__ float sm[];  // scores[max_len] | partial outputs [kAttnWarps][head_dim]
+    pdl_enter();
+    __shared__ float red[32];
+    float* sc = sm;
+    float* part = sm + max_len;
+    const uint32_t h = blockIdx.x, H = heads * head_dim, D = head_dim / 32;
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    const int32_t n = *pos + 1;
+    float qv[8], acc[8];
+    for (uint32_t i = 0; i < D; ++i) {
+        qv[i] = h2f(q[h * head_dim + l * D + i]);
+        acc[i] = 0.0f;
+    }
+    const float scale = rsqrtf((float)head_dim);
+    for (int32_t t = w; t < n; t += kAttnWarps) {
+        const uint16_t* kr = k_cache + (size_t)t * H + h * head_dim + l * D;
+        float s = 0.0f;
+        for (uint32_t i = 0; i < D; ++i) s += qv[i] * h2f(kr[i]);
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (l == 0) sc[t] = s * scale;
+    }
+    __syncthreads();
+    float mx = -INFINITY;
+    for (int32_t t = threadIdx.x; t < n; t += blockDim.x) mx = fmaxf(mx, sc[t]);
+    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (l == 0) red[w] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int i = 1; i < kAttnWarps; ++i) mx = fmaxf(mx, red[i]);
+    __syncthreads();
+    float sum = 0.0f;
+    for (int32_t t = threadIdx.x; t < n; t += blockDim.x) {
+        const float e = __expf(sc[t] - mx);
+        sc[t] = e;
+        sum += e;
+    }
+    sum = block_sum<kAttnWarps * 32>(sum, red);  // (its barriers also publish sc)
+    for (int32_t t = w; t < n; t += kAttnWarps) {
+        const float pt = sc[t];
+        const uint16_t* vr = v_cache + (size_t)t * H + h * head_dim + l * D;
+        for (uint32_t i = 0; i < D; ++i) acc[i] += pt * h2f(vr[i]);
+    }
+    for (uint32_t i = 0; i < D; ++i) part[w * head_dim + l * D + i] = acc[i];
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < head_dim; d += blockDim.x) {
+        float o = 0.0f;
+        for (int i = 0; i < kAttnWarps; ++i) o += part[i * head_dim + d];
+        out[h * head_dim + d] = f2h(o / sum);
+    }
+}
+
+// gu = [gate; up] (2 * inter): out = silu(gate) * up
+__global__ void silu_mul_kernel(const uint16_t* gu, uint16_t* out, uint32_t inter) {
+    pdl_enter();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < inter; i += gridDim.x * blockDim.x) {
+        const float g = h2f(gu[i]), u = h2f(gu[inter + i]);
+        out[i] = f2h(g / (1.0f + __expf(-g)) * u);
+    }
+}
+
+__global__ void embed_kernel(const uint16_t* table, const int32_t* token, uint16_t* h, uint32_t hidden) {
+    pdl_enter();
+    const int32_t t = *token;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < hidden; i += gridDim.x * blockDim.x)
+        h[i] = table[(size_t)t * hidden + i];
+}
+
+// Greedy sampling: token = argmax(logits) (lowest index on ties), then *pos += 1.
+__global__ void __launch_bounds__(1024) argmax_kernel(const uint16_t* logits, uint32_t n, int32_t* token, int32_t* pos,
+                                                      int32_t* history, uint32_t history_len) {
+    pdl_enter();
+    __shared__ float bv[32];
+    __shared__ int32_t bi[32];
+    float best = -INFINITY;
+    int32_t idx = 0x7FFFFFFF;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const float v = h2f(logits[i]);
+        if (v > best || (v == best && (int32_t)i < idx)) {
+            best = v;
+            idx = (int32_t)i;
+        }
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int32_t oi = __shfl_xor_sync(0xffffffffu, idx, off);
+        if (ov > best || (ov == best && oi < idx)) {
+            best = ov;
+            idx = oi;
+        }
+    }
+    if (threadIdx.x % 32 == 0) {
+        bv[threadIdx.x / 32] = best;
+        bi[threadIdx.x / 32] = idx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < blockDim.x / 32; ++w)
+            if (bv[w] > best || (bv[w] == best && bi[w] < idx)) {
+                best = bv[w];
+                idx = bi[w];
+            }
+        const int32_t p = *pos;
+        *token = idx;
+        if (history && (uint32_t)p < history_len) history[p] = idx;
+        *pos = p + 1;
+    }
+}
+
+template <typename... KArgs, typename... Args>
+int launch(void (*k)(KArgs...), int grid, int block, size_t smem, void* stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+int grid_for(uint32_t n, int threads) { return (int)((n + threads - 1) / threads < 1024 ? (n + threads - 1) / threads : 1024); }
+
+}  // namespace
+
+extern "C" {
+
+int macko_llm_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t* weight, uint16_t* out, uint32_t n,
+                          float eps, void* stream) {
+    return launch(add_rmsnorm_kernel, 1, 1024, 0, stream, h, delta, weight, out, n, eps);
+}
+
+int macko_llm_rope_kv(const uint16_t* qkv, const int32_t* pos, uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache,
+                      uint32_t heads, uint32_t head_dim, float theta, void* stream) {
+    const uint32_t H = heads * head_dim;
+    return launch(rope_kv_kernel, grid_for(H, 256), 256, 0, stream, qkv, pos, q_out, k_cache, v_cache, heads, head_dim,
+                  theta);
+}
+
+int macko_llm_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache, const int32_t* pos,
+                        uint16_t* out, uint32_t heads, uint32_t head_dim, uint32_t max_len, void* stream) {
+    if (head_dim % 32 != 0 || head_dim > 256) return (int)cudaErrorInvalidValue;
+    const size_t smem = (max_len + kAttnWarps * head_dim) * sizeof(float);
+    return launch(attention_kernel, (int)heads, kAttnWarps * 32, smem, stream, q, k_cache, v_cache, pos, out, heads,
+                  head_dim, max_len);
+}
+
+int macko_llm_silu_mul(const uint16_t* gu, uint16_t* out, uint32_t inter, void* stream) {
+    return launch(silu_mul_kernel, grid_for(inter, 256), 256, 0, stream, gu, out, inter);
+}
+
+int macko_llm_embed(const uint16_t* table, const int32_t* token, uint16_t* h, uint32_t hidden, void* stream) {
+    return launch(embed_kernel, grid_for(hidden, 256), 256, 0, stream, table, token, h, hidden);
+}
+
+int macko_llm_argmax(const uint16_t* logits, uint32_t n, int32_t* token, int32_t* pos, int32_t* history,
+                     uint32_t history_len, void* stream) {
+    return launch(argmax_kernel, 1, 1024, 0, stream, logits, n, token, pos, history, history_len);
+}
+
+}  // extern "C"

@@ -85,6 +85,8 @@ class MackoLinear(nn.Module):
         h = self.matrix.handle
         if xs.shape[0] == 1:
             out = torch.ops.macko.spmv(h, xs[0], self.out_features).unsqueeze(0)
+        elif self.matrix.b_delta != 4:  # the SpMM kernel is built for the paper's 4-bit deltas
+            out = torch.stack([torch.ops.macko.spmv(h, xs[i], self.out_features) for i in range(xs.shape[0])])
         else:  # groups of up to 8 vectors: one pass over the weight per group
             out = torch.cat([torch.ops.macko.spmm(h, xs[i:i + 8], self.out_features) for i in range(0, xs.shape[0], 8)])
         if self.bias is not None:
