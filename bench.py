@@ -3,7 +3,7 @@
 36864x12288 fp16 @ 50 % sparsity vs cuBLAS GEMV).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--sweep] [--chain] [--decode] [--strong] [--fused]
+                    [--sweep] [--chain] [--strong] [--fused] [--no-decode] [--no-cpu-baseline]
 
 One step = one SpMV y = A·x over the resident MACKO matrix (GPU-compressed from a synthetic
 random-unstructured fp16 matrix of the configured shape; inputs resident in HBM).
@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--density", type=float, default=HEADLINE["density"])
     p.add_argument("--sweep", action="store_true", help="30/50/70/90 %% sparsity, Llama shapes, 131072x32768")
     p.add_argument("--chain", action="store_true", help="Llama2-7B 32-layer decode SpMV chain (config 4) vs cuBLAS")
-    p.add_argument("--decode", action="store_true", help="Llama2-7B decode (attention, RMSNorm, SiLU) tokens/s")
+    p.add_argument("--no-decode", action="store_true", help="skip the Llama2-7B decode E2E (MACKO vs cuBLAS tokens/s)")
     p.add_argument("--strong", action="store_true", help="config 5 strong scaling also at N = 1")
     p.add_argument("--chain-tokens", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -460,7 +460,11 @@ def main():
         torch.cuda.empty_cache()
         chain = run_chain(args, torch, dist, dev, world, rank, peak)
     decode = None
-    if args.decode and world == 1:
+    if not args.no_decode and world == 1 and rank == 0:
+        if dm is not None:
+            dm.close()
+            dm = None
+        torch.cuda.empty_cache()
         decode = run_decode(torch, dev)
 
     # ---- CPU baselines (rank 0, N = 1): reference SpMV on the same matrix, 1 thread and all cores

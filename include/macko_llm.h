@@ -16,13 +16,12 @@ extern "C" {
 /* h += delta (if delta != NULL, fp16 residual); out = h * rsqrt(mean(h^2) + eps) * weight (RMSNorm). */
 int macko_llm_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t* weight, uint16_t* out, uint32_t n,
                           float eps, void* stream);
-/* qkv = [q; k; v]: rotary embedding (rotate-half, base theta) of q and k at position *pos; q_out = rotated
- * q; k_cache / v_cache row *pos (heads * head_dim each) = rotated k / v. */
-int macko_llm_rope_kv(const uint16_t* qkv, const int32_t* pos, uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache,
-                      uint32_t heads, uint32_t head_dim, float theta, void* stream);
-/* Multi-head attention of one query over cache rows [0, *pos] (fp32 softmax). */
-int macko_llm_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache, const int32_t* pos,
-                        uint16_t* out, uint32_t heads, uint32_t head_dim, uint32_t max_len, void* stream);
+/* qkv = [q; k; v]: rotary embedding (rotate-half, base theta) of q and k at position *pos, k / v appended
+ * to cache row *pos (heads * head_dim each), then multi-head attention of the rotated q over cache rows
+ * [0, *pos] (fp32 softmax) into out.  One CTA per head. */
+int macko_llm_rope_attention(const uint16_t* qkv, const int32_t* pos, uint16_t* k_cache, uint16_t* v_cache,
+                             uint16_t* out, uint32_t heads, uint32_t head_dim, uint32_t max_len, float theta,
+                             void* stream);
 /* gu = [gate; up]: out = silu(gate) * up. */
 int macko_llm_silu_mul(const uint16_t* gu, uint16_t* out, uint32_t inter, void* stream);
 /* h = table[*token]. */

@@ -61,57 +61,59 @@ __global__ void __launch_bounds__(1024) add_rmsnorm_kernel(uint16_t* h, const ui
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = f2h(h2f(h[i]) * inv * h2f(weight[i]));
 }
 
-// Rotary embedding (rotate-half convention) of q and k at position *pos, k / v appended to the
-// layer's cache row *pos.  qkv = [q; k; v] (3 * heads * head_dim).
-__global__ void rope_kv_kernel(const uint16_t* qkv, const int32_t* pos, uint16_t* q_out, uint16_t* k_cache,
-                               uint16_t* v_cache, uint32_t heads, uint32_t head_dim, float theta) {
-    pdl_enter();
-    const uint32_t H = heads * head_dim, half = head_dim / 2;
-    const int32_t p = *pos;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
-        const uint32_t d = i % head_dim, j = d % half;
-        const float inv_freq = powf(theta, -2.0f * (float)j / (float)head_dim);
-        float s, c;
-        sincosf((float)p * inv_freq, &s, &c);
-        const uint32_t partner = d < half ? i + half : i - half;
-        const float sign = d < half ? -1.0f : 1.0f;  // rotate_half: [-x2, x1]
-        const float q = h2f(qkv[i]), qp = h2f(qkv[partner]);
-        const float k = h2f(qkv[H + i]), kp = h2f(qkv[H + partner]);
-        q_out[i] = f2h(q * c + sign * qp * s);
-        k_cache[(size_t)p * H + i] = f2h(k * c + sign * kp * s);
-        v_cache[(size_t)p * H + i] = qkv[2 * H + i];
-    }
-}
+// Rotary embedding + KV append + attention of one query, fused: a CTA of 8 warps per head rotates
+// its head's q and k at position *pos (rotate-half convention, base theta; the rotation partner
+// d +- head_dim/2 is in the same head), appends k / v to cache row *pos, then attends over rows
+// [0, *pos] (fp32 scores and softmax).  Scores: one thread per position, its K row in 16-byte
+// loads; output: warp w takes positions t = w (mod 8), lane l owns dims [l D, l D + D), D =
+// head_dim / 32, one D-element vector load per row, partial sums combined in shared memory.
+// qkv = [q; k; v] (3 * heads * head_dim).
+constexpr int kAttnWarps = 8;
 
-// One query against positions [0, *pos]: a CTA of 4 warps per head, fp32 scores and softmax.
-// Warp w takes positions t = w (mod 4); lane l owns dims [l D, l D + D) (D = head_dim / 32 <= 8),
-// so every K / V row is read as one coalesced 2 D-byte load per lane.
-constexpr int kAttnWarps = 4;
-
-__global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(const uint16_t* q, const uint16_t* k_cache,
-                                                                    const uint16_t* v_cache, const int32_t* pos,
-                                                                    uint16_t* out, uint32_t heads, uint32_t head_dim,
-                                                                    uint32_t max_len) {
-    extern __shared__ float sm[];  // scores[max_len] | partial outputs [kAttnWarps][head_dim]
+template <int kHeadDim>
+__global__ void __launch_bounds__(kAttnWarps * 32) rope_attention_kernel(const uint16_t* qkv, const int32_t* pos,
+                                                                         uint16_t* k_cache, uint16_t* v_cache,
+                                                                         uint16_t* out, uint32_t heads,
+                                                                         uint32_t max_len, float theta) {
     pdl_enter();
+    constexpr uint32_t D = kHeadDim / 32, half = kHeadDim / 2;
+    extern __shared__ float sm[];  // scores[max_len]
+    __shared__ float part[kAttnWarps][kHeadDim];
+    __shared__ float qs[kHeadDim];
     __shared__ float red[32];
     float* sc = sm;
-    float* part = sm + max_len;
-    const uint32_t h = blockIdx.x, H = heads * head_dim, D = head_dim / 32;
+    const uint32_t h = blockIdx.x, H = heads * kHeadDim;
     const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-    const int32_t n = *pos + 1;
-    float qv[8], acc[8];
-    for (uint32_t i = 0; i < D; ++i) {
-        qv[i] = h2f(q[h * head_dim + l * D + i]);
-        acc[i] = 0.0f;
+    const int32_t p = *pos, n = p + 1;
+    for (uint32_t d = threadIdx.x; d < kHeadDim; d += blockDim.x) {
+        const uint32_t i = h * kHeadDim + d, j = d % half;
+        const float inv_freq = powf(theta, -2.0f * (float)j / (float)kHeadDim);
+        float sn, cs;
+        sincosf((float)p * inv_freq, &sn, &cs);
+        const uint32_t partner = d < half ? i + half : i - half;
+        const float sign = d < half ? -1.0f : 1.0f;  // rotate_half: [-x2, x1]
+        qs[d] = h2f(f2h(h2f(qkv[i]) * cs + sign * h2f(qkv[partner]) * sn));
+        k_cache[(size_t)p * H + i] = f2h(h2f(qkv[H + i]) * cs + sign * h2f(qkv[H + partner]) * sn);
+        v_cache[(size_t)p * H + i] = qkv[2 * H + i];
     }
-    const float scale = rsqrtf((float)head_dim);
-    for (int32_t t = w; t < n; t += kAttnWarps) {
-        const uint16_t* kr = k_cache + (size_t)t * H + h * head_dim + l * D;
+    __syncthreads();
+    const float scale = rsqrtf((float)kHeadDim);
+    for (int32_t t = threadIdx.x; t < n; t += blockDim.x) {
+        const uint4* kr = reinterpret_cast<const uint4*>(k_cache + (size_t)t * H + h * kHeadDim);
+        uint4 kv[kHeadDim / 8];
+#pragma unroll
+        for (uint32_t v = 0; v < kHeadDim / 8; ++v) kv[v] = kr[v];
         float s = 0.0f;
-        for (uint32_t i = 0; i < D; ++i) s += qv[i] * h2f(kr[i]);
-        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (l == 0) sc[t] = s * scale;
+#pragma unroll
+        for (uint32_t v = 0; v < kHeadDim / 8; ++v) {
+            const uint32_t wds[4] = {kv[v].x, kv[v].y, kv[v].z, kv[v].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wds[k]));
+                s += qs[8 * v + 2 * k] * f.x + qs[8 * v + 2 * k + 1] * f.y;
+            }
+        }
+        sc[t] = s * scale;
     }
     __syncthreads();
     float mx = -INFINITY;
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(const uint16
     if (l == 0) red[w] = mx;
     __syncthreads();
     mx = red[0];
+#pragma unroll
     for (int i = 1; i < kAttnWarps; ++i) mx = fmaxf(mx, red[i]);
     __syncthreads();
     float sum = 0.0f;
@@ -129,17 +132,32 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(const uint16
         sum += e;
     }
     sum = block_sum<kAttnWarps * 32>(sum, red);  // (its barriers also publish sc)
+    float acc[D];
+#pragma unroll
+    for (uint32_t i = 0; i < D; ++i) acc[i] = 0.0f;
+#pragma unroll 4
     for (int32_t t = w; t < n; t += kAttnWarps) {
         const float pt = sc[t];
-        const uint16_t* vr = v_cache + (size_t)t * H + h * head_dim + l * D;
-        for (uint32_t i = 0; i < D; ++i) acc[i] += pt * h2f(vr[i]);
+        const uint16_t* vr = v_cache + (size_t)t * H + h * kHeadDim + l * D;
+        uint16_t vv[D];
+        if constexpr (D == 4) {
+            const uint2 q2 = *reinterpret_cast<const uint2*>(vr);
+            vv[0] = (uint16_t)q2.x; vv[1] = (uint16_t)(q2.x >> 16); vv[2] = (uint16_t)q2.y; vv[3] = (uint16_t)(q2.y >> 16);
+        } else {
+#pragma unroll
+            for (uint32_t i = 0; i < D; ++i) vv[i] = vr[i];
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < D; ++i) acc[i] += pt * h2f(vv[i]);
     }
-    for (uint32_t i = 0; i < D; ++i) part[w * head_dim + l * D + i] = acc[i];
+#pragma unroll
+    for (uint32_t i = 0; i < D; ++i) part[w][l * D + i] = acc[i];
     __syncthreads();
-    for (uint32_t d = threadIdx.x; d < head_dim; d += blockDim.x) {
+    for (uint32_t d = threadIdx.x; d < kHeadDim; d += blockDim.x) {
         float o = 0.0f;
-        for (int i = 0; i < kAttnWarps; ++i) o += part[i * head_dim + d];
-        out[h * head_dim + d] = f2h(o / sum);
+#pragma unroll
+        for (int i = 0; i < kAttnWarps; ++i) o += part[i][d];
+        out[h * kHeadDim + d] = f2h(o / sum);
     }
 }
 
@@ -226,19 +244,17 @@ int macko_llm_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t* we
     return launch(add_rmsnorm_kernel, 1, 1024, 0, stream, h, delta, weight, out, n, eps);
 }
 
-int macko_llm_rope_kv(const uint16_t* qkv, const int32_t* pos, uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache,
-                      uint32_t heads, uint32_t head_dim, float theta, void* stream) {
-    const uint32_t H = heads * head_dim;
-    return launch(rope_kv_kernel, grid_for(H, 256), 256, 0, stream, qkv, pos, q_out, k_cache, v_cache, heads, head_dim,
-                  theta);
-}
-
-int macko_llm_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache, const int32_t* pos,
-                        uint16_t* out, uint32_t heads, uint32_t head_dim, uint32_t max_len, void* stream) {
-    if (head_dim % 32 != 0 || head_dim > 256) return (int)cudaErrorInvalidValue;
-    const size_t smem = (max_len + kAttnWarps * head_dim) * sizeof(float);
-    return launch(attention_kernel, (int)heads, kAttnWarps * 32, smem, stream, q, k_cache, v_cache, pos, out, heads,
-                  head_dim, max_len);
+int macko_llm_rope_attention(const uint16_t* qkv, const int32_t* pos, uint16_t* k_cache, uint16_t* v_cache,
+                             uint16_t* out, uint32_t heads, uint32_t head_dim, uint32_t max_len, float theta,
+                             void* stream) {
+    const size_t smem = max_len * sizeof(float);
+    if (head_dim == 128)
+        return launch(rope_attention_kernel<128>, (int)heads, kAttnWarps * 32, smem, stream, qkv, pos, k_cache, v_cache,
+                      out, heads, max_len, theta);
+    if (head_dim == 64)
+        return launch(rope_attention_kernel<64>, (int)heads, kAttnWarps * 32, smem, stream, qkv, pos, k_cache, v_cache,
+                      out, heads, max_len, theta);
+    return (int)cudaErrorInvalidValue;  // head_dim 64 or 128 (Llama)
 }
 
 int macko_llm_silu_mul(const uint16_t* gu, uint16_t* out, uint32_t inter, void* stream) {

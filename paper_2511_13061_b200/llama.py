@@ -8,7 +8,7 @@ norms and the LM head stay dense, as in the paper (the pruner does not touch the
 Both variants use the SAME pruned fp16 weights: the MACKO model compresses exactly the matrices the
 dense model multiplies with cuBLAS (MACKO is lossless), so they differ only by fp32 summation order.
 
-A decode step (per layer: RMSNorm -> qkv -> RoPE + KV append -> attention -> o -> add + RMSNorm ->
+A decode step (per layer: RMSNorm -> qkv -> RoPE + KV append + attention -> o -> add + RMSNorm ->
 gate_up -> SiLU * up -> down, then the final norm, the LM head and greedy argmax) reads its position
 and token from device memory, so one CUDA graph replays token after token.  The per-token kernels
 are libmacko_llm.so (csrc/llm.cu); q/k/v and gate/up are row-stacked into one matrix each (rows are
@@ -41,8 +41,7 @@ def llm_lib() -> C.CDLL:
         vp, u32, i = C.c_void_p, C.c_uint32, C.c_int
         for name, args in {
             "macko_llm_add_rmsnorm": [vp, vp, vp, vp, u32, C.c_float, vp],
-            "macko_llm_rope_kv": [vp, vp, vp, vp, vp, u32, u32, C.c_float, vp],
-            "macko_llm_attention": [vp, vp, vp, vp, vp, u32, u32, u32, vp],
+            "macko_llm_rope_attention": [vp, vp, vp, vp, vp, u32, u32, u32, C.c_float, vp],
             "macko_llm_silu_mul": [vp, vp, u32, vp],
             "macko_llm_embed": [vp, vp, vp, u32, vp],
             "macko_llm_argmax": [vp, u32, vp, vp, vp, u32, vp],
@@ -156,7 +155,7 @@ class LlamaDecoder:
         H, I = cfg.hidden, cfg.inter
         z = lambda n: torch.zeros(n, dtype=torch.float16, device=dev)  # noqa: E731
         self.h, self.x, self.delta = z(H), z(H), z(H)
-        self.qkv, self.q, self.attn = z(3 * H), z(H), z(H)
+        self.qkv, self.attn = z(3 * H), z(H)
         self.gu, self.act, self.logits = z(2 * I), z(I), z(cfg.vocab)
         self.k_cache = torch.zeros((cfg.layers, cfg.max_len, H), dtype=torch.float16, device=dev)
         self.v_cache = torch.zeros_like(self.k_cache)
@@ -191,10 +190,9 @@ class LlamaDecoder:
             _ck(L.macko_llm_add_rmsnorm(p(self.h), p(self.delta) if layer else None, p(nrm["ln1"]), p(self.x), H,
                                         cfg.eps, s), "rmsnorm")
             self._linear(layer, "qkv", self.x, self.qkv, st)
-            _ck(L.macko_llm_rope_kv(p(self.qkv), p(self.pos), p(self.q), p(self.k_cache[layer]),
-                                    p(self.v_cache[layer]), cfg.heads, cfg.head_dim, cfg.theta, s), "rope")
-            _ck(L.macko_llm_attention(p(self.q), p(self.k_cache[layer]), p(self.v_cache[layer]), p(self.pos),
-                                      p(self.attn), cfg.heads, cfg.head_dim, cfg.max_len, s), "attention")
+            _ck(L.macko_llm_rope_attention(p(self.qkv), p(self.pos), p(self.k_cache[layer]), p(self.v_cache[layer]),
+                                           p(self.attn), cfg.heads, cfg.head_dim, cfg.max_len, cfg.theta, s),
+                "rope_attention")
             self._linear(layer, "o", self.attn, self.delta, st)
             _ck(L.macko_llm_add_rmsnorm(p(self.h), p(self.delta), p(nrm["ln2"]), p(self.x), H, cfg.eps, s),
                 "rmsnorm")

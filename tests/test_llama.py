@@ -9,7 +9,7 @@ from paper_2511_13061_b200 import llama as L
 
 pytestmark = pytest.mark.gpu
 
-SMALL = L.LlamaConfig(vocab=1000, hidden=512, layers=3, heads=4, inter=1376, max_len=32)
+SMALL = L.LlamaConfig(vocab=1000, hidden=512, layers=3, heads=4, inter=1376, max_len=32)  # head_dim 128
 
 
 def _forced_logits(dec, tokens):
