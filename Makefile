@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2511_13061_b200
 CSRC := $(PKG)/csrc
-SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu $(CSRC)/convert.cu
+SRCS := $(CSRC)/capi.cu $(CSRC)/spmv.cu $(CSRC)/compress.cu $(CSRC)/generate.cu $(CSRC)/convert.cu $(CSRC)/plan.cu
 HDRS := $(wildcard $(CSRC)/*.cuh) include/macko_cuda.h
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 

@@ -241,6 +241,10 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
  * summation order does not depend on the plan); exposed for tuning and for the grid-independence
  * tests.  Synchronous; not concurrent with SpMVs of the handle. */
 macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_sm, void* stream);
+/* The SpMV work plan (spmv.cuh): launch_info.warps 48-byte warp records and n_split_rows 16-byte
+ * split-row records, copied to host buffers (NULL skips).  Introspection for tests.  Synchronous. */
+macko_status macko_dev_plan_records(const macko_dev_matrix* m, void* recs, uint64_t recs_bytes, void* splits,
+                                    uint64_t splits_bytes, void* stream);
 /* Number of kernels this library has launched in the process (for bench gpu_launches). */
 uint64_t macko_kernel_launches(void);
 

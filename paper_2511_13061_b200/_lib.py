@@ -20,7 +20,7 @@ EXPORTS = (
     "macko_dev_to_dense", "macko_dev_padding_count", "macko_dev_get_info",
     "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_dev_spmm", "macko_spmv_host", "macko_dev_validate", "macko_dev_free",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
-    "macko_dev_launch_info", "macko_dev_configure", "macko_kernel_launches",
+    "macko_dev_launch_info", "macko_dev_plan_records", "macko_dev_configure", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
     "macko_mm_read_dense", "macko_sharded_spmv",
     "macko_dev_set_peers", "macko_dev_set_peer_bank", "macko_wait_flags", "macko_ipc_get_handle", "macko_ipc_open", "macko_ipc_close",
@@ -151,6 +151,8 @@ def load() -> C.CDLL:
     L.macko_mm_read_dense.argtypes = [cp, C.POINTER(u64), C.POINTER(u64), vp]
     L.macko_dev_launch_info.restype = st
     L.macko_dev_launch_info.argtypes = [vp, C.POINTER(LaunchInfo)]
+    L.macko_dev_plan_records.restype = st
+    L.macko_dev_plan_records.argtypes = [vp, vp, u64, vp, u64, vp]
     L.macko_dev_configure.restype = st
     L.macko_dev_configure.argtypes = [vp, i32, i32, vp]
     L.macko_kernel_launches.restype = u64

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -23,6 +24,7 @@
 #include "../../include/macko_cuda.h"
 #include "common.cuh"
 #include "compress.cuh"
+#include "plan.cuh"
 #include "spmv.cuh"
 
 namespace {
@@ -91,6 +93,20 @@ struct DevBuf {
 };
 
 uint64_t align_up(uint64_t n, uint64_t a) { return (n + a - 1) / a * a; }
+
+// MACKO_TIMING=1: host wall time of setup phases (compressor, plan) on stderr.
+struct PhaseTimer {
+    bool on = std::getenv("MACKO_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[macko timing] %-28s %8.3f ms (total %8.3f ms)\n", what,
+                     std::chrono::duration<double, std::milli>(now - last).count(),
+                     std::chrono::duration<double, std::milli>(now - t0).count());
+        last = now;
+    }
+};
 uint64_t values_bytes(uint64_t pad_nnz) { return align_up(pad_nnz * 2, 16); }
 uint64_t delta_bytes(uint64_t pad_nnz, unsigned bits) { return align_up((pad_nnz * bits + 7) / 8, 16); }
 
@@ -174,62 +190,26 @@ void check_bits(uint32_t bits) {
         fail(MACKO_EINVAL, "delta width must be one of 1, 2, 4, 8 bits; got " + std::to_string(bits));
 }
 
-// Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
-void build_plan(macko_dev_matrix* m, cudaStream_t st) {
-    using namespace mk;
-    // Shared memory: fp16 x table with zero guards (every x_mode but 0) + per-warp TMA rings.
-    int optin = 0, per_sm = 0;
-    ck(cudaDeviceGetAttribute(&m->tex_align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
-    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
-    ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
-    // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
-    // the mbarriers)
-    const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
-    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 64;
-    const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunk * m->b_delta / 8);
-    auto x_bytes = [&](int mode) -> size_t {
-        return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
-    };
-    auto ring_for = [&](int mode) -> uint32_t {
-        const size_t xb = x_bytes(mode);
-        if (xb >= budget) return 0;
-        for (uint32_t r = kMaxRing; r >= 2; r /= 2)
-            if (r * per_slot <= budget - xb) return r;
-        return 0;
-    };
-    if (m->force_x_mode >= 0) {
-        m->x_mode = m->force_x_mode;
-    } else {
-        // TEX gathers cost ~1 wavefront per 128-B line a warp gather touches, which grows with the
-        // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
-        // density.  Measured best split (profiles/r01_x_mode_sweep.md, 36864x12288): 4 of 8 slots
-        // by TEX at 0.45 <= d < 0.65 (alternating 4 / 3 at d >= 0.65), 3 at 0.25 <= d < 0.45, 2 below.
-        // At low density the texture gathers need x resident in L1: the unified 256 KB L1/shared
-        // memory keeps what the x table and the rings leave (C = 32768: ~28 KB < 64 KB of x), so
-        // there the shared table alone is faster (131072x32768 @90 %: 51 vs 78 us per 16k-row slab).
-        const double d = (double)m->pad_nnz / ((double)m->rows * (double)m->cols);
-        const size_t smem_all = x_bytes(6) + (size_t)ring_for(6) * per_slot;
-        const bool x_in_l1 = (size_t)per_sm + 24 * 1024 >= smem_all + 2 * m->cols + 16 * 1024;
-        const int split = d >= 0.65 ? 10 : d >= 0.45 ? 7 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
-        m->x_mode = ring_for(split) >= 2 ? split : 0;
+void release_workspaces(macko_dev_matrix* m) {
+    // a re-plan changes the workspace sizes: no launch of the old plan may still be running
+    if (!m->ws_pool.empty()) {
+        ck(cudaDeviceSynchronize(), "re-plan sync");
+        m->ws_of.clear();
+        m->ws_pool.clear();
     }
-    m->smem_budget = budget;
-    m->per_slot = per_slot;
-    m->ring = ring_for(m->x_mode);
-    if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
-    m->ring_offset = x_bytes(m->x_mode);
-    m->smem = m->ring_offset + m->ring * per_slot;
-    ck(spmv_occupancy(m->x_mode, (int)m->b_delta, m->smem, &m->ctas_per_sm), "spmv occupancy");
-    if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
-    if (m->ctas_per_sm < kSpmvCtasPerSm) fail(MACKO_ECUDA, "SpMV CTAs do not fit kSpmvCtasPerSm per SM");
-    m->ctas_per_sm = kSpmvCtasPerSm;  // persistent: 32 warps per SM
-    m->grid = m->sms * m->ctas_per_sm;
-    // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the CTAs (a different plan, same y)
-    if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->grid * m->force_ctas / 4));
-    const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
-    m->n_chunks = W;
-    // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
-    if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
+}
+
+// The plan's reference implementation on the host (MACKO_HOST_PLAN=1; tests compare it with the
+// device builder, plan.cu, record for record).
+void build_plan_host(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
+    using namespace mk;
+    PhaseTimer tm;
+    if (m->h_row_ptrs.size() != m->rows + 1) {
+        m->h_row_ptrs.resize(m->rows + 1);
+        ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (m->rows + 1) * 4, cudaMemcpyDeviceToHost, st),
+           "readback");
+        ck(cudaStreamSynchronize(st), "sync");
+    }
     const uint64_t R = m->rows;
     const std::vector<uint32_t>& rp = m->h_row_ptrs;
 
@@ -306,6 +286,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     }
     const uint32_t S = (uint32_t)split_slot.size();
     m->n_split = S;
+    tm.mark("plan: host unit walk");
     // upload: one 48-byte record per warp, one 16-byte record per split row, counters
     std::vector<mk::WarpPlan> recs(W);
     for (uint32_t k = 0; k < W; ++k) {
@@ -330,12 +311,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
         sp[4 * (size_t)q + 2] = split_pieces[q];
     }
     m->n_slots = slots;
-    // a re-plan changes the workspace sizes: no launch of the old plan may still be running
-    if (!m->ws_pool.empty()) {
-        ck(cudaDeviceSynchronize(), "re-plan sync");
-        m->ws_of.clear();
-        m->ws_pool.clear();
-    }
+    release_workspaces(m);
     m->plan_recs.alloc(recs.size() * sizeof(mk::WarpPlan) / 4);
     m->plan_u32.alloc(sp.size());
     ck(cudaMemcpyAsync(m->plan_recs.p, recs.data(), recs.size() * sizeof(mk::WarpPlan), cudaMemcpyHostToDevice, st),
@@ -350,6 +326,125 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
        "plan colbase");
     g_launches.fetch_add(1);
     ck(cudaStreamSynchronize(st), "plan sync");  // host vectors go out of scope
+    tm.mark("plan (host): upload + colbase + sync");
+}
+
+// The plan built on the device (plan.cu): one readback of the totals.
+void build_plan_device(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
+    using namespace mk;
+    const uint64_t R = m->rows, ub = plan_unit_bound(R, m->pad_nnz);
+    if (ub >= 0xFFFFFFFFull) fail(MACKO_EINVAL, "matrix too large for the u32 unit plan");
+    DevBuf<uint32_t> u32buf;
+    DevBuf<unsigned long long> u64buf;
+    // u32 scratch: nu R | uo R+1 | ku, urow, uj ub | chunk_unit W+1, chunk_row W, chunk_j W | chunk_sid 2W |
+    //              is_split, split_units, first_units, pieces R | sid_of, slot_of R+1
+    const uint64_t n32 = R + (R + 1) + 3 * ub + (W + 1) + 2 * (uint64_t)W + 2 * (uint64_t)W + 4 * R + 2 * (R + 1);
+    u32buf.alloc(n32);
+    u64buf.alloc(R + (R + 1) + 1);
+    PlanTemp t{};
+    uint32_t* q = u32buf.p;
+    auto take = [&](uint64_t n) { uint32_t* p = q; q += n; return p; };
+    t.nu = take(R);
+    t.uo = take(R + 1);
+    t.ku = take(ub);
+    t.urow = take(ub);
+    t.uj = take(ub);
+    t.chunk_unit = take(W + 1);
+    t.chunk_row = take(W);
+    t.chunk_j = take(W);
+    t.chunk_sid = reinterpret_cast<int32_t*>(take(2 * (uint64_t)W));
+    t.is_split = take(R);
+    t.split_units = take(R);
+    t.first_units = take(R);
+    t.pieces = take(R);
+    t.sid_of = take(R + 1);
+    t.slot_of = take(R + 1);
+    t.rw = u64buf.p;
+    t.cw = u64buf.p + R;
+    PlanTotals* d_tot = reinterpret_cast<PlanTotals*>(u64buf.p + R + (R + 1));  // 16 bytes: 2 u64 slots
+    release_workspaces(m);
+    m->plan_recs.alloc((uint64_t)W * sizeof(WarpPlan) / 4);
+    m->plan_u32.alloc(4 * (uint64_t)std::max<uint32_t>(W, 1));
+    ck(plan_build_device(m->row_ptrs.p, (uint32_t)R, (uint32_t)m->pad_nnz, W, ub, m->sms, t,
+                         reinterpret_cast<WarpPlan*>(m->plan_recs.p), reinterpret_cast<uint4*>(m->plan_u32.p), d_tot, st),
+       "plan build");
+    ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<WarpPlan*>(m->plan_recs.p), W, st), "plan colbase");
+    g_launches.fetch_add(13);
+    PlanTotals h{};
+    ck(cudaMemcpyAsync(&h, d_tot, sizeof h, cudaMemcpyDeviceToHost, st), "plan totals");
+    ck(cudaStreamSynchronize(st), "plan sync");  // scratch goes out of scope
+    m->n_units = h.units;
+    m->n_split = h.splits;
+    m->n_slots = h.slots;
+    SpmvPlanDev& P = m->plan;
+    P.warps = reinterpret_cast<const WarpPlan*>(m->plan_recs.p);
+    P.splits = reinterpret_cast<const uint4*>(m->plan_u32.p);
+    P.counters = nullptr;
+    P.partials = nullptr;
+}
+
+// Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
+void build_plan(macko_dev_matrix* m, cudaStream_t st) {
+    using namespace mk;
+    PhaseTimer tm;
+    // Shared memory: fp16 x table with zero guards (every x_mode but 0) + per-warp TMA rings.
+    int optin = 0, per_sm = 0;
+    ck(cudaDeviceGetAttribute(&m->tex_align, cudaDevAttrTextureAlignment, m->device), "texture alignment");
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
+    ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
+    // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
+    // the mbarriers)
+    const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
+    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 64;
+    const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunk * m->b_delta / 8);
+    auto x_bytes = [&](int mode) -> size_t {
+        return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
+    };
+    auto ring_for = [&](int mode) -> uint32_t {
+        const size_t xb = x_bytes(mode);
+        if (xb >= budget) return 0;
+        for (uint32_t r = kMaxRing; r >= 2; r /= 2)
+            if (r * per_slot <= budget - xb) return r;
+        return 0;
+    };
+    if (m->force_x_mode >= 0) {
+        m->x_mode = m->force_x_mode;
+    } else {
+        // TEX gathers cost ~1 wavefront per 128-B line a warp gather touches, which grows with the
+        // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
+        // density.  Measured best split (profiles/r01_x_mode_sweep.md, 36864x12288): 4 of 8 slots
+        // by TEX at 0.45 <= d < 0.65 (alternating 4 / 3 at d >= 0.65), 3 at 0.25 <= d < 0.45, 2 below.
+        // At low density the texture gathers need x resident in L1: the unified 256 KB L1/shared
+        // memory keeps what the x table and the rings leave (C = 32768: ~28 KB < 64 KB of x), so
+        // there the shared table alone is faster (131072x32768 @90 %: 51 vs 78 us per 16k-row slab).
+        const double d = (double)m->pad_nnz / ((double)m->rows * (double)m->cols);
+        const size_t smem_all = x_bytes(6) + (size_t)ring_for(6) * per_slot;
+        const bool x_in_l1 = (size_t)per_sm + 24 * 1024 >= smem_all + 2 * m->cols + 16 * 1024;
+        const int split = d >= 0.65 ? 10 : d >= 0.45 ? 7 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
+        m->x_mode = ring_for(split) >= 2 ? split : 0;
+    }
+    m->smem_budget = budget;
+    m->per_slot = per_slot;
+    m->ring = ring_for(m->x_mode);
+    if (m->ring < 2) fail(MACKO_EINVAL, "x staging mode does not leave room for the TMA rings");
+    m->ring_offset = x_bytes(m->x_mode);
+    m->smem = m->ring_offset + m->ring * per_slot;
+    ck(spmv_occupancy(m->x_mode, (int)m->b_delta, m->smem, &m->ctas_per_sm), "spmv occupancy");
+    if (m->ctas_per_sm < 1) fail(MACKO_ECUDA, "SpMV kernel cannot be resident (shared memory / registers)");
+    if (m->ctas_per_sm < kSpmvCtasPerSm) fail(MACKO_ECUDA, "SpMV CTAs do not fit kSpmvCtasPerSm per SM");
+    m->ctas_per_sm = kSpmvCtasPerSm;  // persistent: 32 warps per SM
+    m->grid = m->sms * m->ctas_per_sm;
+    // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the CTAs (a different plan, same y)
+    if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->grid * m->force_ctas / 4));
+    const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
+    m->n_chunks = W;
+    // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
+    if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
+    if (std::getenv("MACKO_HOST_PLAN"))
+        build_plan_host(m, st, W);
+    else
+        build_plan_device(m, st, W);
+    tm.mark("plan");
 }
 
 void device_validate(macko_dev_matrix* m, cudaStream_t st) {
@@ -708,6 +803,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         if (ld < cols) fail(MACKO_EINVAL, "leading dimension < cols");
         DeviceGuard g(device);
         cudaStream_t st = (cudaStream_t)stream;
+        PhaseTimer tm;
         auto* m = new macko_dev_matrix;
         std::unique_ptr<macko_dev_matrix> hold(m);
         m->device = device;
@@ -729,6 +825,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         unsigned long long pad_nnz = 0;
         ck(cudaMemcpyAsync(&pad_nnz, total.p, 8, cudaMemcpyDeviceToHost, st), "readback");
         ck(cudaStreamSynchronize(st), "sync");
+        tm.mark("alloc + count + scan + sync");
         if (pad_nnz > 0xFFFFFFFFull) fail(MACKO_EINVAL, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
         m->pad_nnz = pad_nnz;
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
@@ -742,10 +839,9 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
                                     m->values.p, reinterpret_cast<uint32_t*>(m->deltas.p), m->sms, st),
                "emit_rows");
         g_launches.fetch_add(1);
-        m->h_row_ptrs.resize(rows + 1);
-        ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
-        ck(cudaStreamSynchronize(st), "sync");
+        tm.mark("alloc + emit launch");
         build_plan(m, st);
+        tm.mark("build_plan");
         *out = hold.release();
     });
 }
@@ -830,9 +926,6 @@ macko_status macko_dev_from_csr(int device, uint64_t rows, uint64_t cols, uint32
             g_launches.fetch_add(2);
             ck(cudaStreamSynchronize(st), "sync");  // codes goes out of scope
         }
-        m->h_row_ptrs.resize(rows + 1);
-        ck(cudaMemcpyAsync(m->h_row_ptrs.data(), m->row_ptrs.p, (rows + 1) * 4, cudaMemcpyDeviceToHost, st), "readback");
-        ck(cudaStreamSynchronize(st), "sync");
         build_plan(m, st);
         *out = hold.release();
     });
@@ -1260,9 +1353,12 @@ macko_status macko_mcko_write_dev(const macko_dev_matrix* m, const char* path, v
         h.rows = m->rows;
         h.cols = m->cols;
         h.pad_nnz = m->pad_nnz;
+        std::vector<uint32_t> rp(m->rows + 1);
+        ck(cudaMemcpyAsync(rp.data(), m->row_ptrs.p, (m->rows + 1) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
         File f(path, "wb");
         write_header(f, h);
-        f.write(m->h_row_ptrs.data(), (m->rows + 1) * 4);
+        f.write(rp.data(), (m->rows + 1) * 4);
         constexpr size_t kBlock = 32u << 20;
         uint8_t* pinned = nullptr;
         ck(cudaMallocHost(&pinned, kBlock), "pinned staging buffer");
@@ -1491,6 +1587,20 @@ macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_s
         m->force_x_mode = x_mode;
         m->force_ctas = ctas_per_sm;
         build_plan(m, (cudaStream_t)stream);
+    });
+}
+
+macko_status macko_dev_plan_records(const macko_dev_matrix* m, void* recs, uint64_t recs_bytes, void* splits,
+                                    uint64_t splits_bytes, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        const uint64_t rb = (uint64_t)m->n_chunks * sizeof(mk::WarpPlan), sb = (uint64_t)m->n_split * 16;
+        if ((recs && recs_bytes < rb) || (splits && splits_bytes < sb)) fail(MACKO_EINVAL, "buffer too small");
+        DeviceGuard g(m->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        if (recs && rb) ck(cudaMemcpyAsync(recs, m->plan_recs.p, rb, cudaMemcpyDeviceToHost, st), "D2H");
+        if (splits && sb) ck(cudaMemcpyAsync(splits, m->plan_u32.p, sb, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
     });
 }
 

@@ -194,6 +194,15 @@ class DeviceMatrix:
         check(_lib.load().macko_dev_launch_info(self._h, C.byref(li)))
         return li
 
+    def plan_records(self):
+        """(warp records as an (W, 12) uint32 array, split records as (S, 4) uint32) — introspection."""
+        li = self.launch_info()
+        recs = np.zeros((li.warps, 12), np.uint32)
+        splits = np.zeros((max(li.n_split_rows, 1), 4), np.uint32)
+        check(_lib.load().macko_dev_plan_records(self._h, recs.ctypes.data, recs.nbytes, splits.ctypes.data,
+                                                 splits.nbytes, None))
+        return recs, splits[: li.n_split_rows]
+
     def configure(self, x_mode: int = -1, ctas_per_sm: int = 0, stream=None) -> None:
         """Re-plan the launch (x_mode: -1 auto, 0 texture only, 1 shared table only, 6 / 7 / 8 / 10
         split; CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""

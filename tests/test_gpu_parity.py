@@ -621,3 +621,34 @@ def test_spmm_errors(cuda):
     dm2 = gpu_encode(A, 2)
     with pytest.raises(ValueError, match="b_delta"):
         dm2.spmm_into(X[:2], torch.zeros((2, 64), dtype=torch.float16, device=cuda))
+
+
+# ------------------------------------------------------------------------------ the plan on the device
+def test_device_plan_equals_host_plan(cuda, monkeypatch):
+    # plan.cu builds the SpMV work plan on the GPU; the host builder (MACKO_HOST_PLAN=1) is its
+    # reference: identical warp records (unit ranges, TMA element ranges, column bases, split ids)
+    # and split records, on row-length mixes that exercise every case
+    rng = np.random.default_rng(5)
+    cases = [O.gen_dense(36, 65536, 0.5, 1), O.gen_dense(1000, 16000, 0.5, 2), O.gen_dense(4096, 64, 0.5, 3),
+             O.gen_dense(7, 37, 0.5, 4), O.gen_dense(2000, 3000, 0.02, 5)]
+    z = O.gen_dense(3000, 9000, 0.4, 6)
+    z[rng.random(3000) < 0.5] = 0  # many empty rows
+    cases.append(z)
+    for A in cases:
+        monkeypatch.setenv("MACKO_HOST_PLAN", "1")
+        dh = gpu_encode(A)
+        monkeypatch.delenv("MACKO_HOST_PLAN")
+        dd = gpu_encode(A)
+        for ctas in (0, 1):
+            if ctas:
+                monkeypatch.setenv("MACKO_HOST_PLAN", "1")
+                dh.configure(-1, 1)
+                monkeypatch.delenv("MACKO_HOST_PLAN")
+                dd.configure(-1, 1)
+            rh, sh = dh.plan_records()
+            rd, sd = dd.plan_records()
+            assert dh.launch_info().n_units == dd.launch_info().n_units
+            assert np.array_equal(rh, rd), (A.shape, ctas)
+            assert np.array_equal(sh, sd), (A.shape, ctas)
+        x = O.gen_vector(A.shape[1], 7)
+        assert np.array_equal(gpu_spmv(dd, x), b200_y(O.encode_dense(A), x))

@@ -10,7 +10,7 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 OUT=build/variants/$NAME
 mkdir -p "$OUT"
-for f in capi spmv compress generate convert; do
+for f in capi spmv compress generate convert plan; do
   $NVCC $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $FLAGS \
     -c paper_2511_13061_b200/csrc/$f.cu -o "$OUT/$f.o" 2> "$OUT/$f.ptxas.log" &
 done
