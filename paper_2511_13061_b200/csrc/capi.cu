@@ -340,7 +340,7 @@ void build_plan_device(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
     //              is_split, split_units, first_units, pieces R | sid_of, slot_of R+1
     const uint64_t n32 = R + (R + 1) + 3 * ub + (W + 1) + 2 * (uint64_t)W + 2 * (uint64_t)W + 4 * R + 2 * (R + 1);
     u32buf.alloc(n32);
-    u64buf.alloc(R + (R + 1) + 1);
+    u64buf.alloc(R + (R + 1) + 2);  // rw | cw | PlanTotals (16 bytes)
     PlanTemp t{};
     uint32_t* q = u32buf.p;
     auto take = [&](uint64_t n) { uint32_t* p = q; q += n; return p; };
