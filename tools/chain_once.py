@@ -14,14 +14,10 @@ p = argparse.ArgumentParser()
 p.add_argument("--layers", type=int, default=32)
 p.add_argument("--tokens", type=int, default=2)
 p.add_argument("--pdl", type=int, default=1)
-p.add_argument("--persistent", type=int, default=0, help="1: one persistent cooperative kernel per token")
 a = p.parse_args()
 ch = D.SparseDecoderChain(D.ChainShape(a.layers, 4096, 11008), density=0.5)
 M.gen_vector(ch.acts["h"], 4096, seed=1)
 for _ in range(a.tokens):
-    if a.persistent:
-        ch.forward_token_persistent()
-    else:
-        ch.forward_token(pdl=bool(a.pdl))
+    ch.forward_token(pdl=bool(a.pdl))
 torch.cuda.synchronize()
 print("ok")

@@ -18,7 +18,6 @@ p.add_argument("--modes", default="-1")
 p.add_argument("--flush", type=int, default=1)
 p.add_argument("--n", type=int, default=40)
 p.add_argument("--bits", type=int, default=4)
-p.add_argument("--orders", default="1,0")
 a = p.parse_args()
 R, C = a.rows, a.cols
 dense = torch.empty((R, C), dtype=torch.float16, device="cuda")
@@ -30,8 +29,7 @@ M.gen_vector(x, C, seed=4321)
 y = torch.empty(R, dtype=torch.float16, device="cuda")
 st = torch.cuda.current_stream()
 flush = torch.ones(256 << 20, dtype=torch.float32, device="cuda")
-for order, mode in [(int(o), int(m)) for o in a.orders.split(",") for m in a.modes.split(",")]:
-    dm.set_order(order)
+for mode in [int(m) for m in a.modes.split(",")]:
     dm.configure(mode)
     for _ in range(3):
         dm.spmv_into(x, y, st)
@@ -45,5 +43,5 @@ for order, mode in [(int(o), int(m)) for o in a.orders.split(",") for m in a.mod
         e1.record(st)
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
-    print(f"order {order} b{a.bits} d={a.density} mode {dm.launch_info().x_in_smem:2d} flush {a.flush}: median {statistics.median(ts):7.2f} us  min {min(ts):7.2f}  "
+    print(f"b{a.bits} d={a.density} mode {dm.launch_info().x_in_smem:2d} flush {a.flush}: median {statistics.median(ts):7.2f} us  min {min(ts):7.2f}  "
           f"GB/s {dm.traffic_bytes / statistics.median(ts) / 1e3:7.1f}")
