@@ -158,6 +158,9 @@ __device__ __forceinline__ Dec8 decode8(uint32_t w0, uint32_t w1) {
 template <int kXMode, bool kMasked, uint32_t kTex = tex_slots<kXMode>(), class D>
 __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& dc, int cb, uint32_t xs_addr,
                                            cudaTextureObject_t xt, uint32_t vm) {
+#ifdef MACKO_EXP_NO_GATHER  // experiment builds only (tools/build_variant.sh): the walk without x gathers
+    return acc + __int_as_float((int)((v.x ^ v.w ^ (uint32_t)cb) & 0x3FFu));
+#endif
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     // shared address of column cb: per element one PRMT (offset extract) + one IADD3
     uint32_t base = xs_addr + 2u * (uint32_t)cb;
