@@ -57,7 +57,9 @@ def parse():
     p.add_argument("--strong", action="store_true", help="config 5 strong scaling also at N = 1")
     p.add_argument("--chain-tokens", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--soak-s", type=float, default=1.0, help="untimed load before timing (clock sampling)")
+    p.add_argument("--soak-s", type=float, default=0.0, help="untimed back-to-back SpMVs before the timed steps")
+    p.add_argument("--sustain-s", type=float, default=1.5,
+                   help="then this long back-to-back and the K steps again under the settled power-cap clocks (0: skip)")
     p.add_argument("--x-mode", type=int, default=-1, help="x gathers: -1 auto, 0 texture, 1 smem table, 6/7/8/10 split")
     p.add_argument("--ctas", type=int, default=0, help="cap on SpMV CTAs (k/4 of the persistent grid, 0 = all)")
     p.add_argument("--fused", action="store_true", help="N > 1: also the chain with the all-gather fused into the SpMV")
@@ -120,48 +122,81 @@ def cpu_model():
 
 
 # ---------------------------------------------------------------------------------- clocks
+_NVML_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    t = time.time()
+    try:
+        c = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:
+        c = -1
+    try:
+        r = int(reasons(h))
+    except Exception:
+        r = -1
+    try:
+        w = pynvml.nvmlDeviceGetPowerUsage(h) / 1e3
+    except Exception:
+        w = -1.0
+    print(f"{t:.6f} {c} {r} {w:.1f}", flush=True)
+    time.sleep(0.001)
+"""
+
+
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu,power.draw")
+    """SM clock, throttle reasons and power of one GPU, sampled every ~1 ms by a separate process
+    (NVML; no GIL shared with the launching thread).  `mark()` brackets a timed region with
+    wall-clock stamps; `summary()` keeps the samples inside it."""
+    REASON_BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+                   0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
-        self.index = index
         self.proc = None
-
-    def start(self):
+        self.sm_max = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()  # ready: NVML initialised
+            self.sm_max = float(first[1]) if len(first) == 2 and first[0] == "max" else None
         except Exception:
             self.proc = None
+        self.lines = []
 
-    def stop(self):
+    def collect(self):
+        """Stop the sampler; returns the samples (t, sm_mhz, reasons, watts)."""
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return []
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except Exception:
             self.proc.kill()
             out = ""
+        self.proc = None
         rows = []
-        for line in out.strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6]), float(parts[7])))
-            except ValueError:
-                continue
+        for line in out.splitlines():
+            parts = line.split()
+            if len(parts) == 4:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), int(parts[2]), float(parts[3])))
+                except ValueError:
+                    pass
+        self.lines = rows
+        return rows
+
+    def summary(self, t0: float, t1: float):
+        rows = [r for r in self.lines if t0 <= r[0] <= t1 and r[1] > 0]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        loaded = [r for r in rows if r[3] > 0] or rows
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
-                "power_w_median": statistics.median(r[4] for r in loaded)}
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["no samples"], "source": "nvml"}
+        reasons = sorted({n for r in rows if r[2] >= 0 for b, n in self.REASON_BITS.items() if r[2] & b})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.sm_max,
+                "sm_mhz_min": min(r[1] for r in rows), "reasons": reasons, "samples": len(rows),
+                "power_w_median": round(statistics.median(r[3] for r in rows), 1),
+                "source": "nvml every ~1 ms (separate process) during the timed steps"}
 
 
 # ---------------------------------------------------------------------------------- reference arm
@@ -377,40 +412,59 @@ def main():
     del dense
     torch.cuda.empty_cache()
 
-    # ---- warmup + soak (clock sampling covers soak + timed region)
-    sampler = ClockSampler(local)
-    if rank == 0:
-        sampler.start()
+    # ---- warmup, then the timed region: exactly K steps, per-step device events around the step
+    # only, clocks sampled during it (rank 0's GPU)
+    sampler = ClockSampler(local) if rank == 0 else None
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    t_end = time.time() + args.soak_s
-    while time.time() < t_end:
-        for _ in range(20):
-            dm.spmv_into(x, y, stream)
-        torch.cuda.synchronize()
 
-    # ---- timed region: exactly K steps, per-step device events around the step only
+    def soak(seconds):
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            for _ in range(20):
+                dm.spmv_into(x, y, stream)
+            torch.cuda.synchronize()
+
+    def timed_steps():
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        for i in range(args.steps):
+            if need_flush:
+                timer.flush()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if world > 1:
+            dist.barrier()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        mean, med = allmax(torch, dist, dev, [sum(step_ms) / len(step_ms), statistics.median(step_ms)])
+        return mean, med, (t0, t1)
+
+    soak(args.soak_s)
     launches0 = M.kernel_launches()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        if need_flush:
-            timer.flush()
-        evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms_mean, ms_med, clocks = timed_steps()
     launches = M.kernel_launches() - launches0
-    clocks = sampler.stop() if rank == 0 else None
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms_mean, ms_med = allmax(torch, dist, dev, [sum(step_ms) / len(step_ms), statistics.median(step_ms)])
     total_bytes = bytes_rank * world
     value = total_bytes / (ms_mean * 1e-3) / 1e9
+    # the same K steps again once the power cap has settled the clocks (back-to-back SpMVs for
+    # --sustain-s first): what a long stream of SpMVs sustains
+    sustained = None
+    if args.sustain_s > 0:
+        soak(args.sustain_s)
+        s_mean, s_med, s_win = timed_steps()
+        sustained = {"value": round(total_bytes / (s_mean * 1e-3) / 1e9, 2), "ms_per_step": round(s_mean, 5),
+                     "us_per_step_median": round(s_med * 1e3, 2), "after_soak_s": args.sustain_s}
+    if sampler is not None:
+        sampler.collect()
+        clocks = sampler.summary(*clocks)
+        if sustained is not None:
+            sustained["clocks"] = sampler.summary(*s_win)
 
     # ---- kernel-only roofline of the dominant kernel (the rank's SpMV)
     kern_ms = ms_mean
@@ -488,7 +542,8 @@ def main():
             "timing": {"l2": ("flushed before every step (sum over a 2xL2 buffer, outside the step events)" if need_flush
                               else f"not flushed: inputs larger than L2 ({bytes_rank / 2**20:.0f} MiB per step vs "
                                    f"{l2 / 2**20:.0f} MiB L2; ncu: L2 hit rate < 1 % back to back)"),
-                       "soak_s": args.soak_s, "events": "CUDA events on the launching stream, max over ranks"},
+                       "soak_s": args.soak_s, "events": "CUDA events on the launching stream, max over ranks",
+                       "clocks": "sampled during the K timed steps only"},
             "matrix": {"pad_nnz_per_rank": pad_nnz, "bytes_per_spmv_per_rank": bytes_rank, "grid": li.grid,
                        "block": li.block, "x_mode": li.x_in_smem, "split_rows": li.n_split_rows},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -503,6 +558,7 @@ def main():
             "compress_s": round(compress_s, 4), "compress_warm_s": round(compress_warm_s, 4),
             "gpu_launches": launches,
             "clocks": clocks,
+            "sustained": sustained,
             "cpu_baseline": cpu,
         }
         if coll_us is not None:

@@ -412,15 +412,17 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     } else {
         // TEX gathers cost ~1 wavefront per 128-B line a warp gather touches, which grows with the
         // column spread of a step (~256/d columns); LDS gathers cost ~3.3 bank wavefronts at any
-        // density.  Measured best split (profiles/r01_x_mode_sweep.md, 36864x12288): 4 of 8 slots
-        // by TEX at 0.45 <= d < 0.65 (alternating 4 / 3 at d >= 0.65), 3 at 0.25 <= d < 0.45, 2 below.
+        // density.  Measured best split (profiles/r01_x_mode_sweep.md, re-measured in
+        // profiles/r02_experiments.md after the IDP.4A addressing, 36864x12288): 4 / 3 of 8 slots
+        // by TEX alternating between the two steps of a pair at d >= 0.45, 3 at 0.25 <= d < 0.45,
+        // 2 below.
         // At low density the texture gathers need x resident in L1: the unified 256 KB L1/shared
         // memory keeps what the x table and the rings leave (C = 32768: ~28 KB < 64 KB of x), so
         // there the shared table alone is faster (131072x32768 @90 %: 51 vs 78 us per 16k-row slab).
         const double d = (double)m->pad_nnz / ((double)m->rows * (double)m->cols);
         const size_t smem_all = x_bytes(6) + (size_t)ring_for(6) * per_slot;
         const bool x_in_l1 = (size_t)per_sm + 24 * 1024 >= smem_all + 2 * m->cols + 16 * 1024;
-        const int split = d >= 0.65 ? 10 : d >= 0.45 ? 7 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
+        const int split = d >= 0.45 ? 10 : d >= 0.25 ? 6 : x_in_l1 ? 8 : 1;
         m->x_mode = ring_for(split) >= 2 ? split : 0;
     }
     m->smem_budget = budget;

@@ -151,6 +151,22 @@ __device__ __forceinline__ Dec8 decode8(uint32_t w0, uint32_t w1) {
     return r;
 }
 
+#ifdef MACKO_OPAQUE_SEL
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    asm("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+#else
+__device__ __forceinline__ uint32_t opaque(uint32_t v) { return v; }
+#endif
+
+// c + (byte-wise dot product of a and sel): with one non-zero selector byte, c + k * byte m of a.
+__device__ __forceinline__ uint32_t dp4a_sel(uint32_t a, uint32_t sel, uint32_t c) {
+    uint32_t d;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(sel), "r"(c));
+    return d;
+}
+
 // 8 gathers + FHFMAs of one lane step.  cb = column before the lane's first element.  Masked
 // steps (row edges): element m gathers and accumulates only if bit m of vm is set (predicated
 // gather and FHFMA), so nothing outside the row reaches the sum, not even 0 * inf.  Skipping
@@ -165,11 +181,28 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
     // shared address of column cb: per element one PRMT (offset extract) + one IADD3
     uint32_t base = xs_addr + 2u * (uint32_t)cb;
     asm("mov.b32 %0, %0;" : "+r"(base));  // opaque: keeps base + 2b a single IADD3 per element
+    uint32_t even2 = 0;
+    if constexpr (!std::is_same<D, Dec8>::value && (kTex & 0x55u) != 0x55u) even2 = dc.even * 2u;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         uint16_t v0, v1;
         split_halves(w[m], v0, v1);
         uint32_t b0, b1;
+#ifndef MACKO_NO_DP4A
+        if constexpr (!std::is_same<D, Dec8>::value) {
+            // one IDP.4A per element: the byte-m prefix times 1 (TEX coordinate) or 2 (shared
+            // address) plus the base, instead of a PRMT extract and an add
+            // Even elements gather from shared memory in every x_mode but 0: their offsets are
+            // pre-doubled (2 x 112 < 256), so they share the TEX elements' selectors.
+            const bool t0 = (kTex >> (2 * m)) & 1u, t1 = (kTex >> (2 * m + 1)) & 1u;
+            const uint32_t a0 = t0 ? dp4a_sel(dc.even, opaque(1u << (8 * m)), (uint32_t)cb)
+                                   : dp4a_sel(even2, opaque(1u << (8 * m)), base);
+            const uint32_t a1 = dp4a_sel(dc.odd, opaque((t1 ? 1u : 2u) << (8 * m)), t1 ? (uint32_t)cb : base);
+            if (!kMasked || ((vm >> (2 * m)) & 1u)) acc = fma_f16f16f32(v0, t0 ? xtex(xt, (int)a0) : lds_u16(a0), acc);
+            if (!kMasked || ((vm >> (2 * m + 1)) & 1u)) acc = fma_f16f16f32(v1, t1 ? xtex(xt, (int)a1) : lds_u16(a1), acc);
+            continue;
+        }
+#endif
         if constexpr (std::is_same<D, Dec8>::value) {
             b0 = __byte_perm(dc.p[m], 0u, 0x4410u);
             b1 = __byte_perm(dc.p[m], 0u, 0x4432u);
@@ -504,13 +537,15 @@ struct Slot {
     uint32_t d, d2;  // the lane's 8 codewords (d2: elements 4..7 when b_delta = 8)
 };
 
+// The lane's 8 elements at ring position 8 q (q: ring position in 8-element groups; 16 value
+// bytes and kBits delta bytes per group).
 template <int kBits>
-__device__ __forceinline__ Slot lds_slot(uint32_t vbase, uint32_t dbase, uint32_t rel) {
+__device__ __forceinline__ Slot lds_slot(uint32_t vbase, uint32_t dbase, uint32_t q) {
     Slot sl;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(sl.v.x), "=r"(sl.v.y), "=r"(sl.v.z), "=r"(sl.v.w)
-                 : "r"(vbase + 2u * rel));
-    const uint32_t da = dbase + (rel / 8u) * kBits;
+                 : "r"(vbase + 16u * q));
+    const uint32_t da = dbase + q * kBits;
     sl.d2 = 0;
     if constexpr (kBits == 8) {
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(sl.d), "=r"(sl.d2) : "r"(da));
@@ -664,12 +699,13 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         if (!next_piece(rs, a, w, lane)) return;
     }
     // loop invariants pinned in registers (not re-derived from the CTA's shared window per pair)
-    uint32_t xs_addr, vbase, dbase, lane_rel, emask;
+    // (ring positions in 8-element groups: the lane's group of a step at S is (S / 8 + lane_q) & qmask)
+    uint32_t xs_addr, vbase, dbase, lane_q, qmask;
     asm volatile("mov.b32 %0, %1;" : "=r"(xs_addr) : "r"(xs_addr_in));
     asm volatile("mov.b32 %0, %1;" : "=r"(vbase) : "r"(g.vbase));
     asm volatile("mov.b32 %0, %1;" : "=r"(dbase) : "r"(g.dbase));
-    asm volatile("mov.b32 %0, %1;" : "=r"(lane_rel) : "r"(g.lane_rel));
-    asm volatile("mov.b32 %0, %1;" : "=r"(emask) : "r"(g.emask));
+    asm volatile("mov.b32 %0, %1;" : "=r"(lane_q) : "r"(g.lane_rel / 8u));
+    asm volatile("mov.b32 %0, %1;" : "=r"(qmask) : "r"(g.emask / 8u));
     uint32_t ev = ring_ev(g);
 
     // One step pair (steps t, t+1 of the current row).  Masked pairs: the row's first pair
@@ -681,10 +717,10 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
             ring_advance<kBits>(g, a, S, ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts);
             ev = ring_ev(g);
         }
-        const uint32_t relA = (S + lane_rel) & emask;
-        const uint32_t relB = (relA + kStepElts) & emask;
-        Slot A = lds_slot<kBits>(vbase, dbase, relA);
-        Slot B = lds_slot<kBits>(vbase, dbase, relB);
+        const uint32_t qA = ((rs.al >> 3) + t * (kStepElts / 8u) + lane_q) & qmask;  // S is 8-aligned
+        const uint32_t qB = (qA + kStepElts / 8u) & qmask;
+        Slot A = lds_slot<kBits>(vbase, dbase, qA);
+        Slot B = lds_slot<kBits>(vbase, dbase, qB);
         uint32_t vmA = 0xFFu, vmB = 0xFFu;
         if constexpr (kMasked) {
             const uint32_t eb = S + 8u * lane;

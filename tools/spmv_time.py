@@ -92,9 +92,11 @@ for spec in a.shapes.split(","):
     th.join()
     us = [e0.elapsed_time(e1) * 1e3 for e0, e1 in ts]
     med = statistics.median(us)
+    # back-to-back launches (no flush): the mean over the whole run resolves below the event tick
+    mean = ts[0][0].elapsed_time(ts[-1][1]) * 1e3 / a.n if not need_flush else float("nan")
     mhz = statistics.median(clocks) if clocks else float("nan")
     li = dm.launch_info()
     print(f"{a.tag:40s} {R}x{C}@{d}: {med:8.2f} us  {dm.traffic_bytes / med / 1e3:7.1f} GB/s  "
-          f"sm {mhz:6.0f} MHz  {med * mhz / 1e3:7.1f} kcyc  x_mode {li.x_in_smem} y {ok}", flush=True)
+          f"sm {mhz:6.0f} MHz  {med * mhz / 1e3:7.1f} kcyc  mean {mean:8.2f} us  x_mode {li.x_in_smem} y {ok}", flush=True)
     dm.close()
     torch.cuda.empty_cache()
