@@ -403,9 +403,7 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     auto ring_for = [&](int mode) -> uint32_t {
         const size_t xb = x_bytes(mode);
         if (xb >= budget) return 0;
-        for (uint32_t r = kMaxRing; r >= 2; r /= 2)
-            if (r * per_slot <= budget - xb) return r;
-        return 0;
+        return kMaxRing * per_slot <= budget - xb ? kMaxRing : 0u;  // the kernel's compile-time ring
     };
     if (m->force_x_mode >= 0) {
         m->x_mode = m->force_x_mode;
@@ -1182,13 +1180,13 @@ macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint
         a.cols = (uint32_t)m->cols;
         a.value_elems = m->values.n;
         a.delta_bytes = m->deltas.n;
-        a.ring = 2;
+        a.ring = mk::kMaxRing;
         a.ring_offset = mode == 7 ? (uint32_t)table : 0u;
         a.plan = m->plan;
         a.plan.counters = w->counters.p;
         a.plan.partials = w->partials.p;
         a.value_count = (uint32_t)m->pad_nnz;
-        const size_t smem = (mode == 7 ? table : 0) + 2 * m->per_slot;
+        const size_t smem = (mode == 7 ? table : 0) + mk::kMaxRing * m->per_slot;
         ck(mk::launch_spmm(a, (int)kb, m->grid, mode, smem, st), "macko_spmm launch");
         g_launches.fetch_add(2);
     });

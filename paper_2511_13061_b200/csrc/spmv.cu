@@ -160,6 +160,15 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 __device__ __forceinline__ uint32_t opaque(uint32_t v) { return v; }
 #endif
 
+#ifdef MACKO_CONST_SEL
+// dp4a byte selectors k << 8m (k = 1, 2) in the constant bank, so IDP.4A reads them as c[3][...]
+// operands instead of re-materialising uniform registers every step pair.
+__constant__ uint32_t c_sel[2][4] = {{1u, 1u << 8, 1u << 16, 1u << 24}, {2u, 2u << 8, 2u << 16, 2u << 24}};
+#define MK_SEL(k, m) c_sel[(k) - 1][m]
+#else
+#define MK_SEL(k, m) opaque((uint32_t)(k) << (8 * (m)))
+#endif
+
 // c + (byte-wise dot product of a and sel): with one non-zero selector byte, c + k * byte m of a.
 __device__ __forceinline__ uint32_t dp4a_sel(uint32_t a, uint32_t sel, uint32_t c) {
     uint32_t d;
@@ -195,9 +204,8 @@ __device__ __forceinline__ float lane_step(float acc, const uint4& v, const D& d
             // Even elements gather from shared memory in every x_mode but 0: their offsets are
             // pre-doubled (2 x 112 < 256), so they share the TEX elements' selectors.
             const bool t0 = (kTex >> (2 * m)) & 1u, t1 = (kTex >> (2 * m + 1)) & 1u;
-            const uint32_t a0 = t0 ? dp4a_sel(dc.even, opaque(1u << (8 * m)), (uint32_t)cb)
-                                   : dp4a_sel(even2, opaque(1u << (8 * m)), base);
-            const uint32_t a1 = dp4a_sel(dc.odd, opaque((t1 ? 1u : 2u) << (8 * m)), t1 ? (uint32_t)cb : base);
+            const uint32_t a0 = t0 ? dp4a_sel(dc.even, MK_SEL(1, m), (uint32_t)cb) : dp4a_sel(even2, MK_SEL(1, m), base);
+            const uint32_t a1 = dp4a_sel(dc.odd, MK_SEL(t1 ? 1 : 2, m), t1 ? (uint32_t)cb : base);
             if (!kMasked || ((vm >> (2 * m)) & 1u)) acc = fma_f16f16f32(v0, t0 ? xtex(xt, (int)a0) : lds_u16(a0), acc);
             if (!kMasked || ((vm >> (2 * m + 1)) & 1u)) acc = fma_f16f16f32(v1, t1 ? xtex(xt, (int)a1) : lds_u16(a1), acc);
             continue;
@@ -477,6 +485,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // only grows, by at most one step pair per pair, so at most one chunk is released per pair.
 constexpr uint32_t kNever = 0xFFFFFFFFu;
 
+// Edge step pairs (run_rows): which steps are masked, and whether the pair is a single step.
+constexpr uint32_t kEdgeMaskA = 1u, kEdgeMaskB = 2u, kEdgeSingle = 4u;
+
 struct Ring {
     uint32_t vbase, dbase, bar0;  // this warp's value ring, delta ring, first mbarrier (smem)
     uint32_t e0;                  // first element of the warp's chunk stream (chunk aligned)
@@ -486,8 +497,9 @@ struct Ring {
     uint32_t released;            // chunks consumed and refilled (or nothing left to refill)
     uint32_t landed;              // chunks waited for
     uint32_t rel_at, wait_at;     // S thresholds of the next release / the next wait (kNever: none)
-    uint32_t rshift;              // log2(ring)
+#ifdef MACKO_L2_HINT
     uint64_t policy;              // L2 evict_first (the matrix streams once per SpMV)
+#endif
 };
 
 __device__ __forceinline__ uint32_t ring_ev(const Ring& g) { return min(g.rel_at, g.wait_at); }
@@ -497,11 +509,13 @@ __device__ __forceinline__ uint32_t ring_ev(const Ring& g) { return min(g.rel_at
 // warp-uniform operands: elect.sync inside the asm keeps the copies to one lane without a
 // divergent branch around them.
 template <int kBits>
-__device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, uint32_t ring) {
+__device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a) {
+    constexpr uint32_t ring = kMaxRing;
     const uint32_t slot = g.released & (ring - 1u);
     const uint32_t e = g.e0 + (g.released + ring) * kChunk;
     const uint32_t bar = g.bar0 + 8u * slot;
     // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
+#ifdef MACKO_L2_HINT
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
@@ -512,6 +526,37 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, uin
         "l"(a.values + e), "r"(g.dbase + slot * dbytes<kBits>()), "l"(a.deltas + (size_t)(e / 8u) * kBits), "r"(bar),
         "l"(g.policy), "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
         : "memory");
+#else
+    // No L2 eviction hint: the policy operand costs two uniform-register moves per copy and two
+    // live registers in the walk, and the streamed matrix does not displace anything the SpMV
+    // re-reads (x is staged once per CTA, the plan record once per warp).
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %5;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %6, [%4];\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %7, [%4];\n\t}" ::"r"(
+            g.vbase + slot * kChunkVBytes),
+        "l"(a.values + e), "r"(g.dbase + slot * dbytes<kBits>()), "l"(a.deltas + (size_t)(e / 8u) * kBits), "r"(bar),
+        "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
+        : "memory");
+#endif
+}
+
+#ifndef MACKO_L2_PREFETCH
+#define MACKO_L2_PREFETCH 0
+#endif
+// cp.async.bulk.prefetch.L2 of chunk c of the warp's stream (values + codewords; one lane).
+template <int kBits>
+__device__ __forceinline__ void l2_prefetch_chunk(const Ring& g, const SpmvArgs& a, uint32_t c) {
+    const uint32_t e = g.e0 + c * kChunk;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.prefetch.L2.global [%0], %2;\n\t"
+        "@p cp.async.bulk.prefetch.L2.global [%1], %3;\n\t}" ::"l"(a.values + e),
+        "l"(a.deltas + (size_t)(e / 8u) * kBits), "n"(kChunkVBytes), "n"(dbytes<kBits>())
+        : "memory");
 }
 
 // The walk reached S (slow path, S >= ring_ev): release the chunk the walk has left (every lane's
@@ -519,16 +564,21 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a, uin
 // chunks holding [S, S + span) have landed.
 template <int kBits>
 __device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_t S, uint32_t span) {
-    const uint32_t ring = a.ring;
+    constexpr uint32_t ring = kMaxRing;
     if (S >= g.rel_at) {
         __syncwarp();
-        ring_issue<kBits>(g, a, ring);
+        ring_issue<kBits>(g, a);
+#if MACKO_L2_PREFETCH > 0
+        // L2 prefetch of the chunk MACKO_L2_PREFETCH past the refill: its refill then waits on an
+        // L2 hit instead of an HBM round trip (the ring alone keeps only one chunk ahead)
+        if (g.released + ring + MACKO_L2_PREFETCH < g.n_chunks) l2_prefetch_chunk<kBits>(g, a, g.released + ring + MACKO_L2_PREFETCH);
+#endif
         ++g.released;
         g.rel_at = g.released + ring < g.n_chunks ? g.e0 + (g.released + 1u) * kChunk : kNever;
     }
     const uint32_t need = min(g.n_chunks, (S + span - 1u - g.e0) / kChunk + 1u);
     for (; g.landed < need; ++g.landed)
-        mbar_wait(g.bar0 + 8u * (g.landed & (ring - 1u)), (g.landed >> g.rshift) & 1u);
+        mbar_wait(g.bar0 + 8u * (g.landed & (ring - 1u)), (g.landed / ring) & 1u);
     g.wait_at = g.landed < g.n_chunks ? g.e0 + g.landed * kChunk - (2u * kStepElts - 1u) : kNever;
 }
 
@@ -590,29 +640,45 @@ __device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w)
     return PlanRecord{__ldg(rec), __ldg(rec + 1), __ldg(rec + 2)};
 }
 
+// One bulk global -> shared copy completing on mbarrier bar (one lane).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, const Ring& g) {
+#ifdef MACKO_L2_HINT
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar), "l"(g.policy)
+                 : "memory");
+#else
+    (void)g;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst), "l"(src),
+                 "r"(bytes), "r"(bar)
+                 : "memory");
+#endif
+}
+
 // Ring set-up for the warp's element stream [E0, E1): the barriers are initialised and the first
 // fill is one copy per array.
 template <int kBits>
 __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint32_t E1, uint32_t warp, int lane,
                                            uint32_t smem_base, uint32_t bar0, Ring& g) {
-    g.vbase = smem_base + a.ring_offset + warp * a.ring * kChunkVBytes;
-    g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * a.ring * kChunkVBytes + warp * a.ring * dbytes<kBits>();
+    constexpr uint32_t ring = kMaxRing;  // the host sizes a.ring_offset for exactly this ring
+    g.vbase = smem_base + a.ring_offset + warp * ring * kChunkVBytes;
+    g.dbase = smem_base + a.ring_offset + kSpmvWarpsPerCta * ring * kChunkVBytes + warp * ring * dbytes<kBits>();
     g.bar0 = bar0;
     g.e0 = E0 & ~(kChunk - 1u);
-    g.emask = a.ring * kChunk - 1u;
+    g.emask = ring * kChunk - 1u;
     g.lane_rel = 8u * (uint32_t)lane - g.e0;
     g.n_chunks = E1 > E0 ? ((E1 - 1u) - g.e0) / kChunk + 1u : 0u;
-    g.rshift = 31u - __clz(a.ring);
     g.released = 0;
     g.landed = 0;
-    g.rel_at = a.ring < g.n_chunks ? g.e0 + kChunk : kNever;
+    g.rel_at = ring < g.n_chunks ? g.e0 + kChunk : kNever;
     g.wait_at = g.n_chunks ? 0u : kNever;  // the first pair waits for the first fill
+#ifdef MACKO_L2_HINT
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(g.policy));
-    const uint32_t n = min(a.ring, g.n_chunks);
+#endif
+    const uint32_t n = min(ring, g.n_chunks);
     if (lane == 0) {
         // The barriers are used by this warp and its own bulk copies only (no cluster): the
         // async-proxy fence orders their initialisation before the copies' complete_tx.
-        for (uint32_t i = 0; i < a.ring; ++i) mbar_init(g.bar0 + 8u * i);
+        for (uint32_t i = 0; i < ring; ++i) mbar_init(g.bar0 + 8u * i);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         MK_TRACE(5);
         // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so one
@@ -622,19 +688,21 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
             asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
                          "r"(n * (kChunkVBytes + dbytes<kBits>()))
                          : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-                    g.vbase),
-                "l"(a.values + g.e0), "r"(n * kChunkVBytes), "r"(g.bar0), "l"(g.policy)
-                : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-                    g.dbase),
-                "l"(a.deltas + (size_t)(g.e0 / 8u) * kBits), "r"(n * dbytes<kBits>()), "r"(g.bar0), "l"(g.policy)
-                : "memory");
+            bulk_g2s(g.vbase, a.values + g.e0, n * kChunkVBytes, g.bar0, g);
+            bulk_g2s(g.dbase, a.deltas + (size_t)(g.e0 / 8u) * kBits, n * dbytes<kBits>(), g.bar0, g);
             for (uint32_t i = 1; i < n; ++i)
                 asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
         }
+#if MACKO_L2_PREFETCH > 0
+        if (g.n_chunks > ring) {
+            const uint32_t e = g.e0 + ring * kChunk;
+            const uint32_t nc = min(g.n_chunks - ring, (uint32_t)MACKO_L2_PREFETCH);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.values + e), "r"(nc * kChunkVBytes) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.deltas + (size_t)(e / 8u) * kBits),
+                         "r"(nc * dbytes<kBits>())
+                         : "memory");
+        }
+#endif
         MK_TRACE(7);
     }
     __syncwarp();
@@ -708,67 +776,86 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     asm volatile("mov.b32 %0, %1;" : "=r"(qmask) : "r"(g.emask / 8u));
     uint32_t ev = ring_ev(g);
 
-    // One step pair (steps t, t+1 of the current row).  Masked pairs: the row's first pair
-    // (ROMA) and its last (partial / phantom second step).
-    auto pair = [&](auto masked, uint32_t t) {
-        constexpr bool kMasked = decltype(masked)::value;
+    // One step pair (steps t, t+1 of the current row); `edge` (kEdge*) says which of its steps
+    // need the valid-element mask and whether step B exists.  Only a row's first pair (the ROMA
+    // head in step A) and its last (the row end) are edges: the first pair's B is whole when the
+    // row has >= 3 steps, the last pair's A is whole unless it is also the first step, and a row
+    // with an odd number of steps ends in a single step (no phantom B).
+    auto pair = [&](auto edge, uint32_t t) {
+        constexpr uint32_t kE = decltype(edge)::value;
+        constexpr bool kMaskA = kE & kEdgeMaskA, kMaskB = kE & kEdgeMaskB, kHasB = !(kE & kEdgeSingle);
         const uint32_t S = rs.al + t * kStepElts;
         if (S >= ev) {
-            ring_advance<kBits>(g, a, S, ((!kMasked || t + 1u < rs.T) ? 2u : 1u) * kStepElts);
+            ring_advance<kBits>(g, a, S, (kHasB ? 2u : 1u) * kStepElts);
             ev = ring_ev(g);
         }
         const uint32_t qA = ((rs.al >> 3) + t * (kStepElts / 8u) + lane_q) & qmask;  // S is 8-aligned
-        const uint32_t qB = (qA + kStepElts / 8u) & qmask;
         Slot A = lds_slot<kBits>(vbase, dbase, qA);
-        Slot B = lds_slot<kBits>(vbase, dbase, qB);
+        Slot B{};
+        if constexpr (kHasB) B = lds_slot<kBits>(vbase, dbase, (qA + kStepElts / 8u) & qmask);
         uint32_t vmA = 0xFFu, vmB = 0xFFu;
-        if constexpr (kMasked) {
-            const uint32_t eb = S + 8u * lane;
-            vmA = mask_slot<kBits>(A, eb, rs.s, rs.e);
-            vmB = mask_slot<kBits>(B, eb + kStepElts, rs.s, rs.e);
-        }
+        if constexpr (kMaskA) vmA = mask_slot<kBits>(A, S + 8u * lane, rs.s, rs.e);
+        if constexpr (kMaskB) vmB = mask_slot<kBits>(B, S + kStepElts + 8u * lane, rs.s, rs.e);
         using D = typename std::conditional<kBits == 8, Dec8, Dec>::type;
-        D dA, dB;
+        D dA, dB{};
         uint32_t bias = 0;  // b = 8: lane totals reach 2048, so the packed scan runs on (total - 8)
         if constexpr (kBits == 8) {
             dA = decode8(A.d, A.d2);
-            dB = decode8(B.d, B.d2);
+            if constexpr (kHasB) dB = decode8(B.d, B.d2);
             bias = 8;
         } else {
             dA = decode<kBits>(A.d);
-            dB = decode<kBits>(B.d);
+            if constexpr (kHasB) dB = decode<kBits>(B.d);
         }
-        const uint32_t pk = (dA.local - bias) | ((dB.local - bias) << 16);
+        const uint32_t pk = (dA.local - bias) | (kHasB ? (dB.local - bias) << 16 : 0u);
         const uint32_t incl = warp_incl_scan_p(pk);
         const uint32_t tot = __reduce_add_sync(kFull, pk);
         const uint32_t lane_bias = bias * (uint32_t)lane, tot_bias = bias * kWarp;
         const int cbA = rs.col_base + (int)((incl & 0xFFFFu) - (dA.local - bias) + lane_bias);
-        const int cbB = rs.col_base + (int)((tot & 0xFFFFu) + tot_bias) + (int)((incl >> 16) - (dB.local - bias) + lane_bias);
-        // Edge pairs (the row's first and last): both steps predicated by their valid-element
-        // masks; a phantom second step (the row ends in step A) has vmB = 0.
         if constexpr (kB == 1) {
-            rs.acc[0] = lane_step<kXMode, kMasked>(rs.acc[0], A.v, dA, cbA, xs_addr, a.xtex, vmA);
-            rs.acc[0] = lane_step<kXMode, kMasked, tex_slots_b<kXMode>()>(rs.acc[0], B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            rs.acc[0] = lane_step<kXMode, kMaskA>(rs.acc[0], A.v, dA, cbA, xs_addr, a.xtex, vmA);
         } else {
-            lane_step_b<kXMode, kMasked, kB>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
-            lane_step_b<kXMode, kMasked, kB, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            lane_step_b<kXMode, kMaskA, kB>(rs.acc, A.v, dA, cbA, xs_addr, a.xtex, vmA);
         }
-        rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16) + 2 * (int)tot_bias;
+        if constexpr (kHasB) {
+            const int cbB = rs.col_base + (int)((tot & 0xFFFFu) + tot_bias) + (int)((incl >> 16) - (dB.local - bias) + lane_bias);
+            if constexpr (kB == 1) {
+                rs.acc[0] = lane_step<kXMode, kMaskB, tex_slots_b<kXMode>()>(rs.acc[0], B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            } else {
+                lane_step_b<kXMode, kMaskB, kB, tex_slots_b<kXMode>()>(rs.acc, B.v, dB, cbB, xs_addr, a.xtex, vmB);
+            }
+            rs.col_base += (int)(tot & 0xFFFFu) + (int)(tot >> 16) + 2 * (int)tot_bias;
+        }
     };
+    using EdgeFirst = std::integral_constant<uint32_t, kEdgeMaskA>;                  // ROMA head, B whole
+    using EdgeFirstLast = std::integral_constant<uint32_t, kEdgeMaskA | kEdgeMaskB>; // a two-step row
+    using EdgeLast = std::integral_constant<uint32_t, kEdgeMaskB>;                   // A whole, B ends the row
+    using EdgeSingle = std::integral_constant<uint32_t, kEdgeMaskA | kEdgeSingle>;   // the row's last step alone
+    using Interior = std::integral_constant<uint32_t, 0u>;
 
     for (;;) {
-        // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T).  Pair t is masked
+        // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T).  Pair t is an edge
         // iff it is the row's first (t = 0) or last (t + 2 >= T); interior pairs run unmasked.
         for (uint32_t t = rs.t; t < rs.tend;) {
             const uint32_t ue = t < rs.last_b ? t + kUnitSteps : rs.tend;
             if (t == 0u) {
-                pair(std::true_type{}, 0u);
+                if (rs.T >= 3u) {
+                    pair(EdgeFirst{}, 0u);
+                } else if (rs.T == 2u) {
+                    pair(EdgeFirstLast{}, 0u);
+                } else {
+                    pair(EdgeSingle{}, 0u);
+                }
                 t = 2u;
             }
             const uint32_t lim = min(ue, rs.T - min(rs.T, 2u));
-            for (; t < lim; t += 2u) pair(std::false_type{}, t);
-            if (t < ue) {
-                pair(std::true_type{}, t);
+            for (; t < lim; t += 2u) pair(Interior{}, t);
+            if (t < ue) {  // the row's last pair (t >= 2)
+                if (rs.T - t == 2u) {
+                    pair(EdgeLast{}, t);
+                } else {
+                    pair(EdgeSingle{}, t);
+                }
                 t += 2u;
             }
             const uint32_t pslot = rs.slot + min((ue - 1u) / kUnitSteps, rs.n_r - 1u);

@@ -48,7 +48,7 @@ struct SpmvArgs {
     uint64_t value_elems, delta_bytes;  // allocated sizes (payload + one zeroed chunk of slack)
     uint32_t value_count;               // pad_nnz
     uint32_t rows, cols;
-    uint32_t ring;         // TMA ring slots per warp (power of two, 2..kMaxRing)
+    uint32_t ring;         // TMA ring slots per warp (always kMaxRing; the kernel uses the constant)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
     uint32_t pdl;          // launched as a PDL dependent: x may still be written by the producer
     uint32_t n_peer;       // fused all-gather: y rows also go to peers->y[0..n_peer) and each CTA adds 1
@@ -78,10 +78,13 @@ constexpr int kSpmvCtasPerSm = MACKO_WARPS_PER_SM / kSpmvWarpsPerCta;
 constexpr uint32_t kChunk = MACKO_CHUNK;      // elements per TMA chunk (two step pairs)
 constexpr uint32_t kChunkVBytes = 2 * kChunk; // 2 KiB of values
 constexpr uint32_t kChunkDBytes = kChunk / 2; // 512 B of 4-bit deltas (b_delta = 4; kChunk * b / 8 in general)
+// TMA ring slots per warp, a compile-time power of two: two 1024-element chunks (5 KiB at b_delta
+// = 4) per warp, 160 KiB per SM; four would not fit beside the x table for any b_delta.
 #ifndef MACKO_MAX_RING
-#define MACKO_MAX_RING 4
+#define MACKO_MAX_RING 2
 #endif
 constexpr uint32_t kMaxRing = MACKO_MAX_RING;
+static_assert(kMaxRing >= 2 && (kMaxRing & (kMaxRing - 1)) == 0, "ring slots: a power of two >= 2");
 // fp16 x table in shared memory with zero guards: kXGuardLo entries before x[0] (the ROMA-masked
 // elements of a row's first step decode to columns -7..-1) and kXGuardHi after x[C-1] (a phantom
 // step past the row end is pointed at column C, its elements land on C+1..C+8).

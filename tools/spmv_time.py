@@ -22,6 +22,7 @@ p.add_argument("--n", type=int, default=100)
 p.add_argument("--soak", type=float, default=0.5)
 p.add_argument("--x-mode", type=int, default=-1)
 p.add_argument("--tag", default=os.environ.get("MACKO_LIB", "default"))
+p.add_argument("--no-flush", action="store_true", help="never flush L2 between launches (L2-resident runs)")
 p.add_argument("--check", type=int, default=1, help="compare y with the oracle order (small shapes only)")
 a = p.parse_args()
 
@@ -67,7 +68,7 @@ for spec in a.shapes.split(","):
         m = O.Macko(hm.rows, hm.cols, 4, hm.values, hm.packed_deltas, hm.row_pointers)
         ok = "ok" if (to_host_u16(y) == b200_y(m, to_host_u16(x))).all() else "MISMATCH"
     del dense
-    need_flush = dm.traffic_bytes < 3 * l2
+    need_flush = dm.traffic_bytes < 3 * l2 and not a.no_flush
     t_end = time.time() + a.soak
     while time.time() < t_end:
         for _ in range(10):
