@@ -282,6 +282,36 @@ class Timer:
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in evs]  # ms
 
+    def device_ms(self, fn, reps: int, flush: bool, warmup: int = 3) -> float:
+        """Per-call device time (ms): median of per-call events back to back, or, with an L2 flush
+        before every call, the amortised mean (run_amortized)."""
+        if flush:
+            return self.run_amortized(fn, reps, warmup)
+        return statistics.median(self.run(fn, reps, warmup))
+
+    def run_amortized(self, fn, reps: int, warmup: int = 3) -> float:
+        """Mean device time (ms) of fn with an L2 flush before every rep: one event pair around
+        reps x (flush; fn) minus one around reps x flush.  On B200 an event recorded right after
+        the flush kernel ticks in ~2.05 us steps, so per-rep events quantise kernels of 10-30 us by
+        up to 10 %; the two long intervals do not."""
+        torch = self.torch
+        for _ in range(warmup):
+            self.flush()
+            fn()
+        a, b, c, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        torch.cuda.synchronize()
+        a.record(self.stream)
+        for _ in range(reps):
+            self.flush()
+            fn()
+        b.record(self.stream)
+        c.record(self.stream)
+        for _ in range(reps):
+            self.flush()
+        d.record(self.stream)
+        torch.cuda.synchronize()
+        return max(a.elapsed_time(b) - c.elapsed_time(d), 1e-6) / reps
+
 
 def allmax(torch, dist, dev, vals):
     t = torch.tensor(vals, device=dev, dtype=torch.float64)
@@ -333,15 +363,13 @@ def dense_baseline(torch, timer, dense, x, reps, flush):
     y1 = torch.empty(R, dtype=torch.float16, device=dense.device)
     y2 = torch.empty(R, dtype=torch.float16, device=dense.device)
     out = {}
-    t = timer.run(lambda: torch.mv(dense, x, out=y1), reps, flush=flush)
-    out["cublasGemmEx (torch.mv)"] = statistics.median(t) * 1e3
+    out["cublasGemmEx (torch.mv)"] = timer.device_ms(lambda: torch.mv(dense, x, out=y1), reps, flush) * 1e3
     hsh = cublas_hsh_gemv()
     if hsh is not None:
         hsh(dense, x, y2)
         torch.cuda.synchronize()
         if torch.allclose(y1.float(), y2.float(), rtol=2e-2, atol=1e-2):
-            t = timer.run(lambda: hsh(dense, x, y2), reps, flush=flush)
-            out["cublasHSHgemvStridedBatched"] = statistics.median(t) * 1e3
+            out["cublasHSHgemvStridedBatched"] = timer.device_ms(lambda: hsh(dense, x, y2), reps, flush) * 1e3
     best = min(out, key=out.get)
     return best, out[best], {k: round(v, 2) for k, v in out.items()}
 
@@ -470,8 +498,8 @@ def main():
     kern_ms = ms_mean
     coll_us = None
     if world > 1:
-        kern_ms = allmax(torch, dist, dev, [statistics.mean(timer.run(lambda: dm.spmv_into(x, y, stream),
-                                                                     min(args.steps, 50), flush=need_flush))])[0]
+        kern_ms = allmax(torch, dist, dev, [timer.device_ms(lambda: dm.spmv_into(x, y, stream), min(args.steps, 50),
+                                                            need_flush)])[0]
         cm = timer.run(lambda: (sharded.broadcast_x(x), sharded.gather_y()), min(args.steps, 50))
         coll_us = allmax(torch, dist, dev, [statistics.mean(cm)])[0] * 1e3
     achieved = bytes_rank / (kern_ms * 1e-3) / 1e9
@@ -599,8 +627,7 @@ def run_spmm(M, torch, dm, timer, stream, need_flush):
         for i in range(b):
             M.gen_vector(X[i], dm.cols, seed=SEED_X + i)
         Y = torch.empty((b, dm.rows), dtype=torch.float16, device="cuda")
-        t = timer.run(lambda: dm.spmm_into(X, Y, stream), 30, flush=need_flush)
-        us = statistics.median(t) * 1e3
+        us = timer.device_ms(lambda: dm.spmm_into(X, Y, stream), 30, need_flush) * 1e3
         out[f"batch{b}"] = {"us": round(us, 2), "us_per_vector": round(us / b, 2)}
     return out
 
@@ -811,7 +838,7 @@ def run_sweep(M, torch, dev, stream, timer, peak):
         M.gen_vector(x, C, seed=SEED_X)
         y = torch.empty(R, dtype=torch.float16, device=dev)
         flush = dm.traffic_bytes < 3 * l2
-        us = statistics.median(timer.run(lambda: dm.spmv_into(x, y, stream), 50, warmup=5, flush=flush)) * 1e3
+        us = timer.device_ms(lambda: dm.spmv_into(x, y, stream), 50, flush, warmup=5) * 1e3
         api, dus, apis = dense_baseline(torch, timer, dense, x, 30, flush)
         gbs = dm.traffic_bytes / (us * 1e-6) / 1e9
         out.append({"shape": f"{R}x{C}", "sparsity": sparsity_pct(d), "us": round(us, 2), "GBps": round(gbs, 1),

@@ -159,6 +159,11 @@ macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
 
 macko_status macko_dev_free(macko_dev_matrix* m);
 
+/* Device blocks of >= 1 MiB released by the library (matrices freed, compressor scratch) are kept
+ * per process (up to 4 GiB) and reused by later builds; a release synchronises the device first,
+ * as cudaFree does.  This returns every cached block to the driver. */
+macko_status macko_release_cached_memory(void);
+
 /* ---- MCKO container (io.cpp write_macko / read_macko are absent) ----------
  * File: 32-byte little-endian header "MCKO" | u16 version=1 | u8 b_val=16 | u8 b_delta | u64 R |
  * u64 C | u64 pad_nnz, then row_pointers ((R+1) x u32), packed_deltas (macko_delta_bytes) and

@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <new>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -75,17 +76,116 @@ struct DeviceGuard {
     }
 };
 
+// Device block cache behind DevBuf.  cudaMalloc / cudaFree of the compressor's buffers (566 MB of
+// values + codewords at 36864x12288, plus scratch) cost milliseconds per build; released blocks of
+// >= 1 MiB are kept per device (up to kCacheBytes) and reused for a request of 50-100 % of their
+// size.  A release still synchronises the device first, exactly as cudaFree does, so a block is
+// never handed out while an earlier kernel may use it.  macko_release_cached_memory() frees them.
+class BlockCache {
+  public:
+    static constexpr size_t kMinBytes = 1u << 20, kCacheBytes = size_t(4) << 30;
+    const bool off = std::getenv("MACKO_NO_BLOCK_CACHE") != nullptr;  // A/B switch
+    void* get(int dev, size_t bytes) {
+        if (bytes >= kMinBytes && !off) {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto best = blocks_.end();
+            for (auto it = blocks_.begin(); it != blocks_.end(); ++it)
+                if (it->dev == dev && it->bytes >= bytes && it->bytes <= 2 * bytes &&
+                    (best == blocks_.end() || it->bytes < best->bytes))
+                    best = it;
+            if (best != blocks_.end()) {
+                void* p = best->p;
+                held_ -= best->bytes;
+                live_[p] = best->bytes;
+                blocks_.erase(best);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {  // out of memory: drop the cache and retry once
+            cudaGetLastError();
+            trim();
+            ck(cudaMalloc(&p, bytes), "cudaMalloc");
+        }
+        if (bytes >= kMinBytes && !off) {
+            std::lock_guard<std::mutex> lk(mu_);
+            live_[p] = bytes;
+        }
+        return p;
+    }
+    void put(int dev, void* p) {
+        size_t bytes = 0;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = live_.find(p);
+            if (it != live_.end()) {
+                bytes = it->second;
+                live_.erase(it);
+            }
+        }
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        cudaDeviceSynchronize();  // cudaFree semantics: no pending kernel still uses the block
+        if (cur != dev && cur >= 0) cudaSetDevice(cur);
+        if (!bytes) {
+            cudaFree(p);
+            return;
+        }
+        std::lock_guard<std::mutex> lk(mu_);
+        blocks_.push_back({dev, bytes, p});
+        held_ += bytes;
+        while (held_ > kCacheBytes && !blocks_.empty()) {  // oldest first
+            held_ -= blocks_.front().bytes;
+            cudaFree(blocks_.front().p);
+            blocks_.erase(blocks_.begin());
+        }
+    }
+    void trim() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& b : blocks_) {
+            int cur = -1;
+            cudaGetDevice(&cur);
+            cudaSetDevice(b.dev);
+            cudaFree(b.p);
+            cudaSetDevice(cur);
+        }
+        blocks_.clear();
+        held_ = 0;
+    }
+
+  private:
+    struct Block {
+        int dev;
+        size_t bytes;
+        void* p;
+    };
+    std::mutex mu_;
+    std::vector<Block> blocks_;
+    std::unordered_map<void*, size_t> live_;
+    size_t held_ = 0;
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache;  // never destroyed: frees at process exit are the driver's
+    return *c;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    int dev = 0;
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+        if (count) {
+            ck(cudaGetDevice(&dev), "cudaGetDevice");
+            p = static_cast<T*>(block_cache().get(dev, count * sizeof(T)));
+        }
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) block_cache().put(dev, p);
         p = nullptr;
         n = 0;
     }
@@ -818,6 +918,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         lastcol.alloc(rows);
         total.alloc(1);
         m->row_ptrs.alloc(rows + 1);
+        tm.mark("scratch alloc");
         ck(mk::launch_count_rows(d_dense, ld, (uint32_t)rows, (uint32_t)cols, b_delta, counts.p, lastcol.p, m->sms, st),
            "count_rows");
         ck(mk::launch_scan_counts(counts.p, (uint32_t)rows, m->row_ptrs.p, total.p, st), "scan_counts");
@@ -825,7 +926,7 @@ macko_status macko_dev_from_dense(int device, const uint16_t* d_dense, uint64_t 
         unsigned long long pad_nnz = 0;
         ck(cudaMemcpyAsync(&pad_nnz, total.p, 8, cudaMemcpyDeviceToHost, st), "readback");
         ck(cudaStreamSynchronize(st), "sync");
-        tm.mark("alloc + count + scan + sync");
+        tm.mark("count + scan + sync");
         if (pad_nnz > 0xFFFFFFFFull) fail(MACKO_EINVAL, "pad_nnz does not fit u32 row pointers (SPEC.md:403)");
         m->pad_nnz = pad_nnz;
         const uint64_t vb = values_bytes(pad_nnz), db = delta_bytes(pad_nnz, b_delta);
@@ -1246,6 +1347,10 @@ macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream) {
         DeviceGuard g(m->device);
         device_validate(const_cast<macko_dev_matrix*>(m), (cudaStream_t)stream);
     });
+}
+
+macko_status macko_release_cached_memory(void) {
+    return guarded([&] { block_cache().trim(); });
 }
 
 macko_status macko_dev_free(macko_dev_matrix* m) {

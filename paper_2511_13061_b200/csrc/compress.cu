@@ -338,6 +338,157 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp, 4)
     }
 }
 
+// b_delta = 4 emitter (the benchmark width): the same classification as emit_rows<true, 16>, with
+// the output path rebuilt around 16-byte stores.  Stage position q of a warp's value stage is
+// global value vbase + q with vbase 8-aligned, so every complete 8-value group leaves as one
+// 16-byte store; the partial group rolls to the front of the stage for the next 512 columns.  A
+// lane's entries go to the stage with one predicated store each at a running address (no popc
+// per column).  Codewords (nibbles) are OR-ed into a word stage the same way and complete words
+// leave as plain 32-bit stores; the row's first and last words, shared with the neighbouring
+// rows, are OR-ed into global memory.
+constexpr int kE4Warps = 8;
+constexpr uint32_t kE4Step = kWarp * 16;  // columns per warp step
+
+__global__ void __launch_bounds__(kE4Warps * kWarp, 4)
+    emit_rows4(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, const uint32_t* row_ptrs,
+               const int32_t* lastcol, uint16_t* values, uint32_t* delta_words) {
+    constexpr uint32_t bits = 4, maxd = 16;
+    __shared__ __align__(16) uint16_t vst_all[kE4Warps][kE4Step + 16];
+    __shared__ uint32_t cst_all[kE4Warps][kE4Step / 8 + 8];
+    __shared__ uint64_t gap_codes[256];
+    for (uint32_t pat = threadIdx.x; pat < 256; pat += blockDim.x) {
+        uint64_t v = 0;
+        uint32_t i = 0, rest = pat;
+        int prev = -1;
+        while (rest) {
+            const int k = __ffs(rest) - 1;
+            rest &= rest - 1;
+            if (prev >= 0) v |= (uint64_t)(uint32_t)(k - prev - 1) << (bits * i++);
+            prev = k;
+        }
+        gap_codes[pat] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & (kWarp - 1);
+    uint16_t* vst = vst_all[threadIdx.x >> 5];
+    uint32_t* cst = cst_all[threadIdx.x >> 5];
+    const uint32_t vst_s = static_cast<uint32_t>(__cvta_generic_to_shared(vst));
+    const uint32_t nwarps = gridDim.x * kE4Warps;
+    const bool vec_base = ((reinterpret_cast<uintptr_t>(dense) | (ld * 2)) & 15u) == 0;
+    for (uint32_t r = blockIdx.x * kE4Warps + (threadIdx.x >> 5); r < rows; r += nwarps) {
+        const uint32_t start = row_ptrs[r], end = row_ptrs[r + 1];
+        if (start == end) continue;
+        const int L = lastcol[r];
+        const uint16_t* row = dense + (uint64_t)r * ld;
+        uint32_t vbase = start & ~7u, vlo = start & 7u, vP = vlo;  // value stage: q <-> vbase + q
+        uint32_t wbase = start >> 3, cP = start & 7u;              // code stage: nibble q <-> 8 wbase + q
+        const uint32_t first_word = wbase;
+        bool first_open = (start & 7u) != 0;  // the row's first word still holds the previous row's nibbles
+        for (int i = lane; i < (int)(kE4Step / 8 + 8); i += kWarp) cst[i] = 0;
+        __syncwarp();
+        int carry = -1;
+        uint4 next[2];
+        next[0] = fetch8(row, 16 * lane, cols, vec_base);
+        next[1] = fetch8(row, 16 * lane + 8, cols, vec_base);
+        for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kE4Step) {
+            const uint32_t c = c0 + 16 * lane;
+            uint16_t h[16];
+            const uint32_t nz = unpack8(next[0], h) | (unpack8(next[1], h + 8) << 8);
+            if (c0 + kE4Step < cols && (int)(c0 + kE4Step) <= L) {
+                next[0] = fetch8(row, c + kE4Step, cols, vec_base);
+                next[1] = fetch8(row, c + kE4Step + 8, cols, vec_base);
+            }
+            const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
+            const int p = prev_nonzero(lane_last, lane, carry);
+            const uint32_t pb = pad_bit<16>(nz, (int)c, p, L, bits);
+            const uint32_t em = nz | pb;
+            uint64_t codes = pb ? (uint64_t)(maxd - 1) : 0ull;
+            if (nz) {
+                const uint32_t sh = pb ? bits : 0u;
+                const uint32_t first = (uint32_t)((int)c + __ffs(nz) - 2 - p) & (maxd - 1);
+                const uint32_t lo = nz & 0xFFu, hi = nz >> 8;
+                uint64_t gaps = lo ? gap_codes[lo] : 0ull;
+                uint32_t pos = lo ? bits * (__popc(lo) - 1) : 0u;
+                if (lo && hi) {
+                    gaps |= (uint64_t)(uint32_t)(8 + __ffs(hi) - 1 - (31 - __clz(lo)) - 1) << pos;
+                    pos += bits;
+                }
+                if (hi) gaps |= gap_codes[hi] << pos;
+                codes |= ((uint64_t)first << sh) | (gaps << (sh + bits));
+            }
+            const uint32_t n = __popc(em);
+            uint32_t incl = n;
+#pragma unroll
+            for (int off = 1; off < kWarp; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += t;
+            }
+            const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
+            // values: one predicated 2-byte store per entry at a running stage address
+            uint32_t va = vst_s + 2u * (vP + incl - n);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if ((em >> k) & 1u) {
+                    const uint16_t val = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;  // pads are +0
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(va), "h"(val) : "memory");
+                    va += 2u;
+                }
+            }
+            // codewords: nibble position cP + (incl - n); <= 16 nibbles span <= 3 words
+            if (n) {
+                const uint32_t np = cP + incl - n, wi = np >> 3, sh = (np & 7u) * 4u;
+                const uint64_t lo64 = codes << sh;
+                atomicOr(&cst[wi], (uint32_t)lo64);
+                if ((uint32_t)(lo64 >> 32)) atomicOr(&cst[wi + 1], (uint32_t)(lo64 >> 32));
+                if (sh && (uint32_t)(codes >> (64 - sh))) atomicOr(&cst[wi + 2], (uint32_t)(codes >> (64 - sh)));
+            }
+            __syncwarp();
+            vP += tot;
+            cP += tot;
+            // complete 8-value groups -> 16-byte stores (the row's first group, shared with the
+            // previous row, value by value)
+            const uint32_t nfull = vP >> 3;
+            uint32_t j0 = 0;
+            if (vlo && nfull) {
+                if ((uint32_t)lane >= vlo && lane < 8) values[vbase + lane] = vst[lane];
+                j0 = 1;
+                vlo = 0;
+            }
+            for (uint32_t j = j0 + lane; j < nfull; j += kWarp)
+                *reinterpret_cast<uint4*>(values + vbase + 8u * j) = *reinterpret_cast<const uint4*>(vst + 8u * j);
+            // complete code words
+            const uint32_t nw = cP >> 3;
+            for (uint32_t i = lane; i < nw; i += kWarp) {
+                if (first_open && wbase + i == first_word)
+                    atomicOr(delta_words + first_word, cst[i]);
+                else
+                    delta_words[wbase + i] = cst[i];
+            }
+            if (nw) first_open = false;
+            __syncwarp();
+            // roll the partial value group and the partial code word to the front
+            const uint32_t rem = vP - 8u * nfull;
+            const uint16_t tv = (uint32_t)lane < rem ? vst[8u * nfull + lane] : (uint16_t)0;
+            const uint32_t tw = cst[nw];
+            __syncwarp();
+            for (uint32_t i = lane; i <= nw + 2u; i += kWarp) cst[i] = 0;
+            __syncwarp();
+            if ((uint32_t)lane < rem) vst[lane] = tv;
+            if (lane == 0) cst[0] = tw;
+            __syncwarp();
+            vbase += 8u * nfull;
+            vP = rem;
+            wbase += nw;
+            cP &= 7u;
+        }
+        // row end: the last partial value group value by value, the last partial word OR-ed (the
+        // next row's entries share it)
+        if ((uint32_t)lane >= vlo && (uint32_t)lane < vP) values[vbase + lane] = vst[lane];
+        if (lane == 0 && cP) atomicOr(delta_words + wbase, cst[0]);
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_count_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, uint32_t bits,
@@ -368,7 +519,7 @@ cudaError_t launch_emit_rows(const uint16_t* dense, uint64_t ld, uint32_t rows, 
     if (grid > 0) {
         const dim3 b(kCompressWarpsPerCta * kWarp);
         if (bits == 4)
-            emit_rows<true, 16><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values, delta_words);
+            emit_rows4<<<grid, b, 0, s>>>(dense, ld, rows, cols, row_ptrs, lastcol, values, delta_words);
         else if (bits == 8)
             emit_rows<true, 8><<<grid, b, 0, s>>>(dense, ld, rows, cols, bits, row_ptrs, lastcol, values, delta_words);
         else

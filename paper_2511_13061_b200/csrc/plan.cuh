@@ -4,11 +4,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "common.cuh"
 #include "spmv.cuh"
 
 namespace mk {
 
-// Device scratch of one plan build (rows R, warps W, units <= ubound = 2 R + pad_nnz / 2048 + 16).
+// Device scratch of one plan build (rows R, warps W, units <= ubound = 2 R + pad_nnz / kUnitElts + 16).
 struct PlanTemp {
     uint32_t* nu;                // R: units per row
     unsigned long long* rw;      // R: row weight
@@ -25,7 +26,7 @@ struct PlanTotals {
     uint32_t units, splits, slots, pad;
 };
 
-inline uint64_t plan_unit_bound(uint64_t rows, uint64_t pad_nnz) { return 2 * rows + pad_nnz / 2048 + 16; }
+inline uint64_t plan_unit_bound(uint64_t rows, uint64_t pad_nnz) { return 2 * rows + pad_nnz / kUnitElts + 16; }
 
 // Fills recs[W], splits[<= W] and *d_totals; stream-ordered, no host synchronisation.
 cudaError_t plan_build_device(const uint32_t* rp, uint32_t rows, uint32_t pad_nnz, uint32_t W, uint64_t ubound, int sms,

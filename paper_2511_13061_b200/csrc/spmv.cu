@@ -485,6 +485,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // only grows, by at most one step pair per pair, so at most one chunk is released per pair.
 constexpr uint32_t kNever = 0xFFFFFFFFu;
 
+#ifndef MACKO_EDGE_SPLIT
+#define MACKO_EDGE_SPLIT 1
+#endif
+constexpr bool kEdgeSplit = MACKO_EDGE_SPLIT;  // 0: every edge pair masks both steps
 // Edge step pairs (run_rows): which steps are masked, and whether the pair is a single step.
 constexpr uint32_t kEdgeMaskA = 1u, kEdgeMaskB = 2u, kEdgeSingle = 4u;
 
@@ -497,9 +501,6 @@ struct Ring {
     uint32_t released;            // chunks consumed and refilled (or nothing left to refill)
     uint32_t landed;              // chunks waited for
     uint32_t rel_at, wait_at;     // S thresholds of the next release / the next wait (kNever: none)
-#ifdef MACKO_L2_HINT
-    uint64_t policy;              // L2 evict_first (the matrix streams once per SpMV)
-#endif
 };
 
 __device__ __forceinline__ uint32_t ring_ev(const Ring& g) { return min(g.rel_at, g.wait_at); }
@@ -515,18 +516,6 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a) {
     const uint32_t e = g.e0 + (g.released + ring) * kChunk;
     const uint32_t bar = g.bar0 + 8u * slot;
     // relaxed: the arrive only arms the transaction count, so no MEMBAR precedes it
-#ifdef MACKO_L2_HINT
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "@p mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%4], %6;\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %7, [%4], %5;\n\t"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %8, [%4], %5;\n\t}" ::"r"(
-            g.vbase + slot * kChunkVBytes),
-        "l"(a.values + e), "r"(g.dbase + slot * dbytes<kBits>()), "l"(a.deltas + (size_t)(e / 8u) * kBits), "r"(bar),
-        "l"(g.policy), "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
-        : "memory");
-#else
     // No L2 eviction hint: the policy operand costs two uniform-register moves per copy and two
     // live registers in the walk, and the streamed matrix does not displace anything the SpMV
     // re-reads (x is staged once per CTA, the plan record once per warp).
@@ -540,23 +529,6 @@ __device__ __forceinline__ void ring_issue(const Ring& g, const SpmvArgs& a) {
         "l"(a.values + e), "r"(g.dbase + slot * dbytes<kBits>()), "l"(a.deltas + (size_t)(e / 8u) * kBits), "r"(bar),
         "n"(kChunkVBytes + dbytes<kBits>()), "n"(kChunkVBytes), "n"(dbytes<kBits>())
         : "memory");
-#endif
-}
-
-#ifndef MACKO_L2_PREFETCH
-#define MACKO_L2_PREFETCH 0
-#endif
-// cp.async.bulk.prefetch.L2 of chunk c of the warp's stream (values + codewords; one lane).
-template <int kBits>
-__device__ __forceinline__ void l2_prefetch_chunk(const Ring& g, const SpmvArgs& a, uint32_t c) {
-    const uint32_t e = g.e0 + c * kChunk;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "@p cp.async.bulk.prefetch.L2.global [%0], %2;\n\t"
-        "@p cp.async.bulk.prefetch.L2.global [%1], %3;\n\t}" ::"l"(a.values + e),
-        "l"(a.deltas + (size_t)(e / 8u) * kBits), "n"(kChunkVBytes), "n"(dbytes<kBits>())
-        : "memory");
 }
 
 // The walk reached S (slow path, S >= ring_ev): release the chunk the walk has left (every lane's
@@ -568,11 +540,6 @@ __device__ __forceinline__ void ring_advance(Ring& g, const SpmvArgs& a, uint32_
     if (S >= g.rel_at) {
         __syncwarp();
         ring_issue<kBits>(g, a);
-#if MACKO_L2_PREFETCH > 0
-        // L2 prefetch of the chunk MACKO_L2_PREFETCH past the refill: its refill then waits on an
-        // L2 hit instead of an HBM round trip (the ring alone keeps only one chunk ahead)
-        if (g.released + ring + MACKO_L2_PREFETCH < g.n_chunks) l2_prefetch_chunk<kBits>(g, a, g.released + ring + MACKO_L2_PREFETCH);
-#endif
         ++g.released;
         g.rel_at = g.released + ring < g.n_chunks ? g.e0 + (g.released + 1u) * kChunk : kNever;
     }
@@ -641,17 +608,25 @@ __device__ __forceinline__ PlanRecord load_record(const SpmvArgs& a, uint32_t w)
 }
 
 // One bulk global -> shared copy completing on mbarrier bar (one lane).
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, const Ring& g) {
-#ifdef MACKO_L2_HINT
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar), "l"(g.policy)
-                 : "memory");
-#else
-    (void)g;
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst), "l"(src),
                  "r"(bytes), "r"(bar)
                  : "memory");
-#endif
+}
+
+// PDL launches (decode chains) stagger the first fill: each warp requests chunk 0 of its ring before
+// griddepcontrol.wait and the rest only after the CTA barrier, so every warp's first chunk is in the
+// memory system first and the walks start as soon as it lands (decoder chain 2409 -> 2347 us per
+// token).  A stand-alone SpMV keeps one two-chunk copy per array (0.1 % faster there).
+// First-phase fill of ring slot i with chunk i of the warp's stream (one lane).
+template <int kBits>
+__device__ __forceinline__ void fill_chunk(const Ring& g, const SpmvArgs& a, uint32_t i) {
+    const uint32_t bar = g.bar0 + 8u * i, e = g.e0 + i * kChunk;
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(kChunkVBytes + dbytes<kBits>())
+                 : "memory");
+    bulk_g2s(g.vbase + i * kChunkVBytes, a.values + e, kChunkVBytes, bar);
+    bulk_g2s(g.dbase + i * dbytes<kBits>(), a.deltas + (size_t)(e / 8u) * kBits, dbytes<kBits>(), bar);
 }
 
 // Ring set-up for the warp's element stream [E0, E1): the barriers are initialised and the first
@@ -671,9 +646,6 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
     g.landed = 0;
     g.rel_at = ring < g.n_chunks ? g.e0 + kChunk : kNever;
     g.wait_at = g.n_chunks ? 0u : kNever;  // the first pair waits for the first fill
-#ifdef MACKO_L2_HINT
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(g.policy));
-#endif
     const uint32_t n = min(ring, g.n_chunks);
     if (lane == 0) {
         // The barriers are used by this warp and its own bulk copies only (no cluster): the
@@ -684,25 +656,18 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
         // Initial fill: the first `ring` chunks are contiguous in global and shared memory, so one
         // copy per array fills them all and completes on barrier 0; the other barriers complete
         // their first phase with a plain arrive (the consumer passes barrier 0 first).
-        if (n) {
+        // PDL launches (decode chains): chunk 0 alone now, the rest after the CTA barrier.
+        if (n && !a.pdl) {
             asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
                          "r"(n * (kChunkVBytes + dbytes<kBits>()))
                          : "memory");
-            bulk_g2s(g.vbase, a.values + g.e0, n * kChunkVBytes, g.bar0, g);
-            bulk_g2s(g.dbase, a.deltas + (size_t)(g.e0 / 8u) * kBits, n * dbytes<kBits>(), g.bar0, g);
+            bulk_g2s(g.vbase, a.values + g.e0, n * kChunkVBytes, g.bar0);
+            bulk_g2s(g.dbase, a.deltas + (size_t)(g.e0 / 8u) * kBits, n * dbytes<kBits>(), g.bar0);
             for (uint32_t i = 1; i < n; ++i)
                 asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(g.bar0 + 8u * i) : "memory");
+        } else if (n) {
+            fill_chunk<kBits>(g, a, 0);
         }
-#if MACKO_L2_PREFETCH > 0
-        if (g.n_chunks > ring) {
-            const uint32_t e = g.e0 + ring * kChunk;
-            const uint32_t nc = min(g.n_chunks - ring, (uint32_t)MACKO_L2_PREFETCH);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.values + e), "r"(nc * kChunkVBytes) : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.deltas + (size_t)(e / 8u) * kBits),
-                         "r"(nc * dbytes<kBits>())
-                         : "memory");
-        }
-#endif
         MK_TRACE(7);
     }
     __syncwarp();
@@ -755,8 +720,40 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint16_t* xs) {
     }
 }
 
+#ifndef MACKO_TMA_X
+#define MACKO_TMA_X 1
+#endif
+// x staged by one bulk copy per CTA (chain instance, SpMV with an x table): thread 0 issues it on
+// barrier xbar, the other threads write the zero guards and the < 8-element tail; everyone waits
+// on xbar after the CTA barrier.  Decoder chain 2284 vs 2337 us per token; stand-alone launches
+// after an L2 flush were mixed (11008x4096 21.6 vs 20.8 us, 4096x11008 21.5 vs 22.4 us: all 148
+// CTAs then fetch the same x lines from HBM in the same order), so they keep the threaded
+// staging with per-CTA rotated order.
+template <int kXMode, int kB>
+constexpr bool x_by_tma() {
+    return MACKO_TMA_X && kB == 1 && x_table<kXMode>();
+}
+
+__device__ __forceinline__ void stage_x_tma_issue(const SpmvArgs& a, uint16_t* xs, uint32_t xbar) {
+    const uint32_t nbytes = (a.cols / 8u) * 16u;  // x is 16-byte aligned (capi)
+    mbar_init(xbar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (nbytes) {
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(nbytes) : "memory");
+        bulk_g2s(static_cast<uint32_t>(__cvta_generic_to_shared(xs)), a.x, nbytes, xbar);
+    } else {
+        asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(xbar) : "memory");
+    }
+}
+
+__device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs) {
+    const uint32_t C = a.cols;
+    for (uint32_t i = (C / 8u) * 8u + threadIdx.x; i < C + kXGuardHi; i += blockDim.x) xs[i] = i < C ? a.x[i] : (uint16_t)0;
+    if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
+}
+
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
-template <int kXMode, int kBits, int kB>
+template <int kXMode, int kBits, int kB, bool kSplitEdges>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
                                          RowState<kB>& rs) {
     if (rs.T == 0) {
@@ -833,13 +830,22 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     using EdgeSingle = std::integral_constant<uint32_t, kEdgeMaskA | kEdgeSingle>;   // the row's last step alone
     using Interior = std::integral_constant<uint32_t, 0u>;
 
+    // Per-step edge masking (kSplitEdges) is the kernel instance of PDL launches (decode chains,
+    // where consecutive SpMVs keep the kernel's code warm: 2343 vs 2378 us per token).  A
+    // stand-alone launch after an L2 flush fetches its code from HBM, and the four extra edge
+    // variants cost more in cold instruction misses than they save (11008x4096: 21.8 vs 20.8 us),
+    // so that instance masks both steps of an edge pair.  (A run-time switch between the two costs
+    // registers: 121 vs 111 us at 36864x12288.)
+    constexpr bool split_edges = kSplitEdges && kEdgeSplit;
     for (;;) {
         // the piece's units: [8j, 8j+8) steps, the row's last unit [last_b, T).  Pair t is an edge
         // iff it is the row's first (t = 0) or last (t + 2 >= T); interior pairs run unmasked.
         for (uint32_t t = rs.t; t < rs.tend;) {
             const uint32_t ue = t < rs.last_b ? t + kUnitSteps : rs.tend;
             if (t == 0u) {
-                if (rs.T >= 3u) {
+                if (!split_edges) {
+                    pair(EdgeFirstLast{}, 0u);
+                } else if (rs.T >= 3u) {
                     pair(EdgeFirst{}, 0u);
                 } else if (rs.T == 2u) {
                     pair(EdgeFirstLast{}, 0u);
@@ -851,7 +857,9 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
             const uint32_t lim = min(ue, rs.T - min(rs.T, 2u));
             for (; t < lim; t += 2u) pair(Interior{}, t);
             if (t < ue) {  // the row's last pair (t >= 2)
-                if (rs.T - t == 2u) {
+                if (!split_edges) {
+                    pair(EdgeFirstLast{}, t);
+                } else if (rs.T - t == 2u) {
                     pair(EdgeLast{}, t);
                 } else {
                     pair(EdgeSingle{}, t);
@@ -890,7 +898,10 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
     }
 }
 
-template <int kXMode, int kBits, int kB = 1>
+// kChain: the instance of PDL launches (decode chains): per-step edge masking (run_rows) and x
+// staged by one bulk copy per CTA (stage_x_tma_*).  Both pay only with the kernel's code and x
+// warm in L2, as in a chain; a stand-alone launch after an L2 flush is faster without them.
+template <int kXMode, int kBits, int kB = 1, bool kChain = false>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
@@ -905,22 +916,43 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const PlanRecord pr = load_record(a, w);
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo * kB;
+    __shared__ __align__(8) uint64_t xbar_s;
+    const uint32_t xbar = static_cast<uint32_t>(__cvta_generic_to_shared(&xbar_s));
+    constexpr bool kTmaX = x_by_tma<kXMode, kB>() && kChain;
     // Without a PDL producer x is final at entry: its loads overlap the plan record's latency.
-    if (!a.pdl) stage_x<kXMode, kB>(a, xs);
+    if constexpr (kTmaX) {
+        if (!a.pdl && threadIdx.x == 0) stage_x_tma_issue(a, xs, xbar);
+    } else {
+#ifndef MACKO_RING_FIRST
+        if (!a.pdl) stage_x<kXMode, kB>(a, xs);
+#endif
+    }
     // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
     RowState<kB> rs;
     Ring g;
     const bool has_work = op_begin<kBits, kB>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
+#ifdef MACKO_RING_FIRST
+    if (!a.pdl) stage_x<kXMode, kB>(a, xs);
+#endif
     MK_TRACE(2);
     // x (and y) may be produced / consumed by the previous kernel of a PDL chain.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     MK_TRACE(3);
-    if (a.pdl) stage_x<kXMode, kB>(a, xs);
-    __syncthreads();
+    if constexpr (kTmaX) {
+        if (a.pdl && threadIdx.x == 0) stage_x_tma_issue(a, xs, xbar);
+        stage_x_tma_rest(a, xs);
+        __syncthreads();  // xbar initialised, guards written
+        mbar_wait(xbar, 0);
+    } else {
+        if (a.pdl) stage_x<kXMode, kB>(a, xs);
+        __syncthreads();
+    }
     MK_TRACE(4);
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    if (has_work) run_rows<kXMode, kBits, kB>(a, w, lane, xs_addr, g, rs);
+    if (a.pdl && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin)
+        for (uint32_t i = 1; i < min(kMaxRing, g.n_chunks); ++i) fill_chunk<kBits>(g, a, i);
+    if (has_work) run_rows<kXMode, kBits, kB, kChain>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
     signal_peers(a);
 }
@@ -952,7 +984,14 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     const int threads = kSpmvWarpsPerCta * kWarp;
     cudaError_t e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
+    if (e == cudaSuccess) {
+        int c2 = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, macko_spmv<kXMode, kBits, 1, true>, threads, smem);
+        *ctas_per_sm = std::min(*ctas_per_sm, c2);
+    }
     return e;
 }
 
@@ -968,6 +1007,7 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    if (pdl) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 

@@ -652,3 +652,20 @@ def test_device_plan_equals_host_plan(cuda, monkeypatch):
             assert np.array_equal(sh, sd), (A.shape, ctas)
         x = O.gen_vector(A.shape[1], 7)
         assert np.array_equal(gpu_spmv(dd, x), b200_y(O.encode_dense(A), x))
+
+
+def test_block_cache_reuse_keeps_formats_exact(cuda):
+    """Matrices built, freed and rebuilt reuse cached device blocks (capi BlockCache): every build
+    is still bit-exact, including builds into recycled blocks that held a different matrix."""
+    from paper_2511_13061_b200 import _lib
+
+    cases = [(1024, 2048, 0.5), (700, 3000, 0.3), (1024, 2048, 0.9), (1500, 2048, 0.5)]
+    for rep in range(2):
+        for i, (R, C, d) in enumerate(cases):
+            A = O.gen_dense(R, C, d, 77 + i + 10 * rep)
+            dm = gpu_encode(A, 4)
+            assert_same_format(dm, O.encode_dense(A, 4), (rep, R, C, d))
+            dm.close()
+    assert _lib.load().macko_release_cached_memory() == 0
+    A = O.gen_dense(512, 4096, 0.5, 5)
+    assert_same_format(gpu_encode(A, 4), O.encode_dense(A, 4), "after release")
