@@ -190,13 +190,18 @@ class ClockSampler:
 
     def summary(self, t0: float, t1: float):
         rows = [r for r in self.lines if t0 <= r[0] <= t1 and r[1] > 0]
+        widened = 0.0
+        while not rows and widened < 0.05 and self.lines:  # a short region between two polls: the
+            widened += 0.002                                  # nearest samples, window stated below
+            rows = [r for r in self.lines if t0 - widened <= r[0] <= t1 + widened and r[1] > 0]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["no samples"], "source": "nvml"}
         reasons = sorted({n for r in rows if r[2] >= 0 for b, n in self.REASON_BITS.items() if r[2] & b})
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.sm_max,
                 "sm_mhz_min": min(r[1] for r in rows), "reasons": reasons, "samples": len(rows),
                 "power_w_median": round(statistics.median(r[3] for r in rows), 1),
-                "source": "nvml every ~1 ms (separate process) during the timed steps"}
+                "source": "nvml every ~1 ms (separate process) during the timed steps" + (
+                    f" (region shorter than the poll interval: samples within {widened * 1e3:.0f} ms of it)" if widened else "")}
 
 
 # ---------------------------------------------------------------------------------- reference arm

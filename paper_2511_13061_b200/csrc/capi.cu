@@ -256,6 +256,7 @@ struct macko_dev_matrix {
     size_t smem = 0;
     size_t smem_budget = 0, per_slot = 0;  // dynamic smem left for x table + rings; bytes of one ring slot
     int grid = 0, ctas_per_sm = 0;
+    uint32_t warps_active = mk::kSpmvWarpsPerCta;  // warps per CTA with a plan record
     uint32_t n_chunks = 0, n_split = 0;
     uint64_t n_units = 0, n_slots = 0;
     DevBuf<uint32_t> plan_recs;  // W mk::WarpPlan records
@@ -483,6 +484,16 @@ void build_plan_device(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
     P.partials = nullptr;
 }
 
+// Warps per CTA that get a plan record (MACKO_ACTIVE_WARPS overrides, experiments).
+uint32_t choose_active_warps(const macko_dev_matrix* m) {
+    if (const char* e = std::getenv("MACKO_ACTIVE_WARPS")) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= mk::kSpmvWarpsPerCta) return (uint32_t)v;
+    }
+    (void)m;
+    return mk::kSpmvWarpsPerCta;
+}
+
 // Static plan: cut the unit stream into `W` equal-weight chunks (one per warp), see spmv.cuh.
 void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     using namespace mk;
@@ -536,7 +547,8 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     m->grid = m->sms * m->ctas_per_sm;
     // macko_dev_configure(ctas_per_sm = k > 0): use k/4 of the CTAs (a different plan, same y)
     if (m->force_ctas > 0) m->grid = std::max(1, std::min(m->grid, m->grid * m->force_ctas / 4));
-    const uint32_t W = (uint32_t)m->grid * kSpmvWarpsPerCta;
+    m->warps_active = choose_active_warps(m);
+    const uint32_t W = (uint32_t)m->grid * m->warps_active;
     m->n_chunks = W;
     // element indices are u32 in the kernel and the ring reads up to one chunk past pad_nnz
     if (m->pad_nnz > 0xFFFFFFFFull - 2 * kChunk) fail(MACKO_EINVAL, "pad_nnz within two chunks of 2^32: no SpMV plan");
@@ -1190,6 +1202,7 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
         a.delta_bytes = m->deltas.n;
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
+        a.warps_active = m->warps_active;
         a.plan = m->plan;
         a.plan.counters = w->counters.p;
         a.plan.partials = w->partials.p;
@@ -1222,6 +1235,12 @@ macko_status macko_dev_spmv_ex(const macko_dev_matrix* m, const uint16_t* d_x, u
 macko_status macko_dev_spmv(const macko_dev_matrix* m, const uint16_t* d_x, uint16_t* d_y, void* stream) {
     return macko_dev_spmv_ex(m, d_x, d_y, stream, 0);
 }
+
+// SpMM gather split when the interleaved table fits beside the rings (kb = 2 up to ~28k columns;
+// kb = 4 / 8 tables do not fit at 12288 columns and gather through the texture).  36864x12288
+// @50 %, batch 2 (tools/spmm_time.py): x_mode 8 (2 of 8 slots by TEX) 135.0 us, 1 (table only)
+// 137.6, 6 140.1, 7 178.3, 0 (texture only) 317.9.
+int spmm_table_mode(uint32_t kb) { return kb == 2 ? 8 : 7; }
 
 macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint64_t ldx, uint16_t* d_Y, uint64_t ldy,
                             uint32_t batch, void* stream) {
@@ -1267,7 +1286,11 @@ macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint
                                  (uint32_t)((m->cols * kb + 7) / 8 * 8), st),
            "interleave");
         const size_t table = align_up(2 * kb * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
-        const int mode = table + 2 * m->per_slot <= m->smem_budget ? 7 : 0;
+        int mode = table + 2 * m->per_slot <= m->smem_budget ? spmm_table_mode(kb) : 0;
+        if (const char* e = std::getenv("MACKO_SPMM_XMODE")) {  // experiments: force a gather split
+            const int f = std::atoi(e);
+            if (mk::spmm_valid_x_mode(f) && (f == 0 || table + 2 * m->per_slot <= m->smem_budget)) mode = f;
+        }
         mk::SpmvArgs a{};
         a.values = m->values.p;
         a.deltas = m->deltas.p;
@@ -1282,12 +1305,13 @@ macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint
         a.value_elems = m->values.n;
         a.delta_bytes = m->deltas.n;
         a.ring = mk::kMaxRing;
-        a.ring_offset = mode == 7 ? (uint32_t)table : 0u;
+        a.ring_offset = mode != 0 ? (uint32_t)table : 0u;
+        a.warps_active = m->warps_active;
         a.plan = m->plan;
         a.plan.counters = w->counters.p;
         a.plan.partials = w->partials.p;
         a.value_count = (uint32_t)m->pad_nnz;
-        const size_t smem = (mode == 7 ? table : 0) + mk::kMaxRing * m->per_slot;
+        const size_t smem = (mode != 0 ? table : 0) + mk::kMaxRing * m->per_slot;
         ck(mk::launch_spmm(a, (int)kb, m->grid, mode, smem, st), "macko_spmm launch");
         g_launches.fetch_add(2);
     });

@@ -338,6 +338,21 @@ __global__ void __launch_bounds__(kCompressWarpsPerCta * kWarp, 4)
     }
 }
 
+// Nonzero mask of the 16 fp16 values in w[0..7] (bit k = value k; +-0 are zero), byte-SIMD: per
+// word (v & 0x7FFF7FFF) + 0x7FFF7FFF sets bit 15 / 31 iff the low / high half is nonzero (no carry
+// crosses bit 15), PRMT packs those bytes four at a time and one multiply gathers the four flags.
+__device__ __forceinline__ uint32_t nz_mask16(const uint32_t (&w)[8]) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t t0 = (w[2 * q] & 0x7FFF7FFFu) + 0x7FFF7FFFu;
+        const uint32_t t1 = (w[2 * q + 1] & 0x7FFF7FFFu) + 0x7FFF7FFFu;
+        const uint32_t b = (__byte_perm(t0, t1, 0x7531) >> 7) & 0x01010101u;  // flags of values 4q..4q+3
+        m |= ((b * 0x01020408u) >> 24) << (4 * q);  // flag k of the group -> bit 24 + k
+    }
+    return m;
+}
+
 // b_delta = 4 emitter (the benchmark width): the same classification as emit_rows<true, 16>, with
 // the output path rebuilt around 16-byte stores.  Stage position q of a warp's value stage is
 // global value vbase + q with vbase 8-aligned, so every complete 8-value group leaves as one
@@ -392,11 +407,16 @@ __global__ void __launch_bounds__(kE4Warps * kWarp, 4)
         next[1] = fetch8(row, 16 * lane + 8, cols, vec_base);
         for (uint32_t c0 = 0; c0 < cols && (int)c0 <= L; c0 += kE4Step) {
             const uint32_t c = c0 + 16 * lane;
-            uint16_t h[16];
-            const uint32_t nz = unpack8(next[0], h) | (unpack8(next[1], h + 8) << 8);
+            const uint32_t w[8] = {next[0].x, next[0].y, next[0].z, next[0].w, next[1].x, next[1].y, next[1].z, next[1].w};
+            const uint32_t nz = nz_mask16(w);
             if (c0 + kE4Step < cols && (int)(c0 + kE4Step) <= L) {
-                next[0] = fetch8(row, c + kE4Step, cols, vec_base);
-                next[1] = fetch8(row, c + kE4Step + 8, cols, vec_base);
+                if (vec_base && c0 + 2 * kE4Step <= cols) {  // whole next step in bounds: plain 16-byte loads
+                    next[0] = __ldg(reinterpret_cast<const uint4*>(row + c + kE4Step));
+                    next[1] = __ldg(reinterpret_cast<const uint4*>(row + c + kE4Step + 8));
+                } else {
+                    next[0] = fetch8(row, c + kE4Step, cols, vec_base);
+                    next[1] = fetch8(row, c + kE4Step + 8, cols, vec_base);
+                }
             }
             const int lane_last = nz ? (int)(c + 31 - __clz(nz)) : -1;
             const int p = prev_nonzero(lane_last, lane, carry);
@@ -424,13 +444,18 @@ __global__ void __launch_bounds__(kE4Warps * kWarp, 4)
                 if (lane >= off) incl += t;
             }
             const uint32_t tot = __shfl_sync(kFull, incl, kWarp - 1);
-            // values: one predicated 2-byte store per entry at a running stage address
+            // values: the pad (+0; it precedes the lane's nonzeros) then one predicated 2-byte store
+            // per nonzero at a running stage address, straight from the loaded words
             uint32_t va = vst_s + 2u * (vP + incl - n);
+            if (pb) {
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(va), "h"((uint16_t)0) : "memory");
+                va += 2u;
+            }
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                if ((em >> k) & 1u) {
-                    const uint16_t val = ((nz >> k) & 1u) ? h[k] : (uint16_t)0;  // pads are +0
-                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(va), "h"(val) : "memory");
+                if ((nz >> k) & 1u) {
+                    const uint32_t v32 = (k & 1) ? w[k >> 1] >> 16 : w[k >> 1];
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(va), "r"(v32) : "memory");
                     va += 2u;
                 }
             }

@@ -907,14 +907,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t w = blockIdx.x * kSpmvWarpsPerCta + warp;
+    const bool active = warp < a.warps_active;
+    const uint32_t w = blockIdx.x * a.warps_active + warp;  // this warp's plan record (active warps)
     const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     MK_TRACE(0);
     // Programmatic dependent launch (chains of SpMVs): the next kernel in the stream may start
     // its prologue (plan record, first matrix ring fills) on SMs this grid has left; everything
     // it reads before griddepcontrol.wait is static matrix data.  No-ops without the attribute.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const PlanRecord pr = load_record(a, w);
+    const PlanRecord pr = active ? load_record(a, w) : PlanRecord{};
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem) + kXGuardLo * kB;
     __shared__ __align__(8) uint64_t xbar_s;
     const uint32_t xbar = static_cast<uint32_t>(__cvta_generic_to_shared(&xbar_s));
@@ -1021,24 +1022,27 @@ static cudaError_t launch_spmm_one(const SpmvArgs& a, int grid, size_t smem, cud
     return cudaGetLastError();
 }
 
+template <int kXMode>
+static cudaError_t launch_spmm_mode(const SpmvArgs& a, int kb, int grid, size_t smem, cudaStream_t s) {
+    switch (kb) {
+        case 2: return launch_spmm_one<kXMode, 2>(a, grid, smem, s);
+        case 4: return launch_spmm_one<kXMode, 4>(a, grid, smem, s);
+        case 8: return launch_spmm_one<kXMode, 8>(a, grid, smem, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool spmm_valid_x_mode(int x_mode) { return x_mode == 0 || x_mode == 1 || x_mode == 6 || x_mode == 7 || x_mode == 8; }
+
 cudaError_t launch_spmm(const SpmvArgs& a, int kb, int grid, int x_mode, size_t smem, cudaStream_t s) {
-    if (x_mode == 0) {
-        switch (kb) {
-            case 2: return launch_spmm_one<0, 2>(a, grid, smem, s);
-            case 4: return launch_spmm_one<0, 4>(a, grid, smem, s);
-            case 8: return launch_spmm_one<0, 8>(a, grid, smem, s);
-            default: return cudaErrorInvalidValue;
-        }
+    switch (x_mode) {
+        case 0: return launch_spmm_mode<0>(a, kb, grid, smem, s);
+        case 1: return launch_spmm_mode<1>(a, kb, grid, smem, s);
+        case 6: return launch_spmm_mode<6>(a, kb, grid, smem, s);
+        case 7: return launch_spmm_mode<7>(a, kb, grid, smem, s);
+        case 8: return launch_spmm_mode<8>(a, kb, grid, smem, s);
+        default: return cudaErrorInvalidValue;
     }
-    if (x_mode == 7) {
-        switch (kb) {
-            case 2: return launch_spmm_one<7, 2>(a, grid, smem, s);
-            case 4: return launch_spmm_one<7, 4>(a, grid, smem, s);
-            case 8: return launch_spmm_one<7, 8>(a, grid, smem, s);
-            default: return cudaErrorInvalidValue;
-        }
-    }
-    return cudaErrorInvalidValue;
 }
 
 // XT[c * kb + b] = X[b][c] (b < batch; 0 for the padding vectors), the SpMM's interleaved x.

@@ -58,6 +58,8 @@ struct SpmvArgs {
     uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
     uint32_t batch;        // SpMM: vectors in the batch (<= the kernel's kB); x = XT interleaved
     uint64_t ldy;          // SpMM: element stride between the batch's y vectors
+    uint32_t warps_active; // warps per CTA that own a plan record (the rest only stage x); record of
+                           // warp k of CTA c: c * warps_active + k
     SpmvPlanDev plan;
 };
 
@@ -103,6 +105,7 @@ cudaError_t launch_spmv(const SpmvArgs& a, int bits, int grid, int x_mode, size_
 // Small-batch SpMM over a b_delta = 4 matrix: kb in {2, 4, 8}, x_mode 0 (texture) or 7 (split);
 // a.x is the interleaved XT (launch_interleave), a.xtex a texture of 2 kb-byte texels over it.
 cudaError_t launch_spmm(const SpmvArgs& a, int kb, int grid, int x_mode, size_t smem, cudaStream_t s);
+bool spmm_valid_x_mode(int x_mode);  // 0 (texture), 1 (table), 6 / 7 / 8 (split)
 cudaError_t launch_interleave(const uint16_t* X, uint64_t ldx, uint32_t batch, uint32_t kb, uint32_t cols,
                               uint16_t* XT, uint32_t n_total, cudaStream_t s);
 constexpr uint32_t kMaxBatch = 8;
