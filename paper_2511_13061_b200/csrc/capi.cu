@@ -210,7 +210,6 @@ struct PhaseTimer {
 uint64_t values_bytes(uint64_t pad_nnz) { return align_up(pad_nnz * 2, 16); }
 uint64_t delta_bytes(uint64_t pad_nnz, unsigned bits) { return align_up((pad_nnz * bits + 7) / 8, 16); }
 
-constexpr uint64_t kRowOverhead = 128;      // plan weight of starting a row (element equivalents)
 
 }  // namespace
 
@@ -320,9 +319,10 @@ void build_plan_host(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
         n_r = T >= (uint64_t)kUnitSteps ? T / kUnitSteps : 1;  // the last unit absorbs a short remainder
     };
     auto unit_end_step = [&](uint64_t T, uint64_t n_r, uint64_t j) { return j + 1 == n_r ? T : (j + 1) * kUnitSteps; };
+    const uint64_t row_w = plan_row_weight();
     auto unit_weight = [&](uint64_t T, uint64_t n_r, uint64_t j) {
         const uint64_t steps = unit_end_step(T, n_r, j) - std::min<uint64_t>(T, j * kUnitSteps);
-        return steps * kStepElts + (j == 0 ? kRowOverhead : 0);
+        return steps * kStepElts + (j == 0 ? row_w : 0);
     };
     uint64_t total_w = 0, U = 0;
     for (uint64_t r = 0; r < R; ++r) {
@@ -466,7 +466,7 @@ void build_plan_device(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
     release_workspaces(m);
     m->plan_recs.alloc((uint64_t)W * sizeof(WarpPlan) / 4);
     m->plan_u32.alloc(4 * (uint64_t)std::max<uint32_t>(W, 1));
-    ck(plan_build_device(m->row_ptrs.p, (uint32_t)R, (uint32_t)m->pad_nnz, W, ub, m->sms, t,
+    ck(plan_build_device(m->row_ptrs.p, (uint32_t)R, (uint32_t)m->pad_nnz, W, ub, m->sms, plan_row_weight(), t,
                          reinterpret_cast<WarpPlan*>(m->plan_recs.p), reinterpret_cast<uint4*>(m->plan_u32.p), d_tot, st),
        "plan build");
     ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<WarpPlan*>(m->plan_recs.p), W, st), "plan colbase");

@@ -2,7 +2,7 @@
 //
 // The same plan as the host builder (capi.cu build_plan_host): every row is cut into units of
 // kUnitSteps warp steps from its 8-aligned start (the last unit absorbs a shorter remainder), unit
-// weights are steps * 256 elements (+ kRowOverhead for a row's first unit), and unit u goes to
+// weights are steps * 256 elements (+ plan_row_weight() for a row's first unit), and unit u goes to
 // warp k(u) = min(W - 1, floor((2 cw(u) + w(u)) W / (2 total))) — its weight midpoint on an
 // equal-weight grid of W warps, cw(u) the weight before u.  k(u) never decreases, so warp k owns
 // the contiguous units [first unit with k(u) >= k, first unit with k(u) > k).  Rows cut between
@@ -21,12 +21,12 @@
 #include "spmv.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mk {
 
 namespace {
 
-constexpr uint32_t kRowOverheadW = 128;  // plan weight of starting a row (element equivalents)
 
 __device__ __forceinline__ void row_geom(const uint32_t* rp, uint32_t r, uint32_t& s, uint32_t& e, uint32_t& al,
                                          uint32_t& T, uint32_t& n_r) {
@@ -41,12 +41,12 @@ __device__ __forceinline__ uint32_t unit_end_step(uint32_t T, uint32_t n_r, uint
     return j + 1 == n_r ? T : (j + 1) * kUnitSteps;
 }
 
-__global__ void plan_rows_kernel(const uint32_t* rp, uint32_t rows, uint32_t* nu, unsigned long long* rw) {
+__global__ void plan_rows_kernel(const uint32_t* rp, uint32_t rows, uint32_t row_w, uint32_t* nu, unsigned long long* rw) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
         uint32_t s, e, al, T, n_r;
         row_geom(rp, r, s, e, al, T, n_r);
         nu[r] = n_r;
-        rw[r] = (unsigned long long)T * kStepElts + kRowOverheadW;
+        rw[r] = (unsigned long long)T * kStepElts + row_w;
     }
 }
 
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(const T* in, uint32_t n, T* 
     if (t == nt - 1) out[n] = run;
 }
 
-__global__ void plan_units_kernel(const uint32_t* rp, uint32_t rows, const uint32_t* uo,
+__global__ void plan_units_kernel(const uint32_t* rp, uint32_t rows, uint32_t row_w, const uint32_t* uo,
                                   const unsigned long long* cw, uint32_t W, uint32_t* ku, uint32_t* urow,
                                   uint32_t* uj) {
     const unsigned long long total = cw[rows];
@@ -97,7 +97,7 @@ __global__ void plan_units_kernel(const uint32_t* rp, uint32_t rows, const uint3
         unsigned long long c = cw[r];
         for (uint32_t j = 0; j < n_r; ++j) {
             const uint32_t steps = unit_end_step(T, n_r, j) - min(T, j * kUnitSteps);
-            const unsigned long long w = (unsigned long long)steps * kStepElts + (j == 0 ? kRowOverheadW : 0u);
+            const unsigned long long w = (unsigned long long)steps * kStepElts + (j == 0 ? row_w : 0u);
             const unsigned __int128 mid2 = 2 * (unsigned __int128)c + w;
             unsigned long long k = (unsigned long long)(mid2 * W / den);
             if (k >= W) k = W - 1;
@@ -218,12 +218,18 @@ int grid_of(uint64_t n, int sms) { return (int)std::max<uint64_t>(1, std::min<ui
 
 }  // namespace
 
+uint32_t plan_row_weight() {
+    if (const char* e = std::getenv("MACKO_ROW_WEIGHT")) return (uint32_t)std::strtoul(e, nullptr, 10);
+    return kPlanRowWeight;
+}
+
 cudaError_t plan_build_device(const uint32_t* rp, uint32_t rows, uint32_t pad_nnz, uint32_t W, uint64_t ubound, int sms,
-                              const PlanTemp& t, WarpPlan* recs, uint4* splits, PlanTotals* d_totals, cudaStream_t s) {
-    plan_rows_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, t.nu, t.rw);
+                              uint32_t row_weight, const PlanTemp& t, WarpPlan* recs, uint4* splits, PlanTotals* d_totals,
+                              cudaStream_t s) {
+    plan_rows_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, row_weight, t.nu, t.rw);
     scan_kernel<uint32_t><<<1, 1024, 0, s>>>(t.nu, rows, t.uo);
     scan_kernel<unsigned long long><<<1, 1024, 0, s>>>(t.rw, rows, t.cw);
-    plan_units_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, t.uo, t.cw, W, t.ku, t.urow, t.uj);
+    plan_units_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, row_weight, t.uo, t.cw, W, t.ku, t.urow, t.uj);
     plan_chunk_init_kernel<<<grid_of(W + 1, sms), 256, 0, s>>>(W, t.uo + rows, t.chunk_unit, t.chunk_row, t.chunk_j,
                                                               t.chunk_sid);
     plan_starts_kernel<<<grid_of(ubound, sms), 256, 0, s>>>(t.ku, t.urow, t.uj, t.uo + rows, t.chunk_unit, t.chunk_row,

@@ -26,10 +26,22 @@ struct PlanTotals {
     uint32_t units, splits, slots, pad;
 };
 
+// Plan weight of starting a row, in element equivalents (both builders).  Measured (traces of
+// 36864x12288, tools/trace_corr.py): a warp's lateness against its CTA's median regresses on its
+// elements and its rows with 1.64 us per row vs 0.70 us per 1000 elements (R^2 0.84 with split
+// pieces and warp index): a row start (edge pairs, row set-up, y store) costs ~2000 elements of
+// walk, not the 128 the first plans used.  MACKO_ROW_WEIGHT overrides (experiments).
+#ifndef MACKO_PLAN_ROW_WEIGHT
+#define MACKO_PLAN_ROW_WEIGHT 128
+#endif
+constexpr uint32_t kPlanRowWeight = MACKO_PLAN_ROW_WEIGHT;
+uint32_t plan_row_weight();
+
 inline uint64_t plan_unit_bound(uint64_t rows, uint64_t pad_nnz) { return 2 * rows + pad_nnz / kUnitElts + 16; }
 
 // Fills recs[W], splits[<= W] and *d_totals; stream-ordered, no host synchronisation.
 cudaError_t plan_build_device(const uint32_t* rp, uint32_t rows, uint32_t pad_nnz, uint32_t W, uint64_t ubound, int sms,
-                              const PlanTemp& t, WarpPlan* recs, uint4* splits, PlanTotals* d_totals, cudaStream_t s);
+                              uint32_t row_weight, const PlanTemp& t, WarpPlan* recs, uint4* splits, PlanTotals* d_totals,
+                              cudaStream_t s);
 
 }  // namespace mk

@@ -631,7 +631,7 @@ __device__ __forceinline__ void fill_chunk(const Ring& g, const SpmvArgs& a, uin
 
 // Ring set-up for the warp's element stream [E0, E1): the barriers are initialised and the first
 // fill is one copy per array.
-template <int kBits>
+template <int kBits, bool kStagger>
 __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint32_t E1, uint32_t warp, int lane,
                                            uint32_t smem_base, uint32_t bar0, Ring& g) {
     constexpr uint32_t ring = kMaxRing;  // the host sizes a.ring_offset for exactly this ring
@@ -657,7 +657,7 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
         // copy per array fills them all and completes on barrier 0; the other barriers complete
         // their first phase with a plain arrive (the consumer passes barrier 0 first).
         // PDL launches (decode chains): chunk 0 alone now, the rest after the CTA barrier.
-        if (n && !a.pdl) {
+        if (n && !kStagger) {
             asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g.bar0),
                          "r"(n * (kChunkVBytes + dbytes<kBits>()))
                          : "memory");
@@ -674,13 +674,13 @@ __device__ __forceinline__ void ring_begin(const SpmvArgs& a, uint32_t E0, uint3
 }
 
 // Set up the warp's ring and ROMA walk for one SpMV (plan record pr) and issue the first fills.
-template <int kBits, int kB>
+template <int kBits, int kB, bool kStagger>
 __device__ __forceinline__ bool op_begin(const SpmvArgs& a, const PlanRecord& pr, uint32_t warp, int lane,
                                          uint32_t smem_base, uint32_t bar0, Ring& g, RowState<kB>& rs) {
     const uint4 q0 = pr.q0, q1 = pr.q1, q2 = pr.q2;
     MK_TRACE(1);
     if (q0.x == 0) return false;
-    ring_begin<kBits>(a, q0.w, q1.x, warp, lane, smem_base, bar0, g);
+    ring_begin<kBits, kStagger>(a, q0.w, q1.x, warp, lane, smem_base, bar0, g);
     rs.r = q0.y;
     rs.units_left = q0.x;
     rs.s = q1.y;
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     // The first ring fills go out before a PDL wait; x staging overlaps their HBM latency.
     RowState<kB> rs;
     Ring g;
-    const bool has_work = op_begin<kBits, kB>(a, pr, warp, lane, smem_base,
+    const bool has_work = op_begin<kBits, kB, kChain>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
 #ifdef MACKO_RING_FIRST
     if (!a.pdl) stage_x<kXMode, kB>(a, xs);
@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     }
     MK_TRACE(4);
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    if (a.pdl && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin)
+    if (kChain && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin)
         for (uint32_t i = 1; i < min(kMaxRing, g.n_chunks); ++i) fill_chunk<kBits>(g, a, i);
     if (has_work) run_rows<kXMode, kBits, kB, kChain>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
@@ -996,6 +996,11 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     return e;
 }
 
+#ifndef MACKO_CHAIN_FOR_ALL
+#define MACKO_CHAIN_FOR_ALL 0
+#endif
+constexpr bool kChainForAll = MACKO_CHAIN_FOR_ALL;  // experiments: the chain instance for every launch
+
 template <int kXMode, int kBits>
 static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStream_t s, bool pdl) {
     cudaLaunchConfig_t cfg{};
@@ -1008,7 +1013,7 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (pdl) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
+    if (pdl || kChainForAll) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 

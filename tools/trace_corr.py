@@ -2,7 +2,7 @@
 same matrix (trace build, make trace): correlation of each warp's done time relative to its CTA's
 median, and of that with the warp's element count and row count (from the plan records).
     MACKO_LIB=paper_2511_13061_b200/libmacko_cuda_trace.so python tools/trace_corr.py"""
-import ctypes as C
+import ctypes
 import os
 import sys
 
@@ -23,7 +23,7 @@ x = torch.empty(C, dtype=torch.float16, device="cuda")
 M.gen_vector(x, C, seed=4321)
 y = torch.empty(R, dtype=torch.float16, device="cuda")
 L = _lib.load()
-L.macko_trace_read.argtypes = [C.c_void_p, C.c_size_t]
+L.macko_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 flush = torch.ones(256 << 20, dtype=torch.float32, device="cuda")
 
 
@@ -56,3 +56,37 @@ print(f"corr(CTA last warp run1, run2): {np.corrcoef(da.max(axis=1), db.max(axis
 print("CTA last warp (us): run1 min/med/max", np.round([da.max(1).min(), np.median(da.max(1)), da.max(1).max()], 2),
       "run2", np.round([db.max(1).min(), np.median(db.max(1)), db.max(1).max()], 2))
 print("mean done - CTA median by warp index:", " ".join(f"{v:+.1f}" for v in ((a + b) / 2).mean(axis=0)))
+
+# ---- what predicts a warp's lateness: regression on plan features (both runs averaged)
+h = dm.download()
+rp = h.row_pointers.astype(np.int64)
+T = np.where(rp[1:] > rp[:-1], (rp[1:] - (rp[:-1] & ~7) + 255) // 256, 0)
+n_r = np.where(T >= 8, T // 8, 1)
+rows_of = np.zeros(148 * 32)
+for k in range(148 * 32):
+    u_left, r, j = int(rec[k, 0]), int(rec[k, 1]), int(rec[k, 2])
+    cnt = 0
+    while u_left > 0:
+        take = min(int(n_r[r]) - j, u_left)
+        cnt += 1
+        u_left -= take
+        r += 1
+        j = 0
+    rows_of[k] = cnt
+splits = ((rec[:, 8].view(np.int32) >= 0).astype(int) + (rec[:, 9].view(np.int32) >= 0).astype(int)).astype(np.float64)
+y_dev = ((a + b) / 2).reshape(-1)
+wi = np.tile(np.arange(32), 148).astype(np.float64)
+el = elems.reshape(-1).astype(np.float64)
+# deviations from the CTA mean for the per-warp features
+def dev(v):
+    v = v.reshape(148, 32)
+    return (v - v.mean(axis=1, keepdims=True)).reshape(-1)
+X = np.stack([dev(el), dev(rows_of), dev(splits), dev(wi)], axis=1)
+ok = np.isfinite(y_dev)
+coef, *_ = np.linalg.lstsq(X[ok], y_dev[ok], rcond=None)
+pred = X @ coef
+r2 = 1 - np.var(y_dev[ok] - pred[ok]) / np.var(y_dev[ok])
+print("regression of done - CTA median (us) on [elements, rows, split pieces, warp index] deviations:")
+print("  coef:", [f"{c:.3e}" for c in coef], f" R^2 {r2:.3f}")
+print(f"  elements std {dev(el).std():.0f}, rows std {dev(rows_of).std():.2f}, splits std {dev(splits).std():.2f}")
+print(f"  us per 1000 elements {coef[0] * 1e3:.3f}; us per row {coef[1]:.3f}; us per split piece {coef[2]:.3f}; us per warp index {coef[3]:.4f}")
