@@ -364,7 +364,10 @@ __device__ __forceinline__ uint32_t nz_mask16(const uint32_t (&w)[8]) {
 constexpr int kE4Warps = 8;
 constexpr uint32_t kE4Step = kWarp * 16;  // columns per warp step
 
-__global__ void __launch_bounds__(kE4Warps * kWarp, 4)
+#ifndef MACKO_E4_MINB
+#define MACKO_E4_MINB 4
+#endif
+__global__ void __launch_bounds__(kE4Warps * kWarp, MACKO_E4_MINB)
     emit_rows4(const uint16_t* dense, uint64_t ld, uint32_t rows, uint32_t cols, const uint32_t* row_ptrs,
                const int32_t* lastcol, uint16_t* values, uint32_t* delta_words) {
     constexpr uint32_t bits = 4, maxd = 16;

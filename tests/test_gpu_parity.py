@@ -669,3 +669,75 @@ def test_block_cache_reuse_keeps_formats_exact(cuda):
     assert _lib.load().macko_release_cached_memory() == 0
     A = O.gen_dense(512, 4096, 0.5, 5)
     assert_same_format(gpu_encode(A, 4), O.encode_dense(A, 4), "after release")
+
+
+# ------------------------------------------------------------------------------ chain (PDL) instance
+def gpu_spmv_pdl(dm: M.DeviceMatrix, x: np.ndarray) -> np.ndarray:
+    """SpMV through the PDL launch (the chain kernel instance: staggered first fill, per-step edge
+    masking, x staged by one bulk copy)."""
+    xd = to_dev(x)
+    y = torch.empty(dm.rows, dtype=torch.float16, device=xd.device)
+    dm.spmv_into(xd, y, pdl=True)
+    torch.cuda.synchronize()
+    return to_host_u16(y)
+
+
+def _ragged_rows(R, C, seed):
+    """Rows of every edge shape the walk distinguishes: empty, 1..7 elements (ROMA head only),
+    one step (T = 1), two steps (T = 2: first and last pair are one), three (first pair then a
+    single step), odd / even longer rows, rows spanning several warps."""
+    rng = np.random.default_rng(seed)
+    A = np.zeros((R, C), np.uint16)
+    lengths = [0, 1, 3, 7, 9, 200, 256, 300, 511, 512, 513, 700, 768, 1000, 1024, 1500, 2600, C]
+    for r in range(R):
+        n = lengths[r % len(lengths)] if r % 5 else int(rng.integers(0, C))
+        cols = np.sort(rng.choice(C, size=min(n, C), replace=False))
+        A[r, cols] = _random_values(rng, cols.size)
+    return A
+
+
+@pytest.mark.parametrize("x_mode", [-1, 0, 1, 6, 7, 8, 10])
+def test_pdl_instance_every_edge_shape(cuda, x_mode):
+    # The PDL kernel instance masks edge pairs step by step (EdgeFirst / EdgeFirstLast / EdgeLast /
+    # EdgeSingle) and stages x with one bulk copy; its y must equal the plain instance's and the
+    # oracle order bit for bit, for every row shape and ROMA offset.
+    for R, C, seed in ((300, 3000, 1), (97, 4099, 2), (64, 6000, 3)):
+        A = _ragged_rows(R, C, seed)
+        x = O.gen_vector(C, 10 + seed)
+        m = O.encode_dense(A)
+        dm = gpu_encode(A)
+        if x_mode >= 0:
+            dm.configure(x_mode)
+        ref = b200_y(m, x)
+        assert np.array_equal(gpu_spmv_pdl(dm, x), ref), (R, C, x_mode, "pdl")
+        assert np.array_equal(gpu_spmv(dm, x), ref), (R, C, x_mode, "plain")
+
+
+@pytest.mark.parametrize("bits", [1, 2, 8])
+def test_pdl_instance_other_widths(cuda, bits):
+    A = _ragged_rows(200, 5000, 40 + bits)
+    x = O.gen_vector(5000, 41)
+    m = O.encode_dense(A, bits)
+    dm = gpu_encode(A, bits)
+    assert np.array_equal(gpu_spmv_pdl(dm, x), b200_y(m, x)), bits
+
+
+def test_pdl_instance_masked_edges_do_not_leak_inf_nan(cuda):
+    R, C = 240, 1500
+    A = O.gen_dense(R, C, 0.35, 21)
+    A[0::2, 700:] = 0
+    A[0::2, 699] = 0x3C00
+    for r in range(1, R, 2):
+        cols = np.nonzero(A[r])[0]
+        A[r, cols[:: max(1, cols.size // 4)]] = np.uint16(0x7C00)
+        A[r, cols[1]] = np.uint16(0x7E00)
+    x = O.gen_vector(C, 22)
+    x[700::3] = np.uint16(0x7C00)
+    x[701::3] = np.uint16(0xFC00)
+    x[702::3] = np.uint16(0x7E00)
+    dm = gpu_encode(A)
+    m = O.encode_dense(A)
+    y = gpu_spmv_pdl(dm, x)
+    y_ref = b200_y(m, x)
+    assert _same_or_both_nan(y, y_ref)
+    assert np.array_equal(y[0::2], y_ref[0::2])
