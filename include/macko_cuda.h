@@ -159,6 +159,12 @@ macko_status macko_dev_validate(const macko_dev_matrix* m, void* stream);
 
 macko_status macko_dev_free(macko_dev_matrix* m);
 
+/* Re-plan a matrix for PDL-chained launches (decoder stacks): in a chain, CTA c of an SpMV starts
+ * when the previous SpMV releases the c-th SM, up to start_spread_ns after CTA 0, so the plan gives
+ * late CTAs proportionally less work.  0 restores the equal split.  y is unchanged (the summation
+ * order never depends on the plan).  Synchronises the stream. */
+macko_status macko_dev_set_chain_skew(macko_dev_matrix* m, uint32_t start_spread_ns, void* stream);
+
 /* Device blocks of >= 1 MiB released by the library (matrices freed, compressor scratch) are kept
  * per process (up to 4 GiB) and reused by later builds; a release synchronises the device first,
  * as cudaFree does.  This returns every cached block to the driver. */

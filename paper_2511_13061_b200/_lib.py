@@ -18,7 +18,7 @@ MACKO_OK, MACKO_EINVAL, MACKO_EFORMAT, MACKO_EIO, MACKO_EINFEASIBLE, MACKO_ECUDA
 EXPORTS = (
     "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_from_csr", "macko_csr_from_dense",
     "macko_dev_to_dense", "macko_dev_padding_count", "macko_dev_get_info",
-    "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_dev_spmm", "macko_spmv_host", "macko_dev_validate", "macko_dev_free", "macko_release_cached_memory",
+    "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_dev_spmm", "macko_spmv_host", "macko_dev_validate", "macko_dev_free", "macko_release_cached_memory", "macko_dev_set_chain_skew",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
     "macko_dev_launch_info", "macko_dev_plan_records", "macko_dev_configure", "macko_kernel_launches",
     "macko_mcko_write", "macko_mcko_read_info", "macko_mcko_read", "macko_mcko_write_dev", "macko_mcko_read_dev",
@@ -116,6 +116,8 @@ def load() -> C.CDLL:
     L.macko_dev_free.argtypes = [vp]
     L.macko_release_cached_memory.restype = st
     L.macko_release_cached_memory.argtypes = []
+    L.macko_dev_set_chain_skew.restype = st
+    L.macko_dev_set_chain_skew.argtypes = [vp, C.c_uint32, vp]
     L.macko_density_threshold.restype = u32
     L.macko_density_threshold.argtypes = [C.c_double]
     L.macko_gen_dense.restype = st

@@ -32,6 +32,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint32_t> g_trace_slot{0};  // trace builds: round-robin slot of each SpMV launch
 
 struct Failure {
     macko_status code;
@@ -256,6 +257,7 @@ struct macko_dev_matrix {
     size_t smem_budget = 0, per_slot = 0;  // dynamic smem left for x table + rings; bytes of one ring slot
     int grid = 0, ctas_per_sm = 0;
     uint32_t warps_active = mk::kSpmvWarpsPerCta;  // warps per CTA with a plan record
+    uint32_t plan_skew = 0;                        // PlanGrid::R for K = 65536 (macko_dev_set_chain_skew)
     uint32_t n_chunks = 0, n_split = 0;
     uint64_t n_units = 0, n_slots = 0;
     DevBuf<uint32_t> plan_recs;  // W mk::WarpPlan records
@@ -297,6 +299,10 @@ void release_workspaces(macko_dev_matrix* m) {
         m->ws_of.clear();
         m->ws_pool.clear();
     }
+}
+
+mk::PlanGrid plan_grid(const macko_dev_matrix* m) {
+    return mk::PlanGrid{(uint32_t)m->grid, m->warps_active, 65536u, m->plan_skew};
 }
 
 // The plan's reference implementation on the host (MACKO_HOST_PLAN=1; tests compare it with the
@@ -349,8 +355,7 @@ void build_plan_host(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
         for (uint64_t j = 0; j < n_r; ++j, ++u) {
             const uint64_t w = unit_weight(T, n_r, j);
             const uint64_t mid2 = 2 * cw + w;  // twice the unit midpoint
-            int64_t k = (int64_t)((unsigned __int128)mid2 * W / (2 * (unsigned __int128)std::max<uint64_t>(total_w, 1)));
-            if (k >= (int64_t)W) k = W - 1;
+            int64_t k = (int64_t)plan_warp_of(mid2, 2 * (unsigned __int128)std::max<uint64_t>(total_w, 1), plan_grid(m));
             if (k < prev_k) k = prev_k;
             for (int64_t q = prev_k + 1; q <= k; ++q) {
                 chunk_unit[q] = (uint32_t)u;
@@ -466,7 +471,7 @@ void build_plan_device(macko_dev_matrix* m, cudaStream_t st, uint32_t W) {
     release_workspaces(m);
     m->plan_recs.alloc((uint64_t)W * sizeof(WarpPlan) / 4);
     m->plan_u32.alloc(4 * (uint64_t)std::max<uint32_t>(W, 1));
-    ck(plan_build_device(m->row_ptrs.p, (uint32_t)R, (uint32_t)m->pad_nnz, W, ub, m->sms, plan_row_weight(), t,
+    ck(plan_build_device(m->row_ptrs.p, (uint32_t)R, (uint32_t)m->pad_nnz, plan_grid(m), ub, m->sms, plan_row_weight(), t,
                          reinterpret_cast<WarpPlan*>(m->plan_recs.p), reinterpret_cast<uint4*>(m->plan_u32.p), d_tot, st),
        "plan build");
     ck(launch_plan_colbase(m->deltas.p, m->b_delta, reinterpret_cast<WarpPlan*>(m->plan_recs.p), W, st), "plan colbase");
@@ -1203,6 +1208,9 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
         a.ring = m->ring;
         a.ring_offset = (uint32_t)m->ring_offset;
         a.warps_active = m->warps_active;
+#ifdef MACKO_TRACE
+        a.trace_slot = g_trace_slot.fetch_add(1);
+#endif
         a.plan = m->plan;
         a.plan.counters = w->counters.p;
         a.plan.partials = w->partials.p;
@@ -1719,6 +1727,24 @@ macko_status macko_dev_configure(macko_dev_matrix* m, int x_mode, int ctas_per_s
     });
 }
 
+macko_status macko_dev_set_chain_skew(macko_dev_matrix* m, uint32_t start_spread_ns, void* stream) {
+    return guarded([&] {
+        if (!m) fail(MACKO_EINVAL, "null handle");
+        DeviceGuard g(m->device);
+        std::lock_guard<std::mutex> lk(m->mu);
+        // CTA c of a PDL-chained launch starts ~spread * c / (G-1) after CTA 0; its share is cut by
+        // r (1 - 2c/(G-1)) with r = spread / (2 T), T the mean CTA time at ~14 stored elements per
+        // ns per CTA (36864x12288 @50 %: 226 M elements, 148 CTAs, ~105 us of walk).
+        double r = 0.0;
+        if (start_spread_ns && m->pad_nnz && m->grid > 1) {
+            const double t_cta_ns = (double)m->pad_nnz / (double)m->grid / 14.0;
+            r = std::min(0.45, (double)start_spread_ns / (2.0 * t_cta_ns));
+        }
+        m->plan_skew = (uint32_t)std::lround(r * 65536.0);
+        build_plan(m, (cudaStream_t)stream);
+    });
+}
+
 macko_status macko_dev_plan_records(const macko_dev_matrix* m, void* recs, uint64_t recs_bytes, void* splits,
                                     uint64_t splits_bytes, void* stream) {
     return guarded([&] {
@@ -1752,6 +1778,7 @@ macko_status macko_dev_launch_info(const macko_dev_matrix* m, macko_launch_info*
 #ifdef MACKO_TRACE
 // trace build only (not declared in include/macko_cuda.h): per-warp prologue timestamps
 int macko_trace_read(unsigned long long* host, size_t n) { return (int)mk::trace_read(host, n); }
+unsigned macko_trace_slot_counter(void) { return g_trace_slot.load(); }
 #endif
 
 }  // extern "C"

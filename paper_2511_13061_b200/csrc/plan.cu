@@ -4,7 +4,8 @@
 // kUnitSteps warp steps from its 8-aligned start (the last unit absorbs a shorter remainder), unit
 // weights are steps * 256 elements (+ plan_row_weight() for a row's first unit), and unit u goes to
 // warp k(u) = min(W - 1, floor((2 cw(u) + w(u)) W / (2 total))) — its weight midpoint on an
-// equal-weight grid of W warps, cw(u) the weight before u.  k(u) never decreases, so warp k owns
+// equal-weight grid of W warps, cw(u) the weight before u (plan_warp_of; a chain-skewed grid gives
+// early CTAs larger shares, plan.cuh PlanGrid).  k(u) never decreases, so warp k owns
 // the contiguous units [first unit with k(u) >= k, first unit with k(u) > k).  Rows cut between
 // warps get a split id, per-unit partial slots and an arrival count.
 //
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(const T* in, uint32_t n, T* 
 }
 
 __global__ void plan_units_kernel(const uint32_t* rp, uint32_t rows, uint32_t row_w, const uint32_t* uo,
-                                  const unsigned long long* cw, uint32_t W, uint32_t* ku, uint32_t* urow,
+                                  const unsigned long long* cw, PlanGrid grid, uint32_t* ku, uint32_t* urow,
                                   uint32_t* uj) {
     const unsigned long long total = cw[rows];
     const unsigned __int128 den = 2 * (unsigned __int128)(total ? total : 1ull);
@@ -99,8 +100,7 @@ __global__ void plan_units_kernel(const uint32_t* rp, uint32_t rows, uint32_t ro
             const uint32_t steps = unit_end_step(T, n_r, j) - min(T, j * kUnitSteps);
             const unsigned long long w = (unsigned long long)steps * kStepElts + (j == 0 ? row_w : 0u);
             const unsigned __int128 mid2 = 2 * (unsigned __int128)c + w;
-            unsigned long long k = (unsigned long long)(mid2 * W / den);
-            if (k >= W) k = W - 1;
+            const unsigned long long k = plan_warp_of(mid2, den, grid);
             const uint32_t u = uo[r] + j;
             ku[u] = (uint32_t)k;
             urow[u] = r;
@@ -223,13 +223,14 @@ uint32_t plan_row_weight() {
     return kPlanRowWeight;
 }
 
-cudaError_t plan_build_device(const uint32_t* rp, uint32_t rows, uint32_t pad_nnz, uint32_t W, uint64_t ubound, int sms,
-                              uint32_t row_weight, const PlanTemp& t, WarpPlan* recs, uint4* splits, PlanTotals* d_totals,
-                              cudaStream_t s) {
+cudaError_t plan_build_device(const uint32_t* rp, uint32_t rows, uint32_t pad_nnz, const PlanGrid& grid, uint64_t ubound,
+                              int sms, uint32_t row_weight, const PlanTemp& t, WarpPlan* recs, uint4* splits,
+                              PlanTotals* d_totals, cudaStream_t s) {
+    const uint32_t W = grid.G * grid.A;
     plan_rows_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, row_weight, t.nu, t.rw);
     scan_kernel<uint32_t><<<1, 1024, 0, s>>>(t.nu, rows, t.uo);
     scan_kernel<unsigned long long><<<1, 1024, 0, s>>>(t.rw, rows, t.cw);
-    plan_units_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, row_weight, t.uo, t.cw, W, t.ku, t.urow, t.uj);
+    plan_units_kernel<<<grid_of(rows, sms), 256, 0, s>>>(rp, rows, row_weight, t.uo, t.cw, grid, t.ku, t.urow, t.uj);
     plan_chunk_init_kernel<<<grid_of(W + 1, sms), 256, 0, s>>>(W, t.uo + rows, t.chunk_unit, t.chunk_row, t.chunk_j,
                                                               t.chunk_sid);
     plan_starts_kernel<<<grid_of(ubound, sms), 256, 0, s>>>(t.ku, t.urow, t.uj, t.uo + rows, t.chunk_unit, t.chunk_row,

@@ -39,13 +39,16 @@
 #ifdef MACKO_TRACE
 // Opt-in trace build (`make trace` -> libmacko_cuda_trace.so): per warp, %globaltimer at each
 // prologue phase and at the end, for latency studies of small SpMVs (tools/trace_spmv.py).
-__device__ unsigned long long g_macko_trace[148 * 32 * 8];
+// kTraceSlots launches are kept (SpmvArgs::trace_slot, set by the host round robin), so a chain
+// of SpMVs can be traced op by op (tools/trace_chain.py).
+constexpr int kTraceSlots = 8;
+__device__ unsigned long long g_macko_trace[kTraceSlots * 148 * 32 * 8];
 #define MK_TRACE(i)                                                                                    \
     do {                                                                                                \
         if ((threadIdx.x & 31) == 0 && blockIdx.x < 148) {                                              \
             unsigned long long t_;                                                                      \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
-            g_macko_trace[(blockIdx.x * 32 + (threadIdx.x >> 5)) * 8 + (i)] = t_;                       \
+            g_macko_trace[((a.trace_slot % kTraceSlots) * 148 * 32 + blockIdx.x * 32 + (threadIdx.x >> 5)) * 8 + (i)] = t_; \
         }                                                                                               \
     } while (0)
 #else

@@ -60,6 +60,7 @@ struct SpmvArgs {
     uint64_t ldy;          // SpMM: element stride between the batch's y vectors
     uint32_t warps_active; // warps per CTA that own a plan record (the rest only stage x); record of
                            // warp k of CTA c: c * warps_active + k
+    uint32_t trace_slot;   // trace builds only (MACKO_TRACE): which of the kept launches this is
     SpmvPlanDev plan;
 };
 

@@ -24,6 +24,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Tuple
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -65,11 +67,19 @@ def _out_name(name: str) -> str:
     return "h" if name == "down" else name
 
 
+# Start spread of a chained SpMV's CTAs the plans may be skewed for (macko_dev_set_chain_skew;
+# tools/trace_chain.py measures ~2 us between the first and the last CTA of each op).  Measured on
+# the 32-layer chain: 0 -> 2288, 1000 -> 2325, 2000 -> 2376, 3000 -> 2474 us per token, so the
+# equal split stays the default.
+CHAIN_SKEW_NS = int(os.environ.get("MACKO_CHAIN_SKEW_NS", "0"))
+
+
 class SparseDecoderChain:
     """The decode chain over MACKO matrices built on the GPU (generator -> GPU compressor)."""
 
     def __init__(self, shape: ChainShape = LLAMA2_7B, density: float = 0.5, seed: int = 0x5EEDA000,
-                 device: Optional[torch.device] = None, keep_dense: bool = False, group=None, fused: bool = False):
+                 device: Optional[torch.device] = None, keep_dense: bool = False, group=None, fused: bool = False,
+                 chain_skew_ns: int = CHAIN_SKEW_NS):
         self.shape = shape
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.group = group
@@ -98,6 +108,8 @@ class SparseDecoderChain:
                 w = torch.empty((r1 - r0, C), dtype=torch.float16, device=self.device)
                 M.gen_dense(w, r1 - r0, C, density, seed=weight_seed(seed, layer, name), row0=r0)
                 mats[name] = M.DeviceMatrix.from_dense(w)
+                if chain_skew_ns:  # PDL-chained: late CTAs start up to ~2 us after the first
+                    mats[name].set_chain_skew(chain_skew_ns)
                 if keep_dense:
                     dense[name] = w
                 else:

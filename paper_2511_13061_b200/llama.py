@@ -26,6 +26,7 @@ from typing import Dict, List, Optional
 import torch
 
 from . import macko as M
+from .decoder_chain import CHAIN_SKEW_NS
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _llm = None
@@ -113,6 +114,8 @@ class LlamaWeights:
                 w = _gen((R, Cc), density, seed + 100 + 16 * layer + k, math.sqrt(3.0 / (density * Cc)), dev)
                 if macko:
                     ml[name] = M.DeviceMatrix.from_dense(w)
+                    if CHAIN_SKEW_NS:  # every decode-step SpMV is a PDL dependent (decoder_chain.py)
+                        ml[name].set_chain_skew(CHAIN_SKEW_NS)
                 if keep_dense:
                     dl[name] = w
                 else:

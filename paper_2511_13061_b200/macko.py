@@ -208,6 +208,11 @@ class DeviceMatrix:
         split; CTA cap k/4 or 0 = auto).  y is bit-identical for every setting."""
         check(_lib.load().macko_dev_configure(self._h, x_mode, ctas_per_sm, _stream_ptr(stream)))
 
+    def set_chain_skew(self, start_spread_ns: int = 2000, stream=None) -> None:
+        """Re-plan for PDL-chained launches: later CTAs, which start up to start_spread_ns after
+        the first one in a chain, get proportionally less work (0: equal split).  y unchanged."""
+        check(_lib.load().macko_dev_set_chain_skew(self._h, int(start_spread_ns), _stream_ptr(stream)))
+
     # -- operations -------------------------------------------------------------------------
     def download(self, stream=None) -> MackoMatrix:
         i = self.info

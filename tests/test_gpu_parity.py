@@ -741,3 +741,34 @@ def test_pdl_instance_masked_edges_do_not_leak_inf_nan(cuda):
     y_ref = b200_y(m, x)
     assert _same_or_both_nan(y, y_ref)
     assert np.array_equal(y[0::2], y_ref[0::2])
+
+
+def test_chain_skewed_plan_host_device_and_y(cuda, monkeypatch):
+    # macko_dev_set_chain_skew: early CTAs get larger shares (plan.cuh plan_warp_of).  The device
+    # builder must equal the host reference record for record, shares must fall with the CTA index,
+    # and y (plain and PDL instance) is unchanged.
+    cases = [O.gen_dense(4096, 4096, 0.5, 11), O.gen_dense(1000, 16000, 0.5, 12), O.gen_dense(300, 3000, 0.1, 13)]
+    for A in cases:
+        monkeypatch.setenv("MACKO_HOST_PLAN", "1")
+        dh = gpu_encode(A)
+        dh.set_chain_skew(2000)
+        monkeypatch.delenv("MACKO_HOST_PLAN")
+        dd = gpu_encode(A)
+        dd.set_chain_skew(2000)
+        rh, sh = dh.plan_records()
+        rd, sd = dd.plan_records()
+        assert np.array_equal(rh, rd), A.shape
+        assert np.array_equal(sh, sd), A.shape
+        li = dd.launch_info()
+        units = rd[:, 0].astype(np.int64)
+        assert units.max() <= 2 * int(np.ceil(units.sum() / units.size)) + 2, (A.shape, units.max())
+        if A.shape == (4096, 4096):
+            per_cta = rd[:, 4].astype(np.int64) - rd[:, 3].astype(np.int64)  # TMA element range per warp
+            per_cta = per_cta.reshape(li.grid, -1).sum(axis=1)
+            assert per_cta[: li.grid // 4].mean() > per_cta[-li.grid // 4:].mean() * 1.05
+        x = O.gen_vector(A.shape[1], 14)
+        ref = b200_y(O.encode_dense(A), x)
+        assert np.array_equal(gpu_spmv(dd, x), ref)
+        assert np.array_equal(gpu_spmv_pdl(dd, x), ref)
+        dd.set_chain_skew(0)
+        assert np.array_equal(gpu_spmv(dd, x), ref)

@@ -20,10 +20,13 @@ p.add_argument("--rows", type=int, default=4096)
 p.add_argument("--cols", type=int, default=4096)
 p.add_argument("--density", type=float, default=0.5)
 p.add_argument("--flush", type=int, default=1)
+p.add_argument("--skew", type=int, default=0, help="macko_dev_set_chain_skew start spread (ns)")
 a = p.parse_args()
 dense = torch.empty((a.rows, a.cols), dtype=torch.float16, device="cuda")
 M.gen_dense(dense, a.rows, a.cols, a.density, seed=1234)
 dm = M.DeviceMatrix.from_dense(dense)
+if a.skew:
+    dm.set_chain_skew(a.skew)
 del dense
 x = torch.empty(a.cols, dtype=torch.float16, device="cuda")
 M.gen_vector(x, a.cols, seed=4321)
@@ -41,9 +44,10 @@ e1.record()
 torch.cuda.synchronize()
 L = _lib.load()
 L.macko_trace_read.argtypes = [C.c_void_p, C.c_size_t]
-buf = np.zeros(148 * 32 * 8, np.uint64)
+L.macko_trace_slot_counter.restype = C.c_uint
+buf = np.zeros(8 * 148 * 32 * 8, np.uint64)
 assert L.macko_trace_read(buf.ctypes.data, buf.size) == 0
-t = buf.reshape(148 * 32, 8).astype(np.int64)
+t = buf.reshape(8, 148 * 32, 8)[(L.macko_trace_slot_counter() - 1) % 8].astype(np.int64)  # the last launch
 ok = t[:, 0] > 0
 t0 = t[ok, 0].min()
 rel = (t[ok] - t0) / 1e3
