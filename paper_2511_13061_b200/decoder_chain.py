@@ -72,6 +72,7 @@ def _out_name(name: str) -> str:
 # the 32-layer chain: 0 -> 2288, 1000 -> 2325, 2000 -> 2376, 3000 -> 2474 us per token, so the
 # equal split stays the default.
 CHAIN_SKEW_NS = int(os.environ.get("MACKO_CHAIN_SKEW_NS", "0"))
+CHAIN_X_MODE = int(os.environ.get("MACKO_CHAIN_XMODE", "-1"))
 
 
 class SparseDecoderChain:
@@ -110,6 +111,8 @@ class SparseDecoderChain:
                 mats[name] = M.DeviceMatrix.from_dense(w)
                 if chain_skew_ns:  # PDL-chained: late CTAs start up to ~2 us after the first
                     mats[name].set_chain_skew(chain_skew_ns)
+                if CHAIN_X_MODE >= 0:  # experiments: force the gather split of every chain matrix
+                    mats[name].configure(CHAIN_X_MODE)
                 if keep_dense:
                     dense[name] = w
                 else:
