@@ -515,7 +515,14 @@ def main():
     if world == 1:
         hy = torch.empty(R, dtype=torch.int16, pin_memory=True)
         hxn, hyn = hx.numpy().view(np.uint16), hy.numpy().view(np.uint16)
-        e2e_fn = lambda: dm.spmv_host(hxn, hyn, stream)  # noqa: E731  (C-ABI macko_spmv_host, synchronises)
+        dm.spmv_host(hxn, hyn, stream)  # validated once through the Python wrapper ...
+        from paper_2511_13061_b200 import _lib as _L
+        _c_fn = _L.load().macko_spmv_host  # ... then timed as the bare C-ABI call a C/C++ caller makes
+        _c_args = (dm._h, hxn.ctypes.data, hyn.ctypes.data, M._stream_ptr(stream))
+
+        def e2e_fn():  # C-ABI macko_spmv_host: x pulled from pinned host memory, y written back, synchronises
+            if _c_fn(*_c_args) != 0:
+                raise RuntimeError("macko_spmv_host failed")
         d2h = 2 * R
     else:
         hy = torch.empty(R * world, dtype=torch.int16, pin_memory=True)
@@ -586,7 +593,7 @@ def main():
                                               "+ 4(R+1) + 2C + 2R per SpMV"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * C, "d2h_bytes_per_step": d2h,
                     "us_per_call": round(e2e_mean * 1e3, 2),
-                    "api": ("macko_spmv_host (C-ABI, pinned host x / y)" if world == 1 else
+                    "api": ("macko_spmv_host (bare C-ABI call via ctypes, pinned host x / y, synchronising)" if world == 1 else
                             "pinned H2D x on rank 0 + RowShardedSpmv + D2H y on every rank")},
             "compress_s": round(compress_s, 4), "compress_warm_s": round(compress_warm_s, 4),
             "gpu_launches": launches,
