@@ -737,10 +737,16 @@ constexpr bool x_by_tma() {
     return MACKO_TMA_X && kB == 1 && x_table<kXMode>();
 }
 
+// xbar completes when the bulk copy has landed (thread 0's expect_tx arrival) and warp 0 has
+// written the guards and the tail (its lane 0 arrives after them: release), so every warp waits on
+// it alone — no CTA barrier between griddepcontrol.wait and the walk.
+__device__ __forceinline__ void stage_x_tma_init(uint32_t xbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(xbar) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void stage_x_tma_issue(const SpmvArgs& a, uint16_t* xs, uint32_t xbar) {
     const uint32_t nbytes = (a.cols / 8u) * 16u;  // x is 16-byte aligned (capi)
-    mbar_init(xbar);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (nbytes) {
         asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(nbytes) : "memory");
         bulk_g2s(static_cast<uint32_t>(__cvta_generic_to_shared(xs)), a.x, nbytes, xbar);
@@ -749,10 +755,13 @@ __device__ __forceinline__ void stage_x_tma_issue(const SpmvArgs& a, uint16_t* x
     }
 }
 
-__device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs) {
+// warp 0: zero guards and the < 8-element tail, then its lane 0 arrives on xbar
+__device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs, uint32_t xbar, int lane) {
     const uint32_t C = a.cols;
-    for (uint32_t i = (C / 8u) * 8u + threadIdx.x; i < C + kXGuardHi; i += blockDim.x) xs[i] = i < C ? a.x[i] : (uint16_t)0;
-    if (threadIdx.x < kXGuardLo) xs[(int)threadIdx.x - kXGuardLo] = 0;
+    for (uint32_t i = (C / 8u) * 8u + lane; i < C + kXGuardHi; i += kWarp) xs[i] = i < C ? a.x[i] : (uint16_t)0;
+    if (lane < kXGuardLo) xs[lane - kXGuardLo] = 0;
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(xbar) : "memory");
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
@@ -925,6 +934,8 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     constexpr bool kTmaX = x_by_tma<kXMode, kB>() && kChain;
     // Without a PDL producer x is final at entry: its loads overlap the plan record's latency.
     if constexpr (kTmaX) {
+        if (threadIdx.x == 0) stage_x_tma_init(xbar);
+        __syncthreads();  // xbar initialised before any warp polls it (every warp is here at entry)
         if (!a.pdl && threadIdx.x == 0) stage_x_tma_issue(a, xs, xbar);
     } else {
 #ifndef MACKO_RING_FIRST
@@ -945,16 +956,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     MK_TRACE(3);
     if constexpr (kTmaX) {
         if (a.pdl && threadIdx.x == 0) stage_x_tma_issue(a, xs, xbar);
-        stage_x_tma_rest(a, xs);
-        __syncthreads();  // xbar initialised, guards written
-        mbar_wait(xbar, 0);
+        if (warp == 0) stage_x_tma_rest(a, xs, xbar, lane);
+        mbar_wait(xbar, 0);  // this warp alone: x landed, guards and tail written
     } else {
         if (a.pdl) stage_x<kXMode, kB>(a, xs);
         __syncthreads();
     }
     MK_TRACE(4);
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    if (kChain && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin)
+    if (kChain && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin), once x is in
         for (uint32_t i = 1; i < min(kMaxRing, g.n_chunks); ++i) fill_chunk<kBits>(g, a, i);
     if (has_work) run_rows<kXMode, kBits, kB, kChain>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
