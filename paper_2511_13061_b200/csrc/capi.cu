@@ -1264,6 +1264,20 @@ macko_status macko_dev_spmm(const macko_dev_matrix* m, const uint16_t* d_X, uint
             ck(cudaMemset2DAsync(d_Y, ldy * 2, 0, m->rows * 2, batch, st), "Y = 0");
             return;
         }
+        // batch 3-4 when the 4-wide interleaved table does not fit beside the rings but the 2-wide
+        // one does: two 2-wide passes (2 x 136 us) beat one 4-wide texture-only pass (357 us) at
+        // 36864x12288; each column's y is the same bits either way.
+        if (batch > 2 && batch <= 4 && m->b_delta == 4) {
+            const size_t t4 = align_up(2 * 4 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
+            const size_t t2 = align_up(2 * 2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
+            if (t4 + 2 * m->per_slot > m->smem_budget && t2 + 2 * m->per_slot <= m->smem_budget) {
+                const macko_status s1 = macko_dev_spmm(m, d_X, ldx, d_Y, ldy, 2, stream);
+                if (s1 != MACKO_OK) fail(s1, g_err);
+                const macko_status s2 = macko_dev_spmm(m, d_X + 2 * ldx, ldx, d_Y + 2 * ldy, ldy, batch - 2, stream);
+                if (s2 != MACKO_OK) fail(s2, g_err);
+                return;
+            }
+        }
         const uint32_t kb = batch <= 2 ? 2u : batch <= 4 ? 4u : 8u;
         const int ti = kb == 2 ? 0 : kb == 4 ? 1 : 2;
         std::lock_guard<std::mutex> lk(m->mu);
