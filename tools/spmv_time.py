@@ -21,6 +21,7 @@ p.add_argument("--shapes", default="36864x12288@0.5")
 p.add_argument("--n", type=int, default=100)
 p.add_argument("--soak", type=float, default=0.5)
 p.add_argument("--x-mode", type=int, default=-1)
+p.add_argument("--bits", type=int, default=4, help="b_delta of the format")
 p.add_argument("--tag", default=os.environ.get("MACKO_LIB", "default"))
 p.add_argument("--no-flush", action="store_true", help="never flush L2 between launches (L2-resident runs)")
 p.add_argument("--check", type=int, default=1, help="compare y with the oracle order (small shapes only)")
@@ -51,7 +52,7 @@ for spec in a.shapes.split(","):
     d = float(d)
     dense = torch.empty((R, C), dtype=torch.float16, device="cuda")
     M.gen_dense(dense, R, C, d, seed=1234)
-    dm = M.DeviceMatrix.from_dense(dense)
+    dm = M.DeviceMatrix.from_dense(dense, b_delta=a.bits)
     x = torch.empty(C, dtype=torch.float16, device="cuda")
     M.gen_vector(x, C, seed=4321)
     y = torch.empty(R, dtype=torch.float16, device="cuda")
@@ -65,7 +66,7 @@ for spec in a.shapes.split(","):
         dm.spmv_into(x, y, st)
         torch.cuda.synchronize()
         hm = dm.download()
-        m = O.Macko(hm.rows, hm.cols, 4, hm.values, hm.packed_deltas, hm.row_pointers)
+        m = O.Macko(hm.rows, hm.cols, a.bits, hm.values, hm.packed_deltas, hm.row_pointers)
         ok = "ok" if (to_host_u16(y) == b200_y(m, to_host_u16(x))).all() else "MISMATCH"
     del dense
     need_flush = dm.traffic_bytes < 3 * l2 and not a.no_flush
