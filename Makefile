@@ -24,7 +24,7 @@ oracle:
 
 # libmacko_llm.so: the per-token kernels of the Llama decode benchmark (the caller of the path)
 llm: $(PKG)/libmacko_llm.so
-$(PKG)/libmacko_llm.so: $(CSRC)/llm.cu include/macko_llm.h
+$(PKG)/libmacko_llm.so: $(CSRC)/llm.cu $(CSRC)/llm_ops.cuh include/macko_llm.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/llm.cu -cudart static 2> build/llm.ptxas.log || (cat build/llm.ptxas.log; exit 1)
 

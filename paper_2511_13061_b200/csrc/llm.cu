@@ -15,32 +15,17 @@
 #include <cmath>
 
 #include "../../include/macko_llm.h"
+#include "llm_ops.cuh"
 
 namespace {
 
-__device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+using llmops::block_sum;
+using llmops::f2h;
+using llmops::h2f;
 
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-__device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
-
-template <int kThreads>
-__device__ float block_sum(float v, float* red) {
-    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (w == 0) {
-        v = l < kThreads / 32 ? red[l] : 0.0f;
-        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (l == 0) red[0] = v;
-    }
-    __syncthreads();
-    const float r = red[0];
-    __syncthreads();
-    return r;
 }
 
 // h += delta (fp16 residual stream, as the fp16 model keeps it); out = h / rms(h) * weight
@@ -48,17 +33,7 @@ __global__ void __launch_bounds__(1024) add_rmsnorm_kernel(uint16_t* h, const ui
                                                            uint16_t* out, uint32_t n, float eps) {
     __shared__ float red[32];
     pdl_enter();
-    float ss = 0.0f;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        float v = h2f(h[i]);
-        if (delta) {
-            v = h2f(f2h(v + h2f(delta[i])));
-            h[i] = f2h(v);
-        }
-        ss += v * v;
-    }
-    const float inv = rsqrtf(block_sum<1024>(ss, red) / (float)n + eps);
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = f2h(h2f(h[i]) * inv * h2f(weight[i]));
+    llmops::add_rmsnorm_block(h, delta, weight, out, n, eps, red);
 }
 
 // Rotary embedding + KV append + attention of one query, fused: a CTA of 8 warps per head rotates
@@ -164,10 +139,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) rope_attention_kernel(const u
 // gu = [gate; up] (2 * inter): out = silu(gate) * up
 __global__ void silu_mul_kernel(const uint16_t* gu, uint16_t* out, uint32_t inter) {
     pdl_enter();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < inter; i += gridDim.x * blockDim.x) {
-        const float g = h2f(gu[i]), u = h2f(gu[inter + i]);
-        out[i] = f2h(g / (1.0f + __expf(-g)) * u);
-    }
+    llmops::silu_mul_range(gu, out, inter, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __global__ void embed_kernel(const uint16_t* table, const int32_t* token, uint16_t* h, uint32_t hidden) {
