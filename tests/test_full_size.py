@@ -72,7 +72,11 @@ def build(R, C, d, int_mode=False, row0=0, bits=4):
 
 def check_y(dm, dense, x, int_mode, sample_rows=1024):
     y = to_host_u16(M.spmv(dm, x))
+    # the PDL (decode-chain) kernel instance: staggered fills, per-step edges, bulk-copied x
+    y_pdl = torch.empty(dm.rows, dtype=torch.float16, device=x.device)
+    dm.spmv_into(x, y_pdl, pdl=True)
     torch.cuda.synchronize()
+    assert np.array_equal(to_host_u16(y_pdl), y)
     h = dm.download()
     m = as_oracle(h)
     xh = to_host_u16(x)
