@@ -66,6 +66,9 @@ typedef struct macko_dev_info {
 
 const char* macko_last_error(void);
 const char* macko_version(void);
+/* Steps (256 elements each) per reduction unit of the SpMV's fixed summation order: per lane
+ * sequential, xor-tree over the 32 lanes once per unit, units added in order. */
+uint32_t macko_unit_steps(void);
 
 /* Host MACKO arrays -> device handle (copies).  Replaces the host-resident MackoMatrix
  * produced by macko_from_csr (convert.hpp:12-16) as the SpMV operand.  n_values /

@@ -16,7 +16,7 @@ MACKO_OK, MACKO_EINVAL, MACKO_EFORMAT, MACKO_EIO, MACKO_EINFEASIBLE, MACKO_ECUDA
 
 # Every symbol include/macko_cuda.h declares (tests check the library exports all of them).
 EXPORTS = (
-    "macko_last_error", "macko_version", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_from_csr", "macko_csr_from_dense",
+    "macko_last_error", "macko_version", "macko_unit_steps", "macko_dev_upload", "macko_dev_from_dense", "macko_dev_from_csr", "macko_csr_from_dense",
     "macko_dev_to_dense", "macko_dev_padding_count", "macko_dev_get_info",
     "macko_dev_download", "macko_dev_spmv", "macko_dev_spmv_ex", "macko_dev_spmm", "macko_spmv_host", "macko_dev_validate", "macko_dev_free", "macko_release_cached_memory", "macko_dev_set_chain_skew",
     "macko_density_threshold", "macko_gen_dense", "macko_gen_vector", "macko_shard_rows",
@@ -112,6 +112,8 @@ def load() -> C.CDLL:
     L.macko_spmv_host.argtypes = [vp, vp, vp, vp]
     L.macko_dev_validate.restype = st
     L.macko_dev_validate.argtypes = [vp, vp]
+    L.macko_unit_steps.restype = C.c_uint32
+    L.macko_unit_steps.argtypes = []
     L.macko_dev_free.restype = st
     L.macko_dev_free.argtypes = [vp]
     L.macko_release_cached_memory.restype = st

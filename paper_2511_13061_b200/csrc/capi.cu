@@ -855,6 +855,8 @@ void check_shape(uint64_t rows, uint64_t cols) {
 extern "C" {
 
 const char* macko_last_error(void) { return g_err.c_str(); }
+uint32_t macko_unit_steps(void) { return (uint32_t)mk::kUnitSteps; }
+
 const char* macko_version(void) { return "macko-b200 0.2 (sm_100a; SpMV and compressor for b_delta in {1,2,4,8})"; }
 uint64_t macko_kernel_launches(void) { return g_launches.load(); }
 

@@ -15,11 +15,16 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // unit and unit sums are added sequentially into the row sum.
 constexpr int kEltsPerLane = 8;
 constexpr int kStepElts = kWarp * kEltsPerLane;  // 256
+// 16 steps (4096 elements): fewer split rows (a row of up to 31 steps is one unit, so a warp
+// boundary never cuts it) and half the xor-tree reductions of 8-step units.  Measured (amortised
+// timing, one B200): 36864x12288 @50 % 107.1 vs 111.1 us, 4096x11008 18.8 vs 22.7 us,
+// 131072x32768 @50 % 1022-1026 vs 1056 us, decode chain 2196 vs 2286 us / token; 4 steps was
+// slower everywhere (chain 2586), 24-64 lose on 131072x32768 (1092-1100 us).
 #ifndef MACKO_UNIT_STEPS
-#define MACKO_UNIT_STEPS 8
+#define MACKO_UNIT_STEPS 16
 #endif
 constexpr int kUnitSteps = MACKO_UNIT_STEPS;  // build knob for experiments (the oracle takes it as a parameter)
-constexpr int kUnitElts = kStepElts * kUnitSteps;  // 2048
+constexpr int kUnitElts = kStepElts * kUnitSteps;  // 4096
 
 // ---- streaming loads (read-once data: no L1 allocation) ----
 __device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {

@@ -288,6 +288,11 @@ class DeviceMatrix:
             pass
 
 
+def unit_steps() -> int:
+    """Steps per reduction unit of the SpMV's summation order (oracle b200_order_spmv's unit_steps)."""
+    return int(_lib.load().macko_unit_steps())
+
+
 def macko_from_dense(dense, b_delta: int = 4, stream=None) -> DeviceMatrix:
     """csr_from_dense + macko_from_csr (convert.hpp:8-16) on the GPU."""
     return DeviceMatrix.from_dense(dense, b_delta=b_delta, stream=stream)

@@ -1,14 +1,15 @@
 """Shared test helpers (tolerance bound, torch <-> numpy fp16-bit transfers)."""
 import numpy as np
 
-UNIT_STEPS = 8  # csrc/common.cuh kUnitSteps: the kernel's canonical reduction granularity
+from oracle import oracle as O
+from paper_2511_13061_b200 import macko as M
+
+UNIT_STEPS = M.unit_steps()  # csrc/common.cuh kUnitSteps: the kernel's canonical reduction granularity
 
 
 def b200_y(m, x):
     """The oracle emulation of the GPU's summation order (mo_b200_order_spmv: the ROMA walk,
     per-lane sequential, xor-tree per unit of UNIT_STEPS steps, units in order)."""
-    from oracle import oracle as O
-
     return O.b200_order_spmv(m, x, UNIT_STEPS)
 
 

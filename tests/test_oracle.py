@@ -300,6 +300,7 @@ def test_b200_order_restatement():
         m = O.encode_dense(A)
         assert np.array_equal(O.b200_order_spmv(m, x, 8), _b200_py(m, x, 8)), (R, C, d)
         assert np.array_equal(O.b200_order_spmv(m, x, 2), _b200_py(m, x, 2)), (R, C, d)
+        assert np.array_equal(O.b200_order_spmv(m, x, 16), _b200_py(m, x, 16)), (R, C, d)
 
 
 def test_slab_encoding_equals_global_slice():
