@@ -14,7 +14,7 @@
 // B200 specifics (profiles/r01_pipes.md, r01_experiments.md): the kernel is bound by the L1TEX
 // data pipes and the latency of each warp's pair chain, not by HBM.
 //   * The matrix stream arrives by TMA: every warp owns a contiguous element range (static
-//     equal-weight plan of 2048-element units, built once per matrix) and keeps a ring of
+//     equal-weight plan of 4096-element units, built once per matrix) and keeps a ring of
 //     1024-element chunks in flight with cp.async.bulk + mbarrier (no LSU wavefronts; issued by
 //     one elect.sync lane, L2 evict_first); values and codewords are read back with one LDS.128
 //     + one LDS per lane step.
@@ -28,7 +28,7 @@
 //   * One persistent CTA of 32 warps per SM.  Rows cut between warps are finished by the
 //     last-arriving warp, which adds the per-unit partials in unit order.
 // Summation order (every run, any grid): per lane sequential over its elements, xor-tree over
-// lanes once per unit (8 steps; the row's last unit absorbs a shorter remainder), sequential
+// lanes once per unit (kUnitSteps = 16 steps; the row's last unit absorbs a shorter remainder), sequential
 // over units — mirrored bit-exactly by oracle mo_b200_order_spmv(unit_steps = kUnitSteps).  It
 // depends on a row's elements and on its start offset mod 8 (ROMA), never on the plan.
 #include "common.cuh"
