@@ -92,3 +92,10 @@ def test_package_has_no_cpu_fallback_or_oracle_import():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(from|import)\s+oracle|libmacko_oracle|libmacko_ref|_ref/", src), f
+
+
+def test_unit_steps_is_the_documented_reduction_unit():
+    # the oracle's unit_steps for the kernel's fixed summation order (csrc/common.cuh kUnitSteps)
+    from paper_2511_13061_b200 import macko as M
+
+    assert M.unit_steps() == 16
