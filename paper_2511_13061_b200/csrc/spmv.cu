@@ -737,9 +737,9 @@ constexpr bool x_by_tma() {
     return MACKO_TMA_X && kB == 1 && x_table<kXMode>();
 }
 
-// xbar completes when the bulk copy has landed (thread 0's expect_tx arrival) and warp 0 has
-// written the guards and the tail (its lane 0 arrives after them: release), so every warp waits on
-// it alone — no CTA barrier between griddepcontrol.wait and the walk.
+// xbar completes when the bulk copy has landed (thread 0's expect_tx arrival) and thread 32 has
+// written the guards and the tail (it arrives after them: release), so every warp waits on it
+// alone — no CTA barrier between griddepcontrol.wait and the walk.
 __device__ __forceinline__ void stage_x_tma_init(uint32_t xbar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(xbar) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -755,13 +755,13 @@ __device__ __forceinline__ void stage_x_tma_issue(const SpmvArgs& a, uint16_t* x
     }
 }
 
-// warp 0: zero guards and the < 8-element tail, then its lane 0 arrives on xbar
-__device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs, uint32_t xbar, int lane) {
+// one thread: zero guards and the < 8-element tail (<= 31 entries), then it arrives on xbar itself,
+// so its release covers exactly the writes it made
+__device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs, uint32_t xbar) {
     const uint32_t C = a.cols;
-    for (uint32_t i = (C / 8u) * 8u + lane; i < C + kXGuardHi; i += kWarp) xs[i] = i < C ? a.x[i] : (uint16_t)0;
-    if (lane < kXGuardLo) xs[lane - kXGuardLo] = 0;
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(xbar) : "memory");
+    for (uint32_t i = (C / 8u) * 8u; i < C + kXGuardHi; ++i) xs[i] = i < C ? a.x[i] : (uint16_t)0;
+    for (int i = 1; i <= kXGuardLo; ++i) xs[-i] = 0;
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(xbar) : "memory");
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     MK_TRACE(3);
     if constexpr (kTmaX) {
         if (a.pdl && threadIdx.x == 0) stage_x_tma_issue(a, xs, xbar);
-        if (warp == 0) stage_x_tma_rest(a, xs, xbar, lane);
+        if (threadIdx.x == 32) stage_x_tma_rest(a, xs, xbar);  // warp 1: warp 0's thread 0 issues the copy
         mbar_wait(xbar, 0);  // this warp alone: x landed, guards and tail written
     } else {
         if (a.pdl) stage_x<kXMode, kB>(a, xs);

@@ -26,6 +26,10 @@ for bits in (1, 2, 4, 8):
         bad += int(not np.array_equal(h.values, m.values))
         y = to_host_u16(M.spmv(dm, to_dev(x)))
         bad += int(not np.array_equal(y, b200_y(m, x)))
+        yp = torch.empty(R, dtype=torch.float16, device="cuda")  # the PDL (chain) kernel instance
+        dm.spmv_into(to_dev(x), yp, pdl=True)
+        torch.cuda.synchronize()
+        bad += int(not np.array_equal(to_host_u16(yp), y))
         vals, cols, rp = M.csr_from_dense(A)
         dc = M.DeviceMatrix.from_csr(vals, cols, rp, R, C, bits)
         bad += int(not np.array_equal(dc.download().packed_deltas, m.deltas))
