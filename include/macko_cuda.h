@@ -223,11 +223,13 @@ macko_status macko_sharded_spmv(const macko_dev_matrix* slab, void* nccl_comm, i
 /* Fused all-gather destinations of a row slab (n <= 8, n = 0 disables): peer_y[p] = peer p's
  * full-y buffer already offset to this slab's first row, peer_flags[p] = this rank's u32 counter
  * in peer p's flag array (device or IPC-mapped pointers; one of them may be this rank's own).
- * After a MACKO_SPMV_PEERS launch every counter has grown by the launch's grid size.  Synchronous. */
+ * After a MACKO_SPMV_PEERS launch every counter has grown by the launch's grid size.  Applies to
+ * launches issued after the call: the table travels in the launch parameters (a captured CUDA
+ * graph keeps the pointers it was captured with); `stream` is unused. */
 macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, uint32_t* const* peer_flags, uint32_t n,
                                  void* stream);
 /* Second y destination set (bank 1, used with MACKO_SPMV_PEER_BANK1): same peer count and flags as
- * macko_dev_set_peers, which resets both banks to its peer_y.  Synchronous. */
+ * macko_dev_set_peers, which resets both banks to its peer_y.  Same timing as macko_dev_set_peers. */
 macko_status macko_dev_set_peer_bank(macko_dev_matrix* m, uint32_t bank, uint16_t* const* peer_y, uint32_t n,
                                      void* stream);
 /* Stream-ordered wait until d_flags[i] >= target (wrap-around compare) for i < n (n <= 32): the

@@ -263,8 +263,7 @@ struct macko_dev_matrix {
     DevBuf<uint32_t> plan_recs;  // W mk::WarpPlan records
     DevBuf<uint32_t> plan_u32;   // S split records {slot, first, pieces, 0}
     mk::SpmvPlanDev plan{};      // counters / partials filled per launch from the stream's workspace
-    DevBuf<mk::PeerTable> peer_table;  // fused all-gather destinations (macko_dev_set_peers)
-    mk::PeerTable h_peers{};           // host copy of the table
+    mk::PeerTable h_peers{};  // fused all-gather destinations (macko_dev_set_peers), passed per launch
     uint32_t n_peer = 0;
     int tex_align = 0;
     // per-stream workspaces and the x texture cache (guarded by mu)
@@ -509,9 +508,11 @@ void build_plan(macko_dev_matrix* m, cudaStream_t st) {
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device), "smem attribute");
     ck(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device), "smem attribute");
     // kSpmvCtasPerSm CTAs must fit one SM (1 KiB per CTA is reserved by the system; static smem:
-    // the mbarriers)
+    // the mbarriers and the fused all-gather stash)
     const size_t per_cta = std::min<size_t>((size_t)optin, (size_t)per_sm / kSpmvCtasPerSm - 1024);
-    const size_t budget = per_cta - kSpmvWarpsPerCta * kMaxRing * 8 - 64;
+    const size_t static_smem = spmv_static_smem();
+    if (static_smem == 0) fail(MACKO_ECUDA, "SpMV kernel attributes");
+    const size_t budget = per_cta - static_smem;
     const size_t per_slot = (size_t)kSpmvWarpsPerCta * (kChunkVBytes + kChunk * m->b_delta / 8);
     auto x_bytes = [&](int mode) -> size_t {
         return mode == 0 ? 0 : align_up(2 * (m->cols + mk::kXGuardLo + mk::kXGuardHi), 128);
@@ -1220,8 +1221,11 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
         a.y_mirror = y_mirror;
         if (flags & MACKO_SPMV_PEERS) {
             a.n_peer = m->n_peer;
-            a.peers = m->peer_table.p;
-            a.peer_bank = (flags & MACKO_SPMV_PEER_BANK1) ? 1u : 0u;
+            const uint32_t bank = (flags & MACKO_SPMV_PEER_BANK1) ? 1u : 0u;
+            for (uint32_t p = 0; p < mk::kMaxPeers; ++p) {
+                a.peer_y[p] = m->h_peers.y[bank][p];
+                a.peer_flag[p] = m->h_peers.flag[p];
+            }
         }
         a.value_count = (uint32_t)m->pad_nnz;
         if (m->pad_nnz == 0) {  // no stored entries: every row is empty, y = +0
@@ -1626,9 +1630,7 @@ macko_status macko_dev_set_peers(macko_dev_matrix* m, uint16_t* const* peer_y, u
             t.y[0][p] = t.y[1][p] = peer_y[p];
             t.flag[p] = peer_flags[p];
         }
-        if (!m->peer_table.p) m->peer_table.alloc(1);
-        ck(cudaMemcpyAsync(m->peer_table.p, &t, sizeof t, cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table");
-        ck(cudaStreamSynchronize((cudaStream_t)stream), "peer table");
+        (void)stream;  // the table travels in the launch parameters
         m->h_peers = t;
         m->n_peer = n;
     });
@@ -1646,8 +1648,7 @@ macko_status macko_dev_set_peer_bank(macko_dev_matrix* m, uint32_t bank, uint16_
             if (!peer_y[p]) fail(MACKO_EINVAL, "null peer pointer");
             t.y[bank][p] = peer_y[p];
         }
-        ck(cudaMemcpyAsync(m->peer_table.p, &t, sizeof t, cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table");
-        ck(cudaStreamSynchronize((cudaStream_t)stream), "peer table");
+        (void)stream;
         m->h_peers = t;
     });
 }

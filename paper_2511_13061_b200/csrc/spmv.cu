@@ -302,20 +302,52 @@ __device__ __forceinline__ void lane_step_b(float (&acc)[kB], const uint4& v, co
     }
 }
 
-// y[r] = v, and the same 2 bytes into every peer's y for the fused all-gather (one row per call,
-// lane 0).
+// y[r] = v (lane 0).  Fused all-gather: a split row's last arrival may sit in another CTA than the
+// warps around it, so it stores its 2 bytes straight into every peer's y (kDirect); every other
+// row belongs to the warp that walked it and reaches the peers through the warp's stash
+// (own_row_put).
+template <bool kDirect>
 __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
     a.y[r] = v;
     if (a.y_mirror) a.y_mirror[r] = v;
-    for (uint32_t p = 0; p < a.n_peer; ++p)
-        reinterpret_cast<uint16_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&a.peers->y[a.peer_bank][p])))[r] = v;
+    if constexpr (kDirect)
+        for (uint32_t p = 0; p < a.n_peer; ++p) a.peer_y[p][r] = v;
+}
+
+// Fused all-gather of the rows a warp finishes alone (its whole rows and empty rows): lane 0 parks
+// y[r] in the warp's 16-row stash (slot r mod 16) and the warp stores a full group of 16 rows to
+// every other rank's y with one 32-byte store per peer (round 1: one 2-byte NVLink write per row
+// per peer).  s_own_first: the warp's first own row (its first row unless that one is split).
+// The stash, not a re-read of y: loading just-written y lines (written by many SMs at once) cost
+// 10 us per launch at 4096x4096.  Only the peers instance of the kernel carries it (1 KiB).
+constexpr uint32_t kOwnGroup = 16;
+__shared__ uint16_t s_own_y[kSpmvWarpsPerCta][kOwnGroup];
+__shared__ uint32_t s_own_first[kSpmvWarpsPerCta];
+
+// Store the stashed own rows of [lo, hi) (one group) to the peers (whole warp).
+__device__ __forceinline__ void flush_own(const SpmvArgs& a, uint32_t lo, uint32_t hi, int lane) {
+    const uint32_t warp = threadIdx.x >> 5;
+    __syncwarp();  // lane 0's stash writes
+    const uint32_t r = lo + (uint32_t)lane;
+    if (lane < (int)kOwnGroup && r >= s_own_first[warp] && r < hi) {
+        const uint16_t v = s_own_y[warp][r & (kOwnGroup - 1)];
+        for (uint32_t p = 0; p < a.n_peer; ++p)
+            if (a.peer_y[p] != a.y) a.peer_y[p][r] = v;
+    }
+    __syncwarp();  // before the slots are reused
+}
+
+// Row r (own, y[r] = v in lane 0) is done: stash it; a full group goes out (whole warp).
+__device__ __forceinline__ void own_row_put(const SpmvArgs& a, uint32_t r, uint16_t v, int lane) {
+    if (lane == 0) s_own_y[threadIdx.x >> 5][r & (kOwnGroup - 1)] = v;
+    if ((r & (kOwnGroup - 1)) == kOwnGroup - 1) flush_own(a, r + 1 - kOwnGroup, r + 1, lane);
 }
 
 // Batched outputs (SpMM): Y[b][r] for b < a.batch (Y rows ldy apart).
-template <int kB>
+template <int kB, bool kDirect>
 __device__ __forceinline__ void put_y_b(const SpmvArgs& a, uint32_t r, const uint16_t (&v)[kB]) {
     if constexpr (kB == 1) {
-        put_y(a, r, v[0]);
+        put_y<kDirect>(a, r, v[0]);
     } else {
 #pragma unroll
         for (int b = 0; b < kB; ++b)
@@ -326,11 +358,10 @@ __device__ __forceinline__ void put_y_b(const SpmvArgs& a, uint32_t r, const uin
 // Fused all-gather: once all warps of the CTA wrote their rows, make them visible system-wide and
 // count the CTA in every peer's flag slot for this rank (consumers: wait_flags_kernel).
 __device__ __forceinline__ void signal_peers(const SpmvArgs& a) {
-    if (a.n_peer == 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        for (uint32_t p = 0; p < a.n_peer; ++p) atomicAdd_system(a.peers->flag[p], 1u);
+        for (uint32_t p = 0; p < a.n_peer; ++p) atomicAdd_system(a.peer_flag[p], 1u);
     }
 }
 
@@ -433,7 +464,7 @@ __device__ __forceinline__ bool finish_split_b(uint32_t j0, uint32_t tend, uint3
 
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
 // when the chunk is exhausted.  The row pointer after the next row is prefetched one row ahead.
-template <int kB>
+template <int kB, bool kPeers>
 __device__ __forceinline__ bool next_piece(RowState<kB>& rs, const SpmvArgs& a, uint32_t w, int lane) {
     for (;;) {
         if (rs.units_left == 0) return false;
@@ -450,8 +481,9 @@ __device__ __forceinline__ bool next_piece(RowState<kB>& rs, const SpmvArgs& a, 
         if (rs.T) return true;
         if (lane == 0) {  // empty row: fp16(+0.0)
             const uint16_t z[kB] = {};
-            put_y_b<kB>(a, rs.r, z);
+            put_y_b<kB, false>(a, rs.r, z);
         }
+        if constexpr (kPeers) own_row_put(a, rs.r, 0, lane);
     }
 }
 
@@ -765,15 +797,16 @@ __device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
-template <int kXMode, int kBits, int kB, bool kSplitEdges>
+template <int kXMode, int kBits, int kB, bool kSplitEdges, bool kPeers>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
                                          RowState<kB>& rs) {
     if (rs.T == 0) {
         if (lane == 0) {
             const uint16_t z[kB] = {};
-            put_y_b<kB>(a, rs.r, z);
+            put_y_b<kB, false>(a, rs.r, z);
         }
-        if (!next_piece(rs, a, w, lane)) return;
+        if constexpr (kPeers) own_row_put(a, rs.r, 0, lane);
+        if (!next_piece<kB, kPeers>(rs, a, w, lane)) return;
     }
     // loop invariants pinned in registers (not re-derived from the CTA's shared window per pair)
     // (ring positions in 8-element groups: the lane's group of a step at S is (S / 8 + lane_q) & qmask)
@@ -891,29 +924,31 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         // -- piece end
         if constexpr (kB == 1) {
             if (!rs.split) {
-                if (lane == 0) put_y(a, rs.r, f32_to_f16_rn(rs.row_acc[0]));
+                const uint16_t v = f32_to_f16_rn(rs.row_acc[0]);
+                if (lane == 0) put_y<false>(a, rs.r, v);
+                if constexpr (kPeers) own_row_put(a, rs.r, v, lane);
             } else {
                 const int v = finish_split(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc[0], a.plan, lane);
-                if (v >= 0) put_y(a, rs.r, (uint16_t)v);
+                if (v >= 0) put_y<kPeers>(a, rs.r, (uint16_t)v);
             }
         } else {
             uint16_t out[kB];
             if (!rs.split) {
 #pragma unroll
                 for (int b = 0; b < kB; ++b) out[b] = f32_to_f16_rn(rs.row_acc[b]);
-                if (lane == 0) put_y_b<kB>(a, rs.r, out);
+                if (lane == 0) put_y_b<kB, false>(a, rs.r, out);
             } else if (finish_split_b<kB>(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, lane, out)) {
-                put_y_b<kB>(a, rs.r, out);
+                put_y_b<kB, kPeers>(a, rs.r, out);
             }
         }
-        if (!next_piece(rs, a, w, lane)) break;
+        if (!next_piece<kB, kPeers>(rs, a, w, lane)) break;
     }
 }
 
 // kChain: the instance of PDL launches (decode chains): per-step edge masking (run_rows) and x
 // staged by one bulk copy per CTA (stage_x_tma_*).  Both pay only with the kernel's code and x
 // warm in L2, as in a chain; a stand-alone launch after an L2 flush is faster without them.
-template <int kXMode, int kBits, int kB = 1, bool kChain = false>
+template <int kXMode, int kBits, int kB = 1, bool kChain = false, bool kPeers = false>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
@@ -947,6 +982,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     Ring g;
     const bool has_work = op_begin<kBits, kB, kChain>(a, pr, warp, lane, smem_base,
                                          static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp][0])), g, rs);
+    if (kPeers && has_work && lane == 0) s_own_first[warp] = rs.r + (rs.split ? 1u : 0u);
 #ifdef MACKO_RING_FIRST
     if (!a.pdl) stage_x<kXMode, kB>(a, xs);
 #endif
@@ -966,9 +1002,15 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
     if (kChain && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin), once x is in
         for (uint32_t i = 1; i < min(kMaxRing, g.n_chunks); ++i) fill_chunk<kBits>(g, a, i);
-    if (has_work) run_rows<kXMode, kBits, kB, kChain>(a, w, lane, xs_addr, g, rs);
+    if (has_work) run_rows<kXMode, kBits, kB, kChain, kPeers>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
-    signal_peers(a);
+    if constexpr (kPeers) {
+        if (has_work) {  // the stash's last, partial group
+            const uint32_t r1 = rs.r + (rs.split ? 0u : 1u);
+            flush_own(a, r1 & ~(kOwnGroup - 1), r1, lane);
+        }
+        signal_peers(a);
+    }
 }
 
 // Column just before the first unit of every chunk that starts inside a row: sum of the row's
@@ -1000,10 +1042,16 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+    if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
     if (e == cudaSuccess) {
         int c2 = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, macko_spmv<kXMode, kBits, 1, true>, threads, smem);
+        *ctas_per_sm = std::min(*ctas_per_sm, c2);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, macko_spmv<kXMode, kBits, 1, true, true>, threads, smem);
         *ctas_per_sm = std::min(*ctas_per_sm, c2);
     }
     return e;
@@ -1026,6 +1074,8 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    // fused all-gather: the chain instance with the peer stores (the others carry none of that code)
+    if (a.n_peer) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true, true>, a);
     if (pdl || kChainForAll) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
@@ -1161,6 +1211,15 @@ static cudaError_t launch_bits(const SpmvArgs& a, int grid, int x_mode, size_t s
         default: break;
     }
     return cudaErrorInvalidValue;
+}
+
+size_t spmv_static_smem() {
+    cudaFuncAttributes f0{}, f1{}, f2{};
+    if (cudaFuncGetAttributes(&f0, macko_spmv<10, 2, 1, false>) != cudaSuccess ||
+        cudaFuncGetAttributes(&f1, macko_spmv<10, 2, 1, true>) != cudaSuccess ||
+        cudaFuncGetAttributes(&f2, macko_spmv<10, 2, 1, true, true>) != cudaSuccess)
+        return 0;
+    return std::max(std::max(f0.sharedSizeBytes, f1.sharedSizeBytes), f2.sharedSizeBytes);
 }
 
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm) {

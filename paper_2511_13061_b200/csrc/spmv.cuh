@@ -33,7 +33,7 @@ struct SpmvPlanDev {
 
 // Fused all-gather of y (row-sharded SpMV over NVLink peers): up to kMaxPeers destinations.
 constexpr uint32_t kMaxPeers = 8;
-struct PeerTable {  // device memory, one per matrix (macko_dev_set_peers / macko_dev_set_peer_bank)
+struct PeerTable {  // host side, one per matrix (macko_dev_set_peers / macko_dev_set_peer_bank)
     uint16_t* y[2][kMaxPeers]; // bank b: peer p's full y, already offset to this slab's first row
     uint32_t* flag[kMaxPeers]; // this rank's completion counter in peer p's flag array
 };
@@ -51,10 +51,12 @@ struct SpmvArgs {
     uint32_t ring;         // TMA ring slots per warp (always kMaxRing; the kernel uses the constant)
     uint32_t ring_offset;  // byte offset of the rings in dynamic shared memory (after x)
     uint32_t pdl;          // launched as a PDL dependent: x may still be written by the producer
-    uint32_t n_peer;       // fused all-gather: y rows also go to peers->y[0..n_peer) and each CTA adds 1
-                           // to *peers->flag[p] (system scope) once its rows are written
-    const PeerTable* peers;
-    uint32_t peer_bank;    // which y bank of the peer table this launch stores into (0 / 1)
+    uint32_t n_peer;       // fused all-gather: y rows also go to peer_y[0..n_peer) and each CTA adds 1
+                           // to *peer_flag[p] (system scope) once its rows are written
+    // The launch's bank of the peer table, in the parameter bank: every warp reads the pointers at
+    // its end, and 4736 warps loading one global word at once serialise on its L2 line (+10 us).
+    uint16_t* peer_y[kMaxPeers];
+    uint32_t* peer_flag[kMaxPeers];
     uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
     uint32_t batch;        // SpMM: vectors in the batch (<= the kernel's kB); x = XT interleaved
     uint64_t ldy;          // SpMM: element stride between the batch's y vectors
@@ -111,6 +113,8 @@ cudaError_t launch_interleave(const uint16_t* X, uint64_t ldx, uint32_t batch, u
                               uint16_t* XT, uint32_t n_total, cudaStream_t s);
 constexpr uint32_t kMaxBatch = 8;
 cudaError_t spmv_occupancy(int x_mode, int bits, size_t smem, int* ctas_per_sm);
+// Static shared memory of the SpMV kernels (mbarriers, fused all-gather stash); 0 on error.
+size_t spmv_static_smem();
 bool spmv_valid_config(int x_mode, int bits);
 // Wait until flags[i] >= target for i < n (system-scope acquire; peers' fused all-gathers).
 cudaError_t launch_wait_flags(const uint32_t* flags, uint32_t n, uint32_t target, cudaStream_t s);

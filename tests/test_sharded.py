@@ -173,6 +173,37 @@ def test_fused_allgather_single_rank(cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols", [(600, 40000), (3000, 3000), (4099, 700)])
+def test_fused_peer_stores_stand_in(cuda, rows, cols):
+    # One local buffer stands in for a remote rank's y: rows finished by one warp reach it through
+    # the warp's coalesced copy, rows split across warps / CTAs through their last arrival's
+    # direct stores, empty rows through the copy of the warp that owns them.
+    from oracle import oracle as O
+    from paper_2511_13061_b200 import macko as M
+    from tests.helpers import b200_y, to_dev, to_host_u16
+
+    A = O.gen_dense(rows, cols, 0.5, 91)
+    A[::7] = 0  # empty rows, also at a slab's first and last row
+    A[-1] = 0
+    x = O.gen_vector(cols, 92)
+    dm = M.DeviceMatrix.from_dense(to_dev(A))
+    y = torch.zeros(rows, dtype=torch.float16, device=cuda)
+    other = [torch.full((rows,), -1.0, dtype=torch.float16, device=cuda) for _ in range(2)]
+    flags = torch.zeros(2, dtype=torch.int32, device=cuda)
+    dm.set_peers([y.data_ptr(), other[0].data_ptr()], [flags.data_ptr(), flags.data_ptr() + 4])
+    dm.set_peer_bank(1, [y.data_ptr(), other[1].data_ptr()])
+    ref = b200_y(O.encode_dense(A), x)
+    for bank in (0, 1, 0):
+        dm.spmv_into(to_dev(x), y, peers=True, bank=bank)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host_u16(y), ref)
+        assert np.array_equal(to_host_u16(other[bank]), ref), bank
+    assert int(flags[0].item()) == int(flags[1].item()) == 3 * dm.launch_info().grid
+    dm.set_peers([], [])
+    dm.close()
+
+
+@pytest.mark.gpu
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("world", [2, 4])
 def test_fused_allgather_processes_one_gpu(cuda, tmp_path, world):
