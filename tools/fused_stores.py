@@ -39,6 +39,7 @@ torch.cuda.synchronize()
 peer_ok = torch.equal(y.view(torch.int16), other.view(torch.int16))
 y2 = torch.zeros_like(y)
 dm.spmv_into(x, y2)
+dm.spmv_into(x, y2, pdl=True)  # the chain instance without peers (ncu: compare with the fused launch)
 torch.cuda.synchronize()
 assert torch.equal(y.view(torch.int16), y2.view(torch.int16)), "fused y differs from plain y"
 
