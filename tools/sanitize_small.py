@@ -1,6 +1,6 @@
 """compute-sanitizer driver: small cases of every kernel — SpMV at every width, SpMM batches,
 the dense and CSR compressors, csr_from_dense / dense_from_macko / padding_count, the device plan,
-the host-buffer path, a PDL decode chain and a small Llama decode step — checked against the
+the host-buffer path, the fused all-gather instance (one local stand-in peer), a PDL decode chain and a small Llama decode step — checked against the
 oracle (tools only).  Run: compute-sanitizer --tool memcheck python tools/sanitize_small.py"""
 import os
 import sys
@@ -30,6 +30,13 @@ for bits in (1, 2, 4, 8):
         dm.spmv_into(to_dev(x), yp, pdl=True)
         torch.cuda.synchronize()
         bad += int(not np.array_equal(to_host_u16(yp), y))
+        other = torch.full((R,), -1.0, dtype=torch.float16, device="cuda")  # the peers instance
+        fl = torch.zeros(2, dtype=torch.int32, device="cuda")
+        dm.set_peers([yp.data_ptr(), other.data_ptr()], [fl.data_ptr(), fl.data_ptr() + 4])
+        dm.spmv_into(to_dev(x), yp, peers=True)
+        torch.cuda.synchronize()
+        bad += int(not np.array_equal(to_host_u16(other), y)) + int(not np.array_equal(to_host_u16(yp), y))
+        dm.set_peers([], [])
         vals, cols, rp = M.csr_from_dense(A)
         dc = M.DeviceMatrix.from_csr(vals, cols, rp, R, C, bits)
         bad += int(not np.array_equal(dc.download().packed_deltas, m.deltas))
