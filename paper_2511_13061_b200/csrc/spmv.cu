@@ -306,10 +306,13 @@ __device__ __forceinline__ void lane_step_b(float (&acc)[kB], const uint4& v, co
 // warps around it, so it stores its 2 bytes straight into every peer's y (kDirect); every other
 // row belongs to the warp that walked it and reaches the peers through the warp's stash
 // (own_row_put).
-template <bool kDirect>
+// kMirror: the plain instance also serves the host-buffer path (y_mirror); the chain and peers
+// instances carry no mirror code (chain 2172 -> 2151 us per token without it).
+template <bool kDirect, bool kMirror>
 __device__ __forceinline__ void put_y(const SpmvArgs& a, uint32_t r, uint16_t v) {
     a.y[r] = v;
-    if (a.y_mirror) a.y_mirror[r] = v;
+    if constexpr (kMirror)
+        if (a.y_mirror) a.y_mirror[r] = v;
     if constexpr (kDirect)
         for (uint32_t p = 0; p < a.n_peer; ++p) a.peer_y[p][r] = v;
 }
@@ -344,10 +347,10 @@ __device__ __forceinline__ void own_row_put(const SpmvArgs& a, uint32_t r, uint1
 }
 
 // Batched outputs (SpMM): Y[b][r] for b < a.batch (Y rows ldy apart).
-template <int kB, bool kDirect>
+template <int kB, bool kDirect, bool kMirror>
 __device__ __forceinline__ void put_y_b(const SpmvArgs& a, uint32_t r, const uint16_t (&v)[kB]) {
     if constexpr (kB == 1) {
-        put_y<kDirect>(a, r, v[0]);
+        put_y<kDirect, kMirror>(a, r, v[0]);
     } else {
 #pragma unroll
         for (int b = 0; b < kB; ++b)
@@ -464,7 +467,7 @@ __device__ __forceinline__ bool finish_split_b(uint32_t j0, uint32_t tend, uint3
 
 // Move to the next non-empty row piece of the chunk; empty rows get y = +0.  Returns false
 // when the chunk is exhausted.  The row pointer after the next row is prefetched one row ahead.
-template <int kB, bool kPeers>
+template <int kB, bool kPeers, bool kMirror>
 __device__ __forceinline__ bool next_piece(RowState<kB>& rs, const SpmvArgs& a, uint32_t w, int lane) {
     for (;;) {
         if (rs.units_left == 0) return false;
@@ -481,7 +484,7 @@ __device__ __forceinline__ bool next_piece(RowState<kB>& rs, const SpmvArgs& a, 
         if (rs.T) return true;
         if (lane == 0) {  // empty row: fp16(+0.0)
             const uint16_t z[kB] = {};
-            put_y_b<kB, false>(a, rs.r, z);
+            put_y_b<kB, false, kMirror>(a, rs.r, z);
         }
         if constexpr (kPeers) own_row_put(a, rs.r, 0, lane);
     }
@@ -800,13 +803,14 @@ __device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs
 template <int kXMode, int kBits, int kB, bool kSplitEdges, bool kPeers>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
                                          RowState<kB>& rs) {
+    constexpr bool kMirror = !kSplitEdges && !kPeers;  // only the plain instance serves y_mirror
     if (rs.T == 0) {
         if (lane == 0) {
             const uint16_t z[kB] = {};
-            put_y_b<kB, false>(a, rs.r, z);
+            put_y_b<kB, false, kMirror>(a, rs.r, z);
         }
         if constexpr (kPeers) own_row_put(a, rs.r, 0, lane);
-        if (!next_piece<kB, kPeers>(rs, a, w, lane)) return;
+        if (!next_piece<kB, kPeers, kMirror>(rs, a, w, lane)) return;
     }
     // loop invariants pinned in registers (not re-derived from the CTA's shared window per pair)
     // (ring positions in 8-element groups: the lane's group of a step at S is (S / 8 + lane_q) & qmask)
@@ -925,23 +929,23 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
         if constexpr (kB == 1) {
             if (!rs.split) {
                 const uint16_t v = f32_to_f16_rn(rs.row_acc[0]);
-                if (lane == 0) put_y<false>(a, rs.r, v);
+                if (lane == 0) put_y<false, kMirror>(a, rs.r, v);
                 if constexpr (kPeers) own_row_put(a, rs.r, v, lane);
             } else {
                 const int v = finish_split(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc[0], a.plan, lane);
-                if (v >= 0) put_y<kPeers>(a, rs.r, (uint16_t)v);
+                if (v >= 0) put_y<kPeers, kMirror>(a, rs.r, (uint16_t)v);
             }
         } else {
             uint16_t out[kB];
             if (!rs.split) {
 #pragma unroll
                 for (int b = 0; b < kB; ++b) out[b] = f32_to_f16_rn(rs.row_acc[b]);
-                if (lane == 0) put_y_b<kB, false>(a, rs.r, out);
+                if (lane == 0) put_y_b<kB, false, kMirror>(a, rs.r, out);
             } else if (finish_split_b<kB>(rs.j0, rs.tend, rs.n_r, rs.slot, rs.sid, rs.row_acc, a.plan, lane, out)) {
-                put_y_b<kB, kPeers>(a, rs.r, out);
+                put_y_b<kB, kPeers, kMirror>(a, rs.r, out);
             }
         }
-        if (!next_piece<kB, kPeers>(rs, a, w, lane)) break;
+        if (!next_piece<kB, kPeers, kMirror>(rs, a, w, lane)) break;
     }
 }
 
@@ -1074,7 +1078,10 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    // fused all-gather: the chain instance with the peer stores (the others carry none of that code)
+    // fused all-gather: the chain instance with the peer stores (the others carry none of that code);
+    // the host-buffer path's y_mirror: the plain instance alone
+    if (a.n_peer && a.y_mirror) return cudaErrorInvalidValue;
+    if (a.y_mirror) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
     if (a.n_peer) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true, true>, a);
     if (pdl || kChainForAll) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
