@@ -1219,6 +1219,7 @@ macko_status spmv_launch(const macko_dev_matrix* m, const uint16_t* d_x, uint16_
         a.plan.partials = w->partials.p;
         a.pdl = (flags & MACKO_SPMV_PDL) != 0;
         a.y_mirror = y_mirror;
+        a.no_split = m->n_split == 0 ? 1u : 0u;
         if (flags & MACKO_SPMV_PEERS) {
             a.n_peer = m->n_peer;
             const uint32_t bank = (flags & MACKO_SPMV_PEER_BANK1) ? 1u : 0u;

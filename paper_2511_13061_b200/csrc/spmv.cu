@@ -800,7 +800,7 @@ __device__ __forceinline__ void stage_x_tma_rest(const SpmvArgs& a, uint16_t* xs
 }
 
 // The warp's walk over its rows of one SpMV (x staged, ring and walk set up by op_begin).
-template <int kXMode, int kBits, int kB, bool kSplitEdges, bool kPeers>
+template <int kXMode, int kBits, int kB, bool kSplitEdges, bool kPeers, bool kNoSplit>
 __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane, uint32_t xs_addr_in, Ring& g,
                                          RowState<kB>& rs) {
     constexpr bool kMirror = !kSplitEdges && !kPeers;  // only the plain instance serves y_mirror
@@ -920,14 +920,14 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
             for (int b = 0; b < kB; ++b) {
                 const float red = warp_tree_sum(rs.acc[b]);
                 rs.acc[b] = 0.0f;
-                if (rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[(size_t)pslot * kB + b] = red;
+                if (!kNoSplit && rs.split && rs.j0 > 0 && lane == 0) a.plan.partials[(size_t)pslot * kB + b] = red;
                 rs.row_acc[b] += red;
             }
             t = ue;
         }
         // -- piece end
         if constexpr (kB == 1) {
-            if (!rs.split) {
+            if (kNoSplit || !rs.split) {
                 const uint16_t v = f32_to_f16_rn(rs.row_acc[0]);
                 if (lane == 0) put_y<false, kMirror>(a, rs.r, v);
                 if constexpr (kPeers) own_row_put(a, rs.r, v, lane);
@@ -952,7 +952,10 @@ __device__ __forceinline__ void run_rows(const SpmvArgs& a, uint32_t w, int lane
 // kChain: the instance of PDL launches (decode chains): per-step edge masking (run_rows) and x
 // staged by one bulk copy per CTA (stage_x_tma_*).  Both pay only with the kernel's code and x
 // warm in L2, as in a chain; a stand-alone launch after an L2 flush is faster without them.
-template <int kXMode, int kBits, int kB = 1, bool kChain = false, bool kPeers = false>
+// kNoSplit: the chain instance for plans without split rows (every row one unit, as in the Llama
+// linears): no partial stores or split finish in the walk (chain 2154 -> 2129 us per token; the
+// plain instance gains nothing from it).
+template <int kXMode, int kBits, int kB = 1, bool kChain = false, bool kPeers = false, bool kNoSplit = false>
 __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) macko_spmv(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[kSpmvWarpsPerCta][kMaxRing];
@@ -1006,7 +1009,7 @@ __global__ void __launch_bounds__(kSpmvWarpsPerCta * kWarp, kSpmvCtasPerSm) mack
     const uint32_t xs_addr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
     if (kChain && has_work && lane == 0)  // the staggered first fill's remaining chunks (ring_begin), once x is in
         for (uint32_t i = 1; i < min(kMaxRing, g.n_chunks); ++i) fill_chunk<kBits>(g, a, i);
-    if (has_work) run_rows<kXMode, kBits, kB, kChain, kPeers>(a, w, lane, xs_addr, g, rs);
+    if (has_work) run_rows<kXMode, kBits, kB, kChain, kPeers, kNoSplit>(a, w, lane, xs_addr, g, rs);
     MK_TRACE(6);
     if constexpr (kPeers) {
         if (has_work) {  // the stash's last, partial group
@@ -1049,6 +1052,9 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
         e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(macko_spmv<kXMode, kBits, 1, true, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, macko_spmv<kXMode, kBits>, threads, smem);
     if (e == cudaSuccess) {
         int c2 = 0;
@@ -1056,6 +1062,10 @@ static cudaError_t occ_one(size_t smem, int* ctas_per_sm) {
         *ctas_per_sm = std::min(*ctas_per_sm, c2);
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, macko_spmv<kXMode, kBits, 1, true, true>, threads, smem);
+        *ctas_per_sm = std::min(*ctas_per_sm, c2);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c2, macko_spmv<kXMode, kBits, 1, true, false, true>, threads,
+                                                              smem);
         *ctas_per_sm = std::min(*ctas_per_sm, c2);
     }
     return e;
@@ -1083,7 +1093,9 @@ static cudaError_t launch_one(const SpmvArgs& a, int grid, size_t smem, cudaStre
     if (a.n_peer && a.y_mirror) return cudaErrorInvalidValue;
     if (a.y_mirror) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
     if (a.n_peer) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true, true>, a);
-    if (pdl || kChainForAll) return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
+    if (pdl || kChainForAll)
+        return a.no_split ? cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true, false, true>, a)
+                          : cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits, 1, true>, a);
     return cudaLaunchKernelEx(&cfg, macko_spmv<kXMode, kBits>, a);
 }
 

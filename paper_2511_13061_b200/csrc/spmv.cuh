@@ -57,6 +57,7 @@ struct SpmvArgs {
     // its end, and 4736 warps loading one global word at once serialise on its L2 line (+10 us).
     uint16_t* peer_y[kMaxPeers];
     uint32_t* peer_flag[kMaxPeers];
+    uint32_t no_split;     // the plan has no split rows (PDL launches use the kNoSplit instance)
     uint16_t* y_mirror;    // host-buffer SpMV: y rows also stored straight into the mapped host y
     uint32_t batch;        // SpMM: vectors in the batch (<= the kernel's kB); x = XT interleaved
     uint64_t ldy;          // SpMM: element stride between the batch's y vectors

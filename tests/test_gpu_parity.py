@@ -722,6 +722,22 @@ def test_pdl_instance_other_widths(cuda, bits):
     assert np.array_equal(gpu_spmv_pdl(dm, x), b200_y(m, x)), bits
 
 
+@pytest.mark.parametrize("R,C,d,splits", [(64, 40000, 0.5, True), (600, 70000, 0.3, True), (4096, 4096, 0.5, False),
+                                           (300, 6000, 0.9, False)])
+def test_pdl_instance_with_and_without_split_rows(cuda, R, C, d, splits):
+    # PDL launches of a plan with split rows use the chain instance with the split-row finish;
+    # without split rows (every row one unit, the Llama linears) the kNoSplit instance.
+    A = O.gen_dense(R, C, d, R + C)
+    A[5] = 0
+    x = O.gen_vector(C, 3)
+    dm = gpu_encode(A)
+    assert (dm.launch_info().n_split_rows > 0) == splits
+    ref = b200_y(O.encode_dense(A), x)
+    for _ in range(2):  # split counters are reset by the last arrival
+        assert np.array_equal(gpu_spmv_pdl(dm, x), ref)
+    assert np.array_equal(gpu_spmv(dm, x), ref)
+
+
 def test_pdl_instance_masked_edges_do_not_leak_inf_nan(cuda):
     R, C = 240, 1500
     A = O.gen_dense(R, C, 0.35, 21)
