@@ -17,7 +17,7 @@ from tests.helpers import b200_y, to_dev, to_host_u16  # noqa: E402
 
 bad = 0
 for bits in (1, 2, 4, 8):
-    for R, C, d in ((37, 1000, 0.3), (300, 2500, 0.9), (5, 9000, 0.05)):
+    for R, C, d in ((37, 1000, 0.3), (300, 2500, 0.9), (5, 9000, 0.05), (8, 40000, 0.5)):  # last: split rows
         A = O.gen_dense(R, C, d, R + C + bits)
         x = O.gen_vector(C, 3)
         m = O.encode_dense(A, bits)
